@@ -1,0 +1,196 @@
+/*
+ * mlmcp.h — C ABI of libmlmcp.so, the B200 (sm_100a) batched implicit-Euler /
+ * Parareal / MLMC-reduction library behind paper_2507_19246_b200.
+ *
+ * The reference (arXiv 2507.19246, /root/reference/pkg/src/mlmc_parareal) is
+ * pure Python; the interfaces this ABI replaces are Python callables.  Each
+ * entry point below names the reference code it stands in for:
+ *
+ *   mlmcp_assemble         builders models.py:217-302 and the operator
+ *                          formation `model.mass + dt*model.stiffness`
+ *                          timeint.py:65 (per-sample CSR values on one
+ *                          shared pattern instead of dense n x n matrices)
+ *   mlmcp_kl_sigma         (new input kind, config 3; no reference code)
+ *   mlmcp_propagate        implicit_euler_solve timeint.py:88-111 and
+ *                          propagate timeint.py:114-128 (LU factor/solve
+ *                          :64-75,:110,:127 replaced by Jacobi-PCG at a
+ *                          stated tolerance); batched over (sample, slice)
+ *                          tasks; QoI accumulation replaces evaluate_qoi
+ *                          models.py:321-344 for the FE QoI kinds
+ *   mlmcp_parareal_coarse  parareal_solve coarse/update sweep
+ *                          parareal.py:168-178
+ *   mlmcp_parareal_defect  defect parareal.py:93-103 and the stopping test
+ *                          parareal.py:198-207
+ *   mlmcp_parareal_finalize states[k_used:] = fine_end[k_used:]
+ *                          parareal.py:209-210
+ *   mlmcp_energy           new QoI kind 1/2 a^T K a (no reference code)
+ *   mlmcp_level_reduce     LevelStats accumulators SPEC.md:256-260 (absent
+ *                          from the reference code)
+ *
+ * Conventions
+ *   - Every pointer argument named *_d or documented as "device" is a device
+ *     pointer owned by the caller (PyTorch tensors).  The library only keeps
+ *     the sparsity pattern and scalars in the context.
+ *   - Calls are stream-ordered and asynchronous on `stream` (a cudaStream_t
+ *     passed as void*), except where documented (streaming-path iteration
+ *     control reads a device counter back to the host).
+ *   - Return 0 on success or a negative MLMCP_E* code; the message is in
+ *     mlmcp_last_error() (thread-local).  Per-task solver failures are
+ *     reported in status[4*slot + 0..3] = {MLMCP_ST_* code, 0-based step index
+ *     (SingularSystemError.step_index timeint.py:28-30), interval, iteration
+ *     (PropagatorError parareal.py:37-43)}.
+ *   - A context is bound to one device and is not re-entrant across threads.
+ */
+#ifndef MLMCP_H
+#define MLMCP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MLMCP_ABI_VERSION 1
+
+/* return codes */
+#define MLMCP_OK 0
+#define MLMCP_EINVAL (-22)  /* -> ValueError */
+#define MLMCP_ECUDA (-5)    /* -> RuntimeError */
+#define MLMCP_ENOMEM (-12)  /* -> MemoryError / workspace too small */
+
+/* per-task status codes */
+#define MLMCP_ST_OK 0
+#define MLMCP_ST_NOCONV 1    /* PCG hit max_it       -> SingularSystemError */
+#define MLMCP_ST_BREAKDOWN 2 /* PCG curvature <= 0    -> SingularSystemError */
+#define MLMCP_ST_NONFINITE 3 /* non-finite residual   -> SingularSystemError */
+
+/* QoI modes of a task */
+#define MLMCP_QOI_NONE 0
+#define MLMCP_QOI_FINAL_ENERGY 1 /* qoi[slot] = 1/2 x_T^T K x_T               */
+#define MLMCP_QOI_SUM_ENERGY 2   /* qoi[slot] = sum_{g > qoi_from} W(x_g)     */
+
+typedef struct mlmcp_ctx mlmcp_ctx;
+
+/*
+ * One propagation task: n_steps implicit-Euler steps of
+ *     (M + dt K) x_{g} = M x_{g-1} + dt * sin(omega t_g) * profile,
+ *     t_g = t_base + (double)g * dt,  g = k0+1 .. k0+n_steps
+ * (timeint.py:78-85,108-110: the grid is anchored at an origin so that a
+ * sub-interval solve is bitwise the same grid as the whole-interval solve).
+ * Offsets are element offsets into the caller's state buffer `xbuf`.
+ * 88 bytes, natural alignment (mirrored by a numpy structured dtype).
+ */
+typedef struct mlmcp_task {
+  int32_t sample;   /* row of the per-sample M/K value arrays            */
+  int32_t n_steps;  /* >= 0                                              */
+  int64_t k0;       /* grid offset                                       */
+  double dt;        /* step size                                         */
+  double t_base;    /* grid origin                                       */
+  int64_t x_in;     /* offset of the initial state                       */
+  int64_t x_out;    /* offset of the terminal state                      */
+  int64_t traj;     /* offset of (n_steps+1)*N stored states, or -1      */
+  int32_t qoi_slot; /* -1: no QoI                                        */
+  int32_t qoi_mode; /* MLMCP_QOI_*                                       */
+  int64_t qoi_from; /* SUM_ENERGY: accumulate steps with g > qoi_from    */
+  int32_t group;    /* index into `active` (Parareal sample), -1: always */
+  int32_t slot;     /* index into iters / status                         */
+  int32_t tag;      /* copied to status[4*slot+2..3] on failure          */
+  int32_t reserved;
+} mlmcp_task;
+
+/* ---- library ---------------------------------------------------------- */
+int mlmcp_abi_version(void);
+const char* mlmcp_last_error(void);
+/* number of kernels this process launched through the library (evidence) */
+uint64_t mlmcp_launch_count(void);
+
+/* ---- context ---------------------------------------------------------- */
+/* row_ptr (n_rows+1) / col (nnz) are HOST arrays (int32, CSR, columns sorted
+ * per row); they are validated and copied to the device. */
+int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
+                     const int32_t* col, mlmcp_ctx** out);
+int mlmcp_ctx_destroy(mlmcp_ctx* ctx);
+/* max_row_nnz of the pattern and the widest row count the SM-resident path
+ * accepts (tasks with n_rows <= small_max_rows run one CTA per task). */
+int mlmcp_ctx_info(const mlmcp_ctx* ctx, int* max_row_nnz, int* small_max_rows);
+/* Assembly gather map (HOST arrays, copied): for CSR entry q the
+ * contributions c in [cptr[q], cptr[q+1]) are (elem[c], mw[c], kw[c]):
+ *     M_q = sum_c sigma(elem_c) * mw_c,   K_q = sum_c nu(elem_c) * kw_c. */
+int mlmcp_ctx_set_assembly(mlmcp_ctx* ctx, int n_elem, int n_contrib,
+                           const int32_t* cptr, const int32_t* elem,
+                           const double* mw, const double* kw);
+/* Force a path: 0 auto, 1 SM-resident, 2 streaming (tests / benchmarks). */
+int mlmcp_ctx_set_path(mlmcp_ctx* ctx, int path);
+
+/* ---- K1: assembly ------------------------------------------------------ */
+/* sigma(s, e) = sigma_d[s*sigma_stride + (sigma_index_d ? sigma_index_d[e] : e)]
+ * (same for nu).  Writes M_d, K_d: [S][nnz]. */
+int mlmcp_assemble(mlmcp_ctx* ctx, int S, const double* sigma_d,
+                   int64_t sigma_stride, const int32_t* sigma_index_d,
+                   const double* nu_d, int64_t nu_stride,
+                   const int32_t* nu_index_d, double* M_d, double* K_d,
+                   void* stream);
+
+/* sigma_out[s][e] = exp(log_sigma0 + scale * sum_k xi[s][k] * basis[k][e]) */
+int mlmcp_kl_sigma(int S, int n_elem, int n_modes, const double* xi_d,
+                   const double* basis_d, double log_sigma0, double scale,
+                   double* sigma_out_d, void* stream);
+
+/* ---- K2-K4, K6: batched implicit-Euler propagation ---------------------- */
+/* Workspace bytes for mlmcp_propagate / mlmcp_parareal_coarse with n_tasks
+ * tasks over S per-sample operators (0 on the SM-resident path). */
+size_t mlmcp_workspace_bytes(const mlmcp_ctx* ctx, int n_tasks, int S);
+
+int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
+                    int S, const double* M_d, const double* K_d,
+                    const double* profile_d, double omega, double rtol,
+                    int max_it, double* xbuf_d, double* qoi_d,
+                    int32_t* iters_d, int32_t* status_d,
+                    const int32_t* active_d, void* ws_d, size_t ws_bytes,
+                    void* stream);
+
+/* ---- K5: Parareal ------------------------------------------------------ */
+/* Coarse/update sweep of iteration k (1-based) for S samples.
+ *   U: [S][m+1][N] boundary states, F: [S][m+1][N] fine end states,
+ *   C: [S][m][N] previous coarse values, slice_k0/slice_steps: [m] coarse
+ *   grid offsets / step counts of slices 1..m (index n-1).
+ * Samples with active_d[s] == 0 are skipped.  Solver failures set
+ * status[4*s..] = {code, step, interval n, iteration k} and clear active[s]. */
+int mlmcp_parareal_coarse(mlmcp_ctx* ctx, int S, int k, int m,
+                          const double* M_d, const double* K_d,
+                          const double* profile_d, double omega, double dt_c,
+                          double t0, const int64_t* slice_k0_d,
+                          const int32_t* slice_steps_d, double rtol,
+                          int max_it, double* U_d, const double* F_d,
+                          double* C_d, int32_t* iters_d, int32_t* status_d,
+                          const int32_t* active_d, void* ws_d,
+                          size_t ws_bytes, void* stream);
+
+/* Jump defect of iteration k; records defect_d[s*k_max + k-1], sets
+ * k_used_d[s] = k and clears active_d[s] when defect <= tol (or k == m). */
+int mlmcp_parareal_defect(mlmcp_ctx* ctx, int S, int k, int m, int k_max,
+                          const double* U_d, const double* F_d, double tol,
+                          int32_t* active_d, int32_t* k_used_d,
+                          double* defect_d, void* stream);
+
+/* U[s][n] = F[s][n] for n >= k_used[s]. */
+int mlmcp_parareal_finalize(mlmcp_ctx* ctx, int S, int m, double* U_d,
+                            const double* F_d, const int32_t* k_used_d,
+                            void* stream);
+
+/* ---- K6 / K7 ----------------------------------------------------------- */
+/* out[i] = 1/2 x_i^T K_{sample[i]} x_i for x_i = xbuf[x_off[i] ..]. */
+int mlmcp_energy(mlmcp_ctx* ctx, int n, const int32_t* sample_d,
+                 const int64_t* x_off_d, const double* xbuf_d,
+                 const double* K_d, double* out_d, void* stream);
+
+/* Y = q_l - q_lm1 over n samples (fixed order); out = {sum Y, sum Y^2,
+ * mean, var} with var = (sum Y^2 - n mean^2)/(n-1). */
+int mlmcp_level_reduce(int n, const double* q_l_d, const double* q_lm1_d,
+                       double* out_d, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MLMCP_H */

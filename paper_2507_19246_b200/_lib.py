@@ -1,0 +1,142 @@
+"""ctypes binding of libmlmcp.so (include/mlmcp.h).
+
+The library is built in-tree (``make`` or ``__graft_entry__.build()``) and
+loaded from this package directory.  There is no fallback: if the shared
+object is missing or a GPU is absent, every device entry point raises.
+
+Error mapping:
+  MLMCP_EINVAL -> ValueError, MLMCP_ENOMEM -> MemoryError,
+  MLMCP_ECUDA  -> RuntimeError.  Per-task solver failures are mapped by the
+  callers to SingularSystemError (timeint.py:25-30) or PropagatorError
+  (parareal.py:37-43).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+import numpy as np
+
+LIB_NAME = "libmlmcp.so"
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+
+EINVAL = -22
+ECUDA = -5
+ENOMEM = -12
+
+ST_OK, ST_NOCONV, ST_BREAKDOWN, ST_NONFINITE = 0, 1, 2, 3
+STATUS_NAMES = {ST_NOCONV: "PCG did not converge within max_it",
+                ST_BREAKDOWN: "PCG breakdown (operator not SPD)",
+                ST_NONFINITE: "non-finite residual"}
+STATUS_INTS = 4
+
+QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY = 0, 1, 2
+
+# mlmcp_task (88 bytes, natural alignment)
+TASK_DTYPE = np.dtype([
+    ("sample", np.int32), ("n_steps", np.int32), ("k0", np.int64), ("dt", np.float64),
+    ("t_base", np.float64), ("x_in", np.int64), ("x_out", np.int64), ("traj", np.int64),
+    ("qoi_slot", np.int32), ("qoi_mode", np.int32), ("qoi_from", np.int64),
+    ("group", np.int32), ("slot", np.int32), ("tag", np.int32), ("reserved", np.int32),
+], align=True)
+assert TASK_DTYPE.itemsize == 88
+
+# every symbol include/mlmcp.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "mlmcp_abi_version", "mlmcp_last_error", "mlmcp_launch_count",
+    "mlmcp_ctx_create", "mlmcp_ctx_destroy", "mlmcp_ctx_info", "mlmcp_ctx_set_assembly",
+    "mlmcp_ctx_set_path", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
+    "mlmcp_propagate", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
+    "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce",
+)
+
+_lock = threading.Lock()
+_lib = None
+
+P = ctypes.c_void_p
+I32 = ctypes.c_int32
+I64 = ctypes.c_int64
+F64 = ctypes.c_double
+SZ = ctypes.c_size_t
+
+_SIGS = {
+    "mlmcp_abi_version": (ctypes.c_int, []),
+    "mlmcp_last_error": (ctypes.c_char_p, []),
+    "mlmcp_launch_count": (ctypes.c_uint64, []),
+    "mlmcp_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
+                                        ctypes.POINTER(P)]),
+    "mlmcp_ctx_destroy": (ctypes.c_int, [P]),
+    "mlmcp_ctx_info": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int),
+                                      ctypes.POINTER(ctypes.c_int)]),
+    "mlmcp_ctx_set_assembly": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+    "mlmcp_ctx_set_path": (ctypes.c_int, [P, ctypes.c_int]),
+    "mlmcp_assemble": (ctypes.c_int, [P, ctypes.c_int, P, I64, P, P, I64, P, P, P, P]),
+    "mlmcp_kl_sigma": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, F64, F64,
+                                      P, P]),
+    "mlmcp_workspace_bytes": (SZ, [P, ctypes.c_int, ctypes.c_int]),
+    "mlmcp_propagate": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_int, P, P, P, F64, F64,
+                                       ctypes.c_int, P, P, P, P, P, P, SZ, P]),
+    "mlmcp_parareal_coarse": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
+                                             P, F64, F64, F64, P, P, F64, ctypes.c_int, P, P,
+                                             P, P, P, P, P, SZ, P]),
+    "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                             ctypes.c_int, P, P, F64, P, P, P, P]),
+    "mlmcp_parareal_finalize": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+    "mlmcp_energy": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P, P, P]),
+    "mlmcp_level_reduce": (ctypes.c_int, [ctypes.c_int, P, P, P, P]),
+}
+
+
+class LibraryMissingError(RuntimeError):
+    pass
+
+
+def load(path: str = LIB_PATH):
+    """Load libmlmcp.so (once) and bind signatures.  Raises if absent."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(path):
+            raise LibraryMissingError(
+                f"{path} not found: build it with `make` or __graft_entry__.build(); "
+                "there is no CPU fallback")
+        lib = ctypes.CDLL(path)
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def last_error() -> str:
+    return load().mlmcp_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str):
+    if rc == 0:
+        return
+    msg = f"{what}: {last_error()}"
+    if rc == EINVAL:
+        raise ValueError(msg)
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise RuntimeError(f"{msg} (code {rc})")
+
+
+def launch_count() -> int:
+    return int(load().mlmcp_launch_count())
+
+
+def ptr(t) -> ctypes.c_void_p | None:
+    """Device pointer of a torch tensor (None for None)."""
+    if t is None:
+        return None
+    return ctypes.c_void_p(t.data_ptr())
+
+
+def np_ptr(a: np.ndarray) -> ctypes.c_void_p:
+    return a.ctypes.data_as(ctypes.c_void_p)

@@ -1,0 +1,428 @@
+// api.cu — the extern "C" surface of libmlmcp.so (see include/mlmcp.h) plus
+// the small batched kernels that are not PCG: assembly (K1), the KL
+// conductivity field, the Parareal defect / finalize (K5), the magnetic
+// energy QoI (K6) and the MLMC level reduction (K7).
+#include <math.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "mlmcp_internal.cuh"
+
+namespace mlmcp {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+}  // namespace
+
+void set_error(const std::string& msg) { g_last_error = msg; }
+void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+int cuda_fail(cudaError_t err, const char* what) {
+  set_error(std::string(what) + ": " + cudaGetErrorString(err));
+  return MLMCP_ECUDA;
+}
+
+namespace {
+
+int einval(const std::string& msg) {
+  set_error(msg);
+  return MLMCP_EINVAL;
+}
+
+template <typename T>
+int upload(T** dst, const T* src, size_t n) {
+  *dst = nullptr;
+  if (n == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaMalloc(reinterpret_cast<void**>(dst), n * sizeof(T)));
+  MLMCP_CUDA_CHECK(cudaMemcpy(*dst, src, n * sizeof(T), cudaMemcpyHostToDevice));
+  return MLMCP_OK;
+}
+
+// ---------------------------------------------------------------- K1 assembly
+// One thread per (sample, CSR entry); contributions summed in ascending
+// element order (the gather map is sorted on the host).
+__global__ void assemble_kernel(int S, int nnz, const int32_t* __restrict__ cptr,
+                                const int32_t* __restrict__ celem,
+                                const double* __restrict__ cmw, const double* __restrict__ ckw,
+                                const double* __restrict__ sigma, int64_t sstride,
+                                const int32_t* __restrict__ sidx, const double* __restrict__ nu,
+                                int64_t nstride, const int32_t* __restrict__ nidx, double* M,
+                                double* K) {
+  const int s = blockIdx.y;
+  const int q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nnz) return;
+  const double* sg = sigma + s * sstride;
+  const double* nv = nu + s * nstride;
+  double m = 0.0, k = 0.0;
+  for (int c = cptr[q]; c < cptr[q + 1]; ++c) {
+    const int e = celem[c];
+    const double se = sg[sidx ? sidx[e] : e];
+    const double ne = nv[nidx ? nidx[e] : e];
+    m = __dadd_rn(m, __dmul_rn(se, cmw[c]));
+    k = __dadd_rn(k, __dmul_rn(ne, ckw[c]));
+  }
+  M[(int64_t)s * nnz + q] = m;
+  K[(int64_t)s * nnz + q] = k;
+}
+
+// sigma[s][e] = exp(log_sigma0 + scale * sum_k xi[s][k] basis[k][e])
+__global__ void kl_sigma_kernel(int S, int E, int modes, const double* __restrict__ xi,
+                                const double* __restrict__ basis, double log_s0, double scale,
+                                double* out) {
+  extern __shared__ double xs[];
+  const int s = blockIdx.y;
+  for (int k = threadIdx.x; k < modes; k += blockDim.x) xs[k] = xi[(int64_t)s * modes + k];
+  __syncthreads();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  double acc = 0.0;
+  for (int k = 0; k < modes; ++k) acc = fma(xs[k], basis[(int64_t)k * E + e], acc);
+  out[(int64_t)s * E + e] = exp(log_s0 + scale * acc);
+}
+
+// ---------------------------------------------------------------- K6 energy
+__global__ void energy_kernel(int n_items, int N, int64_t nnz, const int32_t* __restrict__ rp,
+                              const int32_t* __restrict__ col, const int32_t* __restrict__ sample,
+                              const int64_t* __restrict__ xoff, const double* __restrict__ xbuf,
+                              const double* __restrict__ K, double* out) {
+  __shared__ double red[2 * 4 * 32];
+  const int it = blockIdx.x;
+  const double* x = xbuf + xoff[it];
+  const double* Ks = K + (int64_t)sample[it] * nnz;
+  double acc = 0.0;
+  for (int i = threadIdx.x; i < N; i += blockDim.x) {
+    double kx = 0.0;
+    for (int q = rp[i]; q < rp[i + 1]; ++q) kx = fma(Ks[q], x[col[q]], kx);
+    acc = fma(x[i], kx, acc);
+  }
+  int par = 0;
+  double v[1] = {acc};
+  block_allsum<1>(v, red, par);
+  if (threadIdx.x == 0) out[it] = 0.5 * v[0];
+}
+
+// ---------------------------------------------------------------- K5 defect
+// parareal.py:93-103 + :198-207 for iteration k of each active sample.
+__global__ void defect_kernel(int S, int k, int m, int k_max, int N, const double* __restrict__ U,
+                              const double* __restrict__ F, double tol, int32_t* active,
+                              int32_t* k_used, double* defect) {
+  __shared__ double red[2 * 4 * 32];
+  const int s = blockIdx.x;
+  if (active[s] == 0) return;
+  const int64_t n64 = N;
+  double d = 0.0;
+  int par = 0;
+  for (int n = k; n < m; ++n) {
+    const double* u = U + ((int64_t)s * (m + 1) + n) * n64;
+    const double* f = F + ((int64_t)s * (m + 1) + n) * n64;
+    double jj = 0.0, ff = 0.0;
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const double diff = f[i] - u[i];
+      jj = fma(diff, diff, jj);
+      ff = fma(f[i], f[i], ff);
+    }
+    double v[2] = {jj, ff};
+    block_allsum<2>(v, red, par);
+    const double ratio = sqrt(v[0]) / fmax(sqrt(v[1]), 1e-30);
+    // np.max propagates NaN; fmax would drop it
+    if (isnan(ratio) || isnan(d)) d = NAN;
+    else d = fmax(d, ratio);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    defect[(int64_t)s * k_max + (k - 1)] = d;
+    k_used[s] = k;
+    if (d <= tol) active[s] = 0;
+  }
+}
+
+__global__ void finalize_kernel(int S, int m, int N, double* U, const double* F,
+                                const int32_t* k_used) {
+  const int s = blockIdx.y;
+  const int64_t n64 = N;
+  const int ku = k_used[s];
+  for (int n = ku; n <= m; ++n) {
+    const int64_t o = ((int64_t)s * (m + 1) + n) * n64;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+      U[o + i] = F[o + i];
+  }
+}
+
+// ---------------------------------------------------------------- K7 level reduce
+// Fixed-order reduction: thread j sums samples j, j+1024, ... in order, then a
+// fixed tree.  Bitwise independent of how the sample slots were filled.
+__global__ void level_reduce_kernel(int n, const double* __restrict__ ql,
+                                    const double* __restrict__ qlm1, double* out) {
+  __shared__ double red[2 * 4 * 32];
+  double sy = 0.0, sy2 = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double y = ql[i] - (qlm1 ? qlm1[i] : 0.0);
+    sy += y;
+    sy2 = fma(y, y, sy2);
+  }
+  int par = 0;
+  double v[2] = {sy, sy2};
+  block_allsum<2>(v, red, par);
+  if (threadIdx.x == 0) {
+    const double mean = v[0] / n;
+    out[0] = v[0];
+    out[1] = v[1];
+    out[2] = mean;
+    out[3] = n > 1 ? (v[1] - n * mean * mean) / (n - 1) : 0.0;
+  }
+}
+
+}  // namespace
+}  // namespace mlmcp
+
+using namespace mlmcp;
+
+struct mlmcp_ctx : public mlmcp::Ctx {};
+
+extern "C" {
+
+int mlmcp_abi_version(void) { return MLMCP_ABI_VERSION; }
+
+const char* mlmcp_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t mlmcp_launch_count(void) { return g_launches.load(); }
+
+int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
+                     const int32_t* col, mlmcp_ctx** out) {
+  if (out == nullptr) return einval("out is null");
+  *out = nullptr;
+  if (n_rows < 1 || nnz < 1 || row_ptr == nullptr || col == nullptr)
+    return einval("empty or null sparsity pattern");
+  if (row_ptr[0] != 0 || row_ptr[n_rows] != nnz) return einval("row_ptr must span [0, nnz]");
+  int max_row = 0;
+  for (int i = 0; i < n_rows; ++i) {
+    const int len = row_ptr[i + 1] - row_ptr[i];
+    if (len < 1) return einval("row " + std::to_string(i) + " is empty (no diagonal)");
+    if (len > kMaxNz)
+      return einval("row " + std::to_string(i) + " has " + std::to_string(len) +
+                    " entries; the kernels accept at most 8");
+    bool diag = false;
+    for (int q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+      if (col[q] < 0 || col[q] >= n_rows) return einval("column index out of range");
+      if (q > row_ptr[i] && col[q] <= col[q - 1]) return einval("columns must be sorted and unique");
+      diag |= col[q] == i;
+    }
+    if (!diag) return einval("row " + std::to_string(i) + " has no diagonal entry");
+    max_row = std::max(max_row, len);
+  }
+  int ndev = 0;
+  MLMCP_CUDA_CHECK(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) return einval("invalid device ordinal");
+  MLMCP_CUDA_CHECK(cudaSetDevice(device));
+  auto* c = new mlmcp_ctx();
+  c->device = device;
+  c->n = n_rows;
+  c->nnz = nnz;
+  c->max_row_nnz = max_row;
+  std::vector<int32_t> ell_col((size_t)max_row * n_rows), ell_pos((size_t)max_row * n_rows);
+  for (int i = 0; i < n_rows; ++i) {
+    const int len = row_ptr[i + 1] - row_ptr[i];
+    for (int j = 0; j < max_row; ++j) {
+      const bool in = j < len;
+      ell_col[(size_t)j * n_rows + i] = in ? col[row_ptr[i] + j] : i;
+      ell_pos[(size_t)j * n_rows + i] = in ? row_ptr[i] + j : -1;
+    }
+  }
+  int rc = upload(&c->row_ptr, row_ptr, (size_t)n_rows + 1);
+  if (!rc) rc = upload(&c->col, col, (size_t)nnz);
+  if (!rc) rc = upload(&c->ell_col, ell_col.data(), ell_col.size());
+  if (!rc) rc = upload(&c->ell_pos, ell_pos.data(), ell_pos.size());
+  if (!rc) {
+    cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&c->host_counters), 64);
+    if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
+  }
+  if (rc) {
+    mlmcp_ctx_destroy(c);
+    return rc;
+  }
+  *out = c;
+  return MLMCP_OK;
+}
+
+int mlmcp_ctx_destroy(mlmcp_ctx* c) {
+  if (c == nullptr) return MLMCP_OK;
+  cudaSetDevice(c->device);
+  cudaFree(c->row_ptr);
+  cudaFree(c->col);
+  cudaFree(c->ell_col);
+  cudaFree(c->ell_pos);
+  cudaFree(c->cptr);
+  cudaFree(c->celem);
+  cudaFree(c->cmw);
+  cudaFree(c->ckw);
+  if (c->host_counters) cudaFreeHost(c->host_counters);
+  delete c;
+  return MLMCP_OK;
+}
+
+int mlmcp_ctx_info(const mlmcp_ctx* c, int* max_row_nnz, int* small_max_rows) {
+  if (c == nullptr) return einval("null context");
+  if (max_row_nnz) *max_row_nnz = c->max_row_nnz;
+  if (small_max_rows) *small_max_rows = kSmallMaxRows;
+  return MLMCP_OK;
+}
+
+int mlmcp_ctx_set_path(mlmcp_ctx* c, int path) {
+  if (c == nullptr) return einval("null context");
+  if (path < 0 || path > 2) return einval("path must be 0 (auto), 1 (SM-resident) or 2 (streaming)");
+  if (path == 1 && c->n > kSmallMaxRows)
+    return einval("SM-resident path holds at most 1024 rows");
+  c->path = path;
+  return MLMCP_OK;
+}
+
+int mlmcp_ctx_set_assembly(mlmcp_ctx* c, int n_elem, int n_contrib, const int32_t* cptr,
+                           const int32_t* elem, const double* mw, const double* kw) {
+  if (c == nullptr) return einval("null context");
+  if (n_elem < 1 || n_contrib < 1 || !cptr || !elem || !mw || !kw)
+    return einval("empty assembly map");
+  if (cptr[0] != 0 || cptr[c->nnz] != n_contrib) return einval("cptr must span [0, n_contrib]");
+  for (int q = 0; q < c->nnz; ++q)
+    if (cptr[q + 1] < cptr[q]) return einval("cptr must be non-decreasing");
+  for (int i = 0; i < n_contrib; ++i)
+    if (elem[i] < 0 || elem[i] >= n_elem) return einval("element index out of range");
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  cudaFree(c->cptr);
+  cudaFree(c->celem);
+  cudaFree(c->cmw);
+  cudaFree(c->ckw);
+  c->n_elem = n_elem;
+  c->n_contrib = n_contrib;
+  int rc = upload(&c->cptr, cptr, (size_t)c->nnz + 1);
+  if (!rc) rc = upload(&c->celem, elem, (size_t)n_contrib);
+  if (!rc) rc = upload(&c->cmw, mw, (size_t)n_contrib);
+  if (!rc) rc = upload(&c->ckw, kw, (size_t)n_contrib);
+  return rc;
+}
+
+int mlmcp_assemble(mlmcp_ctx* c, int S, const double* sigma, int64_t sstride,
+                   const int32_t* sidx, const double* nu, int64_t nstride, const int32_t* nidx,
+                   double* M, double* K, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (c->cptr == nullptr) return einval("assembly map not set (mlmcp_ctx_set_assembly)");
+  if (S < 0 || !sigma || !nu || !M || !K) return einval("null assembly argument");
+  if (S == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  dim3 grid((c->nnz + 255) / 256, S);
+  assemble_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(
+      S, c->nnz, c->cptr, c->celem, c->cmw, c->ckw, sigma, sstride, sidx, nu, nstride, nidx, M, K);
+  MLMCP_LAUNCH_CHECK("assemble_kernel");
+  return MLMCP_OK;
+}
+
+int mlmcp_kl_sigma(int S, int E, int modes, const double* xi, const double* basis,
+                   double log_s0, double scale, double* out, void* stream) {
+  if (S < 0 || E < 1 || modes < 1 || modes > 4096 || !xi || !basis || !out)
+    return einval("bad KL arguments");
+  if (S == 0) return MLMCP_OK;
+  dim3 grid((E + 255) / 256, S);
+  kl_sigma_kernel<<<grid, 256, modes * sizeof(double), (cudaStream_t)stream>>>(
+      S, E, modes, xi, basis, log_s0, scale, out);
+  MLMCP_LAUNCH_CHECK("kl_sigma_kernel");
+  return MLMCP_OK;
+}
+
+size_t mlmcp_workspace_bytes(const mlmcp_ctx* c, int n_tasks, int S) {
+  if (c == nullptr || use_small(c)) return 0;
+  const size_t base = stream_workspace_bytes(c, std::max(n_tasks, S), S);
+  // coarse sweep extras: tasks + cval + tstatus
+  const size_t extra = ((sizeof(mlmcp_task) * S + 255) & ~size_t(255)) +
+                       ((sizeof(double) * (size_t)S * c->n + 255) & ~size_t(255)) +
+                       ((sizeof(int32_t) * 4 * S + 255) & ~size_t(255));
+  return base + extra;
+}
+
+int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
+                    const double* K, const double* profile, double omega, double rtol,
+                    int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
+                    const int32_t* active, void* ws, size_t ws_bytes, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (n_tasks < 0 || S < 1 || !tasks || !M || !K || !profile || !xbuf)
+    return einval("null or empty propagate argument");
+  if (!(rtol > 0.0) || max_it < 1) return einval("rtol must be > 0 and max_it >= 1");
+  if (n_tasks == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  if (use_small(c))
+    return small_propagate(c, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
+                           iters, status, active, (cudaStream_t)stream);
+  return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xbuf, qoi,
+                          iters, status, active, ws, ws_bytes, (cudaStream_t)stream);
+}
+
+int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, const double* K,
+                          const double* profile, double omega, double dt_c, double t0,
+                          const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
+                          int max_it, double* U, const double* F, double* C, int32_t* iters,
+                          int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
+                          void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (S < 0 || m < 1 || k < 1 || k > m || !M || !K || !profile || !slice_k0 || !slice_steps ||
+      !U || !F || !C || !active || !status)
+    return einval("bad Parareal coarse arguments");
+  if (!(rtol > 0.0) || max_it < 1 || !(dt_c > 0.0)) return einval("bad solver tolerances");
+  if (S == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  if (use_small(c))
+    return small_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
+                                 slice_steps, rtol, max_it, U, F, C, iters, status, active,
+                                 (cudaStream_t)stream);
+  return stream_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
+                                slice_steps, rtol, max_it, U, F, C, iters, status, active, ws,
+                                ws_bytes, (cudaStream_t)stream);
+}
+
+int mlmcp_parareal_defect(mlmcp_ctx* c, int S, int k, int m, int k_max, const double* U,
+                          const double* F, double tol, int32_t* active, int32_t* k_used,
+                          double* defect, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (S < 0 || k < 1 || k > m || k_max < k || !U || !F || !active || !k_used || !defect)
+    return einval("bad Parareal defect arguments");
+  if (S == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  defect_kernel<<<S, 512, 0, (cudaStream_t)stream>>>(S, k, m, k_max, c->n, U, F, tol, active,
+                                                      k_used, defect);
+  MLMCP_LAUNCH_CHECK("defect_kernel");
+  return MLMCP_OK;
+}
+
+int mlmcp_parareal_finalize(mlmcp_ctx* c, int S, int m, double* U, const double* F,
+                            const int32_t* k_used, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (S < 0 || m < 1 || !U || !F || !k_used) return einval("bad finalize arguments");
+  if (S == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  dim3 grid(std::min((c->n + 255) / 256, 64), S);
+  finalize_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(S, m, c->n, U, F, k_used);
+  MLMCP_LAUNCH_CHECK("finalize_kernel");
+  return MLMCP_OK;
+}
+
+int mlmcp_energy(mlmcp_ctx* c, int n, const int32_t* sample, const int64_t* xoff,
+                 const double* xbuf, const double* K, double* out, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (n < 0 || !sample || !xoff || !xbuf || !K || !out) return einval("bad energy arguments");
+  if (n == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  energy_kernel<<<n, 512, 0, (cudaStream_t)stream>>>(n, c->n, c->nnz, c->row_ptr, c->col, sample,
+                                                      xoff, xbuf, K, out);
+  MLMCP_LAUNCH_CHECK("energy_kernel");
+  return MLMCP_OK;
+}
+
+int mlmcp_level_reduce(int n, const double* ql, const double* qlm1, double* out, void* stream) {
+  if (n < 1 || !ql || !out) return einval("bad level-reduce arguments");
+  level_reduce_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(n, ql, qlm1, out);
+  MLMCP_LAUNCH_CHECK("level_reduce_kernel");
+  return MLMCP_OK;
+}
+
+}  // extern "C"

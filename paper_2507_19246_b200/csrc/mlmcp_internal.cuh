@@ -1,0 +1,154 @@
+// mlmcp_internal.cuh — shared internals of libmlmcp.so (sm_100a).
+//
+// Numerical contract shared by every kernel (matches the reference's
+// arithmetic where it is observable, timeint.py:65,78-85,108-110):
+//   operator  A_q = M_q + dt*K_q      (rounded product, then rounded sum)
+//   grid      t_g = t_base + (double)g * dt
+//   forcing   dt * (sin(omega*t_g) * profile_i),  omega = (2*pi)*f on host
+//   rhs       b_i = (M x)_i + forcing_i
+// All reductions are deterministic (fixed warp-butterfly + fixed cross-warp
+// order), so every per-task result is bitwise independent of batch
+// composition, launch order and GPU count.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/mlmcp.h"
+
+namespace mlmcp {
+
+constexpr int kMaxNz = 8;         // widest CSR row the kernels accept
+constexpr int kStatusInts = 4;    // status[4*slot + {code, step, interval, iteration}]
+constexpr int kSmallMaxRows = 1024;  // one row per thread, <=1024 threads
+
+struct Ctx {
+  int device = 0;
+  int n = 0;            // rows
+  int nnz = 0;
+  int max_row_nnz = 0;
+  int path = 0;         // 0 auto, 1 small, 2 streaming
+  int32_t* row_ptr = nullptr;   // device [n+1]
+  int32_t* col = nullptr;       // device [nnz]
+  int32_t* ell_col = nullptr;   // device [max_row_nnz][n], padded with the row itself
+  int32_t* ell_pos = nullptr;   // device [max_row_nnz][n], CSR position or -1
+  // assembly gather map
+  int n_elem = 0;
+  int n_contrib = 0;
+  int32_t* cptr = nullptr;
+  int32_t* celem = nullptr;
+  double* cmw = nullptr;
+  double* ckw = nullptr;
+  // pinned host counters for the streaming path
+  int32_t* host_counters = nullptr;
+};
+
+void set_error(const std::string& msg);
+void count_launch(uint64_t n = 1);
+int cuda_fail(cudaError_t err, const char* what);
+
+#define MLMCP_CUDA_CHECK(call)                                   \
+  do {                                                           \
+    cudaError_t _e = (call);                                     \
+    if (_e != cudaSuccess) return ::mlmcp::cuda_fail(_e, #call); \
+  } while (0)
+
+#define MLMCP_LAUNCH_CHECK(what)                                 \
+  do {                                                           \
+    ::mlmcp::count_launch();                                     \
+    cudaError_t _e = cudaGetLastError();                         \
+    if (_e != cudaSuccess) return ::mlmcp::cuda_fail(_e, what);  \
+  } while (0)
+
+// ------------------------------------------------------------------ device
+__device__ __forceinline__ double warp_allsum(double v) {
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
+  return v;
+}
+
+// Block-wide all-reduce of NV doubles; every thread receives bitwise identical
+// totals (xor butterflies are commutative per pair; the cross-warp stage reads
+// one shared copy).  `red` holds 2*4*32 doubles, `par` alternates buffers so
+// back-to-back calls need no extra barrier.  MAXWARPS (power of two >= the
+// block's warp count) bounds the cross-warp butterfly depth.
+template <int NV, int MAXWARPS = 32>
+__device__ __forceinline__ void block_allsum(double (&v)[NV], double* red, int& par) {
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nwarps = blockDim.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  }
+  double* buf = red + par * (4 * 32);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) buf[k * 32 + warp] = v[k];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = (lane < nwarps) ? buf[k * 32 + lane] : 0.0;
+#pragma unroll
+  for (int off = MAXWARPS / 2; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  }
+  par ^= 1;
+}
+
+__device__ __forceinline__ double op_entry(double m, double k, double dt) {
+  return __dadd_rn(m, __dmul_rn(dt, k));
+}
+
+__device__ __forceinline__ double grid_time(double t_base, int64_t g, double dt) {
+  return __dadd_rn(t_base, __dmul_rn((double)g, dt));
+}
+
+__device__ __forceinline__ void write_status(int32_t* status, int slot, int code, int step,
+                                             int interval, int iteration) {
+  if (status == nullptr || slot < 0) return;
+  int32_t* s = status + (int64_t)slot * kStatusInts;
+  s[0] = code;
+  s[1] = step;
+  s[2] = interval;
+  s[3] = iteration;
+}
+
+// ------------------------------------------------------------------ host
+int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
+                    const double* K, const double* profile, double omega, double rtol,
+                    int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
+                    const int32_t* active, cudaStream_t stream);
+
+int small_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
+                          const double* profile, double omega, double dt_c, double t0,
+                          const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
+                          int max_it, double* U, const double* F, double* C, int32_t* iters,
+                          int32_t* status, const int32_t* active, cudaStream_t stream);
+
+size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S);
+
+int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
+                     const double* K, const double* profile, double omega, double rtol,
+                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
+                     const int32_t* active, void* ws, size_t ws_bytes, cudaStream_t stream);
+
+int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
+                           const double* profile, double omega, double dt_c, double t0,
+                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
+                           int max_it, double* U, const double* F, double* C, int32_t* iters,
+                           int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
+                           cudaStream_t stream);
+
+inline bool use_small(const Ctx* ctx) {
+  if (ctx->path == 1) return true;
+  if (ctx->path == 2) return false;
+  return ctx->n <= kSmallMaxRows;
+}
+
+}  // namespace mlmcp

@@ -1,0 +1,197 @@
+"""Device engine: one ``mlmcp_ctx`` per (sparsity pattern, GPU) plus the
+torch-owned buffers and the task tables the C ABI consumes.
+
+PyTorch is plumbing here: it owns device memory (caching allocator), streams
+and ``torch.distributed``; every arithmetic step of the hot path is a
+libmlmcp.so kernel launched through ``_lib``.  There is no CPU fallback — a
+missing library or GPU raises.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import TASK_DTYPE, check, np_ptr, ptr
+
+F64 = torch.float64
+I32 = torch.int32
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2507_19246_b200 needs a CUDA device (sm_100a); "
+                           "there is no CPU fallback")
+    if device is None:
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise ValueError(f"device must be a CUDA device, got {dev}")
+    return torch.device("cuda", dev.index if dev.index is not None else torch.cuda.current_device())
+
+
+def stream_handle(stream=None) -> ctypes.c_void_p:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def new_tasks(n: int) -> np.ndarray:
+    t = np.zeros(n, dtype=TASK_DTYPE)
+    t["traj"] = -1
+    t["qoi_slot"] = -1
+    t["group"] = -1
+    t["slot"] = -1
+    return t
+
+
+def tasks_to_device(tasks: np.ndarray, device) -> torch.Tensor:
+    raw = np.ascontiguousarray(tasks).view(np.uint8)
+    return torch.from_numpy(raw.copy()).to(device, non_blocking=False)
+
+
+class DeviceSystem:
+    """A CSR sparsity pattern bound to one GPU (``mlmcp_ctx``).
+
+    ``assembly`` = (n_elem, cptr, celem, cmw, ckw) enables ``assemble``.
+    """
+
+    def __init__(self, row_ptr, col, device=None, assembly=None):
+        self.device = require_cuda(device)
+        self.lib = _lib.load()
+        row_ptr = np.ascontiguousarray(row_ptr, dtype=np.int32)
+        col = np.ascontiguousarray(col, dtype=np.int32)
+        self.n_rows = len(row_ptr) - 1
+        self.nnz = int(row_ptr[-1])
+        self.row_ptr_h = row_ptr
+        self.col_h = col
+        handle = ctypes.c_void_p()
+        check(self.lib.mlmcp_ctx_create(self.device.index, self.n_rows, self.nnz, np_ptr(row_ptr),
+                                        np_ptr(col), ctypes.byref(handle)), "mlmcp_ctx_create")
+        self.ctx = handle
+        w = ctypes.c_int()
+        small = ctypes.c_int()
+        check(self.lib.mlmcp_ctx_info(self.ctx, ctypes.byref(w), ctypes.byref(small)), "mlmcp_ctx_info")
+        self.max_row_nnz = w.value
+        self.small_max_rows = small.value
+        self._path = 0
+        if assembly is not None:
+            n_elem, cptr, celem, cmw, ckw = assembly
+            cptr = np.ascontiguousarray(cptr, dtype=np.int32)
+            celem = np.ascontiguousarray(celem, dtype=np.int32)
+            cmw = np.ascontiguousarray(cmw, dtype=np.float64)
+            ckw = np.ascontiguousarray(ckw, dtype=np.float64)
+            check(self.lib.mlmcp_ctx_set_assembly(self.ctx, int(n_elem), len(celem), np_ptr(cptr),
+                                                  np_ptr(celem), np_ptr(cmw), np_ptr(ckw)),
+                  "mlmcp_ctx_set_assembly")
+        self._ws = None
+
+    # ------------------------------------------------------------ lifecycle
+    def close(self):
+        if getattr(self, "ctx", None) is not None and self.lib is not None:
+            self.lib.mlmcp_ctx_destroy(self.ctx)
+            self.ctx = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ------------------------------------------------------------ config
+    def set_path(self, path: str):
+        code = {"auto": 0, "small": 1, "stream": 2}[path]
+        check(self.lib.mlmcp_ctx_set_path(self.ctx, code), "mlmcp_ctx_set_path")
+        self._path = code
+
+    @property
+    def sm_resident(self) -> bool:
+        if self._path == 1:
+            return True
+        if self._path == 2:
+            return False
+        return self.n_rows <= self.small_max_rows
+
+    def workspace(self, n_tasks: int, S: int) -> torch.Tensor | None:
+        nbytes = int(self.lib.mlmcp_workspace_bytes(self.ctx, int(n_tasks), int(S)))
+        if nbytes == 0:
+            return None
+        if self._ws is None or self._ws.numel() < nbytes:
+            self._ws = None
+            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+        return self._ws
+
+    # ------------------------------------------------------------ K1
+    def assemble(self, S: int, sigma: torch.Tensor, sigma_stride: int, sigma_index,
+                 nu: torch.Tensor, nu_stride: int, nu_index, stream=None):
+        M = torch.empty((S, self.nnz), dtype=F64, device=self.device)
+        K = torch.empty((S, self.nnz), dtype=F64, device=self.device)
+        check(self.lib.mlmcp_assemble(self.ctx, S, ptr(sigma), int(sigma_stride), ptr(sigma_index),
+                                      ptr(nu), int(nu_stride), ptr(nu_index), ptr(M), ptr(K),
+                                      stream_handle(stream)), "mlmcp_assemble")
+        return M, K
+
+    # ------------------------------------------------------------ K2-K4, K6
+    def propagate(self, tasks: np.ndarray, M, K, profile, omega: float, rtol: float,
+                  max_it: int, xbuf, qoi=None, iters=None, status=None, active=None,
+                  stream=None, tasks_dev: torch.Tensor | None = None):
+        n = len(tasks)
+        if n == 0:
+            return None
+        S = M.shape[0]
+        td = tasks_dev if tasks_dev is not None else tasks_to_device(tasks, self.device)
+        ws = self.workspace(n, S)
+        check(self.lib.mlmcp_propagate(self.ctx, n, ptr(td), S, ptr(M), ptr(K), ptr(profile),
+                                       float(omega), float(rtol), int(max_it), ptr(xbuf), ptr(qoi),
+                                       ptr(iters), ptr(status), ptr(active), ptr(ws),
+                                       0 if ws is None else ws.numel(), stream_handle(stream)),
+              "mlmcp_propagate")
+        return td
+
+    # ------------------------------------------------------------ K5
+    def parareal_coarse(self, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0, slice_steps,
+                        rtol, max_it, U, F, C, iters, status, active, stream=None):
+        ws = self.workspace(S, S)
+        check(self.lib.mlmcp_parareal_coarse(
+            self.ctx, S, k, m, ptr(M), ptr(K), ptr(profile), float(omega), float(dt_c), float(t0),
+            ptr(slice_k0), ptr(slice_steps), float(rtol), int(max_it), ptr(U), ptr(F), ptr(C),
+            ptr(iters), ptr(status), ptr(active), ptr(ws), 0 if ws is None else ws.numel(),
+            stream_handle(stream)), "mlmcp_parareal_coarse")
+
+    def parareal_defect(self, S, k, m, k_max, U, F, tol, active, k_used, defects, stream=None):
+        check(self.lib.mlmcp_parareal_defect(self.ctx, S, k, m, k_max, ptr(U), ptr(F), float(tol),
+                                             ptr(active), ptr(k_used), ptr(defects),
+                                             stream_handle(stream)), "mlmcp_parareal_defect")
+
+    def parareal_finalize(self, S, m, U, F, k_used, stream=None):
+        check(self.lib.mlmcp_parareal_finalize(self.ctx, S, m, ptr(U), ptr(F), ptr(k_used),
+                                               stream_handle(stream)), "mlmcp_parareal_finalize")
+
+    def energy(self, sample_idx: torch.Tensor, x_off: torch.Tensor, xbuf, K, stream=None):
+        out = torch.empty(len(sample_idx), dtype=F64, device=self.device)
+        check(self.lib.mlmcp_energy(self.ctx, len(sample_idx), ptr(sample_idx), ptr(x_off),
+                                    ptr(xbuf), ptr(K), ptr(out), stream_handle(stream)),
+              "mlmcp_energy")
+        return out
+
+
+def kl_sigma(xi: torch.Tensor, basis: torch.Tensor, log_sigma0: float, scale: float,
+             stream=None) -> torch.Tensor:
+    lib = _lib.load()
+    S, modes = xi.shape
+    E = basis.shape[1]
+    out = torch.empty((S, E), dtype=F64, device=xi.device)
+    check(lib.mlmcp_kl_sigma(S, E, modes, ptr(xi), ptr(basis), float(log_sigma0), float(scale),
+                             ptr(out), stream_handle(stream)), "mlmcp_kl_sigma")
+    return out
+
+
+def level_reduce(q_l: torch.Tensor, q_lm1: torch.Tensor | None, stream=None) -> torch.Tensor:
+    """K7: [sum Y, sum Y^2, mean, var] of Y = q_l - q_lm1 (fixed order)."""
+    lib = _lib.load()
+    out = torch.empty(4, dtype=F64, device=q_l.device)
+    check(lib.mlmcp_level_reduce(len(q_l), ptr(q_l), ptr(q_lm1), ptr(out), stream_handle(stream)),
+          "mlmcp_level_reduce")
+    return out

@@ -1,0 +1,261 @@
+"""MLMC estimator over the temporal level hierarchy (the
+reference ships no ``mlmc`` module — ``models.py:308,315`` refers to it).
+
+  ``RandomStream``        SPEC.md:250-254: generator = pure function of
+                          (seed, level, index) via SeedSequence spawn keys
+  ``LevelStats``          SPEC.md:256-260 (mean = sum_Y/N,
+                          var = (sum_Y2 - N mean^2)/(N-1))
+  ``EstimatorResult``     SPEC.md:262-266 (expectation = sum_l mean_Y)
+  ``coupled_sample``      SPEC.md:280-288 (Q_{-1} = 0; Parareal only on the
+                          finest level, the coarser solve stays sequential)
+  ``mc_estimate``
+  ``optimal_allocation``  SPEC.md:290-298 (rmse split eps^2/2; N_l >= 2)
+  ``mlmc_estimate``       SPEC.md:300-314 with a fixed-N policy (the BASELINE
+                          configs) or a warm-up + allocation policy
+
+Batched device path: for a family with ``run_levels`` (EddyCurrentFamily)
+every level's samples run in one batched launch; each rank of a
+``torch.distributed`` group takes a contiguous slice of every level's sample
+indices (keys stay (seed, l, k) with k the global index), fills
+its slots of a per-sample buffer [N_l, 4] = (Q_l, Q_{l-1}, K, PCG iters),
+one all-reduce(SUM) per level combines the buffers (exactly one non-zero
+contributor per slot, so the sum is exact), and the K7 kernel reduces in
+fixed sample order — the estimate is bitwise independent of the GPU count
+(SPEC.md:313).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .models import EvalRecord, LevelSpec, draw_parameters
+
+__all__ = ["RandomStream", "LevelStats", "EstimatorResult", "FixedSamples", "WarmupPolicy",
+           "coupled_sample", "mc_estimate", "optimal_allocation", "mlmc_estimate",
+           "draw_level", "shard_range"]
+
+
+class RandomStream:
+    def __init__(self, master_seed: int, level: int, index: int):
+        self.master_seed = int(master_seed)
+        self.level = int(level)
+        self.index = int(index)
+
+    def generator(self) -> np.random.Generator:
+        return np.random.default_rng(
+            np.random.SeedSequence(self.master_seed, spawn_key=(self.level, self.index)))
+
+
+@dataclass
+class LevelStats:
+    level: int
+    n: int
+    sum_y: float
+    sum_y2: float
+    cost_per_sample: float = 0.0
+    parareal_k: list | None = None
+
+    @property
+    def mean_y(self) -> float:
+        return self.sum_y / self.n if self.n else 0.0
+
+    @property
+    def var_y(self) -> float:
+        if self.n < 2:
+            return 0.0
+        return (self.sum_y2 - self.n * self.mean_y ** 2) / (self.n - 1)
+
+
+@dataclass
+class EstimatorResult:
+    expectation: float
+    per_level: list
+    rmse_estimate: float
+    ledger: dict = field(default_factory=dict)
+
+
+@dataclass(frozen=True)
+class FixedSamples:
+    """SPEC.md:527 'fixed N per level' policy."""
+
+    n_per_level: tuple
+
+
+@dataclass(frozen=True)
+class WarmupPolicy:
+    n_warmup: int = 20
+    rmse: float | None = None
+    budget: float | None = None
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous slice [a, b) of 0..n-1 owned by ``rank``."""
+    base, rem = divmod(n, world)
+    a = rank * base + min(rank, rem)
+    return a, a + base + (1 if rank < rem else 0)
+
+
+def draw_level(uncertain, seed: int, level: int, indices) -> np.ndarray:
+    """Host draws for sample keys (seed, level, k), k in ``indices`` (1-based)."""
+    rows = [draw_parameters(uncertain, RandomStream(seed, level, int(k))).values for k in indices]
+    dim = getattr(uncertain, "dim", None) or len(uncertain.nominal.values)
+    return np.array(rows, dtype=float).reshape(len(rows), dim)
+
+
+def coupled_sample(family, params, level: LevelSpec, hierarchy, parareal_cfg=None):
+    """SPEC.md:280-288 through the per-sample family API."""
+    top = hierarchy[-1].level
+    hi = family.evaluate(params, level, parareal_cfg if (parareal_cfg is not None and
+                                                         level.level == top) else None)
+    if level.level == 0:
+        return hi.q, 0.0, (hi.cost_s, 0.0), hi.parareal_iterations
+    lo = family.evaluate(params, hierarchy[level.level - 1])
+    return hi.q, lo.q, (hi.cost_s, lo.cost_s), hi.parareal_iterations
+
+
+def mc_estimate(family, level: LevelSpec, n: int, seed: int) -> EstimatorResult:
+    if n < 2:
+        raise ValueError("need N >= 2")
+    qs = []
+    for k in range(1, n + 1):
+        p = draw_parameters(family.uncertain, RandomStream(seed, level.level, k))
+        qs.append(family.evaluate(p, level).q)
+    st = LevelStats(level.level, n, float(np.sum(qs)), float(np.sum(np.square(qs))))
+    return EstimatorResult(st.mean_y, [st], math.sqrt(max(st.var_y, 0.0) / n))
+
+
+def optimal_allocation(V, C, rmse: float | None = None, budget: float | None = None):
+    V = np.asarray(V, dtype=float)
+    C = np.asarray(C, dtype=float)
+    if np.any(V < 0) or np.any(C <= 0):
+        raise ValueError("need V >= 0 and C > 0")
+    if np.all(V == 0):
+        return [2] * len(V)
+    w = np.sqrt(V / C)
+    if rmse is not None:
+        if rmse <= 0:
+            raise ValueError("rmse must be > 0")
+        n = np.ceil(2.0 / rmse ** 2 * w * np.sum(np.sqrt(V * C)))
+    elif budget is not None:
+        if budget <= 0:
+            raise ValueError("budget must be > 0")
+        n = np.floor(budget * w / np.sum(w * C))
+    else:
+        raise ValueError("need an rmse or a budget target")
+    return [int(max(2, x)) for x in n]
+
+
+def _dist():
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            return dist
+    except Exception:
+        pass
+    return None
+
+
+def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
+    """Slot buffer -> all-reduce -> fixed-order K7 reduction."""
+    import torch
+    on_gpu = device is not None and torch.device(device).type == "cuda"
+    dev = device if on_gpu else "cpu"
+    slots = torch.zeros((n_global, 4), dtype=torch.float64, device=dev)
+    if b > a:
+        slots[a:b, 0] = batch.q_l.to(dev, torch.float64)
+        slots[a:b, 1] = batch.q_lm1.to(dev, torch.float64)
+        slots[a:b, 2] = batch.k_used.to(dev, torch.float64)
+        if batch.iters is not None:
+            slots[a:b, 3] = batch.iters.to(dev, torch.float64)
+    if dist is not None and dist.get_world_size() > 1:
+        dist.all_reduce(slots, op=dist.ReduceOp.SUM)
+    if on_gpu:
+        from .engine import level_reduce
+        sums = level_reduce(slots[:, 0].contiguous(), slots[:, 1].contiguous())
+    else:
+        # CPU families (tests) — same fixed order as the kernel's definition
+        y = (slots[:, 0] - slots[:, 1]).numpy()
+        sums = torch.tensor([float(np.sum(y)), float(np.sum(y * y)), 0.0, 0.0])
+    return slots, sums
+
+
+def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: int = 0,
+                  device=None, draws=None, csv_path: str | None = None) -> EstimatorResult:
+    """SPEC.md:300-314.  ``policy``: FixedSamples (all levels at once) or
+    WarmupPolicy (warm-up, optimal allocation, then the remainder)."""
+    hierarchy = tuple(hierarchy or family.hierarchy)
+    dist = _dist()
+    rank = dist.get_rank() if dist else 0
+    world = dist.get_world_size() if dist else 1
+    if policy is None:
+        raise ValueError("need a sampling policy")
+    if isinstance(policy, WarmupPolicy):
+        return _mlmc_warmup(family, hierarchy, policy, parareal_cfg, seed, device)
+    counts = list(policy.n_per_level)
+    if len(counts) != len(hierarchy):
+        raise ValueError("one sample count per level is required")
+    t_start = time.perf_counter()
+    ranges = [shard_range(n, rank, world) for n in counts]
+    if draws is None:
+        draws = [draw_level(family.uncertain, seed, lvl, range(a + 1, b + 1))
+                 for lvl, (a, b) in enumerate(ranges)]
+    batches = family.run_levels(draws, parareal_cfg)
+    dev = device
+    if dev is None and hasattr(family, "solver"):
+        dev = family.solver.device
+    per_level, all_slots = [], []
+    sums_dev = []
+    for lvl, (batch, (a, b)) in enumerate(zip(batches, ranges)):
+        slots, sums = _reduce_level(batch, counts[lvl], a, b, dist, dev)
+        all_slots.append(slots)
+        sums_dev.append(sums)
+    if hasattr(family, "check_status"):
+        family.check_status()
+    host = [s.cpu().numpy() for s in sums_dev]
+    wall = time.perf_counter() - t_start
+    for lvl, sums in enumerate(host):
+        ks = None
+        if parareal_cfg is not None and lvl == len(hierarchy) - 1:
+            ks = all_slots[lvl][:, 2].cpu().numpy().astype(int).tolist()
+        per_level.append(LevelStats(lvl, counts[lvl], float(sums[0]), float(sums[1]),
+                                    wall / max(1, sum(counts)), ks))
+    expectation = float(sum(st.mean_y for st in per_level))
+    rmse = math.sqrt(sum(max(st.var_y, 0.0) / st.n for st in per_level if st.n > 0))
+    ledger = {"wall_time_s": wall, "world_size": world,
+              "samples": counts, "mode": "gpu-batched"}
+    if csv_path and rank == 0:
+        _write_csv(csv_path, all_slots, per_level)
+    return EstimatorResult(expectation, per_level, rmse, ledger)
+
+
+def _write_csv(path, all_slots, per_level):
+    """SPEC.md:326 per-sample records: level,index,Q_l,Q_lm1,cost_s,parareal_K."""
+    with open(path, "w") as fh:
+        fh.write("level,index,Q_l,Q_lm1,cost_s,parareal_K\n")
+        for lvl, slots in enumerate(all_slots):
+            s = slots.cpu().numpy()
+            for k in range(len(s)):
+                fh.write(f"{lvl},{k + 1},{s[k, 0]!r},{s[k, 1]!r},"
+                         f"{per_level[lvl].cost_per_sample!r},{int(s[k, 2])}\n")
+
+
+def _mlmc_warmup(family, hierarchy, policy: WarmupPolicy, parareal_cfg, seed, device):
+    n_w = max(2, policy.n_warmup)
+    warm = mlmc_estimate(family, hierarchy, FixedSamples((n_w,) * len(hierarchy)), parareal_cfg,
+                         seed, device)
+    V = [st.var_y for st in warm.per_level]
+    C = [max(st.cost_per_sample, 1e-12) for st in warm.per_level]
+    target = optimal_allocation(V, C, rmse=policy.rmse, budget=policy.budget)
+    counts = tuple(max(n_w, t) for t in target)
+    res = mlmc_estimate(family, hierarchy, FixedSamples(counts), parareal_cfg, seed, device)
+    res.ledger["warmup"] = [n_w] * len(hierarchy)
+    res.ledger["allocation"] = list(counts)
+    return res
+
+
+def evaluate_records(family, params, level, parareal_cfg=None) -> list[EvalRecord]:
+    return family.evaluate_batch(params, level, parareal_cfg)

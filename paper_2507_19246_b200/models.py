@@ -1,0 +1,366 @@
+"""Sampler / level / family API (drop-in for ``mlmc_parareal.models``) with the
+2D eddy-current FE family whose solves run batched on the GPU.
+
+Kept from the reference with the same names, fields and errors:
+  ``ParameterVector``   models.py:54-74 (strict positivity)
+  ``UncertainInput``    models.py:77-88
+  ``LevelSpec``         models.py:91-100
+  ``make_hierarchy``    models.py:103-108
+  ``QoIKind``           models.py:111-113 (+ the two FE kinds below)
+  ``draw_parameters``   models.py:305-318 (uniform; nominal when h == 0)
+  ``EvalRecord``        models.py:347-353
+  ``LinearToyFamily``   models.py:414-428 / ``toy_family`` :456-461
+The family protocol (``uncertain``, ``hierarchy``, ``evaluate``) of
+``MachineFamily`` (models.py:376-411) is implemented by ``EddyCurrentFamily``,
+which adds the batched entry points ``evaluate_batch`` / ``coupled_batch`` /
+``run_levels`` used by the estimator.
+
+New (no reference counterpart; BASELINE.json configs):
+  ``GaussianInput``     xi ~ N(0,1)^d for the config-3 KL field
+  QoIKind.MAGNETIC_ENERGY_T         1/2 a(T)^T K a(T)
+  QoIKind.TIME_AVG_MAGNETIC_ENERGY  (1/T_w) sum_{t_k in last window} W(a_k) dt
+                                    (right end points, like models.py:337-339)
+"""
+
+from __future__ import annotations
+
+import enum
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import fe
+from .parareal import PararealConfig
+
+__all__ = ["ParameterVector", "UncertainInput", "GaussianInput", "LevelSpec", "make_hierarchy",
+           "QoIKind", "draw_parameters", "EvalRecord", "EddyCurrentFamily", "CoupledBatch",
+           "LinearToyFamily", "toy_family", "eddy_current_family"]
+
+
+@dataclass(frozen=True)
+class ParameterVector:
+    model_id: str
+    values: np.ndarray
+
+    def __post_init__(self):
+        vals = np.atleast_1d(np.asarray(self.values, dtype=float))
+        object.__setattr__(self, "values", vals)
+        expected = fe.n_params(self.model_id) if self.model_id in fe.LAYOUTS else None
+        if expected is not None and len(vals) != expected:
+            raise ValueError(f"model '{self.model_id}' takes {expected} parameters, got {len(vals)}")
+        if self.model_id != "kl64" and not np.all(vals > 0.0):
+            bad = int(np.argmin(vals))
+            raise ValueError(f"parameter {bad} of '{self.model_id}' must be strictly positive, "
+                             f"got {vals[bad]}")
+
+
+@dataclass(frozen=True)
+class UncertainInput:
+    nominal: ParameterVector
+    relative_halfwidth: float
+
+    def __post_init__(self):
+        if not 0.0 <= self.relative_halfwidth < 1.0:
+            raise ValueError(f"relative_halfwidth must lie in [0, 1), got {self.relative_halfwidth}")
+
+    @property
+    def dim(self) -> int:
+        return len(self.nominal.values)
+
+
+@dataclass(frozen=True)
+class GaussianInput:
+    """Independent standard normals (KL coefficients of config 3)."""
+
+    model_id: str
+    dim: int
+
+
+@dataclass(frozen=True, order=True)
+class LevelSpec:
+    level: int
+    dt: float
+
+    def __post_init__(self):
+        if self.level < 0 or self.dt <= 0.0:
+            raise ValueError(f"invalid level spec (level={self.level}, dt={self.dt})")
+
+
+def make_hierarchy(dts) -> tuple[LevelSpec, ...]:
+    dts = [float(dt) for dt in dts]
+    if any(b >= a for a, b in zip(dts, dts[1:])):
+        raise ValueError(f"step sizes must be strictly decreasing, got {dts}")
+    return tuple(LevelSpec(level=i, dt=dt) for i, dt in enumerate(dts))
+
+
+class QoIKind(enum.Enum):
+    ELECTRICAL_ENERGY = "electrical_energy"
+    MEAN_JOULE_LOSS = "mean_joule_loss"
+    MAGNETIC_ENERGY_T = "magnetic_energy_T"
+    TIME_AVG_MAGNETIC_ENERGY = "time_avg_magnetic_energy"
+
+
+def draw_parameters(inp, stream) -> ParameterVector:
+    """models.py:305-318 (uniform) and the Gaussian input of config 3."""
+    if isinstance(inp, GaussianInput):
+        rng = stream.generator() if hasattr(stream, "generator") else stream
+        return ParameterVector(inp.model_id, rng.standard_normal(inp.dim))
+    nominal = inp.nominal.values
+    if inp.relative_halfwidth == 0.0:
+        return ParameterVector(inp.nominal.model_id, nominal.copy())
+    rng = stream.generator() if hasattr(stream, "generator") else stream
+    lo = nominal * (1.0 - inp.relative_halfwidth)
+    hi = nominal * (1.0 + inp.relative_halfwidth)
+    return ParameterVector(inp.nominal.model_id, rng.uniform(lo, hi))
+
+
+@dataclass(frozen=True)
+class EvalRecord:
+    q: float
+    cost_s: float
+    parareal_iterations: int | None = None
+
+
+@dataclass
+class CoupledBatch:
+    """Device results of one level: Q_l, Q_{l-1} (0 on level 0) and Parareal K."""
+
+    level: int
+    q_l: object
+    q_lm1: object
+    k_used: object
+    iters: object = None
+    wall_s: float = 0.0
+    defects: object = None
+
+
+@dataclass
+class LinearToyFamily:
+    """models.py:414-428: Q_l(xi) = xi (1 + dt_l); CPU, closed form (tests)."""
+
+    uncertain: UncertainInput
+    hierarchy: tuple
+
+    def evaluate(self, params: ParameterVector, level: LevelSpec, parareal_cfg=None,
+                 pool=None) -> EvalRecord:
+        return EvalRecord(q=float(params.values[0]) * (1.0 + level.dt), cost_s=1e-9)
+
+    def run_levels(self, draws, parareal_cfg=None, levels=None):
+        import torch
+        levels = list(range(len(draws))) if levels is None else levels
+        out = []
+        for lvl, p in zip(levels, draws):
+            xi = torch.as_tensor(np.asarray(p, dtype=float)[:, 0] if len(p) else np.zeros(0))
+            ql = xi * (1.0 + self.hierarchy[lvl].dt)
+            qm = xi * (1.0 + self.hierarchy[lvl - 1].dt) if lvl > 0 else torch.zeros_like(xi)
+            out.append(CoupledBatch(lvl, ql, qm, torch.zeros(len(xi), dtype=torch.int32)))
+        return out
+
+
+def toy_family(hierarchy, nominal: float = 1.0, halfwidth: float = 0.05) -> LinearToyFamily:
+    return LinearToyFamily(UncertainInput(ParameterVector("toy", np.array([nominal])), halfwidth),
+                           tuple(hierarchy))
+
+
+@dataclass
+class EddyCurrentFamily:
+    """2D linear eddy-current P1 FE family; one sample = one transient solve.
+
+    ``evaluate`` follows MachineFamily.evaluate (models.py:389-411): a
+    Parareal configuration switches the solve to Parareal with
+    ``parareal_cfg.with_dt_fine(level.dt)``; the QoI is evaluated from the
+    device-resident solution.  Batched entry points run many samples in one
+    launch.
+    """
+
+    model_id: str
+    uncertain: object
+    hierarchy: tuple
+    horizon: float
+    n: int
+    layout: str
+    qoi: QoIKind = QoIKind.MAGNETIC_ENERGY_T
+    avg_window: float = 0.0
+    device: object = None
+    rtol: float = 1e-12
+    max_it: int = 20000
+    path: str = "auto"
+    _solver: object = field(default=None, repr=False, compare=False)
+
+    # ------------------------------------------------------------ setup
+    @property
+    def solver(self):
+        if self._solver is None:
+            from .solver import FESolver
+            self._solver = FESolver(self.n, self.layout, self.device, self.rtol, self.max_it,
+                                    self.path)
+        return self._solver
+
+    def _level_index(self, level) -> int:
+        if isinstance(level, LevelSpec):
+            return level.level
+        return int(level)
+
+    def _seq_job(self, rows, dt):
+        from . import _lib
+        from .solver import SeqJob
+        from .timeint import step_count
+        n = step_count(0.0, self.horizon, dt)
+        if self.qoi is QoIKind.MAGNETIC_ENERGY_T:
+            return SeqJob(rows, dt, n, _lib.QOI_FINAL_ENERGY, 0)
+        if self.qoi is QoIKind.TIME_AVG_MAGNETIC_ENERGY:
+            n_w = int(round(self.avg_window / dt))
+            return SeqJob(rows, dt, n, _lib.QOI_SUM_ENERGY, n - n_w)
+        raise ValueError(f"QoI kind {self.qoi} is not defined for the FE family")
+
+    def _finish_q(self, acc, dt):
+        if self.qoi is QoIKind.TIME_AVG_MAGNETIC_ENERGY:
+            return acc * dt / self.avg_window
+        return acc
+
+    # ------------------------------------------------------------ batched
+    def run_levels(self, draws, parareal_cfg: PararealConfig | None = None, levels=None,
+                   concurrent: bool = True) -> list[CoupledBatch]:
+        """Coupled (Q_l, Q_{l-1}) for every level at once.
+
+        draws[i]: [N_i, P] parameters of level ``levels[i]`` (default 0..L).
+        All levels' operators are assembled in one launch; every sequential
+        solve of every level goes into one batched launch (longest first);
+        the finest level's Parareal runs concurrently on a second stream.
+        Returns device tensors (no host sync)."""
+        import torch
+        sol = self.solver
+        levels = list(range(len(draws))) if levels is None else list(levels)
+        top = len(self.hierarchy) - 1
+        sizes = [len(d) for d in draws]
+        offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+        allp = np.concatenate([np.asarray(d, dtype=float).reshape(len(d), -1) for d in draws], axis=0) \
+            if sum(sizes) else np.zeros((0, fe.n_params(self.layout)))
+        params = torch.from_numpy(allp).to(sol.device)
+        M, K = sol.assemble(params)
+        jobs, where = [], []
+        pr_level = None
+        for i, lvl in enumerate(levels):
+            rows = np.arange(offs[i], offs[i + 1])
+            if len(rows) == 0:
+                continue
+            dt = self.hierarchy[lvl].dt
+            if parareal_cfg is not None and lvl == top:
+                pr_level = i
+            else:
+                jobs.append(self._seq_job(rows, dt))
+                where.append((i, "hi", dt))
+            if lvl > 0:
+                dtm = self.hierarchy[lvl - 1].dt
+                jobs.append(self._seq_job(rows, dtm))
+                where.append((i, "lo", dtm))
+        main = torch.cuda.current_stream()
+        pr = None
+        if pr_level is not None:
+            cfg = parareal_cfg.with_dt_fine(self.hierarchy[levels[pr_level]].dt)
+            a, b = offs[pr_level], offs[pr_level + 1]
+            side = torch.cuda.Stream(device=sol.device) if (concurrent and sol.sys.sm_resident) else main
+            if side is not main:
+                side.wait_stream(main)
+            with torch.cuda.stream(side):
+                pr = sol.run_parareal(M[a:b], K[a:b], 0.0, self.horizon, cfg.num_subintervals,
+                                      cfg.dt_fine, cfg.dt_coarse, cfg.tolerance, cfg.k_max,
+                                      stream=side)
+        res = sol.run_sequential(M, K, jobs) if jobs else []
+        if pr is not None and side is not main:
+            main.wait_stream(side)
+            for t in (pr.qoi, pr.k_used, pr.defects):
+                t.record_stream(main)
+        out = []
+        for i, lvl in enumerate(levels):
+            S = sizes[i]
+            dev = sol.device
+            ql = torch.zeros(S, dtype=torch.float64, device=dev)
+            qm = torch.zeros(S, dtype=torch.float64, device=dev)
+            ku = torch.zeros(S, dtype=torch.int32, device=dev)
+            its = torch.zeros(S, dtype=torch.int64, device=dev)
+            defects = None
+            for (j, kind, dt), r in zip(where, res):
+                if j != i:
+                    continue
+                q = self._finish_q(r.qoi, dt)
+                if kind == "hi":
+                    ql = q
+                else:
+                    qm = q
+                its = its + r.iters.to(torch.int64)
+            if i == pr_level:
+                ql = pr.qoi
+                ku = pr.k_used
+                defects = pr.defects
+            out.append(CoupledBatch(lvl, ql, qm, ku, its, defects=defects))
+        self._last = (res, pr, M, K)
+        return out
+
+    def check_status(self):
+        """Raise SingularSystemError / PropagatorError for failed samples of the
+        last run (one host sync)."""
+        from .parareal import raise_parareal_status
+        from .solver import raise_on_status
+        res, pr, _, _ = self._last
+        for r in res:
+            raise_on_status(r.status, "implicit Euler solve")
+        if pr is not None:
+            raise_parareal_status(pr.status.cpu().numpy(), pr.fine_status.cpu().numpy())
+
+    def coupled_batch(self, params, level, parareal_cfg=None) -> CoupledBatch:
+        lvl = self._level_index(level)
+        return self.run_levels([np.asarray(params, dtype=float)], parareal_cfg, levels=[lvl])[0]
+
+    def evaluate_batch(self, params, level: LevelSpec, parareal_cfg=None) -> list[EvalRecord]:
+        """Q at one level for a batch of samples (no coupling)."""
+        import torch
+        lvl = self._level_index(level)
+        params = np.asarray(params, dtype=float).reshape(-1, fe.n_params(self.layout))
+        sol = self.solver
+        t = time.perf_counter()
+        M, K = sol.assemble(torch.from_numpy(params).to(sol.device))
+        top = len(self.hierarchy) - 1
+        dt = self.hierarchy[lvl].dt
+        ks = None
+        if parareal_cfg is not None:
+            cfg = parareal_cfg.with_dt_fine(dt)
+            pr = sol.run_parareal(M, K, 0.0, self.horizon, cfg.num_subintervals, cfg.dt_fine,
+                                  cfg.dt_coarse, cfg.tolerance, cfg.k_max)
+            from .parareal import raise_parareal_status
+            raise_parareal_status(pr.status.cpu().numpy(), pr.fine_status.cpu().numpy())
+            q = pr.qoi.cpu().numpy()
+            ks = pr.k_used.cpu().numpy()
+        else:
+            from .solver import raise_on_status
+            r = sol.run_sequential(M, K, [self._seq_job(np.arange(len(params)), dt)])[0]
+            raise_on_status(r.status, "implicit Euler solve")
+            q = self._finish_q(r.qoi, dt).cpu().numpy()
+        wall = time.perf_counter() - t
+        del top
+        cost = wall / max(1, len(params))
+        return [EvalRecord(float(q[i]), cost, None if ks is None else int(ks[i]))
+                for i in range(len(params))]
+
+    def evaluate(self, params: ParameterVector, level: LevelSpec, parareal_cfg=None,
+                 pool=None) -> EvalRecord:
+        """models.py:389-411 (``pool`` accepted and ignored)."""
+        vals = params.values if isinstance(params, ParameterVector) else np.asarray(params)
+        return self.evaluate_batch(np.asarray(vals, dtype=float)[None, :], level, parareal_cfg)[0]
+
+
+def eddy_current_family(config: int | str, device=None, **kw) -> EddyCurrentFamily:
+    """The family of one BASELINE.json config (see configs.py)."""
+    from .configs import get_config
+    c = get_config(config)
+    if c.layout == "kl64":
+        unc = GaussianInput("kl64", fe.KL_MODES)
+    else:
+        nominal = np.array([fe.NU0] * (fe.n_params(c.layout) // 2)
+                           + [fe.SIGMA0] * (fe.n_params(c.layout) // 2))
+        unc = UncertainInput(ParameterVector(c.layout, nominal), c.halfwidth)
+    qoi = QoIKind.TIME_AVG_MAGNETIC_ENERGY if c.qoi == "time_avg_energy" else QoIKind.MAGNETIC_ENERGY_T
+    return EddyCurrentFamily(model_id=c.layout, uncertain=unc, hierarchy=make_hierarchy(c.dts),
+                             horizon=c.horizon, n=c.n, layout=c.layout, qoi=qoi,
+                             avg_window=c.avg_window, device=device, **kw)

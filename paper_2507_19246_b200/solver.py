@@ -1,0 +1,266 @@
+"""Batched FE transient solves on one GPU: operator assembly per sample,
+sequential implicit-Euler jobs and on-device Parareal.
+
+This is the batched replacement of the per-sample work under
+``MachineFamily.evaluate`` (models.py:389-411):
+  * ``assemble``       builders + ``mass + dt*stiffness`` (models.py:217-302,
+                       timeint.py:65) -> per-sample CSR values (K1)
+  * ``run_sequential`` implicit_euler_solve (timeint.py:88-111) for many
+                       (sample, dt) jobs in ONE launch (longest job first)
+  * ``run_parareal``   parareal_solve (parareal.py:121-220) for a batch of
+                       samples: K_max rounds of [coarse sweep, all fine
+                       slices of all samples, jump defect], convergence
+                       masks on the device, one host sync at the end.
+All per-sample results are bitwise independent of the batch composition.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib, fe
+from .engine import DeviceSystem, F64, I32, kl_sigma, new_tasks, tasks_to_device
+from .timeint import SingularSystemError, step_count
+
+DEFAULT_RTOL = 1e-12
+DEFAULT_MAX_IT = 20000
+
+
+@dataclass
+class SeqJob:
+    """n_steps implicit-Euler steps of dt from the zero state for M/K rows
+    ``rows``; QoI 'energy_T' (1/2 a(T)^T K a(T)) or ('sum', from_step)."""
+
+    rows: np.ndarray
+    dt: float
+    n_steps: int
+    qoi_mode: int = _lib.QOI_FINAL_ENERGY
+    qoi_from: int = 0
+
+
+@dataclass
+class SeqResult:
+    qoi: torch.Tensor       # (len(rows),) device
+    iters: torch.Tensor     # (len(rows),) device, PCG iterations
+    status: torch.Tensor    # (len(rows), 4) device
+
+
+@dataclass
+class PararealBatchResult:
+    qoi: torch.Tensor           # (S,) energy of the final fine state
+    k_used: torch.Tensor        # (S,) int32
+    defects: torch.Tensor       # (S, k_max) NaN beyond k_used
+    status: torch.Tensor        # (S, 4) coarse failures: code, step, interval, iteration
+    fine_status: torch.Tensor   # (S*m, 4) fine failures
+    U: torch.Tensor             # (S, m+1, N) boundary states (after finalize)
+    F: torch.Tensor             # (S, m+1, N) fine end states
+    traj: torch.Tensor | None   # (S, m, steps+1, N) last fine solve of each slice
+    fine_iters: torch.Tensor
+    coarse_iters: torch.Tensor
+
+
+def parareal_grid(t0: float, t1: float, m: int, dt_fine: float, dt_coarse: float):
+    """parareal.py:133-150: boundaries on the fine grid and per-slice
+    (k0, n_steps) of the fine and coarse propagators (origin t0)."""
+    nf = step_count(t0, t1, dt_fine)
+    nc = step_count(t0, t1, dt_coarse)
+    if nf % m != 0 or nc % m != 0:
+        raise ValueError(
+            f"[{t0}, {t1}] with M={m} sub-intervals is incompatible with dt_fine={dt_fine} "
+            f"({nf} steps) and dt_coarse={dt_coarse} ({nc} steps)")
+    m_f = nf // m
+    bounds = t0 + (np.arange(m + 1) * m_f) * dt_fine
+    fk0 = np.array([int(round((bounds[n - 1] - t0) / dt_fine)) for n in range(1, m + 1)], dtype=np.int64)
+    fst = np.array([step_count(bounds[n - 1], bounds[n], dt_fine) for n in range(1, m + 1)], dtype=np.int32)
+    ck0 = np.array([int(round((bounds[n - 1] - t0) / dt_coarse)) for n in range(1, m + 1)], dtype=np.int64)
+    cst = np.array([step_count(bounds[n - 1], bounds[n], dt_coarse) for n in range(1, m + 1)], dtype=np.int32)
+    return bounds, fk0, fst, ck0, cst
+
+
+class FESolver:
+    """One mesh + material layout on one GPU."""
+
+    def __init__(self, n: int, layout: str, device=None, rtol: float = DEFAULT_RTOL,
+                 max_it: int = DEFAULT_MAX_IT, path: str = "auto"):
+        if layout not in fe.LAYOUTS:
+            raise ValueError(f"unknown layout {layout!r}")
+        self.n = n
+        self.layout = layout
+        self.rtol = float(rtol)
+        self.max_it = int(max_it)
+        self.mesh = fe.structured_mesh(n)
+        m = self.mesh
+        self.sys = DeviceSystem(m.row_ptr, m.col, device,
+                                assembly=(m.n_elem, m.cptr, m.celem, m.cmw, m.ckw))
+        if path != "auto":
+            self.sys.set_path(path)
+        dev = self.sys.device
+        self.device = dev
+        self.N = m.n_rows
+        self.profile = torch.tensor(fe.source_profile(m, layout), dtype=F64, device=dev)
+        self.omega = 2.0 * np.pi * fe.FREQ          # same rounding as np.sin(2.0*np.pi*f*t)
+        if layout == "kl64":
+            self.kl_basis = torch.tensor(fe.kl_basis(m), dtype=F64, device=dev)
+            self.nu_const = torch.full((1,), fe.NU0, dtype=F64, device=dev)
+            self.nu_index = torch.zeros(m.n_elem, dtype=I32, device=dev)
+        else:
+            self.region = torch.tensor(fe.region_map(m, layout), dtype=I32, device=dev)
+            self.mask = torch.tensor(fe.conducting_mask(layout), dtype=F64, device=dev)
+            self.n_regions = len(fe.conducting_mask(layout))
+
+    # ------------------------------------------------------------ K1
+    def assemble(self, params: torch.Tensor, stream=None):
+        """Per-sample CSR values (M, K) [S, nnz] from parameters [S, P]."""
+        params = params.to(device=self.device, dtype=F64).contiguous()
+        S = params.shape[0]
+        if params.shape[1] != fe.n_params(self.layout):
+            raise ValueError(f"layout {self.layout} takes {fe.n_params(self.layout)} parameters, "
+                             f"got {params.shape[1]}")
+        if self.layout == "kl64":
+            sigma = kl_sigma(params, self.kl_basis, float(np.log(fe.SIGMA0)), fe.KL_SCALE, stream)
+            return self.sys.assemble(S, sigma, self.mesh.n_elem, None, self.nu_const, 0,
+                                     self.nu_index, stream)
+        R = self.n_regions
+        # sigma masked to 0 in non-conducting regions *after* drawing (ParameterVector
+        # positivity, models.py:69-74); a plain elementwise product (plumbing)
+        nu = params[:, :R].contiguous()
+        sigma = (params[:, R:2 * R] * self.mask).contiguous()
+        return self.sys.assemble(S, sigma, R, self.region, nu, R, self.region, stream)
+
+    # ------------------------------------------------------------ sequential
+    def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+        """All jobs in one batched launch (SM-resident path) or one launch per
+        dt (streaming path).  Returns one SeqResult per job (device tensors)."""
+        sizes = [len(j.rows) for j in jobs]
+        T = int(sum(sizes))
+        N = self.N
+        tasks = new_tasks(T)
+        off = 0
+        for j in jobs:
+            sl = slice(off, off + len(j.rows))
+            tasks["sample"][sl] = j.rows
+            tasks["n_steps"][sl] = j.n_steps
+            tasks["k0"][sl] = 0
+            tasks["dt"][sl] = j.dt
+            tasks["t_base"][sl] = 0.0
+            tasks["qoi_mode"][sl] = j.qoi_mode
+            tasks["qoi_from"][sl] = j.qoi_from
+            off += len(j.rows)
+        idx = np.arange(T)
+        tasks["x_in"] = idx * N
+        tasks["x_out"] = idx * N
+        tasks["qoi_slot"] = idx
+        tasks["slot"] = idx
+        traj = None
+        if keep_traj:
+            steps = tasks["n_steps"].astype(np.int64)
+            base = T * N
+            tstart = base + np.concatenate([[0], np.cumsum((steps + 1) * N)[:-1]])
+            tasks["traj"] = tstart
+            xbuf = torch.zeros(int(base + np.sum((steps + 1) * N)), dtype=F64, device=self.device)
+        else:
+            xbuf = torch.zeros(T * N, dtype=F64, device=self.device)
+        qoi = torch.zeros(T, dtype=F64, device=self.device)
+        iters = torch.zeros(T, dtype=I32, device=self.device)
+        status = torch.zeros((T, _lib.STATUS_INTS), dtype=I32, device=self.device)
+        if self.sys.sm_resident:
+            order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
+            self.sys.propagate(tasks[order], M, K, self.profile, self.omega, self.rtol, self.max_it,
+                               xbuf, qoi, iters, status, None, stream)
+        else:
+            for dt in sorted(set(tasks["dt"].tolist())):
+                sel = tasks[tasks["dt"] == dt]
+                self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it,
+                                   xbuf, qoi, iters, status, None, stream)
+        out = []
+        off = 0
+        for j in jobs:
+            sl = slice(off, off + len(j.rows))
+            out.append(SeqResult(qoi[sl], iters[sl], status[sl]))
+            off += len(j.rows)
+        self._last_xbuf = xbuf
+        self._last_tasks = tasks
+        return out
+
+    # ------------------------------------------------------------ Parareal
+    def run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
+                     dt_coarse: float, tol: float, k_max: int, stream=None,
+                     keep_traj: bool = False) -> PararealBatchResult:
+        """parareal_solve for the S samples whose operators are M/K rows 0..S-1
+        (slice the level's M/K to pass a sub-batch), from the zero state."""
+        if not 1 <= k_max <= m:
+            raise ValueError(f"max_iterations must lie in [1, M={m}], got {k_max}")
+        S = M.shape[0]
+        N = self.N
+        dev = self.device
+        bounds, fk0, fst, ck0, cst = parareal_grid(t0, t1, m, dt_fine, dt_coarse)
+        uf_size = S * (m + 1) * N
+        traj_steps = int(fst.max()) + 1
+        traj_size = S * m * traj_steps * N if keep_traj else 0
+        buf = torch.zeros(2 * uf_size + traj_size, dtype=F64, device=dev)
+        U = buf[:uf_size].view(S, m + 1, N)
+        F = buf[uf_size:2 * uf_size].view(S, m + 1, N)
+        C = torch.zeros((S, m, N), dtype=F64, device=dev)
+        active = torch.ones(S, dtype=I32, device=dev)
+        k_used = torch.zeros(S, dtype=I32, device=dev)
+        defects = torch.full((S, k_max), float("nan"), dtype=F64, device=dev)
+        status = torch.zeros((S, _lib.STATUS_INTS), dtype=I32, device=dev)
+        fine_status = torch.zeros((S * m, _lib.STATUS_INTS), dtype=I32, device=dev)
+        fine_iters = torch.zeros(S * m, dtype=I32, device=dev)
+        coarse_iters = torch.zeros(S, dtype=I32, device=dev)
+        ck0_d = torch.tensor(ck0, device=dev)
+        cst_d = torch.tensor(cst, device=dev)
+        # fine task tables: one per iteration k (intervals k..m of every sample)
+        s_idx, n_idx = np.meshgrid(np.arange(S), np.arange(1, m + 1), indexing="ij")
+        s_idx, n_idx = s_idx.ravel(), n_idx.ravel()
+        all_tasks = new_tasks(S * m)
+        all_tasks["sample"] = s_idx
+        all_tasks["n_steps"] = fst[n_idx - 1]
+        all_tasks["k0"] = fk0[n_idx - 1]
+        all_tasks["dt"] = dt_fine
+        all_tasks["t_base"] = t0
+        all_tasks["x_in"] = (s_idx * (m + 1) + (n_idx - 1)) * N
+        all_tasks["x_out"] = uf_size + (s_idx * (m + 1) + n_idx) * N
+        if keep_traj:
+            all_tasks["traj"] = 2 * uf_size + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
+        all_tasks["group"] = s_idx
+        all_tasks["slot"] = s_idx * m + (n_idx - 1)
+        tables = []
+        for k in range(1, k_max + 1):
+            sel = all_tasks[n_idx >= k].copy()
+            sel["tag"] = k
+            tables.append(tasks_to_device(sel, dev))
+        for k in range(1, k_max + 1):
+            self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
+                                     ck0_d, cst_d, self.rtol, self.max_it, U, F, C, coarse_iters,
+                                     status, active, stream)
+            tk = tables[k - 1]
+            n_tk = tk.numel() // _lib.TASK_DTYPE.itemsize
+            sel = all_tasks[n_idx >= k]
+            self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it, buf,
+                               None, fine_iters, fine_status, active, stream, tasks_dev=tk)
+            assert n_tk == len(sel)
+            self.sys.parareal_defect(S, k, m, k_max, U, F, tol, active, k_used, defects, stream)
+        self.sys.parareal_finalize(S, m, U, F, k_used, stream)
+        x_off = torch.tensor((uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64), device=dev)
+        qoi = self.sys.energy(torch.arange(S, dtype=I32, device=dev), x_off, buf, K, stream)
+        traj = None
+        if keep_traj:
+            traj = buf[2 * uf_size:].view(S, m, traj_steps, N)
+        self._keep = tables
+        return PararealBatchResult(qoi, k_used, defects, status, fine_status, U, F, traj,
+                                   fine_iters, coarse_iters)
+
+
+def raise_on_status(status: torch.Tensor, what: str):
+    """Map per-task failure codes to SingularSystemError (timeint.py:25-30)."""
+    st = status.cpu().numpy()
+    bad = np.nonzero(st[:, 0] != _lib.ST_OK)[0]
+    if len(bad):
+        i = int(bad[0])
+        code, step = int(st[i, 0]), int(st[i, 1])
+        raise SingularSystemError(f"{what}: task {i}: {_lib.STATUS_NAMES.get(code, code)} "
+                                  f"at step {step}", step_index=step)
