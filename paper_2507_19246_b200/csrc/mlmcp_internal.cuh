@@ -91,8 +91,11 @@ __device__ __forceinline__ void block_allsum(double (&v)[NV], double* red, int& 
     for (int k = 0; k < NV; ++k) buf[k * 32 + warp] = v[k];
   }
   __syncthreads();
+  // every group of MAXWARPS lanes reads the same partials, so the shortened
+  // butterfly leaves all 32 lanes with bitwise identical totals
+  const int src = lane & (MAXWARPS - 1);
 #pragma unroll
-  for (int k = 0; k < NV; ++k) v[k] = (lane < nwarps) ? buf[k * 32 + lane] : 0.0;
+  for (int k = 0; k < NV; ++k) v[k] = (src < nwarps) ? buf[k * 32 + src] : 0.0;
 #pragma unroll
   for (int off = MAXWARPS / 2; off > 0; off >>= 1) {
 #pragma unroll

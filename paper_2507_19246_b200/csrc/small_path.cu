@@ -264,7 +264,15 @@ template <int W, int R>
 __global__ void __launch_bounds__(kSmallThreads, 1) small_propagate_kernel(SmallArgs a) {
   extern __shared__ double smem[];
   const mlmcp_task t = a.tasks[blockIdx.x];
-  if (a.active != nullptr && t.group >= 0 && a.active[t.group] == 0) return;
+  {
+    // another CTA of the same group may clear active[] concurrently (on a
+    // failure): decide once per block so the barriers below never diverge
+    __shared__ int skip;
+    if (threadIdx.x == 0)
+      skip = (a.active != nullptr && t.group >= 0 && a.active[t.group] == 0) ? 1 : 0;
+    __syncthreads();
+    if (skip) return;
+  }
   const int padN = R * blockDim.x;
   SmallShared sh{smem, smem + padN, smem + 2 * padN, 0};
   const double* Ms = a.M + (int64_t)t.sample * a.nnz;

@@ -150,6 +150,17 @@ __device__ __forceinline__ bool task_live(const SArgs& a, const mlmcp_task& tk, 
   return true;
 }
 
+// Block-uniform read of a flag another block may be writing: thread 0 reads,
+// the block agrees (barriers below must not diverge).
+__device__ __forceinline__ bool block_uniform(bool v) {
+  __shared__ int flag;
+  if (threadIdx.x == 0) flag = v ? 1 : 0;
+  __syncthreads();
+  const bool out = flag != 0;
+  __syncthreads();
+  return out;
+}
+
 __global__ void form_ell_kernel(SArgs a, double dt) {
   const int s = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -191,7 +202,7 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) 
   __shared__ double red[2 * 4 * 32];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
-  if (step >= tk.n_steps || !task_live(a, tk, t)) return;
+  if (!block_uniform(step < tk.n_steps && task_live(a, tk, t))) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = tk.sample;
   const int64_t g = tk.k0 + step + 1;
@@ -231,9 +242,8 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) 
 __global__ void __launch_bounds__(kThreads) spmv_kernel(SArgs a) {
   __shared__ double red[2 * 4 * 32];
   const int t = blockIdx.y;
-  if (a.w.ti[t * kTI + I_STATE] != ST_RUN) return;
   const mlmcp_task tk = a.tasks[t];
-  if (!task_live(a, tk, t)) return;
+  if (!block_uniform(a.w.ti[t * kTI + I_STATE] == ST_RUN && task_live(a, tk, t))) return;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int s = tk.sample;
   double ru = 0.0, wu = 0.0, rr = 0.0;
@@ -333,21 +343,21 @@ __global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step, i
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   int32_t* ti = a.w.ti + t * kTI;
   double* td = a.w.td + t * kTD;
-  const bool inactive = a.active != nullptr && tk.group >= 0 && a.active[tk.group] == 0 &&
-                        ti[I_CODE] == MLMCP_ST_OK;
+  const bool inactive = block_uniform(a.active != nullptr && tk.group >= 0 &&
+                                      a.active[tk.group] == 0 && ti[I_CODE] == MLMCP_ST_OK);
   if (inactive) return;
   const double* X = a.w.X + (int64_t)t * a.N;
   const double* Ks = a.K + (int64_t)tk.sample * a.nnz;
   bool energy = false;
+  const int code_now = block_uniform(ti[I_CODE] != MLMCP_ST_OK) ? 1 : 0;
   if (mode == 0) {
-    if (step >= tk.n_steps || ti[I_CODE] != MLMCP_ST_OK) return;
+    if (step >= tk.n_steps || code_now) return;
     if (tk.traj >= 0 && i < a.N) a.xbuf[tk.traj + (int64_t)(step + 1) * a.N + i] = X[i];
     const int64_t g = tk.k0 + step + 1;
     energy = tk.qoi_mode == MLMCP_QOI_SUM_ENERGY && g > tk.qoi_from && tk.qoi_slot >= 0;
   } else {
     if (tk.x_out >= 0 && i < a.N) a.xbuf[tk.x_out + i] = X[i];
-    energy = tk.qoi_mode == MLMCP_QOI_FINAL_ENERGY && tk.qoi_slot >= 0 &&
-             ti[I_CODE] == MLMCP_ST_OK;
+    energy = tk.qoi_mode == MLMCP_QOI_FINAL_ENERGY && tk.qoi_slot >= 0 && !code_now;
   }
   double e = 0.0;
   if (energy && i < a.N) {
