@@ -221,7 +221,7 @@ class EddyCurrentFamily:
 
     # ------------------------------------------------------------ batched
     def run_levels(self, draws, parareal_cfg: PararealConfig | None = None, levels=None,
-                   concurrent: bool = True) -> list[CoupledBatch]:
+                   concurrent: bool = True, params_dev=None) -> list[CoupledBatch]:
         """Coupled (Q_l, Q_{l-1}) for every level at once.
 
         draws[i]: [N_i, P] parameters of level ``levels[i]`` (default 0..L).
@@ -235,9 +235,12 @@ class EddyCurrentFamily:
         top = len(self.hierarchy) - 1
         sizes = [len(d) for d in draws]
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-        allp = np.concatenate([np.asarray(d, dtype=float).reshape(len(d), -1) for d in draws], axis=0) \
-            if sum(sizes) else np.zeros((0, fe.n_params(self.layout)))
-        params = torch.from_numpy(allp).to(sol.device)
+        if params_dev is not None:
+            params = params_dev                   # already resident in HBM
+        else:
+            allp = np.concatenate([np.asarray(d, dtype=float).reshape(len(d), -1) for d in draws],
+                                  axis=0) if sum(sizes) else np.zeros((0, fe.n_params(self.layout)))
+            params = torch.from_numpy(allp).pin_memory().to(sol.device, non_blocking=True)
         M, K = sol.assemble(params)
         jobs, where = [], []
         pr_level = None

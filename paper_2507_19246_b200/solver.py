@@ -101,6 +101,8 @@ class FESolver:
         self.device = dev
         self.N = m.n_rows
         self.profile = torch.tensor(fe.source_profile(m, layout), dtype=F64, device=dev)
+        self._task_cache: dict = {}
+        self.events = None    # optional (start, end) CUDA events around the sequential launch
         self.omega = 2.0 * np.pi * fe.FREQ          # same rounding as np.sin(2.0*np.pi*f*t)
         if layout == "kl64":
             self.kl_basis = torch.tensor(fe.kl_basis(m), dtype=F64, device=dev)
@@ -116,6 +118,9 @@ class FESolver:
         """Per-sample CSR values (M, K) [S, nnz] from parameters [S, P]."""
         params = params.to(device=self.device, dtype=F64).contiguous()
         S = params.shape[0]
+        if S == 0:
+            empty = torch.empty((0, self.mesh.nnz), dtype=F64, device=self.device)
+            return empty, empty.clone()
         if params.shape[1] != fe.n_params(self.layout):
             raise ValueError(f"layout {self.layout} takes {fe.n_params(self.layout)} parameters, "
                              f"got {params.shape[1]}")
@@ -168,8 +173,17 @@ class FESolver:
         status = torch.zeros((T, _lib.STATUS_INTS), dtype=I32, device=self.device)
         if self.sys.sm_resident:
             order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
+            key = (tasks.tobytes(), N)
+            td = self._task_cache.get(key)
+            if td is None:
+                td = tasks_to_device(tasks[order], self.device)
+                self._task_cache[key] = td
+            if self.events is not None:
+                self.events[0].record(stream if stream is not None else torch.cuda.current_stream())
             self.sys.propagate(tasks[order], M, K, self.profile, self.omega, self.rtol, self.max_it,
-                               xbuf, qoi, iters, status, None, stream)
+                               xbuf, qoi, iters, status, None, stream, tasks_dev=td)
+            if self.events is not None:
+                self.events[1].record(stream if stream is not None else torch.cuda.current_stream())
         else:
             for dt in sorted(set(tasks["dt"].tolist())):
                 sel = tasks[tasks["dt"] == dt]
@@ -184,6 +198,14 @@ class FESolver:
         self._last_xbuf = xbuf
         self._last_tasks = tasks
         return out
+
+    def _grid_tensors(self, ck0, cst):
+        key = ("grid", ck0.tobytes(), cst.tobytes())
+        v = self._task_cache.get(key)
+        if v is None:
+            v = (torch.tensor(ck0, device=self.device), torch.tensor(cst, device=self.device))
+            self._task_cache[key] = v
+        return v
 
     # ------------------------------------------------------------ Parareal
     def run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
@@ -211,8 +233,7 @@ class FESolver:
         fine_status = torch.zeros((S * m, _lib.STATUS_INTS), dtype=I32, device=dev)
         fine_iters = torch.zeros(S * m, dtype=I32, device=dev)
         coarse_iters = torch.zeros(S, dtype=I32, device=dev)
-        ck0_d = torch.tensor(ck0, device=dev)
-        cst_d = torch.tensor(cst, device=dev)
+        ck0_d, cst_d = self._grid_tensors(ck0, cst)
         # fine task tables: one per iteration k (intervals k..m of every sample)
         s_idx, n_idx = np.meshgrid(np.arange(S), np.arange(1, m + 1), indexing="ij")
         s_idx, n_idx = s_idx.ravel(), n_idx.ravel()
@@ -228,11 +249,15 @@ class FESolver:
             all_tasks["traj"] = 2 * uf_size + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
         all_tasks["group"] = s_idx
         all_tasks["slot"] = s_idx * m + (n_idx - 1)
-        tables = []
-        for k in range(1, k_max + 1):
-            sel = all_tasks[n_idx >= k].copy()
-            sel["tag"] = k
-            tables.append(tasks_to_device(sel, dev))
+        key = ("pr", all_tasks.tobytes(), k_max)
+        tables = self._task_cache.get(key)
+        if tables is None:
+            tables = []
+            for k in range(1, k_max + 1):
+                sel = all_tasks[n_idx >= k].copy()
+                sel["tag"] = k
+                tables.append(tasks_to_device(sel, dev))
+            self._task_cache[key] = tables
         for k in range(1, k_max + 1):
             self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
                                      ck0_d, cst_d, self.rtol, self.max_it, U, F, C, coarse_iters,
@@ -245,8 +270,14 @@ class FESolver:
             assert n_tk == len(sel)
             self.sys.parareal_defect(S, k, m, k_max, U, F, tol, active, k_used, defects, stream)
         self.sys.parareal_finalize(S, m, U, F, k_used, stream)
-        x_off = torch.tensor((uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64), device=dev)
-        qoi = self.sys.energy(torch.arange(S, dtype=I32, device=dev), x_off, buf, K, stream)
+        ekey = ("energy", S, m, N)
+        ev = self._task_cache.get(ekey)
+        if ev is None:
+            ev = (torch.arange(S, dtype=I32, device=dev),
+                  torch.tensor((uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64),
+                               device=dev))
+            self._task_cache[ekey] = ev
+        qoi = self.sys.energy(ev[0], ev[1], buf, K, stream)
         traj = None
         if keep_traj:
             traj = buf[2 * uf_size:].view(S, m, traj_steps, N)
