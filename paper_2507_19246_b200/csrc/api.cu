@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -232,7 +233,38 @@ int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
       ell_pos[(size_t)j * n_rows + i] = in ? row_ptr[i] + j : -1;
     }
   }
+  // uniform-offset stencil detection
+  {
+    std::vector<int> offs;
+    bool stencil = true;
+    for (int i = 0; i < n_rows && stencil; ++i)
+      for (int q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+        const int d = col[q] - i;
+        if (std::find(offs.begin(), offs.end(), d) == offs.end()) {
+          offs.push_back(d);
+          if ((int)offs.size() > kMaxNz) { stencil = false; break; }
+        }
+      }
+    if (stencil) {
+      std::sort(offs.begin(), offs.end());
+      c->stencil_w = (int)offs.size();
+      int pad = 0;
+      for (int k = 0; k < c->stencil_w; ++k) {
+        c->stencil_off[k] = offs[k];
+        pad = std::max(pad, std::abs(offs[k]));
+      }
+      c->stencil_pad = pad;
+    }
+  }
+  std::vector<int32_t> spos((size_t)std::max(c->stencil_w, 1) * n_rows, -1);
+  for (int i = 0; i < n_rows && c->stencil_w; ++i)
+    for (int q = row_ptr[i]; q < row_ptr[i + 1]; ++q) {
+      const int d = col[q] - i;
+      const int k = (int)(std::find(c->stencil_off, c->stencil_off + c->stencil_w, d) - c->stencil_off);
+      spos[(size_t)k * n_rows + i] = q;
+    }
   int rc = upload(&c->row_ptr, row_ptr, (size_t)n_rows + 1);
+  if (!rc && c->stencil_w) rc = upload(&c->stencil_pos, spos.data(), spos.size());
   if (!rc) rc = upload(&c->col, col, (size_t)nnz);
   if (!rc) rc = upload(&c->ell_col, ell_col.data(), ell_col.size());
   if (!rc) rc = upload(&c->ell_pos, ell_pos.data(), ell_pos.size());
@@ -255,6 +287,7 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->col);
   cudaFree(c->ell_col);
   cudaFree(c->ell_pos);
+  cudaFree(c->stencil_pos);
   cudaFree(c->cptr);
   cudaFree(c->celem);
   cudaFree(c->cmw);

@@ -35,6 +35,13 @@ struct Ctx {
   int32_t* col = nullptr;       // device [nnz]
   int32_t* ell_col = nullptr;   // device [max_row_nnz][n], padded with the row itself
   int32_t* ell_pos = nullptr;   // device [max_row_nnz][n], CSR position or -1
+  // uniform-offset stencil view of the pattern (every col - row lies in a set
+  // of <= 8 offsets): structured FE meshes, banded models.  stencil_w == 0
+  // when the pattern is not a stencil.
+  int stencil_w = 0;
+  int stencil_off[kMaxNz] = {0};
+  int stencil_pad = 0;          // max |offset|
+  int32_t* stencil_pos = nullptr;  // device [stencil_w][n]: CSR position or -1
   // assembly gather map
   int n_elem = 0;
   int n_contrib = 0;
@@ -64,6 +71,17 @@ int cuda_fail(cudaError_t err, const char* what);
   } while (0)
 
 // ------------------------------------------------------------------ device
+// Reciprocal to ~1 ulp: MUFU approximation + two Newton steps (no slow-path
+// branch, so it schedules freely; deterministic).
+__device__ __forceinline__ double fast_rcp(double d) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(d));
+  double e = fma(-d, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-d, y, 1.0);
+  return fma(y, e, y);
+}
+
 __device__ __forceinline__ double warp_allsum(double v) {
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);

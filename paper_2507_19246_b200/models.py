@@ -306,6 +306,8 @@ class EddyCurrentFamily:
         last run (one host sync)."""
         from .parareal import raise_parareal_status
         from .solver import raise_on_status
+        if getattr(self, "_last", None) is None:
+            return
         res, pr, _, _ = self._last
         for r in res:
             raise_on_status(r.status, "implicit Euler solve")
