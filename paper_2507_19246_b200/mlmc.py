@@ -179,7 +179,8 @@ def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
     else:
         # CPU families (tests) — same fixed order as the kernel's definition
         y = (slots[:, 0] - slots[:, 1]).numpy()
-        sums = torch.tensor([float(np.sum(y)), float(np.sum(y * y)), 0.0, 0.0])
+        sums = torch.tensor([float(np.sum(y)), float(np.sum(y * y)), 0.0, 0.0],
+                            dtype=torch.float64)
     return slots, sums
 
 

@@ -1,0 +1,180 @@
+"""GPU estimator path vs the CPU oracle: per-sample Q_l / Q_{l-1}, Parareal K,
+level sums and the MLMC estimate (parity bar: 1e-8 relative per sample;
+level statistics with an absolute tolerance of 1e-8 |E|);
+bitwise independence of the sample partitioning (emulated ranks on one GPU);
+large meshes through the HBM-streaming path vs the splu oracle; failures map
+to the reference's exception types."""
+
+import numpy as np
+import pytest
+
+from oracle import mlmc_oracle as mo
+
+pytestmark = pytest.mark.gpu
+
+T = mo.T
+
+
+def small_family(n=8, dts=(T / 32, T / 64, T / 128), **kw):
+    from paper_2507_19246_b200 import fe
+    from paper_2507_19246_b200.models import (EddyCurrentFamily, ParameterVector, QoIKind,
+                                              UncertainInput, make_hierarchy)
+    nominal = np.array([fe.NU0] * 4 + [fe.SIGMA0] * 4)
+    return EddyCurrentFamily("quad4", UncertainInput(ParameterVector("quad4", nominal), 0.1),
+                             make_hierarchy(list(dts)), T, n, "quad4",
+                             QoIKind.MAGNETIC_ENERGY_T, device="cuda:0", **kw)
+
+
+def oracle_levels(n, dts, counts, pr, seed=0):
+    cfg = mo.OracleConfig("t", n, "quad4", T, tuple(dts), tuple(counts), "energy_T", parareal=pr)
+    prob = mo.FEProblem(n, "quad4")
+    out = []
+    for lvl, N in enumerate(counts):
+        rows = [mo.coupled(prob, cfg, lvl, mo.draw(cfg, seed, lvl, k), dense=True)
+                for k in range(1, N + 1)]
+        out.append(rows)
+    return out
+
+
+def check_estimate(n, dts, counts, pr):
+    from paper_2507_19246_b200.mlmc import FixedSamples, mlmc_estimate
+    from paper_2507_19246_b200.parareal import PararealConfig
+    fam = small_family(n, dts)
+    pcfg = PararealConfig(pr[0], dts[-1], pr[1], pr[2], pr[3]) if pr else None
+    res = mlmc_estimate(fam, policy=FixedSamples(tuple(counts)), parareal_cfg=pcfg, seed=0)
+    ora = oracle_levels(n, dts, counts, pr)
+    stats = [mo.level_statistics(lvl, [r[0] for r in rows], [r[1] for r in rows])
+             for lvl, rows in enumerate(ora)]
+    E = sum(st.mean for st in stats)
+    for lvl, st in enumerate(stats):
+        g = res.per_level[lvl]
+        assert g.n == st.n
+        assert abs(g.mean_y - st.mean) <= 1e-8 * abs(E)
+        if lvl == len(counts) - 1 and pr:
+            assert g.parareal_k == [r[2] for r in ora[lvl]]
+    assert abs(res.expectation - E) <= 1e-8 * abs(E)
+    return fam, ora
+
+
+def test_estimator_small_mesh_with_parareal(cuda):
+    check_estimate(8, (T / 32, T / 64, T / 128), (6, 4, 3), (4, T / 16, 1e-8, 4))
+
+
+def test_estimator_config1_subset(cuda):
+    """Config-1 settings on the 32x32 mesh (Parareal M=16, K<=5, tol 1e-8)."""
+    from paper_2507_19246_b200.parareal import PararealConfig
+    fam, ora = check_estimate(32, (T / 256, T / 512, T / 1024), (3, 2, 1), (16, T / 16, 1e-8, 5))
+    # per-sample parity through the batched family entry point
+    draws = [np.array([mo.draw(mo.CONFIGS[1], 0, lvl, k) for k in range(1, N + 1)])
+             for lvl, N in enumerate((3, 2, 1))]
+    out = fam.run_levels(draws, PararealConfig(16, T / 1024, T / 16, 1e-8, 5))
+    for lvl, b in enumerate(out):
+        ql, qm = b.q_l.cpu().numpy(), b.q_lm1.cpu().numpy()
+        for i, (hi, lo, k) in enumerate(ora[lvl]):
+            assert abs(ql[i] - hi) <= 1e-8 * abs(hi)
+            if lvl:
+                assert abs(qm[i] - lo) <= 1e-8 * abs(lo)
+        if lvl == 2:
+            assert b.k_used.cpu().numpy().tolist() == [r[2] for r in ora[lvl]]
+
+
+def test_partition_bitwise_independent(cuda):
+    """Emulated 3-rank run (contiguous shards, slot buffers summed, fixed-order
+    reduction) equals the 1-rank run bitwise."""
+    import torch
+    from paper_2507_19246_b200.engine import level_reduce
+    from paper_2507_19246_b200.mlmc import draw_level, shard_range
+    from paper_2507_19246_b200.parareal import PararealConfig
+    fam = small_family()
+    pcfg = PararealConfig(4, T / 128, T / 16, 1e-8, 4)
+    counts = (7, 5, 4)
+    full = fam.run_levels([draw_level(fam.uncertain, 0, l, range(1, n + 1))
+                           for l, n in enumerate(counts)], pcfg)
+    slots = [torch.zeros((n, 4), dtype=torch.float64, device="cuda") for n in counts]
+    for rank in range(3):
+        rngs = [shard_range(n, rank, 3) for n in counts]
+        part = fam.run_levels([draw_level(fam.uncertain, 0, l, range(a + 1, b + 1))
+                               for l, (a, b) in enumerate(rngs)], pcfg)
+        for l, (b, (a, e)) in enumerate(zip(part, rngs)):
+            slots[l][a:e, 0] += b.q_l
+            slots[l][a:e, 1] += b.q_lm1
+            slots[l][a:e, 2] += b.k_used.to(torch.float64)
+    for l, b in enumerate(full):
+        np.testing.assert_array_equal(slots[l][:, 0].cpu().numpy(), b.q_l.cpu().numpy())
+        np.testing.assert_array_equal(slots[l][:, 1].cpu().numpy(), b.q_lm1.cpu().numpy())
+        s1 = level_reduce(slots[l][:, 0].contiguous(), slots[l][:, 1].contiguous()).cpu().numpy()
+        s2 = level_reduce(b.q_l, b.q_lm1).cpu().numpy()
+        np.testing.assert_array_equal(s1, s2)
+
+
+def test_level_reduce_kernel_formulas(cuda):
+    import torch
+    from paper_2507_19246_b200.engine import level_reduce
+    rng = np.random.default_rng(0)
+    a, b = rng.random(1000), rng.random(1000)
+    out = level_reduce(torch.tensor(a, device="cuda"), torch.tensor(b, device="cuda")).cpu().numpy()
+    y = a - b
+    np.testing.assert_allclose(out[:2], [y.sum(), (y * y).sum()], rtol=1e-13)
+    assert abs(out[2] - y.mean()) < 1e-15 and abs(out[3] - y.var(ddof=1)) < 1e-14
+
+
+def test_failures_map_to_reference_errors(cuda):
+    from paper_2507_19246_b200.parareal import PararealConfig, PropagatorError
+    from paper_2507_19246_b200.timeint import SingularSystemError
+    fam = small_family(max_it=2)
+    draws = [np.array([mo.draw(mo.CONFIGS[0], 0, 0, 1)])]
+    fam.run_levels(draws, levels=[0])
+    with pytest.raises(SingularSystemError):
+        fam.check_status()
+    fam.run_levels([np.array([mo.draw(mo.CONFIGS[0], 0, 2, 1)])],
+                   PararealConfig(4, T / 128, T / 16, 1e-8, 4), levels=[2])
+    with pytest.raises((PropagatorError, SingularSystemError)):
+        fam.check_status()
+
+
+# ---------------------------------------------------------------- large meshes
+def large_family(cfg_i):
+    from paper_2507_19246_b200.models import eddy_current_family
+    return eddy_current_family(cfg_i, device="cuda:0")
+
+
+@pytest.mark.slow
+def test_cfg3_128_kl_sequential_and_parareal(cuda):
+    """128x128 lognormal KL field (config 3): streaming path vs splu oracle."""
+    import torch
+    from paper_2507_19246_b200.parareal import PararealConfig
+    fam = large_family(3)
+    assert not fam.solver.sys.sm_resident
+    cfg = mo.CONFIGS[3]
+    prob = mo.FEProblem(128, "kl64")
+    p = np.array([mo.draw(cfg, 0, 0, k) for k in (1, 2)])
+    out = fam.run_levels([p], levels=[0])[0]
+    for i in range(2):
+        q = mo.evaluate(prob, cfg, p[i], T / 128, False).q
+        assert abs(out.q_l[i].item() - q) <= 1e-8 * abs(q)
+    pp = np.array([mo.draw(cfg, 0, 2, 1)])
+    b = fam.run_levels([pp], PararealConfig(32, T / 512, T / 32, 1e-8, 6), levels=[2])[0]
+    rec = mo.evaluate(prob, cfg, pp[0], T / 512, True)
+    assert int(b.k_used[0].item()) == rec.k_used
+    assert abs(b.q_l[0].item() - rec.q) <= 1e-8 * abs(rec.q)
+    del torch
+
+
+@pytest.mark.slow
+def test_cfg2_256_time_averaged(cuda):
+    fam = large_family(2)
+    cfg = mo.CONFIGS[2]
+    p = np.array([mo.draw(cfg, 0, 0, 1)])
+    out = fam.run_levels([p], levels=[0])[0]
+    q = mo.evaluate(mo.FEProblem(256, "blocks8"), cfg, p[0], cfg.dts[0], False).q
+    assert abs(out.q_l[0].item() - q) <= 1e-8 * abs(q)
+
+
+@pytest.mark.slow
+def test_cfg4_512_level0(cuda):
+    fam = large_family(4)
+    cfg = mo.CONFIGS[4]
+    p = np.array([mo.draw(cfg, 0, 0, 1)])
+    out = fam.run_levels([p], levels=[0])[0]
+    q = mo.evaluate(mo.FEProblem(512, "blocks8"), cfg, p[0], cfg.dts[0], False).q
+    assert abs(out.q_l[0].item() - q) <= 1e-8 * abs(q)

@@ -1,0 +1,169 @@
+"""CPU: host-side logic of the product package — configs, grids, validation,
+draws, FE setup vs the oracle, the estimator with the closed-form toy family
+(SPEC.md KATs for the mlmc / parareal host pieces)."""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+from oracle import mlmc_oracle as mo
+from paper_2507_19246_b200 import fe
+from paper_2507_19246_b200.configs import CONFIGS, T
+from paper_2507_19246_b200.mlmc import (FixedSamples, RandomStream, draw_level, mlmc_estimate,
+                                        optimal_allocation, shard_range)
+from paper_2507_19246_b200.models import (GaussianInput, LevelSpec, ParameterVector, UncertainInput,
+                                          draw_parameters, make_hierarchy, toy_family)
+from paper_2507_19246_b200.parareal import PararealConfig, defect
+from paper_2507_19246_b200.solver import parareal_grid
+from paper_2507_19246_b200.timeint import step_count
+
+
+def test_seq_equivalent_steps():
+    assert CONFIGS[1].seq_equiv_steps() == 278528
+    assert CONFIGS[0].seq_equiv_steps() == 67520
+    assert CONFIGS[2].seq_equiv_steps() == 2424832
+    assert CONFIGS[3].seq_equiv_steps() == 557056
+    assert CONFIGS[4].seq_equiv_steps() == 1212416
+
+
+def test_step_count_rules():
+    assert step_count(0.0, T, T / 256) == 256
+    with pytest.raises(ValueError):
+        step_count(0.0, 1.0, 0.3)
+    with pytest.raises(ValueError):
+        step_count(0.0, 1.0, 0.0)
+
+
+def test_parareal_config_validation():
+    with pytest.raises(ValueError):
+        PararealConfig(0, 1e-3, 1e-2)
+    with pytest.raises(ValueError):
+        PararealConfig(4, 1e-2, 1e-3)        # dt_coarse < dt_fine
+    with pytest.raises(ValueError):
+        PararealConfig(4, 1e-3, 1e-2, max_iterations=5)
+    with pytest.raises(ValueError):
+        PararealConfig(4, 1e-3, 1e-2, tolerance=-1.0)
+    c = PararealConfig(4, 1e-3, 1e-2)
+    assert c.k_max == 4 and c.with_dt_fine(1e-3) is c and c.with_dt_fine(5e-4).dt_fine == 5e-4
+
+
+def test_parareal_grid_config1():
+    bounds, fk0, fst, ck0, cst = parareal_grid(0.0, T, 16, T / 1024, T / 16)
+    assert np.all(fst == 64) and np.all(cst == 1)
+    np.testing.assert_array_equal(fk0, np.arange(16) * 64)
+    np.testing.assert_array_equal(ck0, np.arange(16))
+    with pytest.raises(ValueError):
+        parareal_grid(0.0, T, 3, T / 1024, T / 16)
+
+
+def test_defect_examples():
+    # SPEC.md:218-220
+    assert defect([[1.0, 2.0]], [[1.0, 2.0]]) == 0.0
+    assert abs(defect([[1.0, 0.0]], [[1.0, 1.0]]) - 2 ** -0.5) < 1e-15
+    a, b = np.random.default_rng(1).random((2, 3, 5))
+    assert abs(defect(a * 1e3, b * 1e3) - defect(a, b)) <= 1e-12 * defect(a, b)
+    assert defect(np.zeros((0, 3)), np.zeros((0, 3))) == 0.0
+
+
+def test_draws_identical_to_reference_and_oracle():
+    g = golden("draws")
+    inp = UncertainInput(ParameterVector("quad4", g["nominal"]), 0.1)
+    for key, row in zip(g["keys"], g["uniform"]):
+        np.testing.assert_array_equal(draw_parameters(inp, RandomStream(*key)).values, row)
+    gi = GaussianInput("kl64", 64)
+    np.testing.assert_array_equal(draw_parameters(gi, RandomStream(0, 2, 1)).values, g["gaussian"][0])
+    d = draw_level(inp, 0, 1, [1, 2, 3])
+    np.testing.assert_array_equal(d[1], mo.draw(mo.CONFIGS[0], 0, 1, 2))
+
+
+def test_draw_halfwidth_zero_and_positivity():
+    inp = UncertainInput(ParameterVector("quad4", np.ones(8)), 0.0)
+    np.testing.assert_array_equal(draw_parameters(inp, RandomStream(0, 0, 1)).values, np.ones(8))
+    with pytest.raises(ValueError):
+        ParameterVector("quad4", -np.ones(8))
+    with pytest.raises(ValueError):
+        ParameterVector("quad4", np.ones(7))
+    with pytest.raises(ValueError):
+        UncertainInput(ParameterVector("quad4", np.ones(8)), 1.0)
+
+
+def test_hierarchy():
+    h = make_hierarchy([T / 32, T / 64])
+    assert h[1] == LevelSpec(1, T / 64)
+    with pytest.raises(ValueError):
+        make_hierarchy([T / 64, T / 32])
+
+
+@pytest.mark.parametrize("n,layout", [(8, "quad4"), (16, "blocks8"), (16, "kl64"), (32, "quad4")])
+def test_product_fe_setup_matches_oracle(n, layout):
+    """Pattern, gather map and source profile of fe.py vs the oracle's element
+    loop (independent implementations)."""
+    m = fe.structured_mesh(n)
+    cfg = {"quad4": mo.CONFIGS[0], "blocks8": mo.CONFIGS[2], "kl64": mo.CONFIGS[3]}[layout]
+    p = mo.draw(cfg, 0, 1, 5)
+    model = mo.FEProblem(n, layout).model(p, dense=False)
+    if layout == "kl64":
+        sig = np.exp(np.log(fe.SIGMA0) + fe.KL_SCALE * (p @ fe.kl_basis(m)))
+        nu = np.full(m.n_elem, fe.NU0)
+    else:
+        reg = fe.region_map(m, layout)
+        R = len(fe.conducting_mask(layout))
+        nu = p[:R][reg]
+        sig = (p[R:2 * R] * fe.conducting_mask(layout))[reg]
+    Mv = np.add.reduceat(sig[m.celem] * m.cmw, m.cptr[:-1])
+    Kv = np.add.reduceat(nu[m.celem] * m.ckw, m.cptr[:-1])
+    Mo, Ko = model.mass.tocsr(), model.stiffness.tocsr()
+    Mo.sort_indices()
+    Ko.sort_indices()
+    np.testing.assert_array_equal(Mo.indptr, m.row_ptr)
+    np.testing.assert_array_equal(Mo.indices, m.col)
+    np.testing.assert_allclose(Mv, Mo.data, rtol=1e-13, atol=1e-13 * np.abs(Mo.data).max())
+    np.testing.assert_allclose(Kv, Ko.data, rtol=1e-13, atol=1e-13 * np.abs(Ko.data).max())
+    np.testing.assert_allclose(fe.source_profile(m, layout), model.forcing.profile, rtol=1e-13)
+    assert int(np.diff(m.row_ptr).max()) == 7
+
+
+def test_shard_range_covers_exactly():
+    for n in (0, 1, 7, 512):
+        for world in (1, 2, 3, 8):
+            parts = [shard_range(n, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+
+
+def test_optimal_allocation_examples():
+    # SPEC.md:296-298
+    V, C = [1.0, 1e-2, 1e-4], [1.0, 10.0, 100.0]
+    n = optimal_allocation(V, C, rmse=1e-3)
+    w = np.sqrt(np.array(V) / np.array(C))
+    np.testing.assert_allclose(w / w[0], [1.0, 0.0316228, 0.001], rtol=1e-5)
+    assert n[0] > n[1] > n[2] >= 2
+    assert optimal_allocation([0.0, 0.0], [1.0, 1.0], rmse=1.0) == [2, 2]
+    assert optimal_allocation([2.0], [1.0], rmse=0.1) == [int(np.ceil(2 * 2.0 / 0.01))]
+    a = optimal_allocation(V, C, rmse=1e-2)
+    b = optimal_allocation(V, [c * 7 for c in C], rmse=1e-2)   # homogeneous in C
+    assert a == b
+
+
+def test_toy_estimator_telescoping_and_coupling():
+    fam = toy_family(make_hierarchy([0.1, 0.05, 0.025]), halfwidth=0.05)
+    res = mlmc_estimate(fam, policy=FixedSamples((200, 50, 20)), seed=3)
+    assert abs(res.expectation - sum(st.mean_y for st in res.per_level)) < 1e-15
+    # E[Q_L] = 1 + dt_L for xi ~ U[0.95, 1.05]
+    assert abs(res.expectation - 1.025) < 4 * res.rmse_estimate + 1e-3
+    # level-0 mean equals a plain MC mean of the same keys
+    qs = [draw_parameters(fam.uncertain, RandomStream(3, 0, k)).values[0] * 1.1 for k in range(1, 201)]
+    assert abs(res.per_level[0].mean_y - np.mean(qs)) < 1e-14
+
+
+def test_toy_estimator_equal_dt_levels_zero():
+    # SPEC.md:287 / :309: identical dt on two levels -> Y = 0 on level 1
+    fam = toy_family([LevelSpec(0, 0.1), LevelSpec(1, 0.1)])
+    res = mlmc_estimate(fam, policy=FixedSamples((10, 10)), seed=0)
+    assert res.per_level[1].sum_y == 0.0 and res.per_level[1].var_y == 0.0
+
+
+def test_toy_estimator_constant_qoi():
+    fam = toy_family(make_hierarchy([0.1, 0.05]), nominal=2.0, halfwidth=0.0)
+    res = mlmc_estimate(fam, policy=FixedSamples((5, 5)), seed=0)
+    assert abs(res.expectation - 2.0 * 1.05) <= 1e-15 * 2.1 and res.rmse_estimate == 0.0
