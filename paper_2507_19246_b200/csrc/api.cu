@@ -263,8 +263,38 @@ int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
       const int k = (int)(std::find(c->stencil_off, c->stencil_off + c->stencil_w, d) - c->stencil_off);
       spos[(size_t)k * n_rows + i] = q;
     }
+  // 2D grid detection (structured FE mesh small enough for the grid-tiled kernel)
+  std::vector<int32_t> gpos;
+  for (int wd = 2; wd <= 32 && c->grid_wd == 0; ++wd) {
+    if (n_rows % wd != 0 || n_rows / wd > 32) continue;
+    std::vector<int32_t> g((size_t)7 * n_rows, -1);
+    bool ok = true;
+    for (int i = 0; i < n_rows && ok; ++i) {
+      const int x = i % wd, y = i / wd;
+      for (int q = row_ptr[i]; q < row_ptr[i + 1] && ok; ++q) {
+        const int j = col[q], xj = j % wd, yj = j / wd;
+        const int dx = xj - x, dy = yj - y;
+        int slot = -1;
+        if (dx == -1 && dy == -1) slot = 0;
+        else if (dx == 0 && dy == -1) slot = 1;
+        else if (dx == -1 && dy == 0) slot = 2;
+        else if (dx == 0 && dy == 0) slot = 3;
+        else if (dx == 1 && dy == 0) slot = 4;
+        else if (dx == 0 && dy == 1) slot = 5;
+        else if (dx == 1 && dy == 1) slot = 6;
+        if (slot < 0) ok = false;
+        else g[(size_t)slot * n_rows + i] = q;
+      }
+    }
+    if (ok) {
+      c->grid_wd = wd;
+      c->grid_h = n_rows / wd;
+      gpos.swap(g);
+    }
+  }
   int rc = upload(&c->row_ptr, row_ptr, (size_t)n_rows + 1);
   if (!rc && c->stencil_w) rc = upload(&c->stencil_pos, spos.data(), spos.size());
+  if (!rc && c->grid_wd) rc = upload(&c->grid_pos, gpos.data(), gpos.size());
   if (!rc) rc = upload(&c->col, col, (size_t)nnz);
   if (!rc) rc = upload(&c->ell_col, ell_col.data(), ell_col.size());
   if (!rc) rc = upload(&c->ell_pos, ell_pos.data(), ell_pos.size());
@@ -288,6 +318,7 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->ell_col);
   cudaFree(c->ell_pos);
   cudaFree(c->stencil_pos);
+  cudaFree(c->grid_pos);
   cudaFree(c->cptr);
   cudaFree(c->celem);
   cudaFree(c->cmw);

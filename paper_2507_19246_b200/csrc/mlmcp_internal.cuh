@@ -42,6 +42,12 @@ struct Ctx {
   int stencil_off[kMaxNz] = {0};
   int stencil_pad = 0;          // max |offset|
   int32_t* stencil_pos = nullptr;  // device [stencil_w][n]: CSR position or -1
+  // 2D grid view (structured 7-point FE stencil on a wd x gh interior grid,
+  // row = y*wd + x, neighbours (dx,dy) in {(0,0),(+-1,0),(0,+-1),(1,1),(-1,-1)}),
+  // wd <= 32 and gh <= 32: the grid-tiled SM-resident kernel applies.
+  int grid_wd = 0;
+  int grid_h = 0;
+  int32_t* grid_pos = nullptr;     // device [7][n] in order SW,S,W,C,E,N,NE: CSR position or -1
   // assembly gather map
   int n_elem = 0;
   int n_contrib = 0;

@@ -3,29 +3,28 @@
 // Replaces the per-step dense LU solve of the reference
 // (timeint.py:64-75 factorise, :108-110 / :126-127 per-step solve) for
 // meshes whose interior system has <= 1024 rows (the 32x32 mesh of configs
-// 0/1 has 961).  Each CTA owns one (sample, slice) task for its lifetime:
-//   * a thread owns R rows (rows tid, tid+256, ...; 256 threads per CTA): the
-//     <= 8 coefficients of A = M + dt*K per row and D^-1 sit in registers for
-//     every step and every PCG iteration (no HBM traffic for the operator
-//     after the first load);
-//   * column addressing has two policies:
-//       STENCIL  the pattern is a uniform-offset stencil (every col - row in a
-//                set of <= 8 offsets: the structured 7-point FE mesh, banded
-//                models) -> neighbour j of row i is v[i + off_j], off_j
-//                block-uniform; zero-padded smem vectors absorb the missing
-//                boundary neighbours (their coefficients are 0).  No per-row
-//                column registers: two CTAs fit one SM.
-//       CSR      generic pattern -> packed 16-bit smem byte offsets per entry.
-//   * the only shared-memory traffic is the neighbour gather of the SpMV
-//     operand, conflict-free because consecutive lanes own consecutive rows;
-//   * PCG is the Chronopoulos-Gear single-reduction variant: one fused block
-//     all-reduce (r.u, w.u, r.r) per iteration, two __syncthreads; the
-//     alpha/beta recurrence needs one reciprocal on the critical path (1/gamma
-//     and 1/alpha for the next iteration are formed off the critical path);
-//   * the cross-warp stage of the reduction is a broadcast smem read of the
-//     <= 8 warp partials + a fixed tree (no second butterfly);
-//   * the QoI (magnetic energy 1/2 x^T K x) is fused into the step loop, so
-//     no trajectory is stored unless asked for.
+// 0/1 has 961).  Each CTA (256 threads) owns one (sample, slice) task for its
+// lifetime; a thread owns 4 rows, whose <= 8 coefficients of A = M + dt*K and
+// D^-1 sit in registers for every step and every PCG iteration (no HBM
+// traffic for the operator after the first load).
+//
+// The SpMV operand exchange is an "operator" policy (publish -> barrier ->
+// apply):
+//   GridOp     structured 7-point FE stencil on a wd x h <= 32 x 32 grid:
+//              thread (warp w, lane l) owns grid points (x=l, y=4w+k); N/S
+//              neighbours come from the thread's own registers, E/W (and
+//              NE/SW) from warp shuffles, only the warp-tile halos (2 values
+//              per lane) go through shared memory.
+//   StencilOp  uniform-offset stencil (every col-row in <= 8 offsets): rows
+//              tid + 256k, neighbour j read from a zero-padded smem vector at
+//              a block-uniform offset.
+//   CsrOp      generic pattern: packed 16-bit smem byte offsets per entry.
+// PCG is the Chronopoulos-Gear single-reduction variant: one fused block
+// all-reduce (r.u, w.u, r.r) per iteration, two __syncthreads; the alpha/beta
+// recurrence has one reciprocal on the critical path.  The cross-warp stage
+// of the reduction is a broadcast smem read of the 8 warp partials + a fixed
+// tree, so every thread holds bitwise identical totals (deterministic).
+// The QoI (magnetic energy 1/2 x^T K x) is fused into the step loop.
 // The Parareal coarse/update sweep (parareal.py:168-178) runs in the same CTA
 // model: one CTA per sample walks slices k..M-1 sequentially, the state stays
 // in registers between slices.
@@ -39,57 +38,56 @@ namespace {
 
 constexpr int kSmallThreads = 256;
 constexpr int kMaxWarps = kSmallThreads / 32;
+constexpr int kHaloLd = 34;                       // grid halo row: 32 lanes + 2 pads
+constexpr int kHaloRows = kMaxWarps + 2;          // 8 warps + 2 zero rows
+constexpr int kHaloBuf = 2 * kHaloRows * kHaloLd; // lo + hi halos
 
-struct StencilArgs {
-  int off[kMaxNz];       // sorted offsets (col - row)
+struct PatternArgs {
+  int N;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  int off[kMaxNz];       // stencil: sorted offsets (col - row)
   int off8[kMaxNz];      // the same in bytes
-  const int32_t* pos;    // [W][N] CSR position of slot j of row i, or -1
+  const int32_t* spos;   // stencil: [W][N] CSR position of slot j of row i, or -1
+  int pad;               // stencil: zero rows before row 0 / after the last padded row
+  int wd, gh;            // grid: width / height
+  const int32_t* gpos;   // grid: [7][N] CSR position per direction, or -1
 };
 
-struct SmallShared {
-  double* vA;   // gather operand for x (and the energy); row 0 at vA[0]
-  double* vB;   // gather operand for u
-  double* red;  // [2][kMaxWarps][4]
-  int par;
-};
+__device__ __forceinline__ double lds_off(const double* base, uint32_t off) {
+  return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) + off);
+}
 
+// ---------------------------------------------------------------- block reduce
 // Block all-reduce of NV <= 4 doubles.  Butterfly inside each warp, then every
-// thread reads the <= 8 warp partials (broadcast) and sums them in a fixed
-// tree: bitwise identical totals in all threads, deterministic.
+// thread reads the 8 warp partials (broadcast) and sums them in a fixed tree.
 template <int NV>
-__device__ __forceinline__ void cta_allsum(double (&v)[NV], SmallShared& sh) {
+__device__ __forceinline__ void cta_allsum(double (&v)[NV], double* red, int& par) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int nwarps = blockDim.x >> 5;
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
   }
-  double* buf = sh.red + sh.par * (kMaxWarps * 4);
+  double* buf = red + par * (kMaxWarps * 4);
   if (lane == 0) {
 #pragma unroll
     for (int k = 0; k < NV; ++k) buf[warp * 4 + k] = v[k];
   }
   __syncthreads();
-  // fixed pairwise tree ((w0+w1)+(w2+w3))+((w4+w5)+(w6+w7)), streamed so that
-  // only a few partials are live at a time (register pressure)
   auto ld = [&](int w, double (&o)[NV]) {
-    if (w < nwarps) {
-      const double2 lo = *reinterpret_cast<const double2*>(buf + w * 4);
-      o[0] = lo.x;
-      if (NV > 1) o[1 % NV] = lo.y;
-      if (NV > 2) {
-        const double2 hi = *reinterpret_cast<const double2*>(buf + w * 4 + 2);
-        o[2 % NV] = hi.x;
-        if (NV > 3) o[3 % NV] = hi.y;
-      }
-    } else {
-#pragma unroll
-      for (int k = 0; k < NV; ++k) o[k] = 0.0;
+    const double2 lo = *reinterpret_cast<const double2*>(buf + w * 4);
+    o[0] = lo.x;
+    if (NV > 1) o[1 % NV] = lo.y;
+    if (NV > 2) {
+      const double2 hi = *reinterpret_cast<const double2*>(buf + w * 4 + 2);
+      o[2 % NV] = hi.x;
+      if (NV > 3) o[3 % NV] = hi.y;
     }
   };
   static_assert(kMaxWarps == 8, "tree below is written for 8 warps");
+  // fixed tree ((w0+w1)+(w2+w3))+((w4+w5)+(w6+w7)), streamed (few live regs)
   double q0[NV], q1[NV], h0[NV], h1[NV];
   ld(0, q0); ld(1, q1);
 #pragma unroll
@@ -103,182 +101,312 @@ __device__ __forceinline__ void cta_allsum(double (&v)[NV], SmallShared& sh) {
   ld(6, q0); ld(7, q1);
 #pragma unroll
   for (int k = 0; k < NV; ++k) v[k] = h0[k] + (h1[k] + (q0[k] + q1[k]));
-  sh.par ^= 1;
+  par ^= 1;
 }
 
-__device__ __forceinline__ double lds_off(const double* base, uint32_t off) {
-  return *reinterpret_cast<const double*>(reinterpret_cast<const char*>(base) + off);
-}
+// ---------------------------------------------------------------- operators
+// Common interface (R = rows per thread):
+//   load(pa, Ms, Ks, dt)               coefficients of A = M + dt K, D^-1
+//   ok(r, pa), row(r, pa)              validity / global row of slot r
+//   publish(v, buf, pa)                store what neighbours need (before a barrier)
+//   apply(v, buf, pa, out)             out = A v (register coefficients)
+//   apply_vals(vals, v, buf, pa, out)  out = B v (B: per-sample CSR values)
+//   buffer_doubles(pad)                smem doubles of one exchange buffer
+// Invalid (padding) slots hold v = 0, a = 0, dinv = 0.
 
-// Every SM-resident CTA has exactly kSmallThreads threads (rows beyond N are
-// zero padding), so row addresses fold into compile-time immediates.
-template <int R>
-__device__ __forceinline__ int row_of(int r) {
-  return threadIdx.x + r * kSmallThreads;
-}
-
-template <int R>
-__device__ __forceinline__ bool row_ok(int r, int N) {
-  return row_of<R>(r) < N;
-}
-
-// Register state of the R rows of one thread.
-template <int W, int R, bool ST>
-struct Rows {
+template <int W, int R_>
+struct StencilOp {
+  static constexpr int R = R_;
   double a[R][W];
-  uint32_t cp[ST ? 1 : R][ST ? 1 : (W + 1) / 2];  // CSR: packed smem byte offsets
   double dinv[R];
+  __device__ static int row(int r, const PatternArgs&) { return threadIdx.x + r * kSmallThreads; }
+  __device__ static bool ok(int r, const PatternArgs& pa) { return row(r, pa) < pa.N; }
+  static int buffer_doubles(int pad) { return pad + R * kSmallThreads + pad; }
 
-  __device__ __forceinline__ uint32_t off(int r, int j) const {
-    const uint32_t w = cp[ST ? 0 : r][ST ? 0 : (j >> 1)];
-    return (j & 1) ? (w >> 16) : (w & 0xffffu);
-  }
-
-  __device__ __forceinline__ void load(const int32_t* __restrict__ row_ptr,
-                                       const int32_t* __restrict__ col, const StencilArgs& st,
-                                       const double* __restrict__ Ms,
-                                       const double* __restrict__ Ks, double dt, int N) {
+  __device__ void load(const PatternArgs& pa, const double* __restrict__ Ms,
+                       const double* __restrict__ Ks, double dt) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int row = row_of<R>(r);
-      const bool ok = row < N;
+      const bool v = ok(r, pa);
       double diag = 1.0;
-      if (ST) {
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          const int q = ok ? st.pos[j * N + row] : -1;
-          a[r][j] = q >= 0 ? op_entry(__ldg(Ms + q), __ldg(Ks + q), dt) : 0.0;
-          if (st.off[j] == 0 && q >= 0) diag = a[r][j];
-        }
-      } else {
-        const int q0 = ok ? row_ptr[row] : 0;
-        const int len = ok ? row_ptr[row + 1] - q0 : 0;
-#pragma unroll
-        for (int j = 0; j < (W + 1) / 2; ++j) cp[ST ? 0 : r][ST ? 0 : j] = 0u;
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-          uint32_t o;
-          if (j < len) {
-            const int q = q0 + j;
-            const int c = col[q];
-            o = (uint32_t)c * 8u;
-            a[r][j] = op_entry(__ldg(Ms + q), __ldg(Ks + q), dt);
-            if (c == row) diag = a[r][j];
-          } else {
-            o = ok ? (uint32_t)row * 8u : 0u;
-            a[r][j] = 0.0;
-          }
-          cp[ST ? 0 : r][ST ? 0 : (j >> 1)] |= (j & 1) ? (o << 16) : o;
-        }
-      }
-      dinv[r] = ok ? 1.0 / diag : 0.0;
-    }
-  }
-
-  __device__ __forceinline__ double gather(int r, int j, const double* v,
-                                           const StencilArgs& st) const {
-    if (ST) return lds_off(v + row_of<R>(r), (uint32_t)st.off8[j]);
-    return lds_off(v, off(r, j));
-  }
-
-  // (A v)_row from register coefficients
-  __device__ __forceinline__ double spmv(int r, const double* v, const StencilArgs& st) const {
-    double acc0 = 0.0, acc1 = 0.0;
-#pragma unroll
-    for (int j = 0; j < W; j += 2) {
-      acc0 = fma(a[r][j], gather(r, j, v, st), acc0);
-      if (j + 1 < W) acc1 = fma(a[r][j + 1], gather(r, j + 1, v, st), acc1);
-    }
-    return acc0 + acc1;
-  }
-
-  // (B v)_row for B given by per-sample CSR values in global memory (M for the
-  // right-hand side once per step, K for the energy).  Only for rows < N.
-  __device__ __forceinline__ double spmv_csr(int r, const int32_t* __restrict__ row_ptr,
-                                             const StencilArgs& st, int N,
-                                             const double* __restrict__ vals,
-                                             const double* v) const {
-    const int row = row_of<R>(r);
-    double acc0 = 0.0, acc1 = 0.0;
-    if (ST) {
 #pragma unroll
       for (int j = 0; j < W; ++j) {
-        const int q = __ldg(st.pos + j * N + row);
-        const double t = q >= 0 ? __ldg(vals + q) * v[row + st.off[j]] : 0.0;
-        if (j & 1) acc1 += t;
-        else acc0 += t;
+        const int q = v ? pa.spos[j * pa.N + row(r, pa)] : -1;
+        a[r][j] = q >= 0 ? op_entry(__ldg(Ms + q), __ldg(Ks + q), dt) : 0.0;
+        if (pa.off[j] == 0 && q >= 0) diag = a[r][j];
       }
-    } else {
-      const int q0 = __ldg(row_ptr + row);
-      const int len = __ldg(row_ptr + row + 1) - q0;
+      dinv[r] = v ? 1.0 / diag : 0.0;
+    }
+  }
+  __device__ static double* base(double* buf, const PatternArgs& pa) { return buf + pa.pad; }
+  __device__ void publish(const double (&v)[R], double* buf, const PatternArgs& pa) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) base(buf, pa)[row(r, pa)] = v[r];  // padded: every slot writes
+  }
+  __device__ void apply(const double (&v)[R], double* buf, const PatternArgs& pa,
+                        double (&out)[R]) const {
+    const double* b = base(buf, pa);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc0 = 0.0, acc1 = 0.0;
 #pragma unroll
       for (int j = 0; j < W; j += 2) {
-        if (j < len) acc0 = fma(__ldg(vals + q0 + j), lds_off(v, off(r, j)), acc0);
-        if (j + 1 < W && j + 1 < len)
-          acc1 = fma(__ldg(vals + q0 + j + 1), lds_off(v, off(r, j + 1)), acc1);
+        acc0 = fma(a[r][j], lds_off(b + row(r, pa), (uint32_t)pa.off8[j]), acc0);
+        if (j + 1 < W)
+          acc1 = fma(a[r][j + 1], lds_off(b + row(r, pa), (uint32_t)pa.off8[j + 1]), acc1);
       }
+      out[r] = acc0 + acc1;
     }
-    return acc0 + acc1;
+  }
+  __device__ void apply_vals(const double* __restrict__ vals, const double (&v)[R], double* buf,
+                             const PatternArgs& pa, double (&out)[R]) const {
+    const double* b = base(buf, pa);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+      if (ok(r, pa)) {
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+          const int q = __ldg(pa.spos + j * pa.N + row(r, pa));
+          if (q >= 0) acc = fma(__ldg(vals + q), b[row(r, pa) + pa.off[j]], acc);
+        }
+      }
+      out[r] = acc;
+    }
   }
 };
 
-// 1/2 x^T K x over the block (every thread receives it).  Uses vA.
-template <int W, int R, bool ST>
-__device__ __forceinline__ double block_energy(const Rows<W, R, ST>& rw, const double (&x)[R],
-                                               int N, const int32_t* __restrict__ row_ptr,
-                                               const StencilArgs& st,
-                                               const double* __restrict__ Ks, SmallShared& sh) {
+template <int W, int R_>
+struct CsrOp {
+  static constexpr int R = R_;
+  double a[R][W];
+  uint32_t cp[R][(W + 1) / 2];  // packed 16-bit smem byte offsets of the columns
+  double dinv[R];
+  __device__ static int row(int r, const PatternArgs&) { return threadIdx.x + r * kSmallThreads; }
+  __device__ static bool ok(int r, const PatternArgs& pa) { return row(r, pa) < pa.N; }
+  static int buffer_doubles(int) { return R * kSmallThreads; }
+  __device__ uint32_t off(int r, int j) const {
+    const uint32_t w = cp[r][j >> 1];
+    return (j & 1) ? (w >> 16) : (w & 0xffffu);
+  }
+
+  __device__ void load(const PatternArgs& pa, const double* __restrict__ Ms,
+                       const double* __restrict__ Ks, double dt) {
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (row_ok<R>(r, N)) sh.vA[row_of<R>(r)] = x[r];
+    for (int r = 0; r < R; ++r) {
+      const int rw = row(r, pa);
+      const bool v = ok(r, pa);
+      const int q0 = v ? pa.row_ptr[rw] : 0;
+      const int len = v ? pa.row_ptr[rw + 1] - q0 : 0;
+      double diag = 1.0;
+#pragma unroll
+      for (int j = 0; j < (W + 1) / 2; ++j) cp[r][j] = 0u;
+#pragma unroll
+      for (int j = 0; j < W; ++j) {
+        uint32_t o;
+        if (j < len) {
+          const int q = q0 + j;
+          const int c = pa.col[q];
+          o = (uint32_t)c * 8u;
+          a[r][j] = op_entry(__ldg(Ms + q), __ldg(Ks + q), dt);
+          if (c == rw) diag = a[r][j];
+        } else {
+          o = v ? (uint32_t)rw * 8u : 0u;
+          a[r][j] = 0.0;
+        }
+        cp[r][j >> 1] |= (j & 1) ? (o << 16) : o;
+      }
+      dinv[r] = v ? 1.0 / diag : 0.0;
+    }
+  }
+  __device__ void publish(const double (&v)[R], double* buf, const PatternArgs& pa) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) buf[row(r, pa)] = v[r];
+  }
+  __device__ void apply(const double (&v)[R], double* buf, const PatternArgs&,
+                        double (&out)[R]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc0 = 0.0, acc1 = 0.0;
+#pragma unroll
+      for (int j = 0; j < W; j += 2) {
+        acc0 = fma(a[r][j], lds_off(buf, off(r, j)), acc0);
+        if (j + 1 < W) acc1 = fma(a[r][j + 1], lds_off(buf, off(r, j + 1)), acc1);
+      }
+      out[r] = acc0 + acc1;
+    }
+  }
+  __device__ void apply_vals(const double* __restrict__ vals, const double (&v)[R], double* buf,
+                             const PatternArgs& pa, double (&out)[R]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+      if (ok(r, pa)) {
+        const int q0 = __ldg(pa.row_ptr + row(r, pa));
+        const int len = __ldg(pa.row_ptr + row(r, pa) + 1) - q0;
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+          if (j < len) acc = fma(__ldg(vals + q0 + j), lds_off(buf, off(r, j)), acc);
+      }
+      out[r] = acc;
+    }
+  }
+};
+
+// Structured 7-point stencil, directions SW,S,W,C,E,N,NE = slots 0..6.
+struct GridOp {
+  static constexpr int R = 4;
+  double a[R][7];
+  double dinv[R];
+  __device__ static int lane() { return threadIdx.x & 31; }
+  __device__ static int warp() { return threadIdx.x >> 5; }
+  __device__ static int gy(int r) { return 4 * warp() + r; }
+  __device__ static bool ok(int r, const PatternArgs& pa) { return lane() < pa.wd && gy(r) < pa.gh; }
+  __device__ static int row(int r, const PatternArgs& pa) { return gy(r) * pa.wd + lane(); }
+  static int buffer_doubles(int) { return kHaloBuf; }
+
+  __device__ void load(const PatternArgs& pa, const double* __restrict__ Ms,
+                       const double* __restrict__ Ks, double dt) {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool v = ok(r, pa);
+      const int rw = v ? row(r, pa) : 0;
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        const int q = v ? pa.gpos[j * pa.N + rw] : -1;
+        a[r][j] = q >= 0 ? op_entry(__ldg(Ms + q), __ldg(Ks + q), dt) : 0.0;
+      }
+      dinv[r] = (v && a[r][3] != 0.0) ? 1.0 / a[r][3] : 0.0;
+    }
+  }
+  // halo rows: lo[w+1][l+1] = v[0] of warp w, hi[w+1][l+1] = v[3]
+  __device__ void publish(const double (&v)[R], double* buf, const PatternArgs&) const {
+    const int i = (warp() + 1) * kHaloLd + lane() + 1;
+    buf[i] = v[0];
+    buf[kHaloRows * kHaloLd + i] = v[3];
+  }
+  // the 7 neighbour values of each slot
+  __device__ void neighbours(const double (&v)[R], const double* buf, double (&nb)[R][7]) const {
+    double e[R], w[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      e[r] = __shfl_down_sync(0xffffffffu, v[r], 1);
+      w[r] = __shfl_up_sync(0xffffffffu, v[r], 1);
+    }
+    const double* lo = buf;
+    const double* hi = buf + kHaloRows * kHaloLd;
+    const int up = (warp() + 2) * kHaloLd + lane() + 1;   // warp w+1, lane l
+    const int dn = warp() * kHaloLd + lane() + 1;         // warp w-1, lane l
+    const double n3 = lo[up], ne3 = lo[up + 1];
+    const double s0 = hi[dn], sw0 = hi[dn - 1];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      nb[r][0] = r > 0 ? w[r - 1] : sw0;
+      nb[r][1] = r > 0 ? v[r - 1] : s0;
+      nb[r][2] = w[r];
+      nb[r][3] = v[r];
+      nb[r][4] = e[r];
+      nb[r][5] = r < R - 1 ? v[r + 1] : n3;
+      nb[r][6] = r < R - 1 ? e[r + 1] : ne3;
+    }
+  }
+  __device__ void apply(const double (&v)[R], double* buf, const PatternArgs&,
+                        double (&out)[R]) const {
+    double nb[R][7];
+    neighbours(v, buf, nb);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc0 = a[r][3] * nb[r][3];
+      double acc1 = a[r][0] * nb[r][0];
+      acc0 = fma(a[r][1], nb[r][1], acc0);
+      acc1 = fma(a[r][2], nb[r][2], acc1);
+      acc0 = fma(a[r][4], nb[r][4], acc0);
+      acc1 = fma(a[r][5], nb[r][5], acc1);
+      acc0 = fma(a[r][6], nb[r][6], acc0);
+      out[r] = acc0 + acc1;
+    }
+  }
+  __device__ void apply_vals(const double* __restrict__ vals, const double (&v)[R], double* buf,
+                             const PatternArgs& pa, double (&out)[R]) const {
+    double nb[R][7];
+    neighbours(v, buf, nb);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+      if (ok(r, pa)) {
+        const int rw = row(r, pa);
+#pragma unroll
+        for (int j = 0; j < 7; ++j) {
+          const int q = __ldg(pa.gpos + j * pa.N + rw);
+          if (q >= 0) acc = fma(__ldg(vals + q), nb[r][j], acc);
+        }
+      }
+      out[r] = acc;
+    }
+  }
+};
+
+struct SmallShared {
+  double* bufA;  // exchange buffer for x (and the energy)
+  double* bufB;  // exchange buffer for u
+  double* red;   // [2][kMaxWarps][4]
+  int par;
+};
+
+// 1/2 x^T K x over the block (every thread receives it).  Uses bufA.
+template <class Op>
+__device__ __forceinline__ double block_energy(const Op& op, const double (&x)[Op::R],
+                                               const PatternArgs& pa,
+                                               const double* __restrict__ Ks, SmallShared& sh) {
+  constexpr int R = Op::R;
+  op.publish(x, sh.bufA, pa);
   __syncthreads();
+  double kx[R];
+  op.apply_vals(Ks, x, sh.bufA, pa, kx);
   double v[1] = {0.0};
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (row_ok<R>(r, N)) v[0] += x[r] * rw.spmv_csr(r, row_ptr, st, N, Ks, sh.vA);
-  cta_allsum<1>(v, sh);
+  for (int r = 0; r < R; ++r) v[0] = fma(x[r], kx[r], v[0]);
+  cta_allsum<1>(v, sh.red, sh.par);
   return 0.5 * v[0];
 }
 
 // One implicit-Euler step (M + dt K) x_new = M x + dt*sf*profile by
 // Chronopoulos-Gear Jacobi-PCG warm-started at x.  Returns MLMCP_ST_*.
-template <int W, int R, bool ST>
-__device__ __forceinline__ int ie_step(const Rows<W, R, ST>& rw, double (&x)[R], int N,
-                                       double sf, double dt, const int32_t* __restrict__ row_ptr,
-                                       const StencilArgs& st, const double* __restrict__ Ms,
+template <class Op>
+__device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const PatternArgs& pa,
+                                       double sf, double dt, const double* __restrict__ Ms,
                                        const double* __restrict__ profile, double rtol2,
                                        int max_it, SmallShared& sh, int& iters) {
+  constexpr int R = Op::R;
   // b = M x + dt*(sf*prof);  r = b - A x;  u = D r;  w = A u
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (row_ok<R>(r, N)) sh.vA[row_of<R>(r)] = x[r];
+  op.publish(x, sh.bufA, pa);
   __syncthreads();
-  double res[R], u[R], p[R], s[R], w[R];
+  double res[R], u[R], p[R], s[R], w[R], mx[R], ax[R];
+  op.apply_vals(Ms, x, sh.bufA, pa, mx);
+  op.apply(x, sh.bufA, pa, ax);
   double red4[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     res[r] = 0.0;
     u[r] = 0.0;
-    if (row_ok<R>(r, N)) {
-      const int row = row_of<R>(r);
-      const double mx = rw.spmv_csr(r, row_ptr, st, N, Ms, sh.vA);
-      const double ax = rw.spmv(r, sh.vA, st);
-      const double b = __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, __ldg(profile + row))));
-      res[r] = b - ax;
-      u[r] = rw.dinv[r] * res[r];
+    if (Op::ok(r, pa)) {
+      const int rw = Op::row(r, pa);
+      const double b = __dadd_rn(mx[r], __dmul_rn(dt, __dmul_rn(sf, __ldg(profile + rw))));
+      res[r] = b - ax[r];
+      u[r] = op.dinv[r] * res[r];
       red4[3] += b * b;
     }
-    sh.vB[row_of<R>(r)] = u[r];            // vB is padded to R*256 rows
   }
+  op.publish(u, sh.bufB, pa);
   __syncthreads();
+  op.apply(u, sh.bufB, pa, w);                    // a = 0 on padding slots
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    w[r] = rw.spmv(r, sh.vB, st);          // a = 0 on padding rows
     red4[0] += res[r] * u[r];
     red4[1] += w[r] * u[r];
     red4[2] += res[r] * res[r];
   }
-  cta_allsum<4>(red4, sh);
+  cta_allsum<4>(red4, sh.red, sh.par);
   const double gamma = red4[0];
   double delta = red4[1];
   double rho = red4[2];
@@ -305,20 +433,18 @@ __device__ __forceinline__ int ie_step(const Rows<W, R, ST>& rw, double (&x)[R],
   int it = 1;
   for (;;) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      u[r] = rw.dinv[r] * res[r];          // 0 on padding rows (dinv = 0)
-      sh.vB[row_of<R>(r)] = u[r];
-    }
+    for (int r = 0; r < R; ++r) u[r] = op.dinv[r] * res[r];   // 0 on padding slots
+    op.publish(u, sh.bufB, pa);
     __syncthreads();
+    op.apply(u, sh.bufB, pa, w);
     double red3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      w[r] = rw.spmv(r, sh.vB, st);
-      red3[0] += res[r] * u[r];
-      red3[1] += w[r] * u[r];
-      red3[2] += res[r] * res[r];
+      red3[0] = fma(res[r], u[r], red3[0]);
+      red3[1] = fma(w[r], u[r], red3[1]);
+      red3[2] = fma(res[r], res[r], red3[2]);
     }
-    cta_allsum<3>(red3, sh);
+    cta_allsum<3>(red3, sh.red, sh.par);
     const double gnew = red3[0];
     delta = red3[1];
     rho = red3[2];
@@ -329,13 +455,12 @@ __device__ __forceinline__ int ie_step(const Rows<W, R, ST>& rw, double (&x)[R],
     const double beta = gnew * inv_g;
     const double den = fma(-(gnew * gnew), c, delta);
     if (!(den > 0.0)) { iters += it; return MLMCP_ST_BREAKDOWN; }
-    const double rden = fast_rcp(den);
-    alpha = gnew * rden;
+    alpha = gnew * fast_rcp(den);
     inv_g = fast_rcp(gnew);                // off the critical path (next iteration)
     c = inv_g * (den * inv_g);             // 1/(gnew*alpha)
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      p[r] = fma(beta, p[r], rw.dinv[r] * res[r]);   // u recomputed: fewer live registers
+      p[r] = fma(beta, p[r], op.dinv[r] * res[r]);   // u recomputed: fewer live registers
       s[r] = fma(beta, s[r], w[r]);
       x[r] = fma(alpha, p[r], x[r]);
       res[r] = fma(-alpha, s[r], res[r]);
@@ -349,12 +474,8 @@ __device__ __forceinline__ int ie_step(const Rows<W, R, ST>& rw, double (&x)[R],
 struct SmallArgs {
   const mlmcp_task* tasks;
   int n_tasks;
-  int N;
   int64_t nnz;
-  const int32_t* row_ptr;
-  const int32_t* col;
-  StencilArgs st;
-  int pad;               // zero rows before row 0 / after the last padded row
+  PatternArgs pa;
   const double* M;
   const double* K;
   const double* profile;
@@ -366,19 +487,19 @@ struct SmallArgs {
   int32_t* iters;
   int32_t* status;
   int32_t* active;
+  int buf_doubles;
 };
 
-// Carve and zero the padded smem vectors.
-template <int R>
-__device__ __forceinline__ SmallShared setup_shared(double* smem, int pad) {
-  const int len = pad + R * kSmallThreads + pad;
-  for (int i = threadIdx.x; i < 2 * len; i += blockDim.x) smem[i] = 0.0;
+// Carve and zero the exchange buffers.
+__device__ __forceinline__ SmallShared setup_shared(double* smem, int len) {
+  for (int i = threadIdx.x; i < 2 * len; i += kSmallThreads) smem[i] = 0.0;
   __syncthreads();
-  return SmallShared{smem + pad, smem + len + pad, smem + 2 * len, 0};
+  return SmallShared{smem, smem + len, smem + 2 * len, 0};
 }
 
-template <int W, int R, bool ST, int OCC>
+template <class Op, int OCC>
 __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(SmallArgs a) {
+  constexpr int R = Op::R;
   extern __shared__ __align__(16) double smem[];
   const mlmcp_task t = a.tasks[blockIdx.x];
   {
@@ -390,17 +511,19 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
     __syncthreads();
     if (skip) return;
   }
-  SmallShared sh = setup_shared<R>(smem, a.pad);
+  const PatternArgs& pa = a.pa;
+  SmallShared sh = setup_shared(smem, a.buf_doubles);
   const double* Ms = a.M + (int64_t)t.sample * a.nnz;
   const double* Ks = a.K + (int64_t)t.sample * a.nnz;
-  Rows<W, R, ST> rw;
-  rw.load(a.row_ptr, a.col, a.st, Ms, Ks, t.dt, a.N);
+  Op op;
+  op.load(pa, Ms, Ks, t.dt);
   double x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int row = row_of<R>(r);
-    x[r] = row_ok<R>(r, a.N) ? a.xbuf[t.x_in + row] : 0.0;
-    if (t.traj >= 0 && row_ok<R>(r, a.N)) a.xbuf[t.traj + row] = x[r];
+    const bool v = Op::ok(r, pa);
+    const int rw = v ? Op::row(r, pa) : 0;
+    x[r] = v ? a.xbuf[t.x_in + rw] : 0.0;
+    if (t.traj >= 0 && v) a.xbuf[t.traj + rw] = x[r];
   }
   int iters = 0;
   int code = MLMCP_ST_OK;
@@ -409,24 +532,23 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   for (int step = 0; step < t.n_steps; ++step) {
     const int64_t g = t.k0 + step + 1;
     const double sf = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
-    code = ie_step(rw, x, a.N, sf, t.dt, a.row_ptr, a.st, Ms, a.profile, a.rtol2, a.max_it, sh,
-                   iters);
+    code = ie_step<Op>(op, x, pa, sf, t.dt, Ms, a.profile, a.rtol2, a.max_it, sh, iters);
     if (code != MLMCP_ST_OK) { fail_step = step; break; }
     if (t.traj >= 0) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (row_ok<R>(r, a.N)) a.xbuf[t.traj + (int64_t)(step + 1) * a.N + row_of<R>(r)] = x[r];
+        if (Op::ok(r, pa)) a.xbuf[t.traj + (int64_t)(step + 1) * pa.N + Op::row(r, pa)] = x[r];
     }
     if (t.qoi_mode == MLMCP_QOI_SUM_ENERGY && g > t.qoi_from)
-      acc += block_energy(rw, x, a.N, a.row_ptr, a.st, Ks, sh);
+      acc += block_energy<Op>(op, x, pa, Ks, sh);
   }
   if (t.x_out >= 0) {
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      if (row_ok<R>(r, a.N)) a.xbuf[t.x_out + row_of<R>(r)] = x[r];
+      if (Op::ok(r, pa)) a.xbuf[t.x_out + Op::row(r, pa)] = x[r];
   }
   if (code == MLMCP_ST_OK && t.qoi_mode == MLMCP_QOI_FINAL_ENERGY && t.qoi_slot >= 0)
-    acc = block_energy(rw, x, a.N, a.row_ptr, a.st, Ks, sh);
+    acc = block_energy<Op>(op, x, pa, Ks, sh);
   if (threadIdx.x == 0) {
     if (t.qoi_slot >= 0 && t.qoi_mode != MLMCP_QOI_NONE) a.qoi[t.qoi_slot] = acc;
     if (a.iters != nullptr && t.slot >= 0) a.iters[t.slot] = iters;
@@ -438,12 +560,9 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
 }
 
 struct CoarseArgs {
-  int S, k, m, N;
+  int S, k, m;
   int64_t nnz;
-  const int32_t* row_ptr;
-  const int32_t* col;
-  StencilArgs st;
-  int pad;
+  PatternArgs pa;
   const double* M;
   const double* K;
   const double* profile;
@@ -457,20 +576,23 @@ struct CoarseArgs {
   int32_t* iters;
   int32_t* status;
   int32_t* active;
+  int buf_doubles;
 };
 
 // parareal.py:168-178 for one sample per CTA.
-template <int W, int R, bool ST, int OCC>
+template <class Op, int OCC>
 __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(CoarseArgs a) {
+  constexpr int R = Op::R;
   extern __shared__ __align__(16) double smem[];
   const int s = blockIdx.x;
   if (a.active[s] == 0) return;
-  SmallShared sh = setup_shared<R>(smem, a.pad);
+  const PatternArgs& pa = a.pa;
+  SmallShared sh = setup_shared(smem, a.buf_doubles);
   const double* Ms = a.M + (int64_t)s * a.nnz;
   const double* Ks = a.K + (int64_t)s * a.nnz;
-  Rows<W, R, ST> rw;
-  rw.load(a.row_ptr, a.col, a.st, Ms, Ks, a.dt, a.N);
-  const int64_t N = a.N;
+  Op op;
+  op.load(pa, Ms, Ks, a.dt);
+  const int64_t N = pa.N;
   double* U = a.U + (int64_t)s * (a.m + 1) * N;
   const double* F = a.F + (int64_t)s * (a.m + 1) * N;
   double* C = a.C + (int64_t)s * a.m * N;
@@ -478,13 +600,13 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   double x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    const int i = row_of<R>(r);
-    const bool ok = row_ok<R>(r, a.N);
+    const bool v = Op::ok(r, pa);
+    const int i = v ? Op::row(r, pa) : 0;
     if (a.k == 1) {
-      x[r] = ok ? U[i] : 0.0;
+      x[r] = v ? U[i] : 0.0;
     } else {
-      x[r] = ok ? F[(a.k - 1) * N + i] : 0.0;  // freeze U_{k-1} = F_{k-1}
-      if (ok) U[(a.k - 1) * N + i] = x[r];
+      x[r] = v ? F[(a.k - 1) * N + i] : 0.0;  // freeze U_{k-1} = F_{k-1}
+      if (v) U[(a.k - 1) * N + i] = x[r];
     }
   }
   for (int n = a.k; n < a.m; ++n) {
@@ -493,8 +615,8 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
     for (int step = 0; step < steps; ++step) {
       const int64_t g = k0 + step + 1;
       const double sf = sin(__dmul_rn(a.omega, grid_time(a.t0, g, a.dt)));
-      const int code = ie_step(rw, x, a.N, sf, a.dt, a.row_ptr, a.st, Ms, a.profile, a.rtol2,
-                               a.max_it, sh, iters);
+      const int code = ie_step<Op>(op, x, pa, sf, a.dt, Ms, a.profile, a.rtol2, a.max_it, sh,
+                                   iters);
       if (code != MLMCP_ST_OK) {
         if (threadIdx.x == 0) {
           write_status(a.status, s, code, step, n, a.k);
@@ -506,8 +628,8 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const int i = row_of<R>(r);
-      if (!row_ok<R>(r, a.N)) continue;
+      if (!Op::ok(r, pa)) continue;
+      const int i = Op::row(r, pa);
       if (a.k == 1) {
         U[n * N + i] = x[r];
         C[(n - 1) * N + i] = x[r];
@@ -522,10 +644,11 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   }
   if (a.k > 1) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int i = row_of<R>(r);
-      if (row_ok<R>(r, a.N)) U[a.m * N + i] = F[a.m * N + i];
-    }
+    for (int r = 0; r < R; ++r)
+      if (Op::ok(r, pa)) {
+        const int i = Op::row(r, pa);
+        U[a.m * N + i] = F[a.m * N + i];
+      }
   }
   if (threadIdx.x == 0 && a.iters != nullptr) a.iters[s] += iters;
   (void)Ks;
@@ -536,45 +659,68 @@ inline int rows_per_thread(int N) {
   if (N <= 2 * kSmallThreads) return 2;
   return 4;
 }
-inline int block_threads(int, int) { return kSmallThreads; }
-inline size_t small_smem(int padN, int pad) {
-  return (size_t)(2 * (padN + 2 * pad) + 2 * kMaxWarps * 4) * sizeof(double);
+inline size_t small_smem(int buf_doubles) {
+  return (size_t)(2 * buf_doubles + 2 * kMaxWarps * 4) * sizeof(double);
 }
 
-template <template <int, int, bool, int> class Launch, typename Args>
+// kernel variant: 0 auto (grid > stencil > csr), 1 no grid tiling (tests / A-B)
+int variant_pref() {
+  static const int v = [] {
+    const char* e = getenv("MLMCP_SMALL_VARIANT");
+    return e ? atoi(e) : 0;
+  }();
+  return v;
+}
+int occ_pref() {
+  static const int o = [] {
+    const char* e = getenv("MLMCP_SMALL_OCC");
+    return (e && atoi(e) == 2) ? 2 : 1;
+  }();
+  return o;
+}
+
+template <template <class, int> class Launch, typename Args>
 int dispatch(const Ctx* ctx, Args& a, unsigned grid, cudaStream_t stream) {
   const int N = ctx->n;
+  PatternArgs& pa = a.pa;
+  pa.N = N;
+  pa.row_ptr = ctx->row_ptr;
+  pa.col = ctx->col;
+  pa.pad = 0;
+  pa.spos = nullptr;
+  pa.gpos = nullptr;
+  pa.wd = pa.gh = 0;
+  const int occ = occ_pref();
+  if (ctx->grid_wd > 0 && variant_pref() != 1) {
+    pa.wd = ctx->grid_wd;
+    pa.gh = ctx->grid_h;
+    pa.gpos = ctx->grid_pos;
+    a.buf_doubles = GridOp::buffer_doubles(0);
+    const size_t smem = small_smem(a.buf_doubles);
+    return occ == 2 ? Launch<GridOp, 2>::run(a, grid, kSmallThreads, smem, stream)
+                    : Launch<GridOp, 1>::run(a, grid, kSmallThreads, smem, stream);
+  }
   const int R = rows_per_thread(N);
-  const int nt = block_threads(N, R);
   const bool st = ctx->stencil_w > 0;
   const int W = st ? ctx->stencil_w : ctx->max_row_nnz;
-  a.pad = st ? ctx->stencil_pad : 0;
   if (st) {
+    pa.pad = ctx->stencil_pad;
+    pa.spos = ctx->stencil_pos;
     for (int k = 0; k < kMaxNz; ++k) {
-      a.st.off[k] = k < W ? ctx->stencil_off[k] : 0;
-      a.st.off8[k] = a.st.off[k] * 8;
+      pa.off[k] = k < W ? ctx->stencil_off[k] : 0;
+      pa.off8[k] = pa.off[k] * 8;
     }
-    a.st.pos = ctx->stencil_pos;
-  } else {
-    a.st.pos = nullptr;
   }
-  const size_t smem = small_smem(R * nt, a.pad);
+  a.buf_doubles = R * kSmallThreads + 2 * pa.pad;
+  const size_t smem = small_smem(a.buf_doubles);
   if (smem > 200 * 1024) {
     set_error("SM-resident path: shared-memory footprint too large for this pattern");
     return MLMCP_EINVAL;
   }
-  // two CTAs per SM for the stencil path (128 registers per thread) unless
-  // MLMCP_SMALL_OCC=1 asks for one (255 registers, no spills)
-  static const int occ = [] {
-    const char* e = getenv("MLMCP_SMALL_OCC");
-    return (e && atoi(e) == 1) ? 1 : 2;
-  }();
-#define MLMCP_CASE_R(WW, RR)                                                       \
-  if (W == WW && R == RR) {                                                        \
-    if (!st) return Launch<WW, RR, false, 1>::run(a, grid, nt, smem, stream);      \
-    if (RR == 4 && occ == 2) return Launch<WW, RR, true, 2>::run(a, grid, nt, smem, stream); \
-    return Launch<WW, RR, true, 1>::run(a, grid, nt, smem, stream);                \
-  }
+#define MLMCP_CASE_R(WW, RR)                                                              \
+  if (W == WW && R == RR)                                                                 \
+    return st ? Launch<StencilOp<WW, RR>, 1>::run(a, grid, kSmallThreads, smem, stream)   \
+              : Launch<CsrOp<WW, RR>, 1>::run(a, grid, kSmallThreads, smem, stream);
 #define MLMCP_CASE(WW) MLMCP_CASE_R(WW, 1) MLMCP_CASE_R(WW, 2) MLMCP_CASE_R(WW, 4)
   MLMCP_CASE(1) MLMCP_CASE(2) MLMCP_CASE(3) MLMCP_CASE(4)
   MLMCP_CASE(5) MLMCP_CASE(6) MLMCP_CASE(7) MLMCP_CASE(8)
@@ -584,25 +730,25 @@ int dispatch(const Ctx* ctx, Args& a, unsigned grid, cudaStream_t stream) {
   return MLMCP_EINVAL;
 }
 
-template <int W, int R, bool ST, int OCC>
+template <class Op, int OCC>
 struct LaunchPropagate {
   static int run(const SmallArgs& a, unsigned grid, int nt, size_t smem, cudaStream_t st) {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(small_propagate_kernel<W, R, ST, OCC>,
+      cudaFuncSetAttribute(small_propagate_kernel<Op, OCC>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    small_propagate_kernel<W, R, ST, OCC><<<grid, nt, smem, st>>>(a);
+    small_propagate_kernel<Op, OCC><<<grid, nt, smem, st>>>(a);
     MLMCP_LAUNCH_CHECK("small_propagate_kernel");
     return MLMCP_OK;
   }
 };
 
-template <int W, int R, bool ST, int OCC>
+template <class Op, int OCC>
 struct LaunchCoarse {
   static int run(const CoarseArgs& a, unsigned grid, int nt, size_t smem, cudaStream_t st) {
     if (smem > 48 * 1024)
-      cudaFuncSetAttribute(small_coarse_kernel<W, R, ST, OCC>,
+      cudaFuncSetAttribute(small_coarse_kernel<Op, OCC>,
                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    small_coarse_kernel<W, R, ST, OCC><<<grid, nt, smem, st>>>(a);
+    small_coarse_kernel<Op, OCC><<<grid, nt, smem, st>>>(a);
     MLMCP_LAUNCH_CHECK("small_coarse_kernel");
     return MLMCP_OK;
   }
@@ -618,10 +764,7 @@ int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double
   SmallArgs a{};
   a.tasks = tasks;
   a.n_tasks = n_tasks;
-  a.N = ctx->n;
   a.nnz = ctx->nnz;
-  a.row_ptr = ctx->row_ptr;
-  a.col = ctx->col;
   a.M = M;
   a.K = K;
   a.profile = profile;
@@ -646,10 +789,7 @@ int small_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const 
   a.S = S;
   a.k = k;
   a.m = m;
-  a.N = ctx->n;
   a.nnz = ctx->nnz;
-  a.row_ptr = ctx->row_ptr;
-  a.col = ctx->col;
   a.M = M;
   a.K = K;
   a.profile = profile;
