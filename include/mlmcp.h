@@ -96,8 +96,14 @@ typedef struct mlmcp_task {
   int32_t group;    /* index into `active` (Parareal sample), -1: always */
   int32_t slot;     /* index into iters / status                         */
   int32_t tag;      /* copied to status[4*slot+2..3] on failure          */
-  int32_t reserved;
+  int32_t flags;    /* MLMCP_TASK_*                                      */
 } mlmcp_task;
+
+/* task flags */
+#define MLMCP_TASK_NO_EXTRAPOLATION 1 /* PCG starts from a_n (one-step method:
+                                         bitwise semigroup); default:
+                                         polynomial extrapolation of the task's
+                                         state history (fewer PCG iterations) */
 
 /* ---- library ---------------------------------------------------------- */
 int mlmcp_abi_version(void);

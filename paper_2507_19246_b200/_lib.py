@@ -33,13 +33,14 @@ STATUS_NAMES = {ST_NOCONV: "PCG did not converge within max_it",
 STATUS_INTS = 4
 
 QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY = 0, 1, 2
+TASK_NO_EXTRAPOLATION = 1
 
 # mlmcp_task (88 bytes, natural alignment)
 TASK_DTYPE = np.dtype([
     ("sample", np.int32), ("n_steps", np.int32), ("k0", np.int64), ("dt", np.float64),
     ("t_base", np.float64), ("x_in", np.int64), ("x_out", np.int64), ("traj", np.int64),
     ("qoi_slot", np.int32), ("qoi_mode", np.int32), ("qoi_from", np.int64),
-    ("group", np.int32), ("slot", np.int32), ("tag", np.int32), ("reserved", np.int32),
+    ("group", np.int32), ("slot", np.int32), ("tag", np.int32), ("flags", np.int32),
 ], align=True)
 assert TASK_DTYPE.itemsize == 88
 

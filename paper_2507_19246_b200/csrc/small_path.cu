@@ -365,7 +365,8 @@ struct StateHistory {
   double h1[R];   // a_n       (after advance(); the right-hand side uses it)
   double h2[R];   // a_{n-1}
   int order;      // usable extrapolation order
-  __device__ explicit StateHistory(const double (&x)[R]) : order(0) {
+  int max_order;  // 0 disables extrapolation (MLMCP_TASK_NO_EXTRAPOLATION)
+  __device__ StateHistory(const double (&x)[R], int max_ord) : order(0), max_order(max_ord) {
 #pragma unroll
     for (int r = 0; r < R; ++r) h1[r] = h2[r] = x[r];
   }
@@ -379,7 +380,7 @@ struct StateHistory {
       h2[r] = h1[r];
       h1[r] = an;
     }
-    order = order < 2 ? order + 1 : 2;
+    order = order < max_order ? order + 1 : max_order;
   }
 };
 
@@ -563,7 +564,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   int code = MLMCP_ST_OK;
   int fail_step = 0;
   double acc = 0.0;
-  StateHistory<R> hist(x);
+  StateHistory<R> hist(x, (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : 2);
   for (int step = 0; step < t.n_steps; ++step) {
     const int64_t g = t.k0 + step + 1;
     const double sf = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
@@ -648,7 +649,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   for (int n = a.k; n < a.m; ++n) {
     const int steps = a.slice_steps[n - 1];
     const int64_t k0 = a.slice_k0[n - 1];
-    StateHistory<R> hist(x);
+    StateHistory<R> hist(x, 2);
     for (int step = 0; step < steps; ++step) {
       const int64_t g = k0 + step + 1;
       const double sf = sin(__dmul_rn(a.omega, grid_time(a.t0, g, a.dt)));

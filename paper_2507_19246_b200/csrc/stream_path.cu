@@ -600,7 +600,7 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
       t.group = s;
       t.slot = s;
       t.tag = n;
-      t.reserved = 0;
+      t.flags = 0;
     }
     MLMCP_CUDA_CHECK(cudaMemcpyAsync(dtasks, h.data(), sizeof(mlmcp_task) * S,
                                      cudaMemcpyHostToDevice, stream));

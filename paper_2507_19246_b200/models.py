@@ -197,6 +197,15 @@ class EddyCurrentFamily:
                                     self.path)
         return self._solver
 
+    def _pr_stream(self, device):
+        import torch
+        st = getattr(self, "_side_stream", None)
+        if st is None:
+            lo, hi = torch.cuda.Stream.priority_range()
+            st = torch.cuda.Stream(device=device, priority=hi)
+            self._side_stream = st
+        return st
+
     def _level_index(self, level) -> int:
         if isinstance(level, LevelSpec):
             return level.level
@@ -263,7 +272,10 @@ class EddyCurrentFamily:
         if pr_level is not None:
             cfg = parareal_cfg.with_dt_fine(self.hierarchy[levels[pr_level]].dt)
             a, b = offs[pr_level], offs[pr_level + 1]
-            side = torch.cuda.Stream(device=sol.device) if (concurrent and sol.sys.sm_resident) else main
+            # Parareal is the critical path (K dependent rounds); its stream gets
+            # the higher priority so its CTAs are dispatched ahead of the big
+            # sequential launch as SMs free up
+            side = self._pr_stream(sol.device) if (concurrent and sol.sys.sm_resident) else main
             if side is not main:
                 side.wait_stream(main)
             with torch.cuda.stream(side):

@@ -154,6 +154,7 @@ def parareal_solve(model, t0: float, t1: float, x0, cfg: PararealConfig, pool=No
     tasks["traj"] = 2 * uf + (n_idx - 1) * steps * N
     tasks["group"] = 0
     tasks["slot"] = n_idx - 1
+    tasks["flags"] = _lib.TASK_NO_EXTRAPOLATION
     for k in range(1, k_max + 1):
         sysd.parareal_coarse(S, k, m, dev.M, dev.K, dev.profile, dev.omega, cfg.dt_coarse, t0,
                              ck0_d, cst_d, rtol, max_it, U, F, C, citers, status, active)

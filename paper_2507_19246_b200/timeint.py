@@ -157,6 +157,7 @@ class _ModelOnDevice:
         tasks["x_in"] = 0
         tasks["x_out"] = N
         tasks["slot"] = 0
+        tasks["flags"] = _lib.TASK_NO_EXTRAPOLATION   # one-step method, as the reference
         if keep_traj:
             tasks["traj"] = 2 * N
         size = 2 * N + ((n_steps + 1) * N if keep_traj else 0)
