@@ -76,8 +76,9 @@ def check_parareal_case(name, path="auto"):
     assert np.max(np.abs(U - g["boundary"])) <= 1e-8 * scale
     d = pr.defects.cpu().numpy()
     for i, k in enumerate(g["k_used"]):
-        # early defects are O(1e-2..1e-7); compare them relatively
-        np.testing.assert_allclose(d[i, :k - 1], g["defects"][i, :k - 1], rtol=1e-5)
+        # early defects are O(1e-2..1e-7) jumps between iterates whose states carry
+        # the PCG tolerance (~1e-11 relative after a slice): relative + absolute slack
+        np.testing.assert_allclose(d[i, :k - 1], g["defects"][i, :k - 1], rtol=1e-5, atol=1e-10)
         assert d[i, k - 1] <= tol
 
 
