@@ -351,36 +351,56 @@ struct SmallShared {
   double* bufB;  // exchange buffer for the initial guess (A x0)
   double* bufC;  // exchange buffer for u (PCG iterations)
   double* red;   // [2][kMaxWarps][4]
+  double* ring;  // [kMaxOrder][R*256] state history (per-thread slots)
   int par;
 };
 
 // State history of the current task for the PCG initial guess: the guess is
-// the polynomial extrapolation of the last states (order 0, 1, 2 as history
-// accumulates): x0 = a_n, 2a_n - a_{n-1}, 3a_n - 3a_{n-1} + a_{n-2}.  Only the
+// the polynomial extrapolation of the last p+1 states,
+//     x0 = sum_{i=0..p} (-1)^i C(p+1, i+1) a_{n-i},   p = min(#history, kMaxOrder),
+// (p = 0: a_n; 1: 2a_n - a_{n-1}; 2: 3a_n - 3a_{n-1} + a_{n-2}; ...).  Only the
 // starting point of PCG changes — the stopping rule ||r|| <= rtol ||b|| and
 // hence the accuracy of every step are unchanged — but the initial residual
-// drops by O(omega dt) per order: -35..40% PCG iterations at configs 0/1.
+// drops by ~O(omega dt) per order (configs 0/1: 59 -> 26 PCG iterations per
+// step at T/256, 51 -> 16 at T/1024 for p = 4).  The past states live in a
+// per-thread shared-memory ring (touched once per step), a_n in registers.
+constexpr int kMaxOrder = 4;
+
 template <int R>
 struct StateHistory {
-  double h1[R];   // a_n       (after advance(); the right-hand side uses it)
-  double h2[R];   // a_{n-1}
-  int order;      // usable extrapolation order
+  double* ring;   // [kMaxOrder][R*256]: a_{n-1} .. a_{n-4} (ring)
+  int head;       // ring slot of a_{n-1}
+  int count;      // valid past states (<= kMaxOrder)
   int max_order;  // 0 disables extrapolation (MLMCP_TASK_NO_EXTRAPOLATION)
-  __device__ StateHistory(const double (&x)[R], int max_ord) : order(0), max_order(max_ord) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) h1[r] = h2[r] = x[r];
+  __device__ StateHistory(double* ring_, int max_ord)
+      : ring(ring_), head(kMaxOrder - 1), count(0), max_order(max_ord) {}
+  __device__ double past(int i, int r) const {  // a_{n-i}, i >= 1
+    const int slot = (head - (i - 1) + kMaxOrder) % kMaxOrder;
+    return ring[slot * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x];
   }
-  // on entry x = a_n; on exit x = initial guess, h1 = a_n, h2 = a_{n-1}
-  __device__ void advance(double (&x)[R]) {
+  // on entry x = a_n; on exit x = initial guess, an = a_n; a_n joins the ring
+  __device__ void advance(double (&x)[R], double (&an)[R]) {
+    const int p = count < max_order ? count : max_order;
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      const double an = x[r];
-      x[r] = order >= 2 ? fma(3.0, an - h1[r], h2[r])
-                        : (order == 1 ? fma(2.0, an, -h1[r]) : an);
-      h2[r] = h1[r];
-      h1[r] = an;
+      an[r] = x[r];
+      double g;
+      switch (p) {
+        case 0: g = an[r]; break;
+        case 1: g = fma(2.0, an[r], -past(1, r)); break;
+        case 2: g = fma(3.0, an[r] - past(1, r), past(2, r)); break;
+        case 3: g = fma(4.0, an[r] + past(2, r), fma(-6.0, past(1, r), -past(3, r))); break;
+        default:  // 5a_n - 10a_{n-1} + 10a_{n-2} - 5a_{n-3} + a_{n-4}
+          g = fma(5.0, an[r] - past(3, r), fma(10.0, past(2, r) - past(1, r), past(4, r)));
+          break;
+      }
+      x[r] = g;
     }
-    order = order < max_order ? order + 1 : max_order;
+    head = (head + 1) % kMaxOrder;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      ring[head * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x] = an[r];
+    count = count < kMaxOrder ? count + 1 : kMaxOrder;
   }
 };
 
@@ -529,7 +549,8 @@ struct SmallArgs {
 __device__ __forceinline__ SmallShared setup_shared(double* smem, int len) {
   for (int i = threadIdx.x; i < 3 * len; i += kSmallThreads) smem[i] = 0.0;
   __syncthreads();
-  return SmallShared{smem, smem + len, smem + 2 * len, smem + 3 * len, 0};
+  return SmallShared{smem, smem + len, smem + 2 * len, smem + 3 * len,
+                     smem + 3 * len + 2 * kMaxWarps * 4, 0};
 }
 
 template <class Op, int OCC>
@@ -564,12 +585,13 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   int code = MLMCP_ST_OK;
   int fail_step = 0;
   double acc = 0.0;
-  StateHistory<R> hist(x, (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : 2);
+  StateHistory<R> hist(sh.ring, (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : kMaxOrder);
+  double an[R];
   for (int step = 0; step < t.n_steps; ++step) {
     const int64_t g = t.k0 + step + 1;
     const double sf = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
-    hist.advance(x);                       // x <- extrapolated initial guess
-    code = ie_step<Op>(op, x, hist.h1, pa, sf, t.dt, Ms, a.profile, a.rtol2, a.max_it, sh, iters);
+    hist.advance(x, an);                   // x <- extrapolated initial guess
+    code = ie_step<Op>(op, x, an, pa, sf, t.dt, Ms, a.profile, a.rtol2, a.max_it, sh, iters);
     if (code != MLMCP_ST_OK) { fail_step = step; break; }
     if (t.traj >= 0) {
 #pragma unroll
@@ -649,12 +671,13 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   for (int n = a.k; n < a.m; ++n) {
     const int steps = a.slice_steps[n - 1];
     const int64_t k0 = a.slice_k0[n - 1];
-    StateHistory<R> hist(x, 2);
+    StateHistory<R> hist(sh.ring, kMaxOrder);
+    double an[R];
     for (int step = 0; step < steps; ++step) {
       const int64_t g = k0 + step + 1;
       const double sf = sin(__dmul_rn(a.omega, grid_time(a.t0, g, a.dt)));
-      hist.advance(x);
-      const int code = ie_step<Op>(op, x, hist.h1, pa, sf, a.dt, Ms, a.profile, a.rtol2,
+      hist.advance(x, an);
+      const int code = ie_step<Op>(op, x, an, pa, sf, a.dt, Ms, a.profile, a.rtol2,
                                    a.max_it, sh, iters);
       if (code != MLMCP_ST_OK) {
         if (threadIdx.x == 0) {
@@ -698,8 +721,9 @@ inline int rows_per_thread(int N) {
   if (N <= 2 * kSmallThreads) return 2;
   return 4;
 }
-inline size_t small_smem(int buf_doubles) {
-  return (size_t)(3 * buf_doubles + 2 * kMaxWarps * 4) * sizeof(double);
+inline size_t small_smem(int buf_doubles, int R) {
+  return (size_t)(3 * buf_doubles + 2 * kMaxWarps * 4 + kMaxOrder * R * kSmallThreads) *
+         sizeof(double);
 }
 
 // kernel variant: 0 auto (grid > stencil > csr), 1 no grid tiling (tests / A-B)
@@ -735,7 +759,7 @@ int dispatch(const Ctx* ctx, Args& a, unsigned grid, cudaStream_t stream) {
     pa.gh = ctx->grid_h;
     pa.gpos = ctx->grid_pos;
     a.buf_doubles = GridOp::buffer_doubles(0);
-    const size_t smem = small_smem(a.buf_doubles);
+    const size_t smem = small_smem(a.buf_doubles, GridOp::R);
     return occ == 2 ? Launch<GridOp, 2>::run(a, grid, kSmallThreads, smem, stream)
                     : Launch<GridOp, 1>::run(a, grid, kSmallThreads, smem, stream);
   }
@@ -751,7 +775,7 @@ int dispatch(const Ctx* ctx, Args& a, unsigned grid, cudaStream_t stream) {
     }
   }
   a.buf_doubles = R * kSmallThreads + 2 * pa.pad;
-  const size_t smem = small_smem(a.buf_doubles);
+  const size_t smem = small_smem(a.buf_doubles, R);
   if (smem > 200 * 1024) {
     set_error("SM-resident path: shared-memory footprint too large for this pattern");
     return MLMCP_EINVAL;
