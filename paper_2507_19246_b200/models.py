@@ -183,7 +183,7 @@ class EddyCurrentFamily:
     qoi: QoIKind = QoIKind.MAGNETIC_ENERGY_T
     avg_window: float = 0.0
     device: object = None
-    rtol: float = 1e-12
+    rtol: float = 1e-13
     max_it: int = 20000
     path: str = "auto"
     _solver: object = field(default=None, repr=False, compare=False)

@@ -106,7 +106,7 @@ def raise_parareal_status(coarse_status: np.ndarray, fine_status: np.ndarray):
 
 
 def parareal_solve(model, t0: float, t1: float, x0, cfg: PararealConfig, pool=None, *,
-                   rtol: float = 1e-12, max_it: int = 20000, device=None) -> PararealResult:
+                   rtol: float = 1e-13, max_it: int = 20000, device=None) -> PararealResult:
     """parareal.py:121-220 for one duck-typed model, on the device."""
     import torch
 

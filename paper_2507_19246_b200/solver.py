@@ -25,7 +25,7 @@ from . import _lib, fe
 from .engine import DeviceSystem, F64, I32, kl_sigma, new_tasks, tasks_to_device
 from .timeint import SingularSystemError, step_count
 
-DEFAULT_RTOL = 1e-12
+DEFAULT_RTOL = 1e-13   # ||r||_2 <= 1e-13 ||b||_2, the stated PCG tolerance
 DEFAULT_MAX_IT = 20000
 
 

@@ -9,7 +9,7 @@ Same names, argument meaning and errors as the reference:
   ``propagate``               timeint.py:114-128
 
 Difference by design: each step's linear solve is Jacobi-PCG on the device
-(tolerance ``rtol``, default 1e-12 — the stated parity tolerance) instead of a
+(tolerance ``rtol``, default 1e-13 — the stated PCG tolerance) instead of a
 dense LU factorisation.  The model is duck-typed like the reference
 (``mass``, ``stiffness`` as dense or scipy-sparse SPD operators with <= 8
 entries per row of their union pattern; ``forcing`` of the form
@@ -179,7 +179,7 @@ class _ModelOnDevice:
 
 
 def implicit_euler_solve(model, t0: float, t1: float, dt: float, x0,
-                         time_origin: float | None = None, *, rtol: float = 1e-12,
+                         time_origin: float | None = None, *, rtol: float = 1e-13,
                          max_it: int = 20000, device=None) -> Trajectory:
     """timeint.py:88-111 on the GPU; returns the full trajectory."""
     if t1 <= t0:
@@ -199,7 +199,7 @@ def implicit_euler_solve(model, t0: float, t1: float, dt: float, x0,
 
 
 def propagate(model, t_start: float, t_end: float, dt: float, x0,
-              time_origin: float | None = None, *, rtol: float = 1e-12, max_it: int = 20000,
+              time_origin: float | None = None, *, rtol: float = 1e-13, max_it: int = 20000,
               device=None) -> np.ndarray:
     """timeint.py:114-128 on the GPU; x0 itself for an empty span."""
     x0 = np.asarray(x0, dtype=float)

@@ -2,7 +2,7 @@
 known-answer tests and the reference's own synthetic bar model (golden
 fixtures written by oracle/pin_reference.py from the unmodified reference).
 
-Tolerances: the device solves each step with Jacobi-PCG at rtol = 1e-12
+Tolerances: the device solves each step with Jacobi-PCG at rtol = 1e-13
 (stated parity tolerance); the reference uses dense LU.  States agree to
 ~1e-11 relative; KATs with exact answers are checked to 1e-12.
 """

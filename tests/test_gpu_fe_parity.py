@@ -3,7 +3,7 @@ unmodified reference integrators on the oracle's FE models) and vs the live
 CPU oracle.
 
 Parity bar (BASELINE.json north_star): per-sample QoI within 1e-8 relative;
-Parareal K equal per sample.  PCG tolerance: ||r||_2 <= 1e-12 ||b||_2.
+Parareal K equal per sample.  PCG tolerance: ||r||_2 <= 1e-13 ||b||_2.
 """
 
 import numpy as np
