@@ -100,10 +100,31 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
 
 
 def draw_level(uncertain, seed: int, level: int, indices) -> np.ndarray:
-    """Host draws for sample keys (seed, level, k), k in ``indices`` (1-based)."""
-    rows = [draw_parameters(uncertain, RandomStream(seed, level, int(k))).values for k in indices]
-    dim = getattr(uncertain, "dim", None) or len(uncertain.nominal.values)
-    return np.array(rows, dtype=float).reshape(len(rows), dim)
+    """Host draws for sample keys (seed, level, k), k in ``indices`` (1-based).
+
+    Row k equals ``draw_parameters(uncertain, RandomStream(seed, level, k)).values``
+    bitwise (same generator, same call, same arithmetic, models.py:305-318); the
+    per-sample ParameterVector validation is done once on the whole block."""
+    from .models import GaussianInput, ParameterVector
+    idx = [int(k) for k in indices]
+    if isinstance(uncertain, GaussianInput):
+        out = np.empty((len(idx), uncertain.dim))
+        for i, k in enumerate(idx):
+            out[i] = RandomStream(seed, level, k).generator().standard_normal(uncertain.dim)
+        return out
+    nominal = uncertain.nominal.values
+    h = uncertain.relative_halfwidth
+    out = np.empty((len(idx), len(nominal)))
+    if h == 0.0:
+        out[:] = nominal
+        return out
+    lo = nominal * (1.0 - h)
+    hi = nominal * (1.0 + h)
+    for i, k in enumerate(idx):
+        out[i] = RandomStream(seed, level, k).generator().uniform(lo, hi)
+    if len(idx) and not np.all(out > 0.0):
+        ParameterVector(uncertain.nominal.model_id, out[np.argmin(out.min(axis=1))])  # raises
+    return out
 
 
 def coupled_sample(family, params, level: LevelSpec, hierarchy, parareal_cfg=None):
