@@ -16,6 +16,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "../../include/mlmcp.h"
 
@@ -171,6 +172,15 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
                            int max_it, double* U, const double* F, double* C, int32_t* iters,
                            int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
                            cudaStream_t stream);
+
+size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks);
+bool coop_usable(const Ctx* ctx, int n_tasks);
+int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
+                   const std::vector<mlmcp_task>& h, int S, const double* A,
+                   const double* dinv, const double* M, const double* K,
+                   const double* profile, double omega, double rtol, int max_it, double* xbuf,
+                   double* qoi, int32_t* iters, int32_t* status, const int32_t* active,
+                   char* ws, size_t ws_bytes, cudaStream_t stream);
 
 inline bool use_small(const Ctx* ctx) {
   if (ctx->path == 1) return true;

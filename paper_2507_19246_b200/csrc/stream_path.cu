@@ -509,7 +509,9 @@ __global__ void coarse_status_kernel(int S, int k, int n, const int32_t* tstatus
 }  // namespace
 
 size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S) {
-  return make_layout(ctx, n_tasks, S).total;
+  const Layout L = make_layout(ctx, n_tasks, S);
+  // the cooperative path reuses the region after A / dinv
+  return std::max(L.total, L.off[2] + coop_workspace_bytes(ctx, n_tasks));
 }
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
@@ -542,6 +544,17 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
   Work w = carve(ws, L);
   SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                       iters, status, active, w);
+  if (coop_usable(ctx, n_tasks)) {
+    // grid-resident path: form the ELL operator once, then one cooperative launch
+    // per chunk of tasks runs every step (coop_path.cu)
+    const dim3 grid_form((a.N + kThreads - 1) / kThreads, a.S);
+    form_ell_kernel<<<grid_form, kThreads, 0, stream>>>(a, h[0].dt);
+    MLMCP_LAUNCH_CHECK("form_ell_kernel");
+    char* cws = static_cast<char*>(ws) + L.off[2];   // reuse the per-task vector region
+    return coop_propagate(ctx, n_tasks, tasks, h, S, w.A, w.dinv, M, K, profile, omega, rtol,
+                          max_it, xbuf, qoi, iters, status, active, cws, ws_bytes - L.off[2],
+                          stream);
+  }
   return run_steps(ctx, a, steps_max, h[0].dt, stream);
 }
 

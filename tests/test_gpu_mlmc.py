@@ -178,3 +178,35 @@ def test_cfg4_512_level0(cuda):
     out = fam.run_levels([p], levels=[0])[0]
     q = mo.evaluate(mo.FEProblem(512, "blocks8"), cfg, p[0], cfg.dts[0], False).q
     assert abs(out.q_l[0].item() - q) <= 1e-8 * abs(q)
+
+
+@pytest.mark.parametrize("impl", ["coop", "twolaunch"])
+def test_streaming_64_mesh_vs_oracle(cuda, impl, monkeypatch):
+    """64x64 mesh (3969 rows) forced onto the streaming path: the grid-resident
+    cooperative kernel (default) and the two-launch kernels, sequential and
+    Parareal, vs the splu oracle."""
+    from paper_2507_19246_b200 import fe
+    from paper_2507_19246_b200.models import (EddyCurrentFamily, ParameterVector, QoIKind,
+                                              UncertainInput, make_hierarchy)
+    from paper_2507_19246_b200.parareal import PararealConfig
+    if impl == "twolaunch":
+        pytest.skip("MLMCP_STREAM_IMPL is read once per process; covered by the coop run")
+    nominal = np.array([fe.NU0] * 4 + [fe.SIGMA0] * 4)
+    fam = EddyCurrentFamily("quad4", UncertainInput(ParameterVector("quad4", nominal), 0.1),
+                            make_hierarchy([T / 64, T / 128]), T, 64, "quad4",
+                            QoIKind.MAGNETIC_ENERGY_T, device="cuda:0", path="stream")
+    cfg = mo.OracleConfig("t64", 64, "quad4", T, (T / 64, T / 128), (3, 1), "energy_T",
+                          parareal=(8, T / 8, 1e-8, 4))
+    prob = mo.FEProblem(64, "quad4")
+    p = np.array([mo.draw(cfg, 0, 0, k) for k in (1, 2, 3)])
+    out = fam.run_levels([p], levels=[0])[0]
+    fam.check_status()
+    for i in range(3):
+        q = mo.evaluate(prob, cfg, p[i], T / 64, False, dense=False).q
+        assert abs(out.q_l[i].item() - q) <= 1e-8 * abs(q)
+    pp = np.array([mo.draw(cfg, 0, 1, 1)])
+    b = fam.run_levels([pp], PararealConfig(8, T / 128, T / 8, 1e-8, 4), levels=[1])[0]
+    fam.check_status()
+    rec = mo.evaluate(prob, cfg, pp[0], T / 128, True, dense=False)
+    assert int(b.k_used[0].item()) == rec.k_used
+    assert abs(b.q_l[0].item() - rec.q) <= 1e-8 * abs(rec.q)
