@@ -62,6 +62,9 @@ struct CoopArgs {
   double* part;     // [T][nb_task][4] per-CTA partial sums
   int32_t* first_blk;  // [T] first CTA of task t
   int32_t* n_blk;      // [T] CTAs of task t
+  int off[kMaxNz];     // stencil offsets (col - row) of the operator slots
+  int pad;             // zero rows before / after each task's exchange vector
+  int ld;              // exchange-vector stride per task = N + 2*pad
 };
 
 // per-task state kept (identically) by every CTA in shared memory
@@ -119,37 +122,58 @@ __device__ void cta_partials(double (&lo)[NV], double (&hi)[NV], int t_lo, int t
   __syncthreads();
 }
 
-// totals[t][k] = sum_j part[t][j][k] in fixed order (every CTA computes the same)
+// totals[t][k] = sum_j part[t][j][k] in a fixed order (every CTA computes the
+// same): warp w reduces tasks w, w+8, ...; lane l sums partials l, l+32, ...
+// sequentially, then a fixed xor butterfly.
 template <int NV>
 __device__ void task_totals(const CoopArgs& a, double* tot) {
-  for (int t = threadIdx.x; t < a.T; t += kCoopThreads) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int t = warp; t < a.T; t += kCoopThreads / 32) {
     double s[NV];
 #pragma unroll
     for (int k = 0; k < NV; ++k) s[k] = 0.0;
     const int nb = a.n_blk[t];
-    for (int j = 0; j < nb; ++j) {
+    for (int j = lane; j < nb; j += 32) {
       const double* p = a.part + ((int64_t)t * a.nb_task + j) * 4;
 #pragma unroll
       for (int k = 0; k < NV; ++k) s[k] += __ldcg(p + k);
     }
 #pragma unroll
-    for (int k = 0; k < NV; ++k) tot[t * 4 + k] = s[k];
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) s[k] += __shfl_xor_sync(0xffffffffu, s[k], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) tot[t * 4 + k] = s[k];
+    }
   }
   __syncthreads();
 }
 
-// y = A v for slot r from the exchange buffer `buf` (ELL, per-sample values)
-template <int R>
-__device__ __forceinline__ double ell_apply(const CoopArgs& a, const Slots<R>& sl, int r,
-                                            const double* buf) {
+// y = A v for slot r from the exchange buffer `buf`: operator in stencil-slot
+// layout A[s][j][i] (coefficient of offset off[j], 0 if absent), neighbour
+// addresses computed (no column loads); padded buffers absorb the boundary.
+template <int R, int W>
+__device__ __forceinline__ double sten_apply(const CoopArgs& a, const Slots<R>& sl, int r,
+                                             const double* buf) {
   const int t = sl.task[r], i = sl.row[r];
-  const int s = a.tasks[t].sample;
-  const double* As = a.A + (int64_t)s * a.W * a.N;
-  const double* v = buf + (int64_t)t * a.N;
+  const double* As = a.A + (int64_t)a.tasks[t].sample * W * a.N + i;
+  const double* v = buf + (int64_t)t * a.ld + a.pad + i;
+  double av[W], vv[W];
+#pragma unroll
+  for (int j = 0; j < W; ++j) {
+    av[j] = __ldg(As + (int64_t)j * a.N);
+    vv[j] = __ldcg(v + a.off[j]);
+  }
   double acc = 0.0;
-  for (int j = 0; j < a.W; ++j)
-    acc = fma(__ldg(As + (int64_t)j * a.N + i), __ldcg(v + __ldg(a.ell_col + j * a.N + i)), acc);
+#pragma unroll
+  for (int j = 0; j < W; ++j) acc = fma(av[j], vv[j], acc);
   return acc;
+}
+
+__device__ __forceinline__ double* xrow(const CoopArgs& a, double* buf, int t, int i) {
+  return buf + (int64_t)t * a.ld + a.pad + i;
 }
 
 // y = B v for slot r with B given by per-sample CSR values (M or K)
@@ -158,14 +182,14 @@ __device__ __forceinline__ double csr_apply(const CoopArgs& a, const Slots<R>& s
                                             const double* vals, const double* buf) {
   const int t = sl.task[r], i = sl.row[r];
   const double* Bs = vals + (int64_t)a.tasks[t].sample * a.nnz;
-  const double* v = buf + (int64_t)t * a.N;
+  const double* v = buf + (int64_t)t * a.ld + a.pad;
   double acc = 0.0;
   for (int q = __ldg(a.row_ptr + i); q < __ldg(a.row_ptr + i + 1); ++q)
     acc = fma(__ldg(Bs + q), __ldcg(v + __ldg(a.col + q)), acc);
   return acc;
 }
 
-template <int R>
+template <int R, int W>
 __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
   cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double csm[];
@@ -217,7 +241,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       const TaskState& st = ts[t];
       const int64_t o = (int64_t)t * a.N + i;
       const double an = sl.x[r];
-      a.Xb[o] = an;
+      *xrow(a, a.Xb, t, i) = an;
       const bool run = st.live && step < a.tasks[t].n_steps;
       const int p = (!run || (a.tasks[t].flags & MLMCP_TASK_NO_EXTRAPOLATION)) ? 0
                                                                              : min(st.order, kCoopOrder);
@@ -227,7 +251,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       else if (p == 2) gss = fma(3.0, an - past(1), past(2));
       else if (p == 3) gss = fma(4.0, an + past(2), fma(-6.0, past(1), -past(3)));
       else if (p >= 4) gss = fma(5.0, an - past(3), fma(10.0, past(2) - past(1), past(4)));
-      a.Gb[o] = gss;
+      *xrow(a, a.Gb, t, i) = gss;
       sl.x[r] = gss;
     }
     grid.sync();
@@ -242,7 +266,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         const int i = sl.row[r];
         const double sf = sin(__dmul_rn(a.omega, grid_time(tk.t_base, tk.k0 + step + 1, tk.dt)));
         const double mx = csr_apply(a, sl, r, a.M, a.Xb);
-        const double ax = ell_apply(a, sl, r, a.Gb);
+        const double ax = sten_apply<R, W>(a, sl, r, a.Gb);
         const double b = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, __ldg(a.profile + i))));
         res = b - ax;
         u = sl.dinv[r] * res;
@@ -250,7 +274,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         acc[3] += b * b;
       }
       sl.r[r] = res;
-      if (t >= 0) a.Ub[(int64_t)t * a.N + sl.row[r]] = u;
+      if (t >= 0) *xrow(a, a.Ub, t, sl.row[r]) = u;
     }
     grid.sync();
     // first SpMV: w = A u; gamma, delta, rho, bb
@@ -259,7 +283,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       const int t = sl.task[r];
       if (t < 0 || !ts[t].live || step >= a.tasks[t].n_steps) continue;
       const double u = sl.dinv[r] * sl.r[r];
-      const double w = ell_apply(a, sl, r, a.Ub);
+      const double w = sten_apply<R, W>(a, sl, r, a.Ub);
       double* acc = (t == t_lo) ? lo4 : hi4;
       acc[0] += sl.r[r] * u;
       acc[1] += w * u;
@@ -311,7 +335,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       for (int r = 0; r < R; ++r) {
         const int t = sl.task[r];
         if (t < 0) continue;
-        a.Ub[(int64_t)t * a.N + sl.row[r]] = ts[t].done ? 0.0 : sl.dinv[r] * sl.r[r];
+        *xrow(a, a.Ub, t, sl.row[r]) = ts[t].done ? 0.0 : sl.dinv[r] * sl.r[r];
       }
       grid.sync();
       double wv[R];
@@ -321,7 +345,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         wv[r] = 0.0;
         if (t < 0 || ts[t].done) continue;
         const double u = sl.dinv[r] * sl.r[r];
-        wv[r] = ell_apply(a, sl, r, a.Ub);
+        wv[r] = sten_apply<R, W>(a, sl, r, a.Ub);
         double* acc = (t == t_lo) ? lo3 : hi3;
         acc[0] += sl.r[r] * u;
         acc[1] += wv[r] * u;
@@ -374,7 +398,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       const int i = sl.row[r];
       const int64_t o = (int64_t)t * a.N + i;
       if (ts[t].live && step < tk.n_steps) {
-        a.ring[(int64_t)(step & (kCoopOrder - 1)) * TN + o] = a.Xb[o];   // a_n joins the ring
+        a.ring[(int64_t)(step & (kCoopOrder - 1)) * TN + o] = *xrow(a, a.Xb, t, i);  // a_n joins the ring
         if (tk.traj >= 0) a.xbuf[tk.traj + (int64_t)(step + 1) * a.N + i] = sl.x[r];
       }
     }
@@ -384,7 +408,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
     if (want_energy) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
-        if (sl.task[r] >= 0) a.Xb[(int64_t)sl.task[r] * a.N + sl.row[r]] = sl.x[r];
+        if (sl.task[r] >= 0) *xrow(a, a.Xb, sl.task[r], sl.row[r]) = sl.x[r];
       grid.sync();
       double lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -415,7 +439,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
     const bool inactive = a.active != nullptr && tk.group >= 0 && a.active[tk.group] == 0 &&
                           ts[t].code == MLMCP_ST_OK;
     if (tk.x_out >= 0 && !inactive) a.xbuf[tk.x_out + sl.row[r]] = sl.x[r];
-    a.Xb[(int64_t)t * a.N + sl.row[r]] = sl.x[r];
+    *xrow(a, a.Xb, t, sl.row[r]) = sl.x[r];
   }
   bool want_final = false;
   for (int t = 0; t < a.T; ++t)
@@ -460,6 +484,7 @@ inline size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 
 int coop_rows_per_thread(int N) {
   if (N >= 8 * kCoopThreads) return 8;
+  // (the stencil-slot operator layout is required: see coop_usable)
   if (N >= 4 * kCoopThreads) return 4;
   return 0;  // too small for this path (rows of > 2 tasks per CTA)
 }
@@ -481,26 +506,27 @@ CoopPlan coop_plan(const Ctx* ctx, int n_tasks) {
   p.chunk = (int)std::min<long>(n_tasks, cap / ctx->n);
   if (p.chunk < 1) { p.R = 0; return p; }
   const size_t TN = (size_t)p.chunk * ctx->n;
+  const size_t TL = (size_t)p.chunk * (ctx->n + 2 * ctx->stencil_pad);
   const int nb_task = ctx->n / (kCoopThreads * p.R) + 2;
-  p.bytes = al256(3 * TN * 8) + al256(kCoopOrder * TN * 8) +
+  p.bytes = al256(3 * TL * 8) + al256(kCoopOrder * TN * 8) +
             al256((size_t)p.chunk * nb_task * 4 * 8) + al256((size_t)p.chunk * 2 * 4);
   return p;
 }
 
-template <int R>
+template <int R, int W>
 int launch_coop(CoopArgs& a, int grid, cudaStream_t stream) {
   const size_t smem = (64 + 4 * (size_t)a.T) * 8 + sizeof(TaskState) * (size_t)a.T;
   if (smem > 48 * 1024)
-    cudaFuncSetAttribute(coop_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(coop_kernel<R, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   int per_sm = 0;
-  MLMCP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_kernel<R>,
+  MLMCP_CUDA_CHECK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coop_kernel<R, W>,
                                                                  kCoopThreads, smem));
   if (per_sm < 1) {
     set_error("cooperative PCG kernel does not fit one CTA per SM");
     return MLMCP_EINVAL;
   }
   void* args[] = {&a};
-  MLMCP_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)coop_kernel<R>, dim3(grid),
+  MLMCP_CUDA_CHECK(cudaLaunchCooperativeKernel((void*)coop_kernel<R, W>, dim3(grid),
                                                dim3(kCoopThreads), args, smem, stream));
   count_launch();
   return MLMCP_OK;
@@ -513,7 +539,7 @@ size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks) { return coop_plan(ctx,
 bool coop_usable(const Ctx* ctx, int n_tasks) {
   const char* e = getenv("MLMCP_STREAM_IMPL");
   if (e && atoi(e) == 1) return false;   // force the two-launch streaming kernels
-  return coop_plan(ctx, n_tasks).R > 0;
+  return ctx->stencil_w > 0 && coop_plan(ctx, n_tasks).R > 0;
 }
 
 int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
@@ -536,12 +562,15 @@ int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
   for (int c0 = 0; c0 < n_tasks; c0 += plan.chunk) {
     const int T = std::min(plan.chunk, n_tasks - c0);
     const size_t TN = (size_t)T * N;
+    const int pad = ctx->stencil_pad;
+    const size_t TL = (size_t)T * (N + 2 * pad);
     char* b = ws;
     CoopArgs a{};
     a.Xb = reinterpret_cast<double*>(b);
-    a.Gb = a.Xb + TN;
-    a.Ub = a.Gb + TN;
-    b += al256(3 * TN * 8);
+    a.Gb = a.Xb + TL;
+    a.Ub = a.Gb + TL;
+    MLMCP_CUDA_CHECK(cudaMemsetAsync(a.Xb, 0, 3 * TL * 8, stream));   // zero pads
+    b += al256(3 * TL * 8);
     a.ring = reinterpret_cast<double*>(b);
     b += al256(kCoopOrder * TN * 8);
     a.part = reinterpret_cast<double*>(b);
@@ -560,10 +589,13 @@ int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
     a.n_blk = blk + T;
     a.T = T;
     a.N = N;
-    a.W = ctx->max_row_nnz;
     a.R = plan.R;
     a.S = S;
     a.nb_task = nb_task;
+    a.pad = pad;
+    a.ld = N + 2 * pad;
+    for (int k = 0; k < kMaxNz; ++k) a.off[k] = k < ctx->stencil_w ? ctx->stencil_off[k] : 0;
+    a.W = ctx->stencil_w;
     a.tasks = tasks_d + c0;
     a.A = A;
     a.dinv = dinv;
@@ -582,7 +614,14 @@ int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
     a.iters = iters;
     a.status = status;
     a.active = const_cast<int32_t*>(active);
-    int rc = plan.R == 8 ? launch_coop<8>(a, plan.grid, stream) : launch_coop<4>(a, plan.grid, stream);
+    int rc = MLMCP_EINVAL;
+    set_error("unsupported stencil width for the cooperative path");
+#define MLMCP_COOP_W(WW)                                                              \
+    if (a.W == WW)                                                                    \
+      rc = plan.R == 8 ? launch_coop<8, WW>(a, plan.grid, stream)                     \
+                       : launch_coop<4, WW>(a, plan.grid, stream);
+    MLMCP_COOP_W(3) MLMCP_COOP_W(5) MLMCP_COOP_W(7)
+#undef MLMCP_COOP_W
     if (rc != MLMCP_OK) return rc;
     // the host vector hb must outlive the async copy: synchronise the copy
     MLMCP_CUDA_CHECK(cudaStreamSynchronize(stream));

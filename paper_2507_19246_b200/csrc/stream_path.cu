@@ -55,7 +55,8 @@ struct Layout {
 };
 
 Layout make_layout(const Ctx* ctx, int T, int S) {
-  const size_t N = ctx->n, W = ctx->max_row_nnz, T_ = T, S_ = S;
+  // operator slots: ELL width, or the stencil width for the cooperative path
+  const size_t N = ctx->n, W = std::max(ctx->max_row_nnz, ctx->stencil_w), T_ = T, S_ = S;
   const size_t nblk = (N + kThreads - 1) / kThreads;
   size_t sizes[12] = {S_ * W * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
                       T_ * N * 8,     T_ * N * 8, T_ * nblk * 4 * 8, T_ * kTD * 8,
@@ -174,7 +175,7 @@ __global__ void form_ell_kernel(SArgs a, double dt) {
     double v = 0.0;
     if (q >= 0) {
       v = op_entry(Ms[q], Ks[q], dt);
-      if (a.ell_col[j * a.N + i] == i) diag = v;
+      if (a.col[q] == i) diag = v;
     }
     As[(int64_t)j * a.N + i] = v;
   }
@@ -548,8 +549,12 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
     // grid-resident path: form the ELL operator once, then one cooperative launch
     // per chunk of tasks runs every step (coop_path.cu)
     const dim3 grid_form((a.N + kThreads - 1) / kThreads, a.S);
-    form_ell_kernel<<<grid_form, kThreads, 0, stream>>>(a, h[0].dt);
-    MLMCP_LAUNCH_CHECK("form_ell_kernel");
+    SArgs as = a;                       // stencil-slot layout: slot j <-> offset j
+    as.ell_pos = ctx->stencil_pos;
+    as.W = ctx->stencil_w;
+    as.ell_col = nullptr;
+    form_ell_kernel<<<grid_form, kThreads, 0, stream>>>(as, h[0].dt);
+    MLMCP_LAUNCH_CHECK("form_ell_kernel(stencil)");
     char* cws = static_cast<char*>(ws) + L.off[2];   // reuse the per-task vector region
     return coop_propagate(ctx, n_tasks, tasks, h, S, w.A, w.dinv, M, K, profile, omega, rtol,
                           max_it, xbuf, qoi, iters, status, active, cws, ws_bytes - L.off[2],
