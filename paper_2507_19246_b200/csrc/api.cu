@@ -302,6 +302,11 @@ int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
     cudaError_t e = cudaMallocHost(reinterpret_cast<void**>(&c->host_counters), 64);
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
   }
+  if (!rc) {
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&c->grid_bar), 2 * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned int));
+    if (e != cudaSuccess) rc = cuda_fail(e, "grid barrier allocation");
+  }
   if (rc) {
     mlmcp_ctx_destroy(c);
     return rc;
@@ -319,6 +324,7 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->ell_pos);
   cudaFree(c->stencil_pos);
   cudaFree(c->grid_pos);
+  cudaFree(c->grid_bar);
   cudaFree(c->cptr);
   cudaFree(c->celem);
   cudaFree(c->cmw);

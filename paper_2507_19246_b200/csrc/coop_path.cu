@@ -62,6 +62,7 @@ struct CoopArgs {
   double* part;     // [T][nb_task][4] per-CTA partial sums
   int32_t* first_blk;  // [T] first CTA of task t
   int32_t* n_blk;      // [T] CTAs of task t
+  unsigned int* bar;   // [2] grid barrier: arrival count, generation
   int off[kMaxNz];     // stencil offsets (col - row) of the operator slots
   int pad;             // zero rows before / after each task's exchange vector
   int ld;              // exchange-vector stride per task = N + 2*pad
@@ -75,6 +76,28 @@ struct TaskState {
   int live;   // task still running (not failed / inactive)
   int zero;   // b == 0 this step: a_{n+1} = 0
 };
+
+// Sense-reversing grid barrier (all CTAs are co-resident: cooperative launch).
+// One atomic per CTA, spin on a generation word in L2; release/acquire fences
+// order the exchange-buffer writes before / reads after it (readers use ld.cg).
+__device__ __forceinline__ void grid_barrier(unsigned int* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned int* gen = bar + 1;
+    const unsigned int g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      atomicExch(bar, 0u);
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) {
+      }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
 
 template <int R>
 struct Slots {
@@ -191,7 +214,6 @@ __device__ __forceinline__ double csr_apply(const CoopArgs& a, const Slots<R>& s
 
 template <int R, int W>
 __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
-  cg::grid_group grid = cg::this_grid();
   extern __shared__ __align__(16) double csm[];
   double* red = csm;                         // [8 warps][8]
   double* tot = csm + 64;                    // [T][4]
@@ -254,7 +276,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       *xrow(a, a.Gb, t, i) = gss;
       sl.x[r] = gss;
     }
-    grid.sync();
+    grid_barrier(a.bar);
     // ---- b = M a_n + dt sf prof, r = b - A x0, u = D r
     double lo4[4] = {0, 0, 0, 0}, hi4[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -276,7 +298,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       sl.r[r] = res;
       if (t >= 0) *xrow(a, a.Ub, t, sl.row[r]) = u;
     }
-    grid.sync();
+    grid_barrier(a.bar);
     // first SpMV: w = A u; gamma, delta, rho, bb
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -292,7 +314,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       sl.s[r] = w;
     }
     cta_partials<4>(lo4, hi4, t_lo, t_hi, a, red);
-    grid.sync();
+    grid_barrier(a.bar);
     task_totals<4>(a, tot);
     // decide per task (identical in every CTA); a block-local copy of the state
     for (int t = threadIdx.x; t < a.T; t += kCoopThreads) {
@@ -337,7 +359,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         if (t < 0) continue;
         *xrow(a, a.Ub, t, sl.row[r]) = ts[t].done ? 0.0 : sl.dinv[r] * sl.r[r];
       }
-      grid.sync();
+      grid_barrier(a.bar);
       double wv[R];
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -353,7 +375,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       }
       double lo4b[4] = {lo3[0], lo3[1], lo3[2], 0.0}, hi4b[4] = {hi3[0], hi3[1], hi3[2], 0.0};
       cta_partials<4>(lo4b, hi4b, t_lo, t_hi, a, red);
-      grid.sync();
+      grid_barrier(a.bar);
       task_totals<3>(a, tot);
       for (int t = threadIdx.x; t < a.T; t += kCoopThreads) {
         TaskState& st = ts[t];
@@ -409,7 +431,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
         if (sl.task[r] >= 0) *xrow(a, a.Xb, sl.task[r], sl.row[r]) = sl.x[r];
-      grid.sync();
+      grid_barrier(a.bar);
       double lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
 #pragma unroll
       for (int r = 0; r < R; ++r) {
@@ -418,7 +440,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         (t == t_lo ? lo : hi)[0] += sl.x[r] * csr_apply(a, sl, r, a.K, a.Xb);
       }
       cta_partials<4>(lo, hi, t_lo, t_hi, a, red);
-      grid.sync();
+      grid_barrier(a.bar);
       task_totals<1>(a, tot);
       if (blockIdx.x == 0)
         for (int t = threadIdx.x; t < a.T; t += kCoopThreads) {
@@ -428,8 +450,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
             a.qoi[tk.qoi_slot] += 0.5 * tot[t * 4 + 0];   // qoi zeroed by the caller
         }
     }
-    grid.sync();    // Xb / Gb / Ub are rewritten at the next step start
-  }
+      }
   // ---- outputs
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -445,7 +466,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
   for (int t = 0; t < a.T; ++t)
     want_final |= ts[t].live && a.tasks[t].qoi_mode == MLMCP_QOI_FINAL_ENERGY && a.tasks[t].qoi_slot >= 0;
   if (want_final) {
-    grid.sync();
+    grid_barrier(a.bar);
     double lo[4] = {0, 0, 0, 0}, hi[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -454,7 +475,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       (t == t_lo ? lo : hi)[0] += sl.x[r] * csr_apply(a, sl, r, a.K, a.Xb);
     }
     cta_partials<4>(lo, hi, t_lo, t_hi, a, red);
-    grid.sync();
+    grid_barrier(a.bar);
     task_totals<1>(a, tot);
     if (blockIdx.x == 0)
       for (int t = threadIdx.x; t < a.T; t += kCoopThreads)
@@ -594,6 +615,7 @@ int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
     a.nb_task = nb_task;
     a.pad = pad;
     a.ld = N + 2 * pad;
+    a.bar = ctx->grid_bar;
     for (int k = 0; k < kMaxNz; ++k) a.off[k] = k < ctx->stencil_w ? ctx->stencil_off[k] : 0;
     a.W = ctx->stencil_w;
     a.tasks = tasks_d + c0;

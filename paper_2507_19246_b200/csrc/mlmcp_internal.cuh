@@ -58,6 +58,8 @@ struct Ctx {
   double* ckw = nullptr;
   // pinned host counters for the streaming path
   int32_t* host_counters = nullptr;
+  // grid-barrier words of the cooperative path (zeroed at creation)
+  unsigned int* grid_bar = nullptr;
 };
 
 void set_error(const std::string& msg);
