@@ -303,8 +303,8 @@ int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
     if (e != cudaSuccess) rc = cuda_fail(e, "cudaMallocHost");
   }
   if (!rc) {
-    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&c->grid_bar), 2 * sizeof(unsigned int));
-    if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, 2 * sizeof(unsigned int));
+    cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&c->grid_bar), (1 + 1024) * sizeof(unsigned int));
+    if (e == cudaSuccess) e = cudaMemset(c->grid_bar, 0, (1 + 1024) * sizeof(unsigned int));
     if (e != cudaSuccess) rc = cuda_fail(e, "grid barrier allocation");
   }
   if (rc) {
