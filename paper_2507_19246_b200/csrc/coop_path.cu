@@ -575,9 +575,16 @@ int launch_coop(CoopArgs& a, int grid, cudaStream_t stream) {
 size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks) { return coop_plan(ctx, n_tasks).bytes; }
 
 bool coop_usable(const Ctx* ctx, int n_tasks) {
+  // MLMCP_STREAM_IMPL: 1 two-launch kernels, 2 cooperative, default auto
   const char* e = getenv("MLMCP_STREAM_IMPL");
-  if (e && atoi(e) == 1) return false;   // force the two-launch streaming kernels
-  return ctx->stencil_w > 0 && coop_plan(ctx, n_tasks).R > 0;
+  const int impl = e ? atoi(e) : 0;
+  if (impl == 1 || ctx->stencil_w == 0) return false;
+  const CoopPlan p = coop_plan(ctx, n_tasks);
+  if (p.R == 0) return false;
+  // auto: the grid-resident kernel is barrier-latency bound (~16 us per PCG
+  // iteration); it wins when the whole batch fits one register-resident chunk.
+  // Larger batches amortise better in the two-launch streaming kernels.
+  return impl == 2 || p.chunk >= n_tasks;
 }
 
 int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
