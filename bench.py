@@ -366,7 +366,7 @@ def main():
                       "l2": "flushed between steps (512 MiB write)", "parallelism": f"samples x{world}"},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": ncu_traffic(),
-                        "kernel": "small_propagate_kernel<7,4> (all sequential solves of all levels, one launch)",
+                        "kernel": "small_propagate_kernel<GridOp,2> (all sequential solves of all levels, one launch)",
                         "algorithmic_bytes": f"{its} PCG iterations x (8 nnz + 56 N) = {its} x {b_it} B",
                         "kernel_ms": seq_kernel_ms, "peak_kind": peak_kind,
                         "note": "32x32 operators live in registers/SMEM (SM-resident CTA per task): "

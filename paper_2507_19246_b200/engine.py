@@ -125,9 +125,15 @@ class DeviceSystem:
 
     # ------------------------------------------------------------ K1
     def assemble(self, S: int, sigma: torch.Tensor, sigma_stride: int, sigma_index,
-                 nu: torch.Tensor, nu_stride: int, nu_index, stream=None):
-        M = torch.empty((S, self.nnz), dtype=F64, device=self.device)
-        K = torch.empty((S, self.nnz), dtype=F64, device=self.device)
+                 nu: torch.Tensor, nu_stride: int, nu_index, stream=None, out=None):
+        if out is not None:
+            M, K = out
+            if M.shape != (S, self.nnz) or K.shape != (S, self.nnz) or not (
+                    M.is_contiguous() and K.is_contiguous()):
+                raise ValueError("assemble(out=...) needs contiguous [S, nnz] tensors")
+        else:
+            M = torch.empty((S, self.nnz), dtype=F64, device=self.device)
+            K = torch.empty((S, self.nnz), dtype=F64, device=self.device)
         check(self.lib.mlmcp_assemble(self.ctx, S, ptr(sigma), int(sigma_stride), ptr(sigma_index),
                                       ptr(nu), int(nu_stride), ptr(nu_index), ptr(M), ptr(K),
                                       stream_handle(stream)), "mlmcp_assemble")

@@ -36,7 +36,7 @@ from .models import EvalRecord, LevelSpec, draw_parameters
 
 __all__ = ["RandomStream", "LevelStats", "EstimatorResult", "FixedSamples", "WarmupPolicy",
            "coupled_sample", "mc_estimate", "optimal_allocation", "mlmc_estimate",
-           "draw_level", "shard_range"]
+           "draw_level", "shard_range", "LazyDraw"]
 
 
 class RandomStream:
@@ -125,6 +125,25 @@ def draw_level(uncertain, seed: int, level: int, indices) -> np.ndarray:
     if len(idx) and not np.all(out > 0.0):
         ParameterVector(uncertain.nominal.model_id, out[np.argmin(out.min(axis=1))])  # raises
     return out
+
+
+class LazyDraw:
+    """Level draws evaluated on first use (``len`` is known up front), so a
+    batched family can launch the finest level before the host draws the
+    rest (host RNG overlaps device work)."""
+
+    def __init__(self, n: int, fn):
+        self.n = int(n)
+        self._fn = fn
+        self._v = None
+
+    def __len__(self):
+        return self.n
+
+    def get(self) -> np.ndarray:
+        if self._v is None:
+            self._v = self._fn()
+        return self._v
 
 
 def coupled_sample(family, params, level: LevelSpec, hierarchy, parareal_cfg=None):
@@ -223,8 +242,9 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
     t_start = time.perf_counter()
     ranges = [shard_range(n, rank, world) for n in counts]
     if draws is None:
-        draws = [draw_level(family.uncertain, seed, lvl, range(a + 1, b + 1))
-                 for lvl, (a, b) in enumerate(ranges)]
+        draws = [LazyDraw(b - a, (lambda lvl=lvl, a=a, b=b: draw_level(
+            family.uncertain, seed, lvl, range(a + 1, b + 1))))
+            for lvl, (a, b) in enumerate(ranges)]
     batches = family.run_levels(draws, parareal_cfg)
     dev = device
     if dev is None and hasattr(family, "solver"):

@@ -151,6 +151,7 @@ class LinearToyFamily:
         levels = list(range(len(draws))) if levels is None else levels
         out = []
         for lvl, p in zip(levels, draws):
+            p = p.get() if hasattr(p, "get") else p
             xi = torch.as_tensor(np.asarray(p, dtype=float)[:, 0] if len(p) else np.zeros(0))
             ql = xi * (1.0 + self.hierarchy[lvl].dt)
             qm = xi * (1.0 + self.hierarchy[lvl - 1].dt) if lvl > 0 else torch.zeros_like(xi)
@@ -244,37 +245,38 @@ class EddyCurrentFamily:
         top = len(self.hierarchy) - 1
         sizes = [len(d) for d in draws]
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-        if params_dev is not None:
-            params = params_dev                   # already resident in HBM
-        else:
-            allp = np.concatenate([np.asarray(d, dtype=float).reshape(len(d), -1) for d in draws],
-                                  axis=0) if sum(sizes) else np.zeros((0, fe.n_params(self.layout)))
-            params = torch.from_numpy(allp).pin_memory().to(sol.device, non_blocking=True)
-        M, K = sol.assemble(params)
-        jobs, where = [], []
-        pr_level = None
-        for i, lvl in enumerate(levels):
-            rows = np.arange(offs[i], offs[i + 1])
-            if len(rows) == 0:
-                continue
-            dt = self.hierarchy[lvl].dt
-            if parareal_cfg is not None and lvl == top:
-                pr_level = i
+        nnz = sol.mesh.nnz
+        M = torch.empty((int(offs[-1]), nnz), dtype=torch.float64, device=sol.device)
+        K = torch.empty_like(M)
+
+        def assemble_level(i):
+            a, b = int(offs[i]), int(offs[i + 1])
+            if b == a:
+                return
+            if params_dev is not None:
+                p = params_dev[a:b]                # already resident in HBM
             else:
-                jobs.append(self._seq_job(rows, dt))
-                where.append((i, "hi", dt))
-            if lvl > 0:
-                dtm = self.hierarchy[lvl - 1].dt
-                jobs.append(self._seq_job(rows, dtm))
-                where.append((i, "lo", dtm))
+                d = draws[i].get() if hasattr(draws[i], "get") else draws[i]
+                host = np.ascontiguousarray(np.asarray(d, dtype=float).reshape(b - a, -1))
+                p = torch.from_numpy(host).pin_memory().to(sol.device, non_blocking=True)
+            sol.assemble(p, out=(M[a:b], K[a:b]))
+
+        pr_level = None
+        if parareal_cfg is not None:
+            for i, lvl in enumerate(levels):
+                if lvl == top and sizes[i] > 0:
+                    pr_level = i
         main = torch.cuda.current_stream()
         pr = None
+        side = main
         if pr_level is not None:
+            # the finest level's Parareal is the critical path: assemble and
+            # launch it first (host draws of the other levels overlap with it)
+            assemble_level(pr_level)
             cfg = parareal_cfg.with_dt_fine(self.hierarchy[levels[pr_level]].dt)
             a, b = offs[pr_level], offs[pr_level + 1]
-            # Parareal is the critical path (K dependent rounds); its stream gets
-            # the higher priority so its CTAs are dispatched ahead of the big
-            # sequential launch as SMs free up
+            # Parareal gets the higher-priority stream so its CTAs are dispatched
+            # ahead of the big sequential launch as SMs free up
             side = self._pr_stream(sol.device) if (concurrent and sol.sys.sm_resident) else main
             if side is not main:
                 side.wait_stream(main)
@@ -282,6 +284,22 @@ class EddyCurrentFamily:
                 pr = sol.run_parareal(M[a:b], K[a:b], 0.0, self.horizon, cfg.num_subintervals,
                                       cfg.dt_fine, cfg.dt_coarse, cfg.tolerance, cfg.k_max,
                                       stream=side)
+        for i in range(len(levels)):
+            if i != pr_level:
+                assemble_level(i)
+        jobs, where = [], []
+        for i, lvl in enumerate(levels):
+            rows = np.arange(offs[i], offs[i + 1])
+            if len(rows) == 0:
+                continue
+            dt = self.hierarchy[lvl].dt
+            if i != pr_level:
+                jobs.append(self._seq_job(rows, dt))
+                where.append((i, "hi", dt))
+            if lvl > 0:
+                dtm = self.hierarchy[lvl - 1].dt
+                jobs.append(self._seq_job(rows, dtm))
+                where.append((i, "lo", dtm))
         res = sol.run_sequential(M, K, jobs) if jobs else []
         if pr is not None and side is not main:
             main.wait_stream(side)

@@ -114,26 +114,27 @@ class FESolver:
             self.n_regions = len(fe.conducting_mask(layout))
 
     # ------------------------------------------------------------ K1
-    def assemble(self, params: torch.Tensor, stream=None):
-        """Per-sample CSR values (M, K) [S, nnz] from parameters [S, P]."""
+    def assemble(self, params: torch.Tensor, stream=None, out=None):
+        """Per-sample CSR values (M, K) [S, nnz] from parameters [S, P]
+        (written into ``out`` = (M, K) slices when given)."""
         params = params.to(device=self.device, dtype=F64).contiguous()
         S = params.shape[0]
         if S == 0:
             empty = torch.empty((0, self.mesh.nnz), dtype=F64, device=self.device)
-            return empty, empty.clone()
+            return (empty, empty.clone()) if out is None else out
         if params.shape[1] != fe.n_params(self.layout):
             raise ValueError(f"layout {self.layout} takes {fe.n_params(self.layout)} parameters, "
                              f"got {params.shape[1]}")
         if self.layout == "kl64":
             sigma = kl_sigma(params, self.kl_basis, float(np.log(fe.SIGMA0)), fe.KL_SCALE, stream)
             return self.sys.assemble(S, sigma, self.mesh.n_elem, None, self.nu_const, 0,
-                                     self.nu_index, stream)
+                                     self.nu_index, stream, out)
         R = self.n_regions
         # sigma masked to 0 in non-conducting regions *after* drawing (ParameterVector
         # positivity, models.py:69-74); a plain elementwise product (plumbing)
         nu = params[:, :R].contiguous()
         sigma = (params[:, R:2 * R] * self.mask).contiguous()
-        return self.sys.assemble(S, sigma, R, self.region, nu, R, self.region, stream)
+        return self.sys.assemble(S, sigma, R, self.region, nu, R, self.region, stream, out)
 
     # ------------------------------------------------------------ sequential
     def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):

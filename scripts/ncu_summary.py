@@ -43,7 +43,8 @@ def main(rep, out, top=False):
             f = float(x["value"].replace(",", ""))
             u = x["unit"].lower()
             mult = {"byte": 1, "kbyte": 1e3, "mbyte": 1e6, "gbyte": 1e9, "nsecond": 1e-9,
-                    "usecond": 1e-6, "msecond": 1e-3, "second": 1}.get(u, 1)
+                    "usecond": 1e-6, "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6,
+                    "ms": 1e-3, "s": 1}.get(u, 1)
             return f * mult / scale
         rd, wr = num("dram__bytes_read.sum", 1), num("dram__bytes_write.sum", 1)
         d["dram_bytes_per_launch"] = (rd or 0) + (wr or 0)
