@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 1
+#define MLMCP_ABI_VERSION 2
 
 /* return codes */
 #define MLMCP_OK 0
@@ -64,11 +64,18 @@ extern "C" {
 #define MLMCP_ST_NOCONV 1    /* PCG hit max_it       -> SingularSystemError */
 #define MLMCP_ST_BREAKDOWN 2 /* PCG curvature <= 0    -> SingularSystemError */
 #define MLMCP_ST_NONFINITE 3 /* non-finite residual   -> SingularSystemError */
+#define MLMCP_ST_SINGULAR 4  /* zero pivot (direct)   -> SingularSystemError */
 
 /* QoI modes of a task */
 #define MLMCP_QOI_NONE 0
 #define MLMCP_QOI_FINAL_ENERGY 1 /* qoi[slot] = 1/2 x_T^T K x_T               */
 #define MLMCP_QOI_SUM_ENERGY 2   /* qoi[slot] = sum_{g > qoi_from} W(x_g)     */
+/* ELECTRICAL_ENERGY models.py:337-339 without the amplitude*dt factor (applied
+ * by the caller): qoi[slot] = sum_{g > qoi_from} sin(omega t_g) x_g[qoi_index] */
+#define MLMCP_QOI_ELECTRICAL 3
+/* MEAN_JOULE_LOSS models.py:340-343 without the 1/(dt*T) factor:
+ * qoi[slot] = sum_{g > qoi_from} (x_g - x_{g-1})^T M (x_g - x_{g-1})        */
+#define MLMCP_QOI_JOULE 4
 
 typedef struct mlmcp_ctx mlmcp_ctx;
 
@@ -79,7 +86,7 @@ typedef struct mlmcp_ctx mlmcp_ctx;
  * (timeint.py:78-85,108-110: the grid is anchored at an origin so that a
  * sub-interval solve is bitwise the same grid as the whole-interval solve).
  * Offsets are element offsets into the caller's state buffer `xbuf`.
- * 88 bytes, natural alignment (mirrored by a numpy structured dtype).
+ * 96 bytes, natural alignment (mirrored by a numpy structured dtype).
  */
 typedef struct mlmcp_task {
   int32_t sample;   /* row of the per-sample M/K value arrays            */
@@ -97,6 +104,8 @@ typedef struct mlmcp_task {
   int32_t slot;     /* index into iters / status                         */
   int32_t tag;      /* copied to status[4*slot+2..3] on failure          */
   int32_t flags;    /* MLMCP_TASK_*                                      */
+  int32_t qoi_index; /* ELECTRICAL: state component of the drive current  */
+  int32_t reserved;  /* 0                                                  */
 } mlmcp_task;
 
 /* task flags */
@@ -126,7 +135,12 @@ int mlmcp_ctx_info(const mlmcp_ctx* ctx, int* max_row_nnz, int* small_max_rows);
 int mlmcp_ctx_set_assembly(mlmcp_ctx* ctx, int n_elem, int n_contrib,
                            const int32_t* cptr, const int32_t* elem,
                            const double* mw, const double* kw);
-/* Force a path: 0 auto, 1 SM-resident, 2 streaming (tests / benchmarks). */
+/* Force a path: 0 auto, 1 SM-resident (PCG), 2 streaming (PCG), 3 direct
+ * (dense LU with partial pivoting per task, one thread per task, n_rows <=
+ * MLMCP_DIRECT_MAX_ROWS; the only path for non-symmetric M + dt K, e.g. the
+ * Steinmetz circuit models.py:217-249).  Auto picks direct for n_rows <=
+ * MLMCP_DIRECT_MAX_ROWS, SM-resident up to small_max_rows, else streaming. */
+#define MLMCP_DIRECT_MAX_ROWS 4
 int mlmcp_ctx_set_path(mlmcp_ctx* ctx, int path);
 
 /* ---- K1: assembly ------------------------------------------------------ */
@@ -148,13 +162,20 @@ int mlmcp_kl_sigma(int S, int n_elem, int n_modes, const double* xi_d,
  * tasks over S per-sample operators (0 on the SM-resident path). */
 size_t mlmcp_workspace_bytes(const mlmcp_ctx* ctx, int n_tasks, int S);
 
+/* elapsed_ns_d (optional, may be NULL): device-clock nanoseconds each task
+ * held its execution slot (one CTA on the SM-resident path, one thread on the
+ * direct path) are ADDED to elapsed_ns_d[slot] (propagate: task.slot; coarse
+ * sweep: sample).  The executor turns these into GPU effort (SM-seconds);
+ * the streaming path leaves them untouched.  QoI modes ELECTRICAL / JOULE are
+ * supported on the SM-resident and direct paths (EINVAL on streaming). */
+
 int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                     int S, const double* M_d, const double* K_d,
                     const double* profile_d, double omega, double rtol,
                     int max_it, double* xbuf_d, double* qoi_d,
                     int32_t* iters_d, int32_t* status_d,
-                    const int32_t* active_d, void* ws_d, size_t ws_bytes,
-                    void* stream);
+                    const int32_t* active_d, int64_t* elapsed_ns_d,
+                    void* ws_d, size_t ws_bytes, void* stream);
 
 /* ---- K5: Parareal ------------------------------------------------------ */
 /* Coarse/update sweep of iteration k (1-based) for S samples.
@@ -170,8 +191,8 @@ int mlmcp_parareal_coarse(mlmcp_ctx* ctx, int S, int k, int m,
                           const int32_t* slice_steps_d, double rtol,
                           int max_it, double* U_d, const double* F_d,
                           double* C_d, int32_t* iters_d, int32_t* status_d,
-                          const int32_t* active_d, void* ws_d,
-                          size_t ws_bytes, void* stream);
+                          const int32_t* active_d, int64_t* elapsed_ns_d,
+                          void* ws_d, size_t ws_bytes, void* stream);
 
 /* Jump defect of iteration k; records defect_d[s*k_max + k-1], sets
  * k_used_d[s] = k and clears active_d[s] when defect <= tol (or k == m). */

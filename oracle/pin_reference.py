@@ -198,6 +198,39 @@ def main():
     pkl = [mo.draw(cfg3, 0, 2, k) for k in (1, 2)]
     fe_case("fe16_kl64_parareal", 16, "kl64", pkl, T / 128, T, pr=(8, T / 8, 1e-8, 6))
     fe_case("fe16_kl64_seq", 16, "kl64", pkl, T / 64, T)
+    # ---------------------------------------------------------- reference's own machine families
+    # MachineFamily.evaluate (models.py:389-411) of the unmodified reference on
+    # steinmetz_family / synthetic_family (models.py:431-453), sequential at
+    # every level and with Parareal at the finest (coarse dt = level L-2).
+    def machine_case(tag, fam, pcfg, n_per_level=3):
+        out = {"dts": np.array([lv.dt for lv in fam.hierarchy]), "horizon": fam.horizon}
+        L = len(fam.hierarchy) - 1
+        for lvl, spec in enumerate(fam.hierarchy):
+            ps = [models.draw_parameters(fam.uncertain, mo.RandomStream(0, lvl, k))
+                  for k in range(1, n_per_level + 1)]
+            out[f"params_l{lvl}"] = np.array([p.values for p in ps])
+            out[f"q_l{lvl}"] = np.array([fam.evaluate(p, spec).q for p in ps])
+            if lvl == L:
+                recs = [fam.evaluate(p, spec, pcfg) for p in ps]
+                out["q_pr"] = np.array([r.q for r in recs])
+                out["k_pr"] = np.array([r.parareal_iterations for r in recs])
+                out["pr_cfg"] = np.array([pcfg.num_subintervals, pcfg.dt_coarse, pcfg.tolerance,
+                                          pcfg.max_iterations])
+        # one full trajectory (the timeint mirror's dense-model parity)
+        p0 = models.ParameterVector(fam.uncertain.nominal.model_id, out["params_l0"][0])
+        model = fam.build(p0)
+        tr = timeint.implicit_euler_solve(model, 0.0, fam.horizon, fam.hierarchy[0].dt,
+                                          model.initial_state)
+        out["traj0"] = tr.states
+        out["traj0_q"] = models.evaluate_qoi(model, tr)
+        np.savez(os.path.join(GOLDEN, f"{tag}.npz"), **out)
+
+    h3 = models.make_hierarchy([1e-3, 1e-4, 1e-5])
+    machine_case("steinmetz", models.steinmetz_family(h3, horizon=0.04),
+                 parareal.PararealConfig(8, 1e-5, 1e-3, 1e-8, 8))
+    hs = models.make_hierarchy([1e-3, 5e-4, 1e-4])
+    machine_case("synthetic_machine", models.synthetic_family(hs, n_dof=64, horizon=0.04),
+                 parareal.PararealConfig(8, 1e-4, 1e-3, 1e-8, 8))
     print("golden fixtures written to", GOLDEN)
 
 

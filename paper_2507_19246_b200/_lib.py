@@ -26,23 +26,27 @@ EINVAL = -22
 ECUDA = -5
 ENOMEM = -12
 
-ST_OK, ST_NOCONV, ST_BREAKDOWN, ST_NONFINITE = 0, 1, 2, 3
+ST_OK, ST_NOCONV, ST_BREAKDOWN, ST_NONFINITE, ST_SINGULAR = 0, 1, 2, 3, 4
 STATUS_NAMES = {ST_NOCONV: "PCG did not converge within max_it",
                 ST_BREAKDOWN: "PCG breakdown (operator not SPD)",
-                ST_NONFINITE: "non-finite residual"}
+                ST_NONFINITE: "non-finite residual",
+                ST_SINGULAR: "(M + dt K) is singular"}
 STATUS_INTS = 4
 
-QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY = 0, 1, 2
+QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2, 3, 4
 TASK_NO_EXTRAPOLATION = 1
+ABI_VERSION = 2
+DIRECT_MAX_ROWS = 4
 
-# mlmcp_task (88 bytes, natural alignment)
+# mlmcp_task (96 bytes, natural alignment)
 TASK_DTYPE = np.dtype([
     ("sample", np.int32), ("n_steps", np.int32), ("k0", np.int64), ("dt", np.float64),
     ("t_base", np.float64), ("x_in", np.int64), ("x_out", np.int64), ("traj", np.int64),
     ("qoi_slot", np.int32), ("qoi_mode", np.int32), ("qoi_from", np.int64),
     ("group", np.int32), ("slot", np.int32), ("tag", np.int32), ("flags", np.int32),
+    ("qoi_index", np.int32), ("reserved", np.int32),
 ], align=True)
-assert TASK_DTYPE.itemsize == 88
+assert TASK_DTYPE.itemsize == 96
 
 # every symbol include/mlmcp.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -78,10 +82,10 @@ _SIGS = {
                                       P, P]),
     "mlmcp_workspace_bytes": (SZ, [P, ctypes.c_int, ctypes.c_int]),
     "mlmcp_propagate": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_int, P, P, P, F64, F64,
-                                       ctypes.c_int, P, P, P, P, P, P, SZ, P]),
+                                       ctypes.c_int, P, P, P, P, P, P, P, SZ, P]),
     "mlmcp_parareal_coarse": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
                                              P, F64, F64, F64, P, P, F64, ctypes.c_int, P, P,
-                                             P, P, P, P, P, SZ, P]),
+                                             P, P, P, P, P, P, SZ, P]),
     "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, P, F64, P, P, P, P]),
     "mlmcp_parareal_finalize": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),
@@ -109,6 +113,9 @@ def load(path: str = LIB_PATH):
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args
+        if lib.mlmcp_abi_version() != ABI_VERSION:
+            raise LibraryMissingError(f"{path} has ABI {lib.mlmcp_abi_version()}, expected "
+                                      f"{ABI_VERSION}: rebuild it")
         _lib = lib
         return lib
 

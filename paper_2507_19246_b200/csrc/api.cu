@@ -343,9 +343,12 @@ int mlmcp_ctx_info(const mlmcp_ctx* c, int* max_row_nnz, int* small_max_rows) {
 
 int mlmcp_ctx_set_path(mlmcp_ctx* c, int path) {
   if (c == nullptr) return einval("null context");
-  if (path < 0 || path > 2) return einval("path must be 0 (auto), 1 (SM-resident) or 2 (streaming)");
+  if (path < 0 || path > 3)
+    return einval("path must be 0 (auto), 1 (SM-resident), 2 (streaming) or 3 (direct)");
   if (path == 1 && c->n > kSmallMaxRows)
     return einval("SM-resident path holds at most 1024 rows");
+  if (path == 3 && c->n > MLMCP_DIRECT_MAX_ROWS)
+    return einval("direct path holds at most MLMCP_DIRECT_MAX_ROWS rows");
   c->path = path;
   return MLMCP_OK;
 }
@@ -402,7 +405,7 @@ int mlmcp_kl_sigma(int S, int E, int modes, const double* xi, const double* basi
 }
 
 size_t mlmcp_workspace_bytes(const mlmcp_ctx* c, int n_tasks, int S) {
-  if (c == nullptr || use_small(c)) return 0;
+  if (c == nullptr || use_small(c) || use_direct(c)) return 0;
   const size_t base = stream_workspace_bytes(c, std::max(n_tasks, S), S);
   // coarse sweep extras: tasks + cval + tstatus
   const size_t extra = ((sizeof(mlmcp_task) * S + 255) & ~size_t(255)) +
@@ -414,16 +417,20 @@ size_t mlmcp_workspace_bytes(const mlmcp_ctx* c, int n_tasks, int S) {
 int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                     const double* K, const double* profile, double omega, double rtol,
                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                    const int32_t* active, void* ws, size_t ws_bytes, void* stream) {
+                    const int32_t* active, int64_t* elapsed, void* ws, size_t ws_bytes,
+                    void* stream) {
   if (c == nullptr) return einval("null context");
   if (n_tasks < 0 || S < 1 || !tasks || !M || !K || !profile || !xbuf)
     return einval("null or empty propagate argument");
   if (!(rtol > 0.0) || max_it < 1) return einval("rtol must be > 0 and max_it >= 1");
   if (n_tasks == 0) return MLMCP_OK;
   MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  if (use_direct(c))
+    return direct_propagate(c, n_tasks, tasks, M, K, profile, omega, xbuf, qoi, iters, status,
+                            active, elapsed, (cudaStream_t)stream);
   if (use_small(c))
     return small_propagate(c, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
-                           iters, status, active, (cudaStream_t)stream);
+                           iters, status, active, elapsed, (cudaStream_t)stream);
   return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                           iters, status, active, ws, ws_bytes, (cudaStream_t)stream);
 }
@@ -432,8 +439,8 @@ int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, co
                           const double* profile, double omega, double dt_c, double t0,
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
-                          int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
-                          void* stream) {
+                          int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
+                          size_t ws_bytes, void* stream) {
   if (c == nullptr) return einval("null context");
   if (S < 0 || m < 1 || k < 1 || k > m || !M || !K || !profile || !slice_k0 || !slice_steps ||
       !U || !F || !C || !active || !status)
@@ -441,10 +448,14 @@ int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, co
   if (!(rtol > 0.0) || max_it < 1 || !(dt_c > 0.0)) return einval("bad solver tolerances");
   if (S == 0) return MLMCP_OK;
   MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  if (use_direct(c))
+    return direct_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
+                                  slice_steps, U, F, C, status, active, elapsed,
+                                  (cudaStream_t)stream);
   if (use_small(c))
     return small_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
                                  slice_steps, rtol, max_it, U, F, C, iters, status, active,
-                                 (cudaStream_t)stream);
+                                 elapsed, (cudaStream_t)stream);
   return stream_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
                                 slice_steps, rtol, max_it, U, F, C, iters, status, active, ws,
                                 ws_bytes, (cudaStream_t)stream);

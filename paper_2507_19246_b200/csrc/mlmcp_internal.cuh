@@ -31,7 +31,7 @@ struct Ctx {
   int n = 0;            // rows
   int nnz = 0;
   int max_row_nnz = 0;
-  int path = 0;         // 0 auto, 1 small, 2 streaming
+  int path = 0;         // 0 auto, 1 small, 2 streaming, 3 direct
   int32_t* row_ptr = nullptr;   // device [n+1]
   int32_t* col = nullptr;       // device [nnz]
   int32_t* ell_col = nullptr;   // device [max_row_nnz][n], padded with the row itself
@@ -153,13 +153,26 @@ __device__ __forceinline__ void write_status(int32_t* status, int slot, int code
 int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
                     const double* K, const double* profile, double omega, double rtol,
                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                    const int32_t* active, cudaStream_t stream);
+                    const int32_t* active, int64_t* elapsed, cudaStream_t stream);
 
 int small_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
                           const double* profile, double omega, double dt_c, double t0,
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
-                          int32_t* status, const int32_t* active, cudaStream_t stream);
+                          int32_t* status, const int32_t* active, int64_t* elapsed,
+                          cudaStream_t stream);
+
+// direct path (dense LU per task, n <= MLMCP_DIRECT_MAX_ROWS)
+int direct_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
+                     const double* K, const double* profile, double omega, double* xbuf,
+                     double* qoi, int32_t* iters, int32_t* status, const int32_t* active,
+                     int64_t* elapsed, cudaStream_t stream);
+
+int direct_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
+                           const double* profile, double omega, double dt_c, double t0,
+                           const int64_t* slice_k0, const int32_t* slice_steps, double* U,
+                           const double* F, double* C, int32_t* status, const int32_t* active,
+                           int64_t* elapsed, cudaStream_t stream);
 
 size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S);
 
@@ -184,10 +197,28 @@ int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                    double* qoi, int32_t* iters, int32_t* status, const int32_t* active,
                    char* ws, size_t ws_bytes, cudaStream_t stream);
 
+inline bool use_direct(const Ctx* ctx) {
+  if (ctx->path == 3) return true;
+  return ctx->path == 0 && ctx->n <= MLMCP_DIRECT_MAX_ROWS;
+}
+
 inline bool use_small(const Ctx* ctx) {
   if (ctx->path == 1) return true;
-  if (ctx->path == 2) return false;
+  if (ctx->path == 2 || ctx->path == 3) return false;
   return ctx->n <= kSmallMaxRows;
+}
+
+// device clock in ns (for the executor's effort accounting)
+__device__ __forceinline__ int64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return (int64_t)t;
+}
+
+__device__ __forceinline__ void add_elapsed(int64_t* elapsed, int slot, int64_t t_start) {
+  if (elapsed != nullptr && slot >= 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(elapsed + slot),
+              (unsigned long long)(global_ns() - t_start));
 }
 
 }  // namespace mlmcp

@@ -542,6 +542,7 @@ struct SmallArgs {
   int32_t* iters;
   int32_t* status;
   int32_t* active;
+  int64_t* elapsed;
   int buf_doubles;
 };
 
@@ -558,6 +559,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   constexpr int R = Op::R;
   extern __shared__ __align__(16) double smem[];
   const mlmcp_task t = a.tasks[blockIdx.x];
+  const int64_t t_start = global_ns();
   {
     // another CTA of the same group may clear active[] concurrently (on a
     // failure): decide once per block so the barriers below never diverge
@@ -598,8 +600,21 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
       for (int r = 0; r < R; ++r)
         if (Op::ok(r, pa)) a.xbuf[t.traj + (int64_t)(step + 1) * pa.N + Op::row(r, pa)] = x[r];
     }
-    if (t.qoi_mode == MLMCP_QOI_SUM_ENERGY && g > t.qoi_from)
-      acc += block_energy<Op>(op, x, pa, Ks, sh);
+    if (g > t.qoi_from) {
+      if (t.qoi_mode == MLMCP_QOI_SUM_ENERGY) {
+        acc += block_energy<Op>(op, x, pa, Ks, sh);
+      } else if (t.qoi_mode == MLMCP_QOI_JOULE) {
+        double d[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) d[r] = x[r] - an[r];   // 0 on padding slots
+        acc += 2.0 * block_energy<Op>(op, d, pa, Ms, sh);
+      } else if (t.qoi_mode == MLMCP_QOI_ELECTRICAL) {
+#pragma unroll
+        for (int r = 0; r < R; ++r)   // only the owner of row qoi_index accumulates
+          if (Op::ok(r, pa) && Op::row(r, pa) == t.qoi_index)
+            acc = __dadd_rn(acc, __dmul_rn(sf, x[r]));
+      }
+    }
   }
   if (t.x_out >= 0) {
 #pragma unroll
@@ -608,9 +623,16 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   }
   if (code == MLMCP_ST_OK && t.qoi_mode == MLMCP_QOI_FINAL_ENERGY && t.qoi_slot >= 0)
     acc = block_energy<Op>(op, x, pa, Ks, sh);
+  if (t.qoi_mode == MLMCP_QOI_ELECTRICAL && t.qoi_slot >= 0) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      if (Op::ok(r, pa) && Op::row(r, pa) == t.qoi_index) a.qoi[t.qoi_slot] = acc;
+  }
   if (threadIdx.x == 0) {
-    if (t.qoi_slot >= 0 && t.qoi_mode != MLMCP_QOI_NONE) a.qoi[t.qoi_slot] = acc;
+    if (t.qoi_slot >= 0 && t.qoi_mode != MLMCP_QOI_NONE && t.qoi_mode != MLMCP_QOI_ELECTRICAL)
+      a.qoi[t.qoi_slot] = acc;
     if (a.iters != nullptr && t.slot >= 0) a.iters[t.slot] = iters;
+    add_elapsed(a.elapsed, t.slot, t_start);
     if (code != MLMCP_ST_OK) {
       write_status(a.status, t.slot, code, fail_step, t.tag, t.tag);
       if (a.active != nullptr && t.group >= 0) a.active[t.group] = 0;
@@ -635,6 +657,7 @@ struct CoarseArgs {
   int32_t* iters;
   int32_t* status;
   int32_t* active;
+  int64_t* elapsed;
   int buf_doubles;
 };
 
@@ -644,6 +667,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   constexpr int R = Op::R;
   extern __shared__ __align__(16) double smem[];
   const int s = blockIdx.x;
+  const int64_t t_start = global_ns();
   if (a.active[s] == 0) return;
   const PatternArgs& pa = a.pa;
   SmallShared sh = setup_shared(smem, a.buf_doubles);
@@ -684,6 +708,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
           write_status(a.status, s, code, step, n, a.k);
           a.active[s] = 0;
           if (a.iters != nullptr) a.iters[s] += iters;
+          add_elapsed(a.elapsed, s, t_start);
         }
         return;
       }
@@ -712,7 +737,10 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
         U[a.m * N + i] = F[a.m * N + i];
       }
   }
-  if (threadIdx.x == 0 && a.iters != nullptr) a.iters[s] += iters;
+  if (threadIdx.x == 0) {
+    if (a.iters != nullptr) a.iters[s] += iters;
+    add_elapsed(a.elapsed, s, t_start);
+  }
   (void)Ks;
 }
 
@@ -825,9 +853,10 @@ struct LaunchCoarse {
 int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
                     const double* K, const double* profile, double omega, double rtol,
                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                    const int32_t* active, cudaStream_t stream) {
+                    const int32_t* active, int64_t* elapsed, cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
   SmallArgs a{};
+  a.elapsed = elapsed;
   a.tasks = tasks;
   a.n_tasks = n_tasks;
   a.nnz = ctx->nnz;
@@ -849,9 +878,11 @@ int small_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const 
                           const double* profile, double omega, double dt_c, double t0,
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
-                          int32_t* status, const int32_t* active, cudaStream_t stream) {
+                          int32_t* status, const int32_t* active, int64_t* elapsed,
+                          cudaStream_t stream) {
   if (S == 0) return MLMCP_OK;
   CoarseArgs a{};
+  a.elapsed = elapsed;
   a.S = S;
   a.k = k;
   a.m = m;

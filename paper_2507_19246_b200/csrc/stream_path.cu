@@ -540,6 +540,10 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
       set_error("task sample index out of range");
       return MLMCP_EINVAL;
     }
+    if (t.qoi_mode == MLMCP_QOI_ELECTRICAL || t.qoi_mode == MLMCP_QOI_JOULE) {
+      set_error("streaming path: QoI modes ELECTRICAL / JOULE need the SM-resident or direct path");
+      return MLMCP_EINVAL;
+    }
     steps_max = std::max(steps_max, t.n_steps);
   }
   Work w = carve(ws, L);

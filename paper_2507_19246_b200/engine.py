@@ -102,13 +102,19 @@ class DeviceSystem:
 
     # ------------------------------------------------------------ config
     def set_path(self, path: str):
-        code = {"auto": 0, "small": 1, "stream": 2}[path]
+        code = {"auto": 0, "small": 1, "stream": 2, "direct": 3}[path]
         check(self.lib.mlmcp_ctx_set_path(self.ctx, code), "mlmcp_ctx_set_path")
         self._path = code
 
     @property
+    def direct(self) -> bool:
+        return self._path == 3 or (self._path == 0 and self.n_rows <= _lib.DIRECT_MAX_ROWS)
+
+    @property
     def sm_resident(self) -> bool:
-        if self._path == 1:
+        """True when every launch is stream-ordered and workspace-free (SM-resident
+        or direct path), so concurrent launches on several streams are safe."""
+        if self._path in (1, 3):
             return True
         if self._path == 2:
             return False
@@ -142,7 +148,7 @@ class DeviceSystem:
     # ------------------------------------------------------------ K2-K4, K6
     def propagate(self, tasks: np.ndarray, M, K, profile, omega: float, rtol: float,
                   max_it: int, xbuf, qoi=None, iters=None, status=None, active=None,
-                  stream=None, tasks_dev: torch.Tensor | None = None):
+                  stream=None, tasks_dev: torch.Tensor | None = None, elapsed=None):
         n = len(tasks)
         if n == 0:
             return None
@@ -151,20 +157,20 @@ class DeviceSystem:
         ws = self.workspace(n, S)
         check(self.lib.mlmcp_propagate(self.ctx, n, ptr(td), S, ptr(M), ptr(K), ptr(profile),
                                        float(omega), float(rtol), int(max_it), ptr(xbuf), ptr(qoi),
-                                       ptr(iters), ptr(status), ptr(active), ptr(ws),
+                                       ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(ws),
                                        0 if ws is None else ws.numel(), stream_handle(stream)),
               "mlmcp_propagate")
         return td
 
     # ------------------------------------------------------------ K5
     def parareal_coarse(self, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0, slice_steps,
-                        rtol, max_it, U, F, C, iters, status, active, stream=None):
+                        rtol, max_it, U, F, C, iters, status, active, stream=None, elapsed=None):
         ws = self.workspace(S, S)
         check(self.lib.mlmcp_parareal_coarse(
             self.ctx, S, k, m, ptr(M), ptr(K), ptr(profile), float(omega), float(dt_c), float(t0),
             ptr(slice_k0), ptr(slice_steps), float(rtol), int(max_it), ptr(U), ptr(F), ptr(C),
-            ptr(iters), ptr(status), ptr(active), ptr(ws), 0 if ws is None else ws.numel(),
-            stream_handle(stream)), "mlmcp_parareal_coarse")
+            ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(ws),
+            0 if ws is None else ws.numel(), stream_handle(stream)), "mlmcp_parareal_coarse")
 
     def parareal_defect(self, S, k, m, k_max, U, F, tol, active, k_used, defects, stream=None):
         check(self.lib.mlmcp_parareal_defect(self.ctx, S, k, m, k_max, ptr(U), ptr(F), float(tol),

@@ -38,6 +38,9 @@ __all__ = ["ParameterVector", "UncertainInput", "GaussianInput", "LevelSpec", "m
            "LinearToyFamily", "toy_family", "eddy_current_family"]
 
 
+_PARAM_COUNTS = {"steinmetz": 6, "synthetic": 32}   # models.py:50
+
+
 @dataclass(frozen=True)
 class ParameterVector:
     model_id: str
@@ -46,7 +49,8 @@ class ParameterVector:
     def __post_init__(self):
         vals = np.atleast_1d(np.asarray(self.values, dtype=float))
         object.__setattr__(self, "values", vals)
-        expected = fe.n_params(self.model_id) if self.model_id in fe.LAYOUTS else None
+        expected = (fe.n_params(self.model_id) if self.model_id in fe.LAYOUTS
+                    else _PARAM_COUNTS.get(self.model_id))
         if expected is not None and len(vals) != expected:
             raise ValueError(f"model '{self.model_id}' takes {expected} parameters, got {len(vals)}")
         if self.model_id != "kl64" and not np.all(vals > 0.0):
@@ -164,39 +168,13 @@ def toy_family(hierarchy, nominal: float = 1.0, halfwidth: float = 0.05) -> Line
                            tuple(hierarchy))
 
 
-@dataclass
-class EddyCurrentFamily:
-    """2D linear eddy-current P1 FE family; one sample = one transient solve.
-
-    ``evaluate`` follows MachineFamily.evaluate (models.py:389-411): a
-    Parareal configuration switches the solve to Parareal with
-    ``parareal_cfg.with_dt_fine(level.dt)``; the QoI is evaluated from the
-    device-resident solution.  Batched entry points run many samples in one
-    launch.
-    """
-
-    model_id: str
-    uncertain: object
-    hierarchy: tuple
-    horizon: float
-    n: int
-    layout: str
-    qoi: QoIKind = QoIKind.MAGNETIC_ENERGY_T
-    avg_window: float = 0.0
-    device: object = None
-    rtol: float = 1e-13
-    max_it: int = 20000
-    path: str = "auto"
-    _solver: object = field(default=None, repr=False, compare=False)
-
-    # ------------------------------------------------------------ setup
-    @property
-    def solver(self):
-        if self._solver is None:
-            from .solver import FESolver
-            self._solver = FESolver(self.n, self.layout, self.device, self.rtol, self.max_it,
-                                    self.path)
-        return self._solver
+class _BatchedFamily:
+    """Batched level evaluation shared by the GPU families.  Subclasses set
+    ``solver`` (a solver.BatchSolver), ``hierarchy``, ``horizon`` and provide
+    the hooks ``_n_params``, ``_assemble_host`` / ``_assemble_dev`` (per-sample
+    operator values into [S, nnz] slices), ``_seq_job`` / ``_finish_q`` (QoI
+    task mode and its host-side scale; ``_pr_qoi`` derives the Parareal
+    level's QoI from them)."""
 
     def _pr_stream(self, device):
         import torch
@@ -212,22 +190,15 @@ class EddyCurrentFamily:
             return level.level
         return int(level)
 
-    def _seq_job(self, rows, dt):
-        from . import _lib
-        from .solver import SeqJob
-        from .timeint import step_count
-        n = step_count(0.0, self.horizon, dt)
-        if self.qoi is QoIKind.MAGNETIC_ENERGY_T:
-            return SeqJob(rows, dt, n, _lib.QOI_FINAL_ENERGY, 0)
-        if self.qoi is QoIKind.TIME_AVG_MAGNETIC_ENERGY:
-            n_w = int(round(self.avg_window / dt))
-            return SeqJob(rows, dt, n, _lib.QOI_SUM_ENERGY, n - n_w)
-        raise ValueError(f"QoI kind {self.qoi} is not defined for the FE family")
+    def _pr_qoi(self, dt_fine) -> dict:
+        """QoI of the Parareal level as run_parareal keywords: the sequential
+        job's task mode over the fine trajectory (final-state energy when
+        the mode is QOI_FINAL_ENERGY)."""
+        j = self._seq_job(np.zeros(0, dtype=np.int64), dt_fine)
+        return {"qoi_mode": j.qoi_mode, "qoi_index": j.qoi_index, "qoi_from": j.qoi_from}
 
-    def _finish_q(self, acc, dt):
-        if self.qoi is QoIKind.TIME_AVG_MAGNETIC_ENERGY:
-            return acc * dt / self.avg_window
-        return acc
+    def _assemble_dev(self, params_dev, M, K):
+        self._assemble_host(params_dev.cpu().numpy(), M, K)
 
     # ------------------------------------------------------------ batched
     def run_levels(self, draws, parareal_cfg: PararealConfig | None = None, levels=None,
@@ -245,7 +216,7 @@ class EddyCurrentFamily:
         top = len(self.hierarchy) - 1
         sizes = [len(d) for d in draws]
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
-        nnz = sol.mesh.nnz
+        nnz = sol.nnz
         M = torch.empty((int(offs[-1]), nnz), dtype=torch.float64, device=sol.device)
         K = torch.empty_like(M)
 
@@ -254,12 +225,11 @@ class EddyCurrentFamily:
             if b == a:
                 return
             if params_dev is not None:
-                p = params_dev[a:b]                # already resident in HBM
+                self._assemble_dev(params_dev[a:b], M[a:b], K[a:b])   # resident in HBM
             else:
                 d = draws[i].get() if hasattr(draws[i], "get") else draws[i]
                 host = np.ascontiguousarray(np.asarray(d, dtype=float).reshape(b - a, -1))
-                p = torch.from_numpy(host).pin_memory().to(sol.device, non_blocking=True)
-            sol.assemble(p, out=(M[a:b], K[a:b]))
+                self._assemble_host(host, M[a:b], K[a:b])
 
         pr_level = None
         if parareal_cfg is not None:
@@ -283,7 +253,8 @@ class EddyCurrentFamily:
             with torch.cuda.stream(side):
                 pr = sol.run_parareal(M[a:b], K[a:b], 0.0, self.horizon, cfg.num_subintervals,
                                       cfg.dt_fine, cfg.dt_coarse, cfg.tolerance, cfg.k_max,
-                                      stream=side)
+                                      stream=side, **self._pr_qoi(cfg.dt_fine))
+                pr_q = self._finish_q(pr.qoi, cfg.dt_fine)
         for i in range(len(levels)):
             if i != pr_level:
                 assemble_level(i)
@@ -324,7 +295,7 @@ class EddyCurrentFamily:
                     qm = q
                 its = its + r.iters.to(torch.int64)
             if i == pr_level:
-                ql = pr.qoi
+                ql = pr_q
                 ku = pr.k_used
                 defects = pr.defects
             out.append(CoupledBatch(lvl, ql, qm, ku, its, defects=defects))
@@ -352,20 +323,23 @@ class EddyCurrentFamily:
         """Q at one level for a batch of samples (no coupling)."""
         import torch
         lvl = self._level_index(level)
-        params = np.asarray(params, dtype=float).reshape(-1, fe.n_params(self.layout))
+        params = np.asarray(params, dtype=float).reshape(-1, self._n_params())
         sol = self.solver
         t = time.perf_counter()
-        M, K = sol.assemble(torch.from_numpy(params).to(sol.device))
+        M = torch.empty((len(params), sol.nnz), dtype=torch.float64, device=sol.device)
+        K = torch.empty_like(M)
+        self._assemble_host(params, M, K)
         top = len(self.hierarchy) - 1
         dt = self.hierarchy[lvl].dt
         ks = None
         if parareal_cfg is not None:
             cfg = parareal_cfg.with_dt_fine(dt)
             pr = sol.run_parareal(M, K, 0.0, self.horizon, cfg.num_subintervals, cfg.dt_fine,
-                                  cfg.dt_coarse, cfg.tolerance, cfg.k_max)
+                                  cfg.dt_coarse, cfg.tolerance, cfg.k_max,
+                                  **self._pr_qoi(cfg.dt_fine))
             from .parareal import raise_parareal_status
             raise_parareal_status(pr.status.cpu().numpy(), pr.fine_status.cpu().numpy())
-            q = pr.qoi.cpu().numpy()
+            q = self._finish_q(pr.qoi, cfg.dt_fine).cpu().numpy()
             ks = pr.k_used.cpu().numpy()
         else:
             from .solver import raise_on_status
@@ -383,6 +357,69 @@ class EddyCurrentFamily:
         """models.py:389-411 (``pool`` accepted and ignored)."""
         vals = params.values if isinstance(params, ParameterVector) else np.asarray(params)
         return self.evaluate_batch(np.asarray(vals, dtype=float)[None, :], level, parareal_cfg)[0]
+
+
+@dataclass
+class EddyCurrentFamily(_BatchedFamily):
+    """2D linear eddy-current P1 FE family; one sample = one transient solve.
+
+    ``evaluate`` follows MachineFamily.evaluate (models.py:389-411): a
+    Parareal configuration switches the solve to Parareal with
+    ``parareal_cfg.with_dt_fine(level.dt)``; the QoI is evaluated from the
+    device-resident solution.  Batched entry points run many samples in one
+    launch.
+    """
+
+    model_id: str
+    uncertain: object
+    hierarchy: tuple
+    horizon: float
+    n: int
+    layout: str
+    qoi: QoIKind = QoIKind.MAGNETIC_ENERGY_T
+    avg_window: float = 0.0
+    device: object = None
+    rtol: float = 1e-13
+    max_it: int = 20000
+    path: str = "auto"
+    _solver: object = field(default=None, repr=False, compare=False)
+
+    # ------------------------------------------------------------ setup
+    @property
+    def solver(self):
+        if self._solver is None:
+            from .solver import FESolver
+            self._solver = FESolver(self.n, self.layout, self.device, self.rtol, self.max_it,
+                                    self.path)
+        return self._solver
+
+    def _seq_job(self, rows, dt):
+        from . import _lib
+        from .solver import SeqJob
+        from .timeint import step_count
+        n = step_count(0.0, self.horizon, dt)
+        if self.qoi is QoIKind.MAGNETIC_ENERGY_T:
+            return SeqJob(rows, dt, n, _lib.QOI_FINAL_ENERGY, 0)
+        if self.qoi is QoIKind.TIME_AVG_MAGNETIC_ENERGY:
+            n_w = int(round(self.avg_window / dt))
+            return SeqJob(rows, dt, n, _lib.QOI_SUM_ENERGY, n - n_w)
+        raise ValueError(f"QoI kind {self.qoi} is not defined for the FE family")
+
+    def _finish_q(self, acc, dt):
+        if self.qoi is QoIKind.TIME_AVG_MAGNETIC_ENERGY:
+            return acc * dt / self.avg_window
+        return acc
+
+    def _n_params(self) -> int:
+        return fe.n_params(self.layout)
+
+    def _assemble_host(self, params, M, K):
+        import torch
+        p = torch.from_numpy(np.ascontiguousarray(params, dtype=np.float64)).pin_memory()
+        self.solver.assemble(p.to(self.solver.device, non_blocking=True), out=(M, K))
+
+    def _assemble_dev(self, params_dev, M, K):
+        self.solver.assemble(params_dev, out=(M, K))
 
 
 def eddy_current_family(config: int | str, device=None, **kw) -> EddyCurrentFamily:

@@ -39,6 +39,7 @@ class SeqJob:
     n_steps: int
     qoi_mode: int = _lib.QOI_FINAL_ENERGY
     qoi_from: int = 0
+    qoi_index: int = 0
 
 
 @dataclass
@@ -46,6 +47,7 @@ class SeqResult:
     qoi: torch.Tensor       # (len(rows),) device
     iters: torch.Tensor     # (len(rows),) device, PCG iterations
     status: torch.Tensor    # (len(rows), 4) device
+    elapsed: torch.Tensor | None = None   # (len(rows),) int64 device ns (timing on)
 
 
 @dataclass
@@ -60,6 +62,7 @@ class PararealBatchResult:
     traj: torch.Tensor | None   # (S, m, steps+1, N) last fine solve of each slice
     fine_iters: torch.Tensor
     coarse_iters: torch.Tensor
+    elapsed: tuple | None = None  # (coarse [S], fine [S*m]) int64 device ns (timing on)
 
 
 def parareal_grid(t0: float, t1: float, m: int, dt_fine: float, dt_coarse: float):
@@ -80,8 +83,72 @@ def parareal_grid(t0: float, t1: float, m: int, dt_fine: float, dt_coarse: float
     return bounds, fk0, fst, ck0, cst
 
 
-class FESolver:
-    """One mesh + material layout on one GPU."""
+class BatchSolver:
+    """Batched sequential / Parareal solves of one sparsity pattern on one GPU.
+
+    Subclasses supply the per-sample operator values (FESolver assembles them
+    on the device; SystemSolver uploads them from host builders)."""
+
+    def __init__(self, row_ptr, col, profile, frequency: float, device=None,
+                 rtol: float = DEFAULT_RTOL, max_it: int = DEFAULT_MAX_IT, path: str = "auto",
+                 assembly=None):
+        self.rtol = float(rtol)
+        self.max_it = int(max_it)
+        self.sys = DeviceSystem(row_ptr, col, device, assembly=assembly)
+        if path != "auto":
+            self.sys.set_path(path)
+        dev = self.sys.device
+        self.device = dev
+        self.N = self.sys.n_rows
+        self.nnz = self.sys.nnz
+        self.profile = torch.tensor(np.asarray(profile, dtype=np.float64), dtype=F64, device=dev)
+        self._task_cache: dict = {}
+        self.events = None    # optional (start, end) CUDA events around the sequential launch
+        self.timing = False   # True: launches record per-task device ns (executor ledger)
+        self.omega = 2.0 * np.pi * frequency       # same rounding as np.sin(2.0*np.pi*f*t)
+
+    # ------------------------------------------------------------ sequential
+    def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+        return _run_sequential(self, M, K, jobs, stream, keep_traj)
+
+    def run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
+                     dt_coarse: float, tol: float, k_max: int, stream=None,
+                     keep_traj: bool = False, qoi_mode: int | None = None,
+                     qoi_index: int = 0, qoi_from: int = -1) -> PararealBatchResult:
+        """qoi_mode None / QOI_FINAL_ENERGY: 1/2 a(T)^T K a(T); otherwise the
+        task QoI accumulated over the fine trajectory (global fine steps g >
+        qoi_from), summed over slices."""
+        return _run_parareal(self, M, K, t0, t1, m, dt_fine, dt_coarse, tol, k_max, stream,
+                             keep_traj, qoi_mode, qoi_index, qoi_from)
+
+    def _grid_tensors(self, ck0, cst):
+        key = ("grid", ck0.tobytes(), cst.tobytes())
+        v = self._task_cache.get(key)
+        if v is None:
+            v = (torch.tensor(ck0, device=self.device), torch.tensor(cst, device=self.device))
+            self._task_cache[key] = v
+        return v
+
+
+class SystemSolver(BatchSolver):
+    """A small linear model family M da/dt + K a = sin(2 pi f t) profile with
+    per-sample M/K values built on the host (the reference's own builders,
+    models.py:217-302) on one shared CSR pattern."""
+
+    def values(self, M_vals, K_vals):
+        """Upload [S, nnz] host value arrays (pinned, asynchronous)."""
+        Mh = np.ascontiguousarray(M_vals, dtype=np.float64).reshape(-1, self.nnz)
+        Kh = np.ascontiguousarray(K_vals, dtype=np.float64).reshape(-1, self.nnz)
+        if Mh.shape != Kh.shape:
+            raise ValueError(f"M/K value arrays differ in shape: {Mh.shape} vs {Kh.shape}")
+        M = torch.from_numpy(Mh).pin_memory().to(self.device, non_blocking=True)
+        K = torch.from_numpy(Kh).pin_memory().to(self.device, non_blocking=True)
+        return M, K
+
+
+class FESolver(BatchSolver):
+    """One structured P1 mesh + material layout on one GPU (K1 assembly on the
+    device)."""
 
     def __init__(self, n: int, layout: str, device=None, rtol: float = DEFAULT_RTOL,
                  max_it: int = DEFAULT_MAX_IT, path: str = "auto"):
@@ -89,21 +156,11 @@ class FESolver:
             raise ValueError(f"unknown layout {layout!r}")
         self.n = n
         self.layout = layout
-        self.rtol = float(rtol)
-        self.max_it = int(max_it)
         self.mesh = fe.structured_mesh(n)
         m = self.mesh
-        self.sys = DeviceSystem(m.row_ptr, m.col, device,
-                                assembly=(m.n_elem, m.cptr, m.celem, m.cmw, m.ckw))
-        if path != "auto":
-            self.sys.set_path(path)
-        dev = self.sys.device
-        self.device = dev
-        self.N = m.n_rows
-        self.profile = torch.tensor(fe.source_profile(m, layout), dtype=F64, device=dev)
-        self._task_cache: dict = {}
-        self.events = None    # optional (start, end) CUDA events around the sequential launch
-        self.omega = 2.0 * np.pi * fe.FREQ          # same rounding as np.sin(2.0*np.pi*f*t)
+        super().__init__(m.row_ptr, m.col, fe.source_profile(m, layout), fe.FREQ, device, rtol,
+                         max_it, path, assembly=(m.n_elem, m.cptr, m.celem, m.cmw, m.ckw))
+        dev = self.device
         if layout == "kl64":
             self.kl_basis = torch.tensor(fe.kl_basis(m), dtype=F64, device=dev)
             self.nu_const = torch.full((1,), fe.NU0, dtype=F64, device=dev)
@@ -136,155 +193,176 @@ class FESolver:
         sigma = (params[:, R:2 * R] * self.mask).contiguous()
         return self.sys.assemble(S, sigma, R, self.region, nu, R, self.region, stream, out)
 
-    # ------------------------------------------------------------ sequential
-    def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
-        """All jobs in one batched launch (SM-resident path) or one launch per
-        dt (streaming path).  Returns one SeqResult per job (device tensors)."""
-        sizes = [len(j.rows) for j in jobs]
-        T = int(sum(sizes))
-        N = self.N
-        tasks = new_tasks(T)
-        off = 0
-        for j in jobs:
-            sl = slice(off, off + len(j.rows))
-            tasks["sample"][sl] = j.rows
-            tasks["n_steps"][sl] = j.n_steps
-            tasks["k0"][sl] = 0
-            tasks["dt"][sl] = j.dt
-            tasks["t_base"][sl] = 0.0
-            tasks["qoi_mode"][sl] = j.qoi_mode
-            tasks["qoi_from"][sl] = j.qoi_from
-            off += len(j.rows)
-        idx = np.arange(T)
-        tasks["x_in"] = idx * N
-        tasks["x_out"] = idx * N
-        tasks["qoi_slot"] = idx
-        tasks["slot"] = idx
-        traj = None
-        if keep_traj:
-            steps = tasks["n_steps"].astype(np.int64)
-            base = T * N
-            tstart = base + np.concatenate([[0], np.cumsum((steps + 1) * N)[:-1]])
-            tasks["traj"] = tstart
-            xbuf = torch.zeros(int(base + np.sum((steps + 1) * N)), dtype=F64, device=self.device)
-        else:
-            xbuf = torch.zeros(T * N, dtype=F64, device=self.device)
-        qoi = torch.zeros(T, dtype=F64, device=self.device)
-        iters = torch.zeros(T, dtype=I32, device=self.device)
-        status = torch.zeros((T, _lib.STATUS_INTS), dtype=I32, device=self.device)
-        if self.sys.sm_resident:
-            order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
-            key = (tasks.tobytes(), N)
-            td = self._task_cache.get(key)
-            if td is None:
-                td = tasks_to_device(tasks[order], self.device)
-                self._task_cache[key] = td
-            if self.events is not None:
-                self.events[0].record(stream if stream is not None else torch.cuda.current_stream())
-            self.sys.propagate(tasks[order], M, K, self.profile, self.omega, self.rtol, self.max_it,
-                               xbuf, qoi, iters, status, None, stream, tasks_dev=td)
-            if self.events is not None:
-                self.events[1].record(stream if stream is not None else torch.cuda.current_stream())
-        else:
-            for dt in sorted(set(tasks["dt"].tolist())):
-                sel = tasks[tasks["dt"] == dt]
-                self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it,
-                                   xbuf, qoi, iters, status, None, stream)
-        out = []
-        off = 0
-        for j in jobs:
-            sl = slice(off, off + len(j.rows))
-            out.append(SeqResult(qoi[sl], iters[sl], status[sl]))
-            off += len(j.rows)
-        self._last_xbuf = xbuf
-        self._last_tasks = tasks
-        return out
 
-    def _grid_tensors(self, ck0, cst):
-        key = ("grid", ck0.tobytes(), cst.tobytes())
-        v = self._task_cache.get(key)
-        if v is None:
-            v = (torch.tensor(ck0, device=self.device), torch.tensor(cst, device=self.device))
-            self._task_cache[key] = v
-        return v
 
-    # ------------------------------------------------------------ Parareal
-    def run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
-                     dt_coarse: float, tol: float, k_max: int, stream=None,
-                     keep_traj: bool = False) -> PararealBatchResult:
-        """parareal_solve for the S samples whose operators are M/K rows 0..S-1
-        (slice the level's M/K to pass a sub-batch), from the zero state."""
-        if not 1 <= k_max <= m:
-            raise ValueError(f"max_iterations must lie in [1, M={m}], got {k_max}")
-        S = M.shape[0]
-        N = self.N
-        dev = self.device
-        bounds, fk0, fst, ck0, cst = parareal_grid(t0, t1, m, dt_fine, dt_coarse)
-        uf_size = S * (m + 1) * N
-        traj_steps = int(fst.max()) + 1
-        traj_size = S * m * traj_steps * N if keep_traj else 0
-        buf = torch.zeros(2 * uf_size + traj_size, dtype=F64, device=dev)
-        U = buf[:uf_size].view(S, m + 1, N)
-        F = buf[uf_size:2 * uf_size].view(S, m + 1, N)
-        C = torch.zeros((S, m, N), dtype=F64, device=dev)
-        active = torch.ones(S, dtype=I32, device=dev)
-        k_used = torch.zeros(S, dtype=I32, device=dev)
-        defects = torch.full((S, k_max), float("nan"), dtype=F64, device=dev)
-        status = torch.zeros((S, _lib.STATUS_INTS), dtype=I32, device=dev)
-        fine_status = torch.zeros((S * m, _lib.STATUS_INTS), dtype=I32, device=dev)
-        fine_iters = torch.zeros(S * m, dtype=I32, device=dev)
-        coarse_iters = torch.zeros(S, dtype=I32, device=dev)
-        ck0_d, cst_d = self._grid_tensors(ck0, cst)
-        # fine task tables: one per iteration k (intervals k..m of every sample)
-        s_idx, n_idx = np.meshgrid(np.arange(S), np.arange(1, m + 1), indexing="ij")
-        s_idx, n_idx = s_idx.ravel(), n_idx.ravel()
-        all_tasks = new_tasks(S * m)
-        all_tasks["sample"] = s_idx
-        all_tasks["n_steps"] = fst[n_idx - 1]
-        all_tasks["k0"] = fk0[n_idx - 1]
-        all_tasks["dt"] = dt_fine
-        all_tasks["t_base"] = t0
-        all_tasks["x_in"] = (s_idx * (m + 1) + (n_idx - 1)) * N
-        all_tasks["x_out"] = uf_size + (s_idx * (m + 1) + n_idx) * N
-        if keep_traj:
-            all_tasks["traj"] = 2 * uf_size + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
-        all_tasks["group"] = s_idx
-        all_tasks["slot"] = s_idx * m + (n_idx - 1)
-        key = ("pr", all_tasks.tobytes(), k_max)
-        tables = self._task_cache.get(key)
-        if tables is None:
-            tables = []
-            for k in range(1, k_max + 1):
-                sel = all_tasks[n_idx >= k].copy()
-                sel["tag"] = k
-                tables.append(tasks_to_device(sel, dev))
-            self._task_cache[key] = tables
+
+# ------------------------------------------------------------ sequential
+def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+    """All jobs in one batched launch (SM-resident path) or one launch per
+    dt (streaming path).  Returns one SeqResult per job (device tensors)."""
+    sizes = [len(j.rows) for j in jobs]
+    T = int(sum(sizes))
+    N = self.N
+    tasks = new_tasks(T)
+    off = 0
+    for j in jobs:
+        sl = slice(off, off + len(j.rows))
+        tasks["sample"][sl] = j.rows
+        tasks["n_steps"][sl] = j.n_steps
+        tasks["k0"][sl] = 0
+        tasks["dt"][sl] = j.dt
+        tasks["t_base"][sl] = 0.0
+        tasks["qoi_mode"][sl] = j.qoi_mode
+        tasks["qoi_from"][sl] = j.qoi_from
+        tasks["qoi_index"][sl] = j.qoi_index
+        off += len(j.rows)
+    idx = np.arange(T)
+    tasks["x_in"] = idx * N
+    tasks["x_out"] = idx * N
+    tasks["qoi_slot"] = idx
+    tasks["slot"] = idx
+    traj = None
+    if keep_traj:
+        steps = tasks["n_steps"].astype(np.int64)
+        base = T * N
+        tstart = base + np.concatenate([[0], np.cumsum((steps + 1) * N)[:-1]])
+        tasks["traj"] = tstart
+        xbuf = torch.zeros(int(base + np.sum((steps + 1) * N)), dtype=F64, device=self.device)
+    else:
+        xbuf = torch.zeros(T * N, dtype=F64, device=self.device)
+    qoi = torch.zeros(T, dtype=F64, device=self.device)
+    iters = torch.zeros(T, dtype=I32, device=self.device)
+    status = torch.zeros((T, _lib.STATUS_INTS), dtype=I32, device=self.device)
+    elapsed = torch.zeros(T, dtype=torch.int64, device=self.device) if self.timing else None
+    if self.sys.sm_resident:
+        order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
+        key = (tasks.tobytes(), N)
+        td = self._task_cache.get(key)
+        if td is None:
+            td = tasks_to_device(tasks[order], self.device)
+            self._task_cache[key] = td
+        if self.events is not None:
+            self.events[0].record(stream if stream is not None else torch.cuda.current_stream())
+        self.sys.propagate(tasks[order], M, K, self.profile, self.omega, self.rtol, self.max_it,
+                           xbuf, qoi, iters, status, None, stream, tasks_dev=td,
+                           elapsed=elapsed)
+        if self.events is not None:
+            self.events[1].record(stream if stream is not None else torch.cuda.current_stream())
+    else:
+        for dt in sorted(set(tasks["dt"].tolist())):
+            sel = tasks[tasks["dt"] == dt]
+            self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it,
+                               xbuf, qoi, iters, status, None, stream, elapsed=elapsed)
+    out = []
+    off = 0
+    for j in jobs:
+        sl = slice(off, off + len(j.rows))
+        out.append(SeqResult(qoi[sl], iters[sl], status[sl],
+                             None if elapsed is None else elapsed[sl]))
+        off += len(j.rows)
+    self._last_xbuf = xbuf
+    self._last_tasks = tasks
+    return out
+
+
+# ------------------------------------------------------------ Parareal
+def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
+                  dt_coarse: float, tol: float, k_max: int, stream=None,
+                  keep_traj: bool = False, qoi_mode: int | None = None,
+                  qoi_index: int = 0, qoi_from: int = -1) -> PararealBatchResult:
+    """parareal_solve for the S samples whose operators are M/K rows 0..S-1
+    (slice the level's M/K to pass a sub-batch), from the zero state."""
+    if not 1 <= k_max <= m:
+        raise ValueError(f"max_iterations must lie in [1, M={m}], got {k_max}")
+    S = M.shape[0]
+    N = self.N
+    dev = self.device
+    bounds, fk0, fst, ck0, cst = parareal_grid(t0, t1, m, dt_fine, dt_coarse)
+    uf_size = S * (m + 1) * N
+    traj_steps = int(fst.max()) + 1
+    traj_size = S * m * traj_steps * N if keep_traj else 0
+    buf = torch.zeros(2 * uf_size + traj_size, dtype=F64, device=dev)
+    U = buf[:uf_size].view(S, m + 1, N)
+    F = buf[uf_size:2 * uf_size].view(S, m + 1, N)
+    C = torch.zeros((S, m, N), dtype=F64, device=dev)
+    active = torch.ones(S, dtype=I32, device=dev)
+    k_used = torch.zeros(S, dtype=I32, device=dev)
+    defects = torch.full((S, k_max), float("nan"), dtype=F64, device=dev)
+    status = torch.zeros((S, _lib.STATUS_INTS), dtype=I32, device=dev)
+    fine_status = torch.zeros((S * m, _lib.STATUS_INTS), dtype=I32, device=dev)
+    fine_iters = torch.zeros(S * m, dtype=I32, device=dev)
+    coarse_iters = torch.zeros(S, dtype=I32, device=dev)
+    ck0_d, cst_d = self._grid_tensors(ck0, cst)
+    pr_elapsed_c = pr_elapsed_f = None
+    if self.timing:                   # executor ledger: per-sample coarse / per-slice fine ns
+        pr_elapsed_c = torch.zeros(S, dtype=torch.int64, device=dev)
+        pr_elapsed_f = torch.zeros(S * m, dtype=torch.int64, device=dev)
+    # fine task tables: one per iteration k (intervals k..m of every sample)
+    s_idx, n_idx = np.meshgrid(np.arange(S), np.arange(1, m + 1), indexing="ij")
+    s_idx, n_idx = s_idx.ravel(), n_idx.ravel()
+    all_tasks = new_tasks(S * m)
+    all_tasks["sample"] = s_idx
+    all_tasks["n_steps"] = fst[n_idx - 1]
+    all_tasks["k0"] = fk0[n_idx - 1]
+    all_tasks["dt"] = dt_fine
+    all_tasks["t_base"] = t0
+    all_tasks["x_in"] = (s_idx * (m + 1) + (n_idx - 1)) * N
+    all_tasks["x_out"] = uf_size + (s_idx * (m + 1) + n_idx) * N
+    if keep_traj:
+        all_tasks["traj"] = 2 * uf_size + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
+    all_tasks["group"] = s_idx
+    all_tasks["slot"] = s_idx * m + (n_idx - 1)
+    slice_qoi = None
+    if qoi_mode is not None and qoi_mode != _lib.QOI_FINAL_ENERGY:
+        # time-accumulated QoI over the fine trajectory (parareal.py:212 concatenates
+        # the last fine solve of every slice): each fine solve of slice n
+        # overwrites its partial sum, so after convergence slot (s, n) holds the
+        # sum over the slice's final sub-trajectory
+        all_tasks["qoi_slot"] = s_idx * m + (n_idx - 1)
+        all_tasks["qoi_mode"] = qoi_mode
+        all_tasks["qoi_from"] = qoi_from
+        all_tasks["qoi_index"] = qoi_index
+        slice_qoi = torch.zeros(S * m, dtype=F64, device=dev)
+    key = ("pr", all_tasks.tobytes(), k_max)
+    tables = self._task_cache.get(key)
+    if tables is None:
+        tables = []
         for k in range(1, k_max + 1):
-            self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
-                                     ck0_d, cst_d, self.rtol, self.max_it, U, F, C, coarse_iters,
-                                     status, active, stream)
-            tk = tables[k - 1]
-            n_tk = tk.numel() // _lib.TASK_DTYPE.itemsize
-            sel = all_tasks[n_idx >= k]
-            self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it, buf,
-                               None, fine_iters, fine_status, active, stream, tasks_dev=tk)
-            assert n_tk == len(sel)
-            self.sys.parareal_defect(S, k, m, k_max, U, F, tol, active, k_used, defects, stream)
-        self.sys.parareal_finalize(S, m, U, F, k_used, stream)
-        ekey = ("energy", S, m, N)
-        ev = self._task_cache.get(ekey)
-        if ev is None:
-            ev = (torch.arange(S, dtype=I32, device=dev),
-                  torch.tensor((uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64),
-                               device=dev))
-            self._task_cache[ekey] = ev
+            sel = all_tasks[n_idx >= k].copy()
+            sel["tag"] = k
+            tables.append(tasks_to_device(sel, dev))
+        self._task_cache[key] = tables
+    for k in range(1, k_max + 1):
+        self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
+                                 ck0_d, cst_d, self.rtol, self.max_it, U, F, C, coarse_iters,
+                                 status, active, stream, elapsed=pr_elapsed_c)
+        tk = tables[k - 1]
+        n_tk = tk.numel() // _lib.TASK_DTYPE.itemsize
+        sel = all_tasks[n_idx >= k]
+        self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it, buf,
+                           slice_qoi, fine_iters, fine_status, active, stream, tasks_dev=tk,
+                           elapsed=pr_elapsed_f)
+        assert n_tk == len(sel)
+        self.sys.parareal_defect(S, k, m, k_max, U, F, tol, active, k_used, defects, stream)
+    self.sys.parareal_finalize(S, m, U, F, k_used, stream)
+    ekey = ("energy", S, m, N)
+    ev = self._task_cache.get(ekey)
+    if ev is None:
+        ev = (torch.arange(S, dtype=I32, device=dev),
+              torch.tensor((uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64),
+                           device=dev))
+        self._task_cache[ekey] = ev
+    if slice_qoi is not None:
+        qoi = slice_qoi.view(S, m).sum(dim=1)
+    else:
         qoi = self.sys.energy(ev[0], ev[1], buf, K, stream)
-        traj = None
-        if keep_traj:
-            traj = buf[2 * uf_size:].view(S, m, traj_steps, N)
-        self._keep = tables
-        return PararealBatchResult(qoi, k_used, defects, status, fine_status, U, F, traj,
-                                   fine_iters, coarse_iters)
+    traj = None
+    if keep_traj:
+        traj = buf[2 * uf_size:].view(S, m, traj_steps, N)
+    self._keep = tables
+    return PararealBatchResult(qoi, k_used, defects, status, fine_status, U, F, traj,
+                               fine_iters, coarse_iters,
+                               (pr_elapsed_c, pr_elapsed_f) if self.timing else None)
 
 
 def raise_on_status(status: torch.Tensor, what: str):

@@ -8,13 +8,17 @@ Same names, argument meaning and errors as the reference:
   ``implicit_euler_solve``    timeint.py:88-111
   ``propagate``               timeint.py:114-128
 
-Difference by design: each step's linear solve is Jacobi-PCG on the device
-(tolerance ``rtol``, default 1e-13 — the stated PCG tolerance) instead of a
-dense LU factorisation.  The model is duck-typed like the reference
-(``mass``, ``stiffness`` as dense or scipy-sparse SPD operators with <= 8
+Difference by design: for systems with more than MLMCP_DIRECT_MAX_ROWS (4)
+states each step's linear solve is Jacobi-PCG on the device (tolerance
+``rtol``, default 1e-13 — the stated PCG tolerance; M and K must be
+symmetric) instead of a dense LU factorisation; smaller systems (the
+Steinmetz circuit, scalar tests) use the device's direct LU path, the
+reference's own algorithm.  The model is duck-typed like the reference
+(``mass``, ``stiffness`` as dense or scipy-sparse operators with <= 8
 entries per row of their union pattern; ``forcing`` of the form
 sin(2*pi*f*t) * profile, i.e. an object with ``frequency`` and ``profile``
-like models.py:171-179, or ``None`` for r = 0).
+like models.py:171-179, a scaled drive ``drive(t) * direction`` like
+models.py:160-168, or ``None`` for r = 0).
 """
 
 from __future__ import annotations
@@ -102,10 +106,23 @@ def operator_pattern(mass, stiffness):
     return row_ptr, col, values(Mc), values(Kc)
 
 
+def _symmetric(a) -> bool:
+    m = _csr(a)
+    d = m - m.T
+    return d.nnz == 0 or float(abs(d).max()) <= 1e-14 * max(float(abs(m).max()), 1e-300)
+
+
 def forcing_profile(model, n: int):
     f = getattr(model, "forcing", None)
     if f is None:
         return 0.0, np.zeros(n)
+    drive = getattr(f, "drive", None)
+    if drive is not None and hasattr(f, "direction") and hasattr(drive, "amplitude"):
+        # u(t) * direction with u = amplitude sin(2 pi f t) (models.py:160-168)
+        prof = float(drive.amplitude) * np.asarray(f.direction, dtype=float)
+        if prof.shape != (n,):
+            raise ValueError(f"forcing direction has shape {prof.shape}, expected ({n},)")
+        return float(drive.frequency), prof
     if hasattr(f, "frequency") and hasattr(f, "profile"):
         prof = np.asarray(f.profile, dtype=float)
         if prof.shape != (n,):
@@ -128,6 +145,12 @@ class _ModelOnDevice:
 
         from .engine import DeviceSystem, F64
         row_ptr, col, mv, kv = operator_pattern(model.mass, model.stiffness)
+        from . import _lib
+        if len(row_ptr) - 1 > _lib.DIRECT_MAX_ROWS and not (_symmetric(model.mass) and
+                                                            _symmetric(model.stiffness)):
+            raise ValueError("systems with more than "
+                             f"{_lib.DIRECT_MAX_ROWS} states need symmetric M and K "
+                             "(Jacobi-PCG path); smaller ones use the direct LU path")
         key = (row_ptr.tobytes(), col.tobytes(), str(device))
         sys = _ModelOnDevice._cache.get(key)
         if sys is None:

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_counters():
     lib = _lib.load()
-    assert lib.mlmcp_abi_version() == 1
+    assert lib.mlmcp_abi_version() == _lib.ABI_VERSION == 2
     assert _lib.launch_count() >= 0
 
 
@@ -42,8 +42,8 @@ def test_task_struct_layout_matches_header():
     size = {"int32_t": 4, "int64_t": 8, "double": 8}
     for (ty, name) in fields:
         assert _lib.TASK_DTYPE.fields[name][0].itemsize == size[ty]
-    assert _lib.TASK_DTYPE.itemsize == 88
-    assert "88 bytes" in src
+    assert _lib.TASK_DTYPE.itemsize == 96
+    assert "96 bytes" in src
 
 
 def create(row_ptr, col):
