@@ -6,10 +6,11 @@ Two modes, as the SPEC asks:
     (``schedule_level``), batch wall time = max task time, Parareal tasks
     timed by costmodel.parareal_time / parareal_effort.
   * ``gpu_ledger`` — the real mode of this framework: one batched device
-    launch per estimate, timed on the device.  Effort is counted in
-    SM-seconds from per-task device timers (each task holds one CTA slot of
-    an SM for its duration), the GPU analogue of "the sum of the time spent
-    over all active processor cores".
+    launch per estimate, timed on the device.  Effort is counted in device
+    task-slot seconds from per-task device timers (each task holds one CTA
+    slot of an SM, or one thread on the direct path, for its duration), the
+    GPU analogue of "the sum of the time spent over all active processor
+    cores" (PAPER.md:136).
 
 Ledger JSON keys follow SPEC.md:497: ``mode``, ``levels[{level, batches,
 wall_s, effort_core_s}]``, ``total_wall_s``, ``total_effort_core_s``.
@@ -23,7 +24,7 @@ from dataclasses import dataclass, field
 from . import costmodel
 
 __all__ = ["Task", "SequentialSolve", "CoupledPair", "PararealSolve", "schedule_level",
-           "LevelLedger", "Ledger", "simulate", "plan_tasks"]
+           "LevelLedger", "Ledger", "simulate", "plan_tasks", "gpu_ledger"]
 
 
 @dataclass(frozen=True)
@@ -177,3 +178,37 @@ def plan_tasks(N, costs, parareal=None):
             plan.append([CoupledPair(lvl, k, cost_hi_s=costs[lvl], cost_lo_s=costs[lvl - 1])
                          for k in range(n)])
     return plan
+
+
+def gpu_ledger(batches, wall_s: float, dist=None) -> Ledger:
+    """Real-mode ledger of one batched device estimate (mlmc_estimate with
+    ``timing=True``).  All levels run in one batched launch (plus the finest
+    level's Parareal on a second stream), so per level: ``batches`` = 1,
+    ``wall_s`` = the longest task of the level (its critical path inside the
+    launch; for the Parareal level the longest coarse sweep or fine slice
+    accumulated over iterations), ``effort_core_s`` = the sum over the
+    level's tasks of the device time each held its execution slot (one CTA
+    on the SM-resident path, one thread on the direct path).  Over ranks:
+    effort summed, wall maxed.  ``total_wall_s`` is the measured host wall
+    time of the whole estimate."""
+    import torch
+    led = Ledger("gpu-batched", extra={"total_wall_s": float(wall_s),
+                                       "effort_unit": "device task-slot seconds"})
+    rows = []
+    for b in batches:
+        eff, longest = 0.0, 0.0
+        for t in b.elapsed:
+            if t.numel():
+                eff += float(t.to(torch.float64).sum().item()) * 1e-9
+                longest = max(longest, float(t.max().item()) * 1e-9)
+        rows.append((eff, longest))
+    if dist is not None and dist.get_world_size() > 1 and rows:
+        dev = batches[0].q_l.device
+        e = torch.tensor([r[0] for r in rows], dtype=torch.float64, device=dev)
+        w = torch.tensor([r[1] for r in rows], dtype=torch.float64, device=dev)
+        dist.all_reduce(e, op=dist.ReduceOp.SUM)
+        dist.all_reduce(w, op=dist.ReduceOp.MAX)
+        rows = list(zip(e.tolist(), w.tolist()))
+    for b, (eff, longest) in zip(batches, rows):
+        led.levels.append(LevelLedger(b.level, 1, longest, eff))
+    return led

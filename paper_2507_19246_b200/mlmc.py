@@ -36,7 +36,8 @@ from .models import EvalRecord, LevelSpec, draw_parameters
 
 __all__ = ["RandomStream", "LevelStats", "EstimatorResult", "FixedSamples", "WarmupPolicy",
            "coupled_sample", "mc_estimate", "optimal_allocation", "mlmc_estimate",
-           "draw_level", "shard_range", "LazyDraw"]
+           "draw_level", "shard_range", "LazyDraw", "estimate_dict",
+           "write_estimate_json"]
 
 
 class RandomStream:
@@ -225,9 +226,12 @@ def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
 
 
 def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: int = 0,
-                  device=None, draws=None, csv_path: str | None = None) -> EstimatorResult:
+                  device=None, draws=None, csv_path: str | None = None,
+                  timing: bool = False) -> EstimatorResult:
     """SPEC.md:300-314.  ``policy``: FixedSamples (all levels at once) or
-    WarmupPolicy (warm-up, optimal allocation, then the remainder)."""
+    WarmupPolicy (warm-up, optimal allocation, then the remainder).
+    ``timing``: record per-task device time and attach the executor ledger
+    (SPEC.md:447-500, executor.gpu_ledger) as ``result.ledger["executor"]``."""
     hierarchy = tuple(hierarchy or family.hierarchy)
     dist = _dist()
     rank = dist.get_rank() if dist else 0
@@ -235,7 +239,7 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
     if policy is None:
         raise ValueError("need a sampling policy")
     if isinstance(policy, WarmupPolicy):
-        return _mlmc_warmup(family, hierarchy, policy, parareal_cfg, seed, device)
+        return _mlmc_warmup(family, hierarchy, policy, parareal_cfg, seed, device, timing)
     counts = list(policy.n_per_level)
     if len(counts) != len(hierarchy):
         raise ValueError("one sample count per level is required")
@@ -245,7 +249,14 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
         draws = [LazyDraw(b - a, (lambda lvl=lvl, a=a, b=b: draw_level(
             family.uncertain, seed, lvl, range(a + 1, b + 1))))
             for lvl, (a, b) in enumerate(ranges)]
-    batches = family.run_levels(draws, parareal_cfg)
+    sol = getattr(family, "solver", None) if timing else None
+    if sol is not None:
+        sol.timing = True
+    try:
+        batches = family.run_levels(draws, parareal_cfg)
+    finally:
+        if sol is not None:
+            sol.timing = False
     dev = device
     if dev is None and hasattr(family, "solver"):
         dev = family.solver.device
@@ -269,6 +280,9 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
     rmse = math.sqrt(sum(max(st.var_y, 0.0) / st.n for st in per_level if st.n > 0))
     ledger = {"wall_time_s": wall, "world_size": world,
               "samples": counts, "mode": "gpu-batched"}
+    if sol is not None:
+        from .executor import gpu_ledger
+        ledger["executor"] = gpu_ledger(batches, wall, dist).to_dict()
     if csv_path and rank == 0:
         _write_csv(csv_path, all_slots, per_level)
     return EstimatorResult(expectation, per_level, rmse, ledger)
@@ -285,7 +299,8 @@ def _write_csv(path, all_slots, per_level):
                          f"{per_level[lvl].cost_per_sample!r},{int(s[k, 2])}\n")
 
 
-def _mlmc_warmup(family, hierarchy, policy: WarmupPolicy, parareal_cfg, seed, device):
+def _mlmc_warmup(family, hierarchy, policy: WarmupPolicy, parareal_cfg, seed, device,
+                 timing=False):
     n_w = max(2, policy.n_warmup)
     warm = mlmc_estimate(family, hierarchy, FixedSamples((n_w,) * len(hierarchy)), parareal_cfg,
                          seed, device)
@@ -293,7 +308,8 @@ def _mlmc_warmup(family, hierarchy, policy: WarmupPolicy, parareal_cfg, seed, de
     C = [max(st.cost_per_sample, 1e-12) for st in warm.per_level]
     target = optimal_allocation(V, C, rmse=policy.rmse, budget=policy.budget)
     counts = tuple(max(n_w, t) for t in target)
-    res = mlmc_estimate(family, hierarchy, FixedSamples(counts), parareal_cfg, seed, device)
+    res = mlmc_estimate(family, hierarchy, FixedSamples(counts), parareal_cfg, seed, device,
+                        timing=timing)
     res.ledger["warmup"] = [n_w] * len(hierarchy)
     res.ledger["allocation"] = list(counts)
     return res
@@ -301,3 +317,19 @@ def _mlmc_warmup(family, hierarchy, policy: WarmupPolicy, parareal_cfg, seed, de
 
 def evaluate_records(family, params, level, parareal_cfg=None) -> list[EvalRecord]:
     return family.evaluate_batch(params, level, parareal_cfg)
+
+
+def estimate_dict(res: EstimatorResult) -> dict:
+    """estimate.json content (SPEC.md cmd_estimate: expectation, rmse, per-level
+    stats); deterministic for a fixed seed (no timings)."""
+    return {"expectation": res.expectation, "rmse_estimate": res.rmse_estimate,
+            "levels": [{"level": st.level, "n": st.n, "sum_y": st.sum_y, "sum_y2": st.sum_y2,
+                        "mean_y": st.mean_y, "var_y": st.var_y,
+                        "parareal_k": st.parareal_k} for st in res.per_level]}
+
+
+def write_estimate_json(path: str, res: EstimatorResult):
+    import json
+    with open(path, "w") as fh:
+        json.dump(estimate_dict(res), fh, indent=1, sort_keys=True)
+

@@ -137,6 +137,7 @@ class CoupledBatch:
     iters: object = None
     wall_s: float = 0.0
     defects: object = None
+    elapsed: list = field(default_factory=list)   # int64 device-ns tensors (timing on)
 
 
 @dataclass
@@ -285,9 +286,12 @@ class _BatchedFamily:
             ku = torch.zeros(S, dtype=torch.int32, device=dev)
             its = torch.zeros(S, dtype=torch.int64, device=dev)
             defects = None
+            elapsed = []
             for (j, kind, dt), r in zip(where, res):
                 if j != i:
                     continue
+                if r.elapsed is not None:
+                    elapsed.append(r.elapsed)
                 q = self._finish_q(r.qoi, dt)
                 if kind == "hi":
                     ql = q
@@ -298,7 +302,9 @@ class _BatchedFamily:
                 ql = pr_q
                 ku = pr.k_used
                 defects = pr.defects
-            out.append(CoupledBatch(lvl, ql, qm, ku, its, defects=defects))
+                if pr.elapsed is not None:
+                    elapsed.extend(pr.elapsed)
+            out.append(CoupledBatch(lvl, ql, qm, ku, its, defects=defects, elapsed=elapsed))
         self._last = (res, pr, M, K)
         return out
 
