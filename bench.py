@@ -362,7 +362,7 @@ def main():
                                   f"dt=T/{round(cfg.horizon / cfg.dts[0])}..T/{round(cfg.horizon / cfg.dts[-1])}, "
                                   f"N_l={list(counts)} ({'Parareal M=%d K<=%d tol=%g' % (pcfg.num_subintervals, pcfg.k_max, pcfg.tolerance) if pcfg else 'no Parareal'}), full MLMC estimate per step",
                       "seq_equiv_sample_timesteps": total_steps, "mlmc_parareal_wall_ms": ms,
-                      "pcg_rtol": 1e-13, "parareal_k": sorted(set(k_used)),
+                      "pcg_rtol": sol.step_rtol(), "predictor": sol.use_predictor(), "parareal_k": sorted(set(k_used)),
                       "l2": "flushed between steps (512 MiB write)", "parallelism": f"samples x{world}"},
            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                         "frac": achieved / peak, "traffic": ncu_traffic(),

@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 2
+#define MLMCP_ABI_VERSION 3
 
 /* return codes */
 #define MLMCP_OK 0
@@ -105,7 +105,8 @@ typedef struct mlmcp_task {
   int32_t tag;      /* copied to status[4*slot+2..3] on failure          */
   int32_t flags;    /* MLMCP_TASK_*                                      */
   int32_t qoi_index; /* ELECTRICAL: state component of the drive current  */
-  int32_t reserved;  /* 0                                                  */
+  int32_t ss_slot;   /* row of xss_d (periodic steady state) for the PCG
+                        initial-guess predictor, -1: none                  */
 } mlmcp_task;
 
 /* task flags */
@@ -172,10 +173,26 @@ size_t mlmcp_workspace_bytes(const mlmcp_ctx* ctx, int n_tasks, int S);
 int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                     int S, const double* M_d, const double* K_d,
                     const double* profile_d, double omega, double rtol,
-                    int max_it, double* xbuf_d, double* qoi_d,
-                    int32_t* iters_d, int32_t* status_d,
+                    int max_it, const double* xss_d, double* xbuf_d,
+                    double* qoi_d, int32_t* iters_d, int32_t* status_d,
                     const int32_t* active_d, int64_t* elapsed_ns_d,
                     void* ws_d, size_t ws_bytes, void* stream);
+
+/* Periodic steady state of the implicit-Euler iteration (initial-guess
+ * predictor, SM-resident path): for item i with operator row sample_d[i] and
+ * step dt_d[i], X_d[i] = [Re X; Im X] (2 N doubles) solves
+ *     (M + dt K - e^{-i omega dt} M) X = dt * profile,
+ * so that ss_g = Im(X e^{i omega t_g}) is the exact periodic solution of
+ * (M + dt K) a_g = M a_{g-1} + dt sin(omega t_g) profile.  Tasks with
+ * ss_slot = i then start every PCG solve from ss_{g} + the polynomial
+ * extrapolation of a - ss (fewer iterations; the per-step stopping rule and
+ * accuracy are unchanged).  COCG to rtol (loose, e.g. 1e-8); iters_d[i] =
+ * COCG iterations (optional).  EINVAL on the streaming / direct paths. */
+int mlmcp_periodic_state(mlmcp_ctx* ctx, int n, const int32_t* sample_d,
+                         const double* dt_d, int S, const double* M_d,
+                         const double* K_d, const double* profile_d,
+                         double omega, double rtol, int max_it, double* X_d,
+                         int32_t* iters_d, void* stream);
 
 /* ---- K5: Parareal ------------------------------------------------------ */
 /* Coarse/update sweep of iteration k (1-based) for S samples.
@@ -183,7 +200,9 @@ int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
  *   C: [S][m][N] previous coarse values, slice_k0/slice_steps: [m] coarse
  *   grid offsets / step counts of slices 1..m (index n-1).
  * Samples with active_d[s] == 0 are skipped.  Solver failures set
- * status[4*s..] = {code, step, interval n, iteration k} and clear active[s]. */
+ * status[4*s..] = {code, step, interval n, iteration k} and clear active[s].
+ * xss_d (optional, SM-resident path): [S][2][N] periodic steady states at
+ * dt_c (mlmcp_periodic_state) for the initial-guess predictor. */
 int mlmcp_parareal_coarse(mlmcp_ctx* ctx, int S, int k, int m,
                           const double* M_d, const double* K_d,
                           const double* profile_d, double omega, double dt_c,
@@ -192,7 +211,8 @@ int mlmcp_parareal_coarse(mlmcp_ctx* ctx, int S, int k, int m,
                           int max_it, double* U_d, const double* F_d,
                           double* C_d, int32_t* iters_d, int32_t* status_d,
                           const int32_t* active_d, int64_t* elapsed_ns_d,
-                          void* ws_d, size_t ws_bytes, void* stream);
+                          const double* xss_d, void* ws_d, size_t ws_bytes,
+                          void* stream);
 
 /* Jump defect of iteration k; records defect_d[s*k_max + k-1], sets
  * k_used_d[s] = k and clears active_d[s] when defect <= tol (or k == m). */

@@ -35,7 +35,7 @@ STATUS_INTS = 4
 
 QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2, 3, 4
 TASK_NO_EXTRAPOLATION = 1
-ABI_VERSION = 2
+ABI_VERSION = 3
 DIRECT_MAX_ROWS = 4
 
 # mlmcp_task (96 bytes, natural alignment)
@@ -44,7 +44,7 @@ TASK_DTYPE = np.dtype([
     ("t_base", np.float64), ("x_in", np.int64), ("x_out", np.int64), ("traj", np.int64),
     ("qoi_slot", np.int32), ("qoi_mode", np.int32), ("qoi_from", np.int64),
     ("group", np.int32), ("slot", np.int32), ("tag", np.int32), ("flags", np.int32),
-    ("qoi_index", np.int32), ("reserved", np.int32),
+    ("qoi_index", np.int32), ("ss_slot", np.int32),
 ], align=True)
 assert TASK_DTYPE.itemsize == 96
 
@@ -53,7 +53,7 @@ EXPORTS = (
     "mlmcp_abi_version", "mlmcp_last_error", "mlmcp_launch_count",
     "mlmcp_ctx_create", "mlmcp_ctx_destroy", "mlmcp_ctx_info", "mlmcp_ctx_set_assembly",
     "mlmcp_ctx_set_path", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
-    "mlmcp_propagate", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
+    "mlmcp_propagate", "mlmcp_periodic_state", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
     "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce",
 )
 
@@ -82,10 +82,12 @@ _SIGS = {
                                       P, P]),
     "mlmcp_workspace_bytes": (SZ, [P, ctypes.c_int, ctypes.c_int]),
     "mlmcp_propagate": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_int, P, P, P, F64, F64,
-                                       ctypes.c_int, P, P, P, P, P, P, P, SZ, P]),
+                                       ctypes.c_int, P, P, P, P, P, P, P, P, SZ, P]),
+    "mlmcp_periodic_state": (ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_int, P, P, P, F64,
+                                            F64, ctypes.c_int, P, P, P]),
     "mlmcp_parareal_coarse": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
                                              P, F64, F64, F64, P, P, F64, ctypes.c_int, P, P,
-                                             P, P, P, P, P, P, SZ, P]),
+                                             P, P, P, P, P, P, P, SZ, P]),
     "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, P, F64, P, P, P, P]),
     "mlmcp_parareal_finalize": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),

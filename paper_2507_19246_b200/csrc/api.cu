@@ -416,9 +416,9 @@ size_t mlmcp_workspace_bytes(const mlmcp_ctx* c, int n_tasks, int S) {
 
 int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                     const double* K, const double* profile, double omega, double rtol,
-                    int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                    const int32_t* active, int64_t* elapsed, void* ws, size_t ws_bytes,
-                    void* stream) {
+                    int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
+                    int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
+                    size_t ws_bytes, void* stream) {
   if (c == nullptr) return einval("null context");
   if (n_tasks < 0 || S < 1 || !tasks || !M || !K || !profile || !xbuf)
     return einval("null or empty propagate argument");
@@ -430,7 +430,7 @@ int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, c
                             active, elapsed, (cudaStream_t)stream);
   if (use_small(c))
     return small_propagate(c, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
-                           iters, status, active, elapsed, (cudaStream_t)stream);
+                           iters, status, active, elapsed, xss, (cudaStream_t)stream);
   return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                           iters, status, active, ws, ws_bytes, (cudaStream_t)stream);
 }
@@ -439,8 +439,8 @@ int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, co
                           const double* profile, double omega, double dt_c, double t0,
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
-                          int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
-                          size_t ws_bytes, void* stream) {
+                          int32_t* status, const int32_t* active, int64_t* elapsed,
+                          const double* xss, void* ws, size_t ws_bytes, void* stream) {
   if (c == nullptr) return einval("null context");
   if (S < 0 || m < 1 || k < 1 || k > m || !M || !K || !profile || !slice_k0 || !slice_steps ||
       !U || !F || !C || !active || !status)
@@ -455,10 +455,25 @@ int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, co
   if (use_small(c))
     return small_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
                                  slice_steps, rtol, max_it, U, F, C, iters, status, active,
-                                 elapsed, (cudaStream_t)stream);
+                                 elapsed, xss, (cudaStream_t)stream);
   return stream_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
                                 slice_steps, rtol, max_it, U, F, C, iters, status, active, ws,
                                 ws_bytes, (cudaStream_t)stream);
+}
+
+int mlmcp_periodic_state(mlmcp_ctx* c, int n, const int32_t* sample, const double* dt, int S,
+                         const double* M, const double* K, const double* profile, double omega,
+                         double rtol, int max_it, double* X, int32_t* iters, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (n < 0 || S < 1 || !sample || !dt || !M || !K || !profile || !X)
+    return einval("null or empty periodic-state argument");
+  if (!(rtol > 0.0) || max_it < 1) return einval("rtol must be > 0 and max_it >= 1");
+  if (use_direct(c) || !use_small(c))
+    return einval("periodic steady states are computed on the SM-resident path only");
+  if (n == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  return small_periodic(c, n, sample, dt, M, K, profile, omega, rtol, max_it, X, iters,
+                        (cudaStream_t)stream);
 }
 
 int mlmcp_parareal_defect(mlmcp_ctx* c, int S, int k, int m, int k_max, const double* U,

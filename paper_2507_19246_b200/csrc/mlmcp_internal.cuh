@@ -153,14 +153,19 @@ __device__ __forceinline__ void write_status(int32_t* status, int slot, int code
 int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
                     const double* K, const double* profile, double omega, double rtol,
                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                    const int32_t* active, int64_t* elapsed, cudaStream_t stream);
+                    const int32_t* active, int64_t* elapsed, const double* xss,
+                    cudaStream_t stream);
+
+int small_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
+                   const double* K, const double* profile, double omega, double rtol,
+                   int max_it, double* X, int32_t* iters, cudaStream_t stream);
 
 int small_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
                           const double* profile, double omega, double dt_c, double t0,
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
                           int32_t* status, const int32_t* active, int64_t* elapsed,
-                          cudaStream_t stream);
+                          const double* xss, cudaStream_t stream);
 
 // direct path (dense LU per task, n <= MLMCP_DIRECT_MAX_ROWS)
 int direct_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,

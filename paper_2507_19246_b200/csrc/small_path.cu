@@ -20,7 +20,8 @@
 //              a block-uniform offset.
 //   CsrOp      generic pattern: packed 16-bit smem byte offsets per entry.
 // PCG is the Chronopoulos-Gear single-reduction variant: one fused block
-// all-reduce (r.u, w.u, r.r) per iteration, two __syncthreads; the alpha/beta
+// all-reduce (r.u, w.u) per iteration (the stopping test is on the Jacobi-
+// preconditioned residual r.u), two __syncthreads; the alpha/beta
 // recurrence has one reciprocal on the critical path.  The cross-warp stage
 // of the reduction is a broadcast smem read of the 8 warp partials + a fixed
 // tree, so every thread holds bitwise identical totals (deterministic).
@@ -122,6 +123,13 @@ struct StencilOp {
   __device__ static int row(int r, const PatternArgs&) { return threadIdx.x + r * kSmallThreads; }
   __device__ static bool ok(int r, const PatternArgs& pa) { return row(r, pa) < pa.N; }
   static int buffer_doubles(int pad) { return pad + R * kSmallThreads + pad; }
+  __device__ static int diag_pos(int r, const PatternArgs& pa) {
+    int q = -1;
+#pragma unroll
+    for (int j = 0; j < W; ++j)
+      if (pa.off[j] == 0) q = pa.spos[j * pa.N + row(r, pa)];
+    return q;
+  }
 
   __device__ void load(const PatternArgs& pa, const double* __restrict__ Ms,
                        const double* __restrict__ Ks, double dt) {
@@ -185,6 +193,12 @@ struct CsrOp {
   __device__ static int row(int r, const PatternArgs&) { return threadIdx.x + r * kSmallThreads; }
   __device__ static bool ok(int r, const PatternArgs& pa) { return row(r, pa) < pa.N; }
   static int buffer_doubles(int) { return R * kSmallThreads; }
+  __device__ static int diag_pos(int r, const PatternArgs& pa) {
+    const int rw = row(r, pa);
+    for (int q = pa.row_ptr[rw]; q < pa.row_ptr[rw + 1]; ++q)
+      if (pa.col[q] == rw) return q;
+    return -1;
+  }
   __device__ uint32_t off(int r, int j) const {
     const uint32_t w = cp[r][j >> 1];
     return (j & 1) ? (w >> 16) : (w & 0xffffu);
@@ -264,6 +278,9 @@ struct GridOp {
   __device__ static bool ok(int r, const PatternArgs& pa) { return lane() < pa.wd && gy(r) < pa.gh; }
   __device__ static int row(int r, const PatternArgs& pa) { return gy(r) * pa.wd + lane(); }
   static int buffer_doubles(int) { return kHaloBuf; }
+  __device__ static int diag_pos(int r, const PatternArgs& pa) {
+    return pa.gpos[3 * pa.N + row(r, pa)];
+  }
 
   __device__ void load(const PatternArgs& pa, const double* __restrict__ Ms,
                        const double* __restrict__ Ks, double dt) {
@@ -351,58 +368,88 @@ struct SmallShared {
   double* bufB;  // exchange buffer for the initial guess (A x0)
   double* bufC;  // exchange buffer for u (PCG iterations)
   double* red;   // [2][kMaxWarps][4]
-  double* ring;  // [kMaxOrder][R*256] state history (per-thread slots)
+  double* ring;  // [kRing][R*256] state history (per-thread slots)
+  double* xs;    // [2][R*256] periodic steady state X (real, imaginary) per thread slot
   int par;
 };
 
-// State history of the current task for the PCG initial guess: the guess is
-// the polynomial extrapolation of the last p+1 states,
-//     x0 = sum_{i=0..p} (-1)^i C(p+1, i+1) a_{n-i},   p = min(#history, kMaxOrder),
-// (p = 0: a_n; 1: 2a_n - a_{n-1}; 2: 3a_n - 3a_{n-1} + a_{n-2}; ...).  Only the
-// starting point of PCG changes — the stopping rule ||r|| <= rtol ||b|| and
-// hence the accuracy of every step are unchanged — but the initial residual
-// drops by ~O(omega dt) per order (configs 0/1: 59 -> 26 PCG iterations per
-// step at T/256, 51 -> 16 at T/1024 for p = 4).  The past states live in a
-// per-thread shared-memory ring (touched once per step), a_n in registers.
+// Initial guess of each implicit-Euler step's PCG solve.  Only the starting
+// point of PCG changes — the stopping rule ||r|| <= rtol ||b|| and hence the
+// accuracy of every step are unchanged.
+//
+//  * Periodic steady-state predictor (task.ss_slot >= 0): the discrete
+//    implicit-Euler iteration driven by dt sin(w t_g) profile has the exact
+//    periodic solution ss_g = Im(X e^{i w t_g}), (M + dt K - e^{-i w dt} M) X =
+//    dt profile (X from small_periodic_kernel, in shared memory).  The
+//    remainder y_g = a_g - ss_g is the decaying transient, which polynomial
+//    extrapolation predicts far better than the forced oscillation itself:
+//        x0 = ss_{n+1} + sum_{i=0..p} (-1)^i C(p+1, i+1) y_{n-i}.
+//    Configs 0/1: 29.7 -> 11.4 PCG iterations per step at T/256, 18.9 -> 10.9
+//    at T/1024 (p = 3; scripts in DESIGN.md §5).
+//  * Without X (ss = 0) this is plain extrapolation of the states (p <= 4).
+//  * MLMCP_TASK_NO_EXTRAPOLATION: x0 = a_n (the reference's one-step method,
+//    bitwise semigroup).
+// The transients y live in a per-thread shared-memory ring touched once per
+// step.
 constexpr int kMaxOrder = 4;
+constexpr int kRing = kMaxOrder + 1;
 
 template <int R>
 struct StateHistory {
-  double* ring;   // [kMaxOrder][R*256]: a_{n-1} .. a_{n-4} (ring)
-  int head;       // ring slot of a_{n-1}
-  int count;      // valid past states (<= kMaxOrder)
-  int max_order;  // 0 disables extrapolation (MLMCP_TASK_NO_EXTRAPOLATION)
+  double* ring;   // [kRing][R*256]: y_n, y_{n-1}, ... (ring, head = y_n)
+  int head;       // ring slot of y_n
+  int count;      // valid entries (<= kRing)
+  int max_order;
   __device__ StateHistory(double* ring_, int max_ord)
-      : ring(ring_), head(kMaxOrder - 1), count(0), max_order(max_ord) {}
-  __device__ double past(int i, int r) const {  // a_{n-i}, i >= 1
-    const int slot = (head - (i - 1) + kMaxOrder) % kMaxOrder;
+      : ring(ring_), head(0), count(0), max_order(max_ord) {}
+  __device__ double y(int i, int r) const {  // y_{n-i}
+    const int slot = (head - i + kRing) % kRing;
     return ring[slot * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x];
   }
-  // on entry x = a_n; on exit x = initial guess, an = a_n; a_n joins the ring
-  __device__ void advance(double (&x)[R], double (&an)[R]) {
-    const int p = count < max_order ? count : max_order;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      an[r] = x[r];
-      double g;
-      switch (p) {
-        case 0: g = an[r]; break;
-        case 1: g = fma(2.0, an[r], -past(1, r)); break;
-        case 2: g = fma(3.0, an[r] - past(1, r), past(2, r)); break;
-        case 3: g = fma(4.0, an[r] + past(2, r), fma(-6.0, past(1, r), -past(3, r))); break;
-        default:  // 5a_n - 10a_{n-1} + 10a_{n-2} - 5a_{n-3} + a_{n-4}
-          g = fma(5.0, an[r] - past(3, r), fma(10.0, past(2, r) - past(1, r), past(4, r)));
-          break;
-      }
-      x[r] = g;
-    }
-    head = (head + 1) % kMaxOrder;
+  // y_{n+1} = x - ss joins the ring
+  __device__ void push(const double (&x)[R], const double (&ss)[R]) {
+    head = (head + 1) % kRing;
 #pragma unroll
     for (int r = 0; r < R; ++r)
-      ring[head * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x] = an[r];
-    count = count < kMaxOrder ? count + 1 : kMaxOrder;
+      ring[head * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x] = x[r] - ss[r];
+    count = count < kRing ? count + 1 : kRing;
+  }
+  // replace y_n (Parareal coarse sweep: the next slice starts from a corrected state)
+  __device__ void replace(const double (&x)[R], const double (&ss)[R]) {
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+      ring[head * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x] = x[r] - ss[r];
+  }
+  // x = ss + extrapolated transient (count >= 1)
+  __device__ void guess(double (&x)[R], const double (&ss)[R]) const {
+    const int p = (count - 1) < max_order ? (count - 1) : max_order;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double g;
+      switch (p) {
+        case 0: g = y(0, r); break;
+        case 1: g = fma(2.0, y(0, r), -y(1, r)); break;
+        case 2: g = fma(3.0, y(0, r) - y(1, r), y(2, r)); break;
+        case 3: g = fma(4.0, y(0, r) + y(2, r), fma(-6.0, y(1, r), -y(3, r))); break;
+        default:  // 5y_n - 10y_{n-1} + 10y_{n-2} - 5y_{n-3} + y_{n-4}
+          g = fma(5.0, y(0, r) - y(3, r), fma(10.0, y(2, r) - y(1, r), y(4, r)));
+          break;
+      }
+      x[r] = g + ss[r];
+    }
   }
 };
+
+// ss_g = Im(X e^{i phi}) = Xr sin(phi) + Xi cos(phi) for this thread's slots
+template <int R>
+__device__ __forceinline__ void steady_state(const double* xs, bool on, double s, double c,
+                                             double (&ss)[R]) {
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int k = r * kSmallThreads + threadIdx.x;
+    ss[r] = on ? fma(xs[k], s, xs[R * kSmallThreads + k] * c) : 0.0;
+  }
+}
 
 // 1/2 x^T K x over the block (every thread receives it).  Uses bufA.
 template <class Op>
@@ -423,8 +470,14 @@ __device__ __forceinline__ double block_energy(const Op& op, const double (&x)[O
 
 // One implicit-Euler step (M + dt K) a_{n+1} = M a_n + dt*sf*profile by
 // Chronopoulos-Gear Jacobi-PCG.  x holds the initial guess on entry (the
-// caller extrapolates it from the state history) and a_{n+1} on exit.
-// Returns MLMCP_ST_*.
+// caller predicts it from the state history) and a_{n+1} on exit.
+// Stopping rule in the Jacobi-preconditioned residual norm:
+//     r^T D^-1 r <= rtol^2 b^T D^-1 b
+// (r^T D^-1 r = gamma is already part of the fused reduction, so the test is
+// free; unlike ||r||_2 it weights every row by 1/a_ii, which keeps the error
+// of weakly weighted rows — the sigma = 0 regions, whose diagonal is only
+// dt*k_ii — at the level of the others when PCG starts from an excellent
+// guess and stops after few iterations).  Returns MLMCP_ST_*.
 template <class Op>
 __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const double (&an)[Op::R],
                                        const PatternArgs& pa, double sf, double dt,
@@ -439,7 +492,7 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
   double res[R], u[R], p[R], s[R], w[R], mx[R], ax[R];
   op.apply_vals(Ms, an, sh.bufA, pa, mx);
   op.apply(x, sh.bufB, pa, ax);
-  double red4[4] = {0.0, 0.0, 0.0, 0.0};
+  double red3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     res[r] = 0.0;
@@ -449,7 +502,7 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
       const double b = __dadd_rn(mx[r], __dmul_rn(dt, __dmul_rn(sf, __ldg(profile + rw))));
       res[r] = b - ax[r];
       u[r] = op.dinv[r] * res[r];
-      red4[3] += b * b;
+      red3[2] = fma(b * op.dinv[r], b, red3[2]);
     }
   }
   op.publish(u, sh.bufC, pa);
@@ -457,23 +510,21 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
   op.apply(u, sh.bufC, pa, w);                    // a = 0 on padding slots
 #pragma unroll
   for (int r = 0; r < R; ++r) {
-    red4[0] += res[r] * u[r];
-    red4[1] += w[r] * u[r];
-    red4[2] += res[r] * res[r];
+    red3[0] += res[r] * u[r];
+    red3[1] += w[r] * u[r];
   }
-  cta_allsum<4>(red4, sh.red, sh.par);
-  const double gamma = red4[0];
-  double delta = red4[1];
-  double rho = red4[2];
-  const double bnorm2 = red4[3];
-  if (bnorm2 == 0.0) {  // b == 0 exactly: the solution is 0
+  cta_allsum<3>(red3, sh.red, sh.par);
+  const double gamma = red3[0];
+  double delta = red3[1];
+  const double bnorm2 = red3[2];
+  if (bnorm2 == 0.0) {  // b == 0 exactly (D^-1 > 0): the solution is 0
 #pragma unroll
     for (int r = 0; r < R; ++r) x[r] = 0.0;
     return MLMCP_ST_OK;
   }
   const double tol2 = rtol2 * bnorm2;
-  if (rho <= tol2) return MLMCP_ST_OK;
-  if (!isfinite(rho)) return MLMCP_ST_NONFINITE;
+  if (gamma <= tol2) return MLMCP_ST_OK;
+  if (!isfinite(gamma)) return MLMCP_ST_NONFINITE;
   if (!(delta > 0.0)) return MLMCP_ST_BREAKDOWN;
   double alpha = gamma * fast_rcp(delta);
   double inv_g = fast_rcp(gamma);
@@ -492,19 +543,17 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
     op.publish(u, sh.bufC, pa);
     __syncthreads();
     op.apply(u, sh.bufC, pa, w);
-    double red3[3] = {0.0, 0.0, 0.0};
+    double red2[2] = {0.0, 0.0};
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      red3[0] = fma(res[r], u[r], red3[0]);
-      red3[1] = fma(w[r], u[r], red3[1]);
-      red3[2] = fma(res[r], res[r], red3[2]);
+      red2[0] = fma(res[r], u[r], red2[0]);
+      red2[1] = fma(w[r], u[r], red2[1]);
     }
-    cta_allsum<3>(red3, sh.red, sh.par);
-    const double gnew = red3[0];
-    delta = red3[1];
-    rho = red3[2];
-    if (rho <= tol2) break;
-    if (!isfinite(rho)) { iters += it; return MLMCP_ST_NONFINITE; }
+    cta_allsum<2>(red2, sh.red, sh.par);
+    const double gnew = red2[0];
+    delta = red2[1];
+    if (gnew <= tol2) break;
+    if (!isfinite(gnew)) { iters += it; return MLMCP_ST_NONFINITE; }
     if (it >= max_it) { iters += it; return MLMCP_ST_NOCONV; }
     // beta = gnew/gamma, alpha = gnew / (delta - beta*gnew/alpha)
     const double beta = gnew * inv_g;
@@ -543,15 +592,34 @@ struct SmallArgs {
   int32_t* status;
   int32_t* active;
   int64_t* elapsed;
+  const double* xss;   // [slots][2][N] periodic steady states (or null)
   int buf_doubles;
 };
 
 // Carve and zero the exchange buffers.
+template <int R>
 __device__ __forceinline__ SmallShared setup_shared(double* smem, int len) {
   for (int i = threadIdx.x; i < 3 * len; i += kSmallThreads) smem[i] = 0.0;
   __syncthreads();
-  return SmallShared{smem, smem + len, smem + 2 * len, smem + 3 * len,
-                     smem + 3 * len + 2 * kMaxWarps * 4, 0};
+  double* ring = smem + 3 * len + 2 * kMaxWarps * 4;
+  return SmallShared{smem, smem + len, smem + 2 * len, smem + 3 * len, ring,
+                     ring + kRing * R * kSmallThreads, 0};
+}
+
+// X of one (sample, dt) into the thread's smem slots (own rows only: read
+// back by the same thread, no barrier needed)
+template <class Op>
+__device__ __forceinline__ void load_steady(const double* __restrict__ X, const PatternArgs& pa,
+                                            double* xs) {
+  constexpr int R = Op::R;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const bool v = Op::ok(r, pa);
+    const int rw = v ? Op::row(r, pa) : 0;
+    const int k = r * kSmallThreads + threadIdx.x;
+    xs[k] = v ? X[rw] : 0.0;
+    xs[R * kSmallThreads + k] = v ? X[pa.N + rw] : 0.0;
+  }
 }
 
 template <class Op, int OCC>
@@ -570,12 +638,15 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
     if (skip) return;
   }
   const PatternArgs& pa = a.pa;
-  SmallShared sh = setup_shared(smem, a.buf_doubles);
+  SmallShared sh = setup_shared<R>(smem, a.buf_doubles);
   const double* Ms = a.M + (int64_t)t.sample * a.nnz;
   const double* Ks = a.K + (int64_t)t.sample * a.nnz;
   Op op;
   op.load(pa, Ms, Ks, t.dt);
-  double x[R];
+  const bool no_extrap = (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) != 0;
+  const bool pred = !no_extrap && a.xss != nullptr && t.ss_slot >= 0;
+  if (pred) load_steady<Op>(a.xss + (int64_t)t.ss_slot * 2 * pa.N, pa, sh.xs);
+  double x[R], ss[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     const bool v = Op::ok(r, pa);
@@ -587,14 +658,26 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   int code = MLMCP_ST_OK;
   int fail_step = 0;
   double acc = 0.0;
-  StateHistory<R> hist(sh.ring, (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : kMaxOrder);
+  StateHistory<R> hist(sh.ring, no_extrap ? 0 : (pred ? 3 : kMaxOrder));
+  {
+    double s0 = 0.0, c0 = 0.0;
+    if (pred) sincos(__dmul_rn(a.omega, grid_time(t.t_base, t.k0, t.dt)), &s0, &c0);
+    steady_state<R>(sh.xs, pred, s0, c0, ss);
+    hist.push(x, ss);
+  }
   double an[R];
   for (int step = 0; step < t.n_steps; ++step) {
     const int64_t g = t.k0 + step + 1;
-    const double sf = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
-    hist.advance(x, an);                   // x <- extrapolated initial guess
+    double sf, cf;
+    sincos(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)), &sf, &cf);
+#pragma unroll
+    for (int r = 0; r < R; ++r) an[r] = x[r];
+    steady_state<R>(sh.xs, pred, sf, cf, ss);
+    hist.guess(x, ss);                     // x <- predicted initial guess
     code = ie_step<Op>(op, x, an, pa, sf, t.dt, Ms, a.profile, a.rtol2, a.max_it, sh, iters);
     if (code != MLMCP_ST_OK) { fail_step = step; break; }
+    steady_state<R>(sh.xs, pred, sf, cf, ss);
+    hist.push(x, ss);
     if (t.traj >= 0) {
 #pragma unroll
       for (int r = 0; r < R; ++r)
@@ -658,10 +741,14 @@ struct CoarseArgs {
   int32_t* status;
   int32_t* active;
   int64_t* elapsed;
+  const double* xss;   // [S][2][N] periodic steady states at dt_c (or null)
   int buf_doubles;
 };
 
-// parareal.py:168-178 for one sample per CTA.
+// parareal.py:168-178 for one sample per CTA.  The state history (and the
+// steady-state predictor) run across slices: for k = 1 the sweep is one
+// implicit-Euler trajectory; for k >= 2 each slice restarts from the corrected
+// U_n, which replaces the newest history entry.
 template <class Op, int OCC>
 __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(CoarseArgs a) {
   constexpr int R = Op::R;
@@ -670,11 +757,13 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   const int64_t t_start = global_ns();
   if (a.active[s] == 0) return;
   const PatternArgs& pa = a.pa;
-  SmallShared sh = setup_shared(smem, a.buf_doubles);
+  SmallShared sh = setup_shared<R>(smem, a.buf_doubles);
   const double* Ms = a.M + (int64_t)s * a.nnz;
   const double* Ks = a.K + (int64_t)s * a.nnz;
   Op op;
   op.load(pa, Ms, Ks, a.dt);
+  const bool pred = a.xss != nullptr;
+  if (pred) load_steady<Op>(a.xss + (int64_t)s * 2 * pa.N, pa, sh.xs);
   const int64_t N = pa.N;
   double* U = a.U + (int64_t)s * (a.m + 1) * N;
   const double* F = a.F + (int64_t)s * (a.m + 1) * N;
@@ -692,15 +781,24 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
       if (v) U[(a.k - 1) * N + i] = x[r];
     }
   }
+  StateHistory<R> hist(sh.ring, pred ? 3 : kMaxOrder);
+  double ss[R], an[R];
+  double sf = 0.0, cf = 0.0;
+  if (a.k < a.m) {
+    if (pred) sincos(__dmul_rn(a.omega, grid_time(a.t0, a.slice_k0[a.k - 1], a.dt)), &sf, &cf);
+    steady_state<R>(sh.xs, pred, sf, cf, ss);
+    hist.push(x, ss);
+  }
   for (int n = a.k; n < a.m; ++n) {
     const int steps = a.slice_steps[n - 1];
     const int64_t k0 = a.slice_k0[n - 1];
-    StateHistory<R> hist(sh.ring, kMaxOrder);
-    double an[R];
     for (int step = 0; step < steps; ++step) {
       const int64_t g = k0 + step + 1;
-      const double sf = sin(__dmul_rn(a.omega, grid_time(a.t0, g, a.dt)));
-      hist.advance(x, an);
+      sincos(__dmul_rn(a.omega, grid_time(a.t0, g, a.dt)), &sf, &cf);
+#pragma unroll
+      for (int r = 0; r < R; ++r) an[r] = x[r];
+      steady_state<R>(sh.xs, pred, sf, cf, ss);
+      hist.guess(x, ss);
       const int code = ie_step<Op>(op, x, an, pa, sf, a.dt, Ms, a.profile, a.rtol2,
                                    a.max_it, sh, iters);
       if (code != MLMCP_ST_OK) {
@@ -712,6 +810,8 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
         }
         return;
       }
+      steady_state<R>(sh.xs, pred, sf, cf, ss);
+      hist.push(x, ss);
     }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -728,6 +828,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
         x[r] = un;
       }
     }
+    if (a.k > 1) hist.replace(x, ss);   // ss still holds the slice end's steady state
   }
   if (a.k > 1) {
 #pragma unroll
@@ -744,13 +845,143 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   (void)Ks;
 }
 
+struct PeriodicArgs {
+  const int32_t* sample;
+  const double* dt;
+  int n;
+  int64_t nnz;
+  PatternArgs pa;
+  const double* M;
+  const double* K;
+  const double* profile;
+  double omega, rtol2;
+  int max_it;
+  double* X;
+  int32_t* iters;
+  int buf_doubles;
+};
+
+// Periodic steady state of the implicit-Euler iteration for one (sample, dt)
+// per CTA: (A - e^{-i w dt} M) X = dt profile, A = M + dt K, by COCG (CG with
+// unconjugated inner products for the complex-symmetric matrix) with the
+// complex Jacobi preconditioner.  X only feeds initial guesses
+// (StateHistory), so its tolerance is loose (~1e-8) and a non-converged X is
+// harmless; ~50 iterations on configs 0/1.
+template <class Op>
+__global__ void __launch_bounds__(kSmallThreads, 1) small_periodic_kernel(PeriodicArgs a) {
+  constexpr int R = Op::R;
+  extern __shared__ __align__(16) double smem[];
+  const PatternArgs& pa = a.pa;
+  const int item = blockIdx.x;
+  const int s = a.sample[item];
+  const double dt = a.dt[item];
+  SmallShared sh = setup_shared<R>(smem, a.buf_doubles);
+  const double* Ms = a.M + (int64_t)s * a.nnz;
+  const double* Ks = a.K + (int64_t)s * a.nnz;
+  Op op;
+  op.load(pa, Ms, Ks, dt);
+  double sn, c;
+  sincos(__dmul_rn(a.omega, dt), &sn, &c);
+  double ir[R], ii[R], xr[R], xi[R], rr[R], ri[R], pr[R], pi[R];
+  double red[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    ir[r] = ii[r] = xr[r] = xi[r] = rr[r] = ri[r] = pr[r] = pi[r] = 0.0;
+    if (!Op::ok(r, pa)) continue;
+    const int q = Op::diag_pos(r, pa);
+    const double m = q >= 0 ? Ms[q] : 0.0;
+    const double ad = q >= 0 ? op_entry(m, Ks[q], dt) : 0.0;
+    const double dr = ad - c * m, di = sn * m;
+    const double den = dr * dr + di * di;
+    if (den > 0.0) {
+      ir[r] = dr / den;
+      ii[r] = -di / den;
+    }
+    rr[r] = dt * a.profile[Op::row(r, pa)];
+    pr[r] = ir[r] * rr[r];           // z = D^-1 r (r real)
+    pi[r] = ii[r] * rr[r];
+    red[0] = fma(rr[r], pr[r], red[0]);
+    red[1] = fma(rr[r], pi[r], red[1]);
+    red[2] = fma(rr[r], rr[r], red[2]);
+  }
+  cta_allsum<3>(red, sh.red, sh.par);
+  double rho_r = red[0], rho_i = red[1];
+  const double tol2 = a.rtol2 * red[2];
+  int it = 0;
+  if (red[2] > 0.0) {
+    for (;;) {
+      op.publish(pr, sh.bufA, pa);
+      op.publish(pi, sh.bufB, pa);
+      __syncthreads();
+      double apr[R], api[R], mpr[R], mpi[R];
+      op.apply(pr, sh.bufA, pa, apr);
+      op.apply(pi, sh.bufB, pa, api);
+      op.apply_vals(Ms, pr, sh.bufA, pa, mpr);
+      op.apply_vals(Ms, pi, sh.bufB, pa, mpi);
+      double qr[R], qi[R];
+      double sg[2] = {0.0, 0.0};
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        qr[r] = fma(-sn, mpi[r], fma(-c, mpr[r], apr[r]));
+        qi[r] = fma(sn, mpr[r], fma(-c, mpi[r], api[r]));
+        sg[0] += pr[r] * qr[r] - pi[r] * qi[r];
+        sg[1] += pr[r] * qi[r] + pi[r] * qr[r];
+      }
+      cta_allsum<2>(sg, sh.red, sh.par);
+      const double sden = sg[0] * sg[0] + sg[1] * sg[1];
+      if (!(sden > 0.0)) break;                      // breakdown: keep the current X
+      const double al_r = (rho_r * sg[0] + rho_i * sg[1]) / sden;
+      const double al_i = (rho_i * sg[0] - rho_r * sg[1]) / sden;
+      double rz[3] = {0.0, 0.0, 0.0};
+      double zr[R], zi[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        xr[r] += al_r * pr[r] - al_i * pi[r];
+        xi[r] += al_r * pi[r] + al_i * pr[r];
+        rr[r] -= al_r * qr[r] - al_i * qi[r];
+        ri[r] -= al_r * qi[r] + al_i * qr[r];
+        zr[r] = ir[r] * rr[r] - ii[r] * ri[r];
+        zi[r] = ir[r] * ri[r] + ii[r] * rr[r];
+        rz[0] += rr[r] * zr[r] - ri[r] * zi[r];
+        rz[1] += rr[r] * zi[r] + ri[r] * zr[r];
+        rz[2] += rr[r] * rr[r] + ri[r] * ri[r];
+      }
+      cta_allsum<3>(rz, sh.red, sh.par);
+      ++it;
+      if (rz[2] <= tol2 || !isfinite(rz[2]) || it >= a.max_it) break;
+      const double rden = rho_r * rho_r + rho_i * rho_i;
+      if (!(rden > 0.0)) break;
+      const double be_r = (rz[0] * rho_r + rz[1] * rho_i) / rden;
+      const double be_i = (rz[1] * rho_r - rz[0] * rho_i) / rden;
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double npr = zr[r] + be_r * pr[r] - be_i * pi[r];
+        const double npi = zi[r] + be_r * pi[r] + be_i * pr[r];
+        pr[r] = npr;
+        pi[r] = npi;
+      }
+      rho_r = rz[0];
+      rho_i = rz[1];
+    }
+  }
+  double* X = a.X + (int64_t)item * 2 * pa.N;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    if (!Op::ok(r, pa)) continue;
+    const bool fin = isfinite(xr[r]) && isfinite(xi[r]);
+    X[Op::row(r, pa)] = fin ? xr[r] : 0.0;
+    X[pa.N + Op::row(r, pa)] = fin ? xi[r] : 0.0;
+  }
+  if (threadIdx.x == 0 && a.iters != nullptr) a.iters[item] = it;
+}
+
 inline int rows_per_thread(int N) {
   if (N <= kSmallThreads) return 1;
   if (N <= 2 * kSmallThreads) return 2;
   return 4;
 }
 inline size_t small_smem(int buf_doubles, int R) {
-  return (size_t)(3 * buf_doubles + 2 * kMaxWarps * 4 + kMaxOrder * R * kSmallThreads) *
+  return (size_t)(3 * buf_doubles + 2 * kMaxWarps * 4 + (kRing + 2) * R * kSmallThreads) *
          sizeof(double);
 }
 
@@ -848,15 +1079,49 @@ struct LaunchCoarse {
   }
 };
 
+template <class Op, int OCC>
+struct LaunchPeriodic {
+  static int run(const PeriodicArgs& a, unsigned grid, int nt, size_t smem, cudaStream_t st) {
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(small_periodic_kernel<Op>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    small_periodic_kernel<Op><<<grid, nt, smem, st>>>(a);
+    MLMCP_LAUNCH_CHECK("small_periodic_kernel");
+    return MLMCP_OK;
+  }
+};
+
 }  // namespace
+
+int small_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
+                   const double* K, const double* profile, double omega, double rtol,
+                   int max_it, double* X, int32_t* iters, cudaStream_t stream) {
+  if (n == 0) return MLMCP_OK;
+  PeriodicArgs a{};
+  a.sample = sample;
+  a.dt = dt;
+  a.n = n;
+  a.nnz = ctx->nnz;
+  a.M = M;
+  a.K = K;
+  a.profile = profile;
+  a.omega = omega;
+  a.rtol2 = rtol * rtol;
+  a.max_it = max_it;
+  a.X = X;
+  a.iters = iters;
+  return dispatch<LaunchPeriodic>(ctx, a, (unsigned)n, stream);
+}
 
 int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
                     const double* K, const double* profile, double omega, double rtol,
                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                    const int32_t* active, int64_t* elapsed, cudaStream_t stream) {
+                    const int32_t* active, int64_t* elapsed, const double* xss,
+                    cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
   SmallArgs a{};
   a.elapsed = elapsed;
+  a.xss = xss;
   a.tasks = tasks;
   a.n_tasks = n_tasks;
   a.nnz = ctx->nnz;
@@ -879,10 +1144,11 @@ int small_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const 
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
                           int32_t* status, const int32_t* active, int64_t* elapsed,
-                          cudaStream_t stream) {
+                          const double* xss, cudaStream_t stream) {
   if (S == 0) return MLMCP_OK;
   CoarseArgs a{};
   a.elapsed = elapsed;
+  a.xss = xss;
   a.S = S;
   a.k = k;
   a.m = m;

@@ -623,6 +623,8 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
       t.slot = s;
       t.tag = n;
       t.flags = 0;
+      t.qoi_index = 0;
+      t.ss_slot = -1;
     }
     MLMCP_CUDA_CHECK(cudaMemcpyAsync(dtasks, h.data(), sizeof(mlmcp_task) * S,
                                      cudaMemcpyHostToDevice, stream));

@@ -44,6 +44,7 @@ def new_tasks(n: int) -> np.ndarray:
     t["qoi_slot"] = -1
     t["group"] = -1
     t["slot"] = -1
+    t["ss_slot"] = -1
     return t
 
 
@@ -148,7 +149,7 @@ class DeviceSystem:
     # ------------------------------------------------------------ K2-K4, K6
     def propagate(self, tasks: np.ndarray, M, K, profile, omega: float, rtol: float,
                   max_it: int, xbuf, qoi=None, iters=None, status=None, active=None,
-                  stream=None, tasks_dev: torch.Tensor | None = None, elapsed=None):
+                  stream=None, tasks_dev: torch.Tensor | None = None, elapsed=None, xss=None):
         n = len(tasks)
         if n == 0:
             return None
@@ -156,7 +157,8 @@ class DeviceSystem:
         td = tasks_dev if tasks_dev is not None else tasks_to_device(tasks, self.device)
         ws = self.workspace(n, S)
         check(self.lib.mlmcp_propagate(self.ctx, n, ptr(td), S, ptr(M), ptr(K), ptr(profile),
-                                       float(omega), float(rtol), int(max_it), ptr(xbuf), ptr(qoi),
+                                       float(omega), float(rtol), int(max_it), ptr(xss),
+                                       ptr(xbuf), ptr(qoi),
                                        ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(ws),
                                        0 if ws is None else ws.numel(), stream_handle(stream)),
               "mlmcp_propagate")
@@ -164,13 +166,29 @@ class DeviceSystem:
 
     # ------------------------------------------------------------ K5
     def parareal_coarse(self, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0, slice_steps,
-                        rtol, max_it, U, F, C, iters, status, active, stream=None, elapsed=None):
+                        rtol, max_it, U, F, C, iters, status, active, stream=None, elapsed=None,
+                        xss=None):
         ws = self.workspace(S, S)
         check(self.lib.mlmcp_parareal_coarse(
             self.ctx, S, k, m, ptr(M), ptr(K), ptr(profile), float(omega), float(dt_c), float(t0),
             ptr(slice_k0), ptr(slice_steps), float(rtol), int(max_it), ptr(U), ptr(F), ptr(C),
-            ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(ws),
+            ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(xss), ptr(ws),
             0 if ws is None else ws.numel(), stream_handle(stream)), "mlmcp_parareal_coarse")
+
+    # ------------------------------------------------------------ predictor
+    def periodic_state(self, sample_idx: torch.Tensor, dts: torch.Tensor, M, K, profile,
+                       omega: float, rtol: float = 1e-8, max_it: int = 500, stream=None):
+        """X [n, 2, N]: periodic steady states of the implicit-Euler iteration
+        for (sample_idx[i], dts[i]) (initial-guess predictor)."""
+        n = len(sample_idx)
+        X = torch.empty((n, 2, self.n_rows), dtype=F64, device=self.device)
+        if n:
+            check(self.lib.mlmcp_periodic_state(self.ctx, n, ptr(sample_idx), ptr(dts),
+                                                M.shape[0], ptr(M), ptr(K), ptr(profile),
+                                                float(omega), float(rtol), int(max_it), ptr(X),
+                                                None, stream_handle(stream)),
+                  "mlmcp_periodic_state")
+        return X
 
     def parareal_defect(self, S, k, m, k_max, U, F, tol, active, k_used, defects, stream=None):
         check(self.lib.mlmcp_parareal_defect(self.ctx, S, k, m, k_max, ptr(U), ptr(F), float(tol),
