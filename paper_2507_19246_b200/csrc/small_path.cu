@@ -166,6 +166,12 @@ struct StencilOp {
       out[r] = acc0 + acc1;
     }
   }
+  // M stays in global memory (L2)
+  __device__ void load_mass(const PatternArgs&, const double* __restrict__, double*) const {}
+  __device__ void apply_mass(const double* __restrict__ Ms, const double*, const double (&v)[R],
+                             double* buf, const PatternArgs& pa, double (&out)[R]) const {
+    apply_vals(Ms, v, buf, pa, out);
+  }
   __device__ void apply_vals(const double* __restrict__ vals, const double (&v)[R], double* buf,
                              const PatternArgs& pa, double (&out)[R]) const {
     const double* b = base(buf, pa);
@@ -249,6 +255,12 @@ struct CsrOp {
       }
       out[r] = acc0 + acc1;
     }
+  }
+  // M stays in global memory (L2)
+  __device__ void load_mass(const PatternArgs&, const double* __restrict__, double*) const {}
+  __device__ void apply_mass(const double* __restrict__ Ms, const double*, const double (&v)[R],
+                             double* buf, const PatternArgs& pa, double (&out)[R]) const {
+    apply_vals(Ms, v, buf, pa, out);
   }
   __device__ void apply_vals(const double* __restrict__ vals, const double (&v)[R], double* buf,
                              const PatternArgs& pa, double (&out)[R]) const {
@@ -343,6 +355,56 @@ struct GridOp {
       out[r] = acc0 + acc1;
     }
   }
+  // Mass matrix in shared memory, symmetric half: slots C, E, N, NE of every
+  // (thread, r) slot (the W/S/SW coefficients of a row are the E/N/NE ones of
+  // its W/S/SW neighbour, M being symmetric).  Loaded once per task; the
+  // per-step rhs M a_n then needs no global loads.
+  static constexpr int kMassSlots = 4;
+  __device__ void load_mass(const PatternArgs& pa, const double* __restrict__ Ms,
+                            double* mm) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const bool v = ok(r, pa);
+      const int rw = v ? row(r, pa) : 0;
+      const int k = r * kSmallThreads + threadIdx.x;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int q = v ? pa.gpos[(3 + j) * pa.N + rw] : -1;
+        mm[j * (R * kSmallThreads) + k] = q >= 0 ? __ldg(Ms + q) : 0.0;
+      }
+    }
+  }
+  __device__ void apply_mass(const double* __restrict__, const double* mm, const double (&v)[R],
+                             double* buf, const PatternArgs& pa, double (&out)[R]) const {
+    double nb[R][7];
+    neighbours(v, buf, nb);
+    constexpr int L = R * kSmallThreads;
+    const int t = threadIdx.x;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int k = r * kSmallThreads + t;
+      // neighbour slots: W = (t-1, r); S = (t, r-1) or (t-32, R-1); SW = S shifted west
+      const int kw = k - 1;                                   // lane 0: a padding slot (0)
+      const int ks = r > 0 ? k - kSmallThreads : t - 32 + (R - 1) * kSmallThreads;
+      const int ksw = ks - 1;
+      const bool has_s = r > 0 || warp() > 0;
+      const double mw = lane() > 0 ? mm[1 * L + kw] : 0.0;
+      const double msn = has_s ? mm[2 * L + ks] : 0.0;
+      const double msw = (has_s && lane() > 0) ? mm[3 * L + ksw] : 0.0;
+      double acc = 0.0;
+      if (ok(r, pa)) {
+        acc = fma(msw, nb[r][0], acc);
+        acc = fma(msn, nb[r][1], acc);
+        acc = fma(mw, nb[r][2], acc);
+        acc = fma(mm[0 * L + k], nb[r][3], acc);
+        acc = fma(mm[1 * L + k], nb[r][4], acc);
+        acc = fma(mm[2 * L + k], nb[r][5], acc);
+        acc = fma(mm[3 * L + k], nb[r][6], acc);
+      }
+      out[r] = acc;
+    }
+    (void)pa;
+  }
   __device__ void apply_vals(const double* __restrict__ vals, const double (&v)[R], double* buf,
                              const PatternArgs& pa, double (&out)[R]) const {
     double nb[R][7];
@@ -370,6 +432,7 @@ struct SmallShared {
   double* red;   // [2][kMaxWarps][4]
   double* ring;  // [kRing][R*256] state history (per-thread slots)
   double* xs;    // [2][R*256] periodic steady state X (real, imaginary) per thread slot
+  double* mm;    // [Op::kMassSlots][R*256] mass coefficients (GridOp), else unused
   int par;
 };
 
@@ -490,7 +553,7 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
   op.publish(x, sh.bufB, pa);
   __syncthreads();
   double res[R], u[R], p[R], s[R], w[R], mx[R], ax[R];
-  op.apply_vals(Ms, an, sh.bufA, pa, mx);
+  op.apply_mass(Ms, sh.mm, an, sh.bufA, pa, mx);
   op.apply(x, sh.bufB, pa, ax);
   double red3[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -602,8 +665,9 @@ __device__ __forceinline__ SmallShared setup_shared(double* smem, int len) {
   for (int i = threadIdx.x; i < 3 * len; i += kSmallThreads) smem[i] = 0.0;
   __syncthreads();
   double* ring = smem + 3 * len + 2 * kMaxWarps * 4;
-  return SmallShared{smem, smem + len, smem + 2 * len, smem + 3 * len, ring,
-                     ring + kRing * R * kSmallThreads, 0};
+  double* xs = ring + kRing * R * kSmallThreads;
+  return SmallShared{smem, smem + len, smem + 2 * len, smem + 3 * len, ring, xs,
+                     xs + 2 * R * kSmallThreads, 0};
 }
 
 // X of one (sample, dt) into the thread's smem slots (own rows only: read
@@ -643,6 +707,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   const double* Ks = a.K + (int64_t)t.sample * a.nnz;
   Op op;
   op.load(pa, Ms, Ks, t.dt);
+  op.load_mass(pa, Ms, sh.mm);
   const bool no_extrap = (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) != 0;
   const bool pred = !no_extrap && a.xss != nullptr && t.ss_slot >= 0;
   if (pred) load_steady<Op>(a.xss + (int64_t)t.ss_slot * 2 * pa.N, pa, sh.xs);
@@ -762,6 +827,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
   const double* Ks = a.K + (int64_t)s * a.nnz;
   Op op;
   op.load(pa, Ms, Ks, a.dt);
+  op.load_mass(pa, Ms, sh.mm);
   const bool pred = a.xss != nullptr;
   if (pred) load_steady<Op>(a.xss + (int64_t)s * 2 * pa.N, pa, sh.xs);
   const int64_t N = pa.N;
@@ -980,9 +1046,9 @@ inline int rows_per_thread(int N) {
   if (N <= 2 * kSmallThreads) return 2;
   return 4;
 }
-inline size_t small_smem(int buf_doubles, int R) {
-  return (size_t)(3 * buf_doubles + 2 * kMaxWarps * 4 + (kRing + 2) * R * kSmallThreads) *
-         sizeof(double);
+inline size_t small_smem(int buf_doubles, int R, int mass_slots) {
+  return (size_t)(3 * buf_doubles + 2 * kMaxWarps * 4 +
+                  (kRing + 2 + mass_slots) * R * kSmallThreads) * sizeof(double);
 }
 
 // kernel variant: 0 auto (grid > stencil > csr), 1 no grid tiling (tests / A-B)
@@ -1021,7 +1087,7 @@ int dispatch(const Ctx* ctx, Args& a, unsigned grid, cudaStream_t stream) {
     pa.gh = ctx->grid_h;
     pa.gpos = ctx->grid_pos;
     a.buf_doubles = GridOp::buffer_doubles(0);
-    const size_t smem = small_smem(a.buf_doubles, GridOp::R);
+    const size_t smem = small_smem(a.buf_doubles, GridOp::R, GridOp::kMassSlots);
     return occ == 2 ? Launch<GridOp, 2>::run(a, grid, kSmallThreads, smem, stream)
                     : Launch<GridOp, 1>::run(a, grid, kSmallThreads, smem, stream);
   }
@@ -1037,7 +1103,7 @@ int dispatch(const Ctx* ctx, Args& a, unsigned grid, cudaStream_t stream) {
     }
   }
   a.buf_doubles = R * kSmallThreads + 2 * pa.pad;
-  const size_t smem = small_smem(a.buf_doubles, R);
+  const size_t smem = small_smem(a.buf_doubles, R, 0);
   if (smem > 200 * 1024) {
     set_error("SM-resident path: shared-memory footprint too large for this pattern");
     return MLMCP_EINVAL;
