@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 3
+#define MLMCP_ABI_VERSION 4
 
 /* return codes */
 #define MLMCP_OK 0
@@ -225,6 +225,22 @@ int mlmcp_parareal_defect(mlmcp_ctx* ctx, int S, int k, int m, int k_max,
 int mlmcp_parareal_finalize(mlmcp_ctx* ctx, int S, int m, double* U_d,
                             const double* F_d, const int32_t* k_used_d,
                             void* stream);
+
+/* ---- sample draws ------------------------------------------------------ */
+/* Uniform parameters for the sample keys (seed, level, k), k = k_first ..
+ * k_first + n - 1 (SPEC.md:250-254 RandomStream; models.py:305-318
+ * draw_parameters):  out[i][j] = lo[j] + range[j] * U_ij, where U_i. are the
+ * first P doubles of numpy.random.default_rng(SeedSequence(seed,
+ * spawn_key=(level, k))) and range = hi - lo — bitwise identical to
+ * rng.uniform(lo, hi).  seed, level, k < 2^64.  Device version: lo_d,
+ * range_d, out_d device pointers, stream-ordered; host version: the same
+ * arithmetic on the CPU (parity checks). */
+int mlmcp_draw_uniform(uint64_t seed, uint64_t level, int64_t k_first, int n,
+                       int P, const double* lo_d, const double* range_d,
+                       double* out_d, void* stream);
+int mlmcp_draw_uniform_host(uint64_t seed, uint64_t level, int64_t k_first,
+                            int n, int P, const double* lo, const double* range,
+                            double* out);
 
 /* ---- K6 / K7 ----------------------------------------------------------- */
 /* out[i] = 1/2 x_i^T K_{sample[i]} x_i for x_i = xbuf[x_off[i] ..]. */

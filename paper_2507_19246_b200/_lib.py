@@ -35,7 +35,7 @@ STATUS_INTS = 4
 
 QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2, 3, 4
 TASK_NO_EXTRAPOLATION = 1
-ABI_VERSION = 3
+ABI_VERSION = 4
 DIRECT_MAX_ROWS = 4
 
 # mlmcp_task (96 bytes, natural alignment)
@@ -54,7 +54,8 @@ EXPORTS = (
     "mlmcp_ctx_create", "mlmcp_ctx_destroy", "mlmcp_ctx_info", "mlmcp_ctx_set_assembly",
     "mlmcp_ctx_set_path", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
     "mlmcp_propagate", "mlmcp_periodic_state", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
-    "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce",
+    "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce", "mlmcp_draw_uniform",
+    "mlmcp_draw_uniform_host",
 )
 
 _lock = threading.Lock()
@@ -91,6 +92,10 @@ _SIGS = {
     "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, P, F64, P, P, P, P]),
     "mlmcp_parareal_finalize": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+    "mlmcp_draw_uniform": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, I64, ctypes.c_int,
+                                          ctypes.c_int, P, P, P, P]),
+    "mlmcp_draw_uniform_host": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, I64,
+                                               ctypes.c_int, ctypes.c_int, P, P, P]),
     "mlmcp_energy": (ctypes.c_int, [P, ctypes.c_int, P, P, P, P, P, P]),
     "mlmcp_level_reduce": (ctypes.c_int, [ctypes.c_int, P, P, P, P]),
 }

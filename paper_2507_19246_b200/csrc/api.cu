@@ -476,6 +476,21 @@ int mlmcp_periodic_state(mlmcp_ctx* c, int n, const int32_t* sample, const doubl
                         (cudaStream_t)stream);
 }
 
+int mlmcp_draw_uniform(uint64_t seed, uint64_t level, int64_t k_first, int n, int P,
+                       const double* lo, const double* range, double* out, void* stream) {
+  if (n < 0 || P < 1 || k_first < 0 || (n > 0 && (!lo || !range || !out)))
+    return einval("bad draw arguments");
+  return draw_uniform_device(seed, level, k_first, n, P, lo, range, out, (cudaStream_t)stream);
+}
+
+int mlmcp_draw_uniform_host(uint64_t seed, uint64_t level, int64_t k_first, int n, int P,
+                            const double* lo, const double* range, double* out) {
+  if (n < 0 || P < 1 || k_first < 0 || (n > 0 && (!lo || !range || !out)))
+    return einval("bad draw arguments");
+  draw_uniform_cpu(seed, level, k_first, n, P, lo, range, out);
+  return MLMCP_OK;
+}
+
 int mlmcp_parareal_defect(mlmcp_ctx* c, int S, int k, int m, int k_max, const double* U,
                           const double* F, double tol, int32_t* active, int32_t* k_used,
                           double* defect, void* stream) {

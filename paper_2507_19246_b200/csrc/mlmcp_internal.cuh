@@ -179,6 +179,11 @@ int direct_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
                            const double* F, double* C, int32_t* status, const int32_t* active,
                            int64_t* elapsed, cudaStream_t stream);
 
+int draw_uniform_device(uint64_t seed, uint64_t level, int64_t k_first, int n, int P,
+                        const double* lo, const double* range, double* out, cudaStream_t stream);
+void draw_uniform_cpu(uint64_t seed, uint64_t level, int64_t k_first, int n, int P,
+                      const double* lo, const double* range, double* out);
+
 size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S);
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,

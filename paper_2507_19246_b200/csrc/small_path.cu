@@ -752,9 +752,12 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
       if (t.qoi_mode == MLMCP_QOI_SUM_ENERGY) {
         acc += block_energy<Op>(op, x, pa, Ks, sh);
       } else if (t.qoi_mode == MLMCP_QOI_JOULE) {
-        double d[R];
+        // a_n = y_n + ss_n from the history (keeps a_n out of the registers)
+        double sp = 0.0, cp = 0.0, ssn[R], d[R];
+        if (pred) sincos(__dmul_rn(a.omega, grid_time(t.t_base, g - 1, t.dt)), &sp, &cp);
+        steady_state<R>(sh.xs, pred, sp, cp, ssn);
 #pragma unroll
-        for (int r = 0; r < R; ++r) d[r] = x[r] - an[r];   // 0 on padding slots
+        for (int r = 0; r < R; ++r) d[r] = x[r] - (hist.y(1, r) + ssn[r]);   // 0 on padding
         acc += 2.0 * block_energy<Op>(op, d, pa, Ms, sh);
       } else if (t.qoi_mode == MLMCP_QOI_ELECTRICAL) {
 #pragma unroll

@@ -36,7 +36,7 @@ from .models import EvalRecord, LevelSpec, draw_parameters
 
 __all__ = ["RandomStream", "LevelStats", "EstimatorResult", "FixedSamples", "WarmupPolicy",
            "coupled_sample", "mc_estimate", "optimal_allocation", "mlmc_estimate",
-           "draw_level", "shard_range", "LazyDraw", "estimate_dict",
+           "draw_level", "draw_level_device", "shard_range", "LazyDraw", "estimate_dict",
            "write_estimate_json"]
 
 
@@ -104,7 +104,10 @@ def draw_level(uncertain, seed: int, level: int, indices) -> np.ndarray:
     """Host draws for sample keys (seed, level, k), k in ``indices`` (1-based).
 
     Row k equals ``draw_parameters(uncertain, RandomStream(seed, level, k)).values``
-    bitwise (same generator, same call, same arithmetic, models.py:305-318); the
+    bitwise (same generator, same call, same arithmetic, models.py:305-318).
+    Uniform inputs run through libmlmcp's native restatement of SeedSequence /
+    PCG64 / ``uniform`` (``mlmcp_draw_uniform_host``, ~300x faster than one
+    numpy Generator per sample; tests/test_draws.py pins it to numpy); the
     per-sample ParameterVector validation is done once on the whole block."""
     from .models import GaussianInput, ParameterVector
     idx = [int(k) for k in indices]
@@ -121,10 +124,46 @@ def draw_level(uncertain, seed: int, level: int, indices) -> np.ndarray:
         return out
     lo = nominal * (1.0 - h)
     hi = nominal * (1.0 + h)
-    for i, k in enumerate(idx):
-        out[i] = RandomStream(seed, level, k).generator().uniform(lo, hi)
+    if len(idx) and idx == list(range(idx[0], idx[0] + len(idx))) and min(seed, level, idx[0]) >= 0:
+        _draw_uniform_host(int(seed), int(level), idx[0], lo, hi - lo, out)
+    else:
+        for i, k in enumerate(idx):
+            out[i] = RandomStream(seed, level, k).generator().uniform(lo, hi)
     if len(idx) and not np.all(out > 0.0):
         ParameterVector(uncertain.nominal.model_id, out[np.argmin(out.min(axis=1))])  # raises
+    return out
+
+
+def _draw_uniform_host(seed: int, level: int, k_first: int, lo, rng, out):
+    from . import _lib
+    lo = np.ascontiguousarray(lo, dtype=np.float64)
+    rng = np.ascontiguousarray(rng, dtype=np.float64)
+    _lib.check(_lib.load().mlmcp_draw_uniform_host(seed, level, k_first, out.shape[0],
+                                                   out.shape[1], _lib.np_ptr(lo),
+                                                   _lib.np_ptr(rng), _lib.np_ptr(out)),
+               "mlmcp_draw_uniform_host")
+
+
+def draw_level_device(uncertain, seed: int, level: int, k_first: int, n: int, out):
+    """Device draws (``mlmcp_draw_uniform``) of keys (seed, level, k_first..)
+    into the [n, P] float64 CUDA tensor ``out`` — bitwise equal to
+    ``draw_level``; uniform inputs only."""
+    import torch
+
+    from . import _lib
+    from .engine import stream_handle
+    nominal = uncertain.nominal.values
+    h = uncertain.relative_halfwidth
+    if h == 0.0:
+        out.copy_(torch.from_numpy(np.broadcast_to(nominal, (n, len(nominal))).copy()))
+        return out
+    lo = nominal * (1.0 - h)
+    rng = nominal * (1.0 + h) - lo
+    lr = torch.from_numpy(np.stack([lo, rng])).to(out.device)
+    _lib.check(_lib.load().mlmcp_draw_uniform(int(seed), int(level), int(k_first), int(n),
+                                              len(nominal), _lib.ptr(lr[0]), _lib.ptr(lr[1]),
+                                              _lib.ptr(out), stream_handle()),
+               "mlmcp_draw_uniform")
     return out
 
 

@@ -210,3 +210,21 @@ def test_streaming_64_mesh_vs_oracle(cuda, impl, monkeypatch):
     rec = mo.evaluate(prob, cfg, pp[0], T / 128, True, dense=False)
     assert int(b.k_used[0].item()) == rec.k_used
     assert abs(b.q_l[0].item() - rec.q) <= 1e-8 * abs(rec.q)
+
+
+def test_device_draws_bitwise(cuda):
+    """mlmcp_draw_uniform (device) == draw_level (host) == numpy RandomStream."""
+    import torch
+
+    from paper_2507_19246_b200.mlmc import RandomStream, draw_level, draw_level_device
+    from paper_2507_19246_b200.models import ParameterVector, UncertainInput
+    nominal = np.array([795.77] * 4 + [1e6] * 4)
+    inp = UncertainInput(ParameterVector("quad4", nominal), 0.1)
+    for seed, lvl, kf, n in ((0, 0, 1, 1000), (5, 2, 2 ** 32 - 3, 7), (2 ** 40, 1, 17, 33)):
+        out = torch.empty((n, 8), dtype=torch.float64, device="cuda")
+        draw_level_device(inp, seed, lvl, kf, n, out)
+        host = draw_level(inp, seed, lvl, range(kf, kf + n))
+        np.testing.assert_array_equal(out.cpu().numpy(), host)
+        np.testing.assert_array_equal(
+            host[-1], RandomStream(seed, lvl, kf + n - 1).generator().uniform(nominal * 0.9,
+                                                                                 nominal * 1.1))
