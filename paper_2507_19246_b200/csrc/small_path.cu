@@ -66,15 +66,27 @@ template <int NV>
 __device__ __forceinline__ void cta_allsum(double (&v)[NV], double* red, int& par) {
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
-  }
   double* buf = red + par * (kMaxWarps * 4);
-  if (lane == 0) {
+  if (NV == 2) {
+    // reduce-scatter butterfly: after the first exchange the lower half-warp
+    // carries v[0], the upper half v[1] (half the shuffles of two butterflies)
+    const bool hi = (lane & 16) != 0;
+    double keep = hi ? v[1 % NV] : v[0];
+    const double send = hi ? v[0] : v[1 % NV];
+    keep += __shfl_xor_sync(0xffffffffu, send, 16);
 #pragma unroll
-    for (int k = 0; k < NV; ++k) buf[warp * 4 + k] = v[k];
+    for (int off = 8; off > 0; off >>= 1) keep += __shfl_xor_sync(0xffffffffu, keep, off);
+    if ((lane & 15) == 0) buf[warp * 4 + (hi ? 1 : 0)] = keep;
+  } else {
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int k = 0; k < NV; ++k) buf[warp * 4 + k] = v[k];
+    }
   }
   __syncthreads();
   auto ld = [&](int w, double (&o)[NV]) {
@@ -302,6 +314,9 @@ struct GridOp {
       const int rw = v ? row(r, pa) : 0;
 #pragma unroll
       for (int j = 0; j < 7; ++j) {
+        // A symmetric: the S coefficient of slot r >= 1 is the N coefficient of
+        // slot r-1 (same thread), so it is never loaded (6 registers)
+        if (j == 1 && r > 0) continue;
         const int q = v ? pa.gpos[j * pa.N + rw] : -1;
         a[r][j] = q >= 0 ? op_entry(__ldg(Ms + q), __ldg(Ks + q), dt) : 0.0;
       }
@@ -347,7 +362,7 @@ struct GridOp {
     for (int r = 0; r < R; ++r) {
       double acc0 = a[r][3] * nb[r][3];
       double acc1 = a[r][0] * nb[r][0];
-      acc0 = fma(a[r][1], nb[r][1], acc0);
+      acc0 = fma(r > 0 ? a[r - 1][5] : a[0][1], nb[r][1], acc0);
       acc1 = fma(a[r][2], nb[r][2], acc1);
       acc0 = fma(a[r][4], nb[r][4], acc0);
       acc1 = fma(a[r][5], nb[r][5], acc1);
