@@ -158,6 +158,11 @@ struct StencilOp {
       dinv[r] = v ? 1.0 / diag : 0.0;
     }
   }
+  // Jacobi: z = D^-1 r
+  __device__ void precond(const double (&r_)[R], double (&z)[R]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[r] = dinv[r] * r_[r];
+  }
   __device__ static double* base(double* buf, const PatternArgs& pa) { return buf + pa.pad; }
   __device__ void publish(const double (&v)[R], double* buf, const PatternArgs& pa) const {
 #pragma unroll
@@ -251,6 +256,11 @@ struct CsrOp {
       dinv[r] = v ? 1.0 / diag : 0.0;
     }
   }
+  // Jacobi: z = D^-1 r
+  __device__ void precond(const double (&r_)[R], double (&z)[R]) const {
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[r] = dinv[r] * r_[r];
+  }
   __device__ void publish(const double (&v)[R], double* buf, const PatternArgs& pa) const {
 #pragma unroll
     for (int r = 0; r < R; ++r) buf[row(r, pa)] = v[r];
@@ -295,7 +305,8 @@ struct CsrOp {
 struct GridOp {
   static constexpr int R = 4;
   double a[R][7];
-  double dinv[R];
+  double dinv[R];     // 1/d_r of the strip's L D L^T
+  double lf[R - 1];   // strip L factor
   __device__ static int lane() { return threadIdx.x & 31; }
   __device__ static int warp() { return threadIdx.x >> 5; }
   __device__ static int gy(int r) { return 4 * warp() + r; }
@@ -320,8 +331,30 @@ struct GridOp {
         const int q = v ? pa.gpos[j * pa.N + rw] : -1;
         a[r][j] = q >= 0 ? op_entry(__ldg(Ms + q), __ldg(Ks + q), dt) : 0.0;
       }
-      dinv[r] = (v && a[r][3] != 0.0) ? 1.0 / a[r][3] : 0.0;
     }
+    // Block-Jacobi preconditioner on the thread's 4-row vertical strip (the
+    // N/S couplings inside the strip): B = L D L^T, tridiagonal, SPD as a
+    // principal submatrix of A.  ~20% fewer PCG iterations than point Jacobi
+    // on configs 0/1 for 10 fp64 ops per application instead of 4.
+    double d = a[0][3];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (r > 0) {
+        const double nprev = a[r - 1][5];            // = S coefficient of slot r
+        lf[r - 1] = (d != 0.0) ? nprev / d : 0.0;
+        d = a[r][3] - lf[r - 1] * nprev;
+      }
+      dinv[r] = (ok(r, pa) && d != 0.0) ? 1.0 / d : 0.0;
+    }
+  }
+  __device__ void precond(const double (&r_)[R], double (&z)[R]) const {
+    double y[R];
+    y[0] = r_[0];
+#pragma unroll
+    for (int r = 1; r < R; ++r) y[r] = fma(-lf[r - 1], y[r - 1], r_[r]);
+    z[R - 1] = dinv[R - 1] * y[R - 1];
+#pragma unroll
+    for (int r = R - 2; r >= 0; --r) z[r] = fma(-lf[r], z[r + 1], dinv[r] * y[r]);
   }
   // halo rows: lo[w+1][l+1] = v[0] of warp w, hi[w+1][l+1] = v[3]
   __device__ void publish(const double (&v)[R], double* buf, const PatternArgs&) const {
@@ -571,18 +604,23 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
   op.apply_mass(Ms, sh.mm, an, sh.bufA, pa, mx);
   op.apply(x, sh.bufB, pa, ax);
   double red3[3] = {0.0, 0.0, 0.0};
+  {
+    double bv[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    res[r] = 0.0;
-    u[r] = 0.0;
-    if (Op::ok(r, pa)) {
-      const int rw = Op::row(r, pa);
-      const double b = __dadd_rn(mx[r], __dmul_rn(dt, __dmul_rn(sf, __ldg(profile + rw))));
-      res[r] = b - ax[r];
-      u[r] = op.dinv[r] * res[r];
-      red3[2] = fma(b * op.dinv[r], b, red3[2]);
+    for (int r = 0; r < R; ++r) {
+      res[r] = 0.0;
+      bv[r] = 0.0;
+      if (Op::ok(r, pa)) {
+        const int rw = Op::row(r, pa);
+        bv[r] = __dadd_rn(mx[r], __dmul_rn(dt, __dmul_rn(sf, __ldg(profile + rw))));
+        res[r] = bv[r] - ax[r];
+      }
     }
+    op.precond(bv, u);                  // u = B^-1 b only for the norm of b
+#pragma unroll
+    for (int r = 0; r < R; ++r) red3[2] = fma(bv[r], u[r], red3[2]);
   }
+  op.precond(res, u);                   // 0 on padding slots
   op.publish(u, sh.bufC, pa);
   __syncthreads();
   op.apply(u, sh.bufC, pa, w);                    // a = 0 on padding slots
@@ -616,8 +654,7 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
   }
   int it = 1;
   for (;;) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) u[r] = op.dinv[r] * res[r];   // 0 on padding slots
+    op.precond(res, u);                 // 0 on padding slots
     op.publish(u, sh.bufC, pa);
     __syncthreads();
     op.apply(u, sh.bufC, pa, w);
@@ -640,9 +677,10 @@ __device__ __forceinline__ int ie_step(const Op& op, double (&x)[Op::R], const d
     alpha = gnew * fast_rcp(den);
     inv_g = fast_rcp(gnew);                // off the critical path (next iteration)
     c = inv_g * (den * inv_g);             // 1/(gnew*alpha)
+    op.precond(res, u);                 // u recomputed: fewer live registers
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-      p[r] = fma(beta, p[r], op.dinv[r] * res[r]);   // u recomputed: fewer live registers
+      p[r] = fma(beta, p[r], u[r]);
       s[r] = fma(beta, s[r], w[r]);
       x[r] = fma(alpha, p[r], x[r]);
       res[r] = fma(-alpha, s[r], res[r]);
