@@ -496,14 +496,15 @@ struct SmallShared {
 //    extrapolation predicts far better than the forced oscillation itself:
 //        x0 = ss_{n+1} + sum_{i=0..p} (-1)^i C(p+1, i+1) y_{n-i}.
 //    Configs 0/1: 29.7 -> 11.4 PCG iterations per step at T/256, 18.9 -> 10.9
-//    at T/1024 (p = 3; scripts in DESIGN.md §5).
-//  * Without X (ss = 0) this is plain extrapolation of the states (p <= 4).
+//    at T/1024 (p = 3, point Jacobi).
+//  * Without X (ss = 0) this is plain extrapolation of the states (p <= 3).
 //  * MLMCP_TASK_NO_EXTRAPOLATION: x0 = a_n (the reference's one-step method,
 //    bitwise semigroup).
 // The transients y live in a per-thread shared-memory ring touched once per
 // step.
-constexpr int kMaxOrder = 4;
-constexpr int kRing = kMaxOrder + 1;
+constexpr int kMaxOrder = 3;
+constexpr int kRing = kMaxOrder + 1;   // power of two: slot arithmetic is a mask
+static_assert((kRing & (kRing - 1)) == 0, "ring size must be a power of two");
 
 template <int R>
 struct StateHistory {
@@ -514,12 +515,12 @@ struct StateHistory {
   __device__ StateHistory(double* ring_, int max_ord)
       : ring(ring_), head(0), count(0), max_order(max_ord) {}
   __device__ double y(int i, int r) const {  // y_{n-i}
-    const int slot = (head - i + kRing) % kRing;
+    const int slot = (head - i) & (kRing - 1);
     return ring[slot * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x];
   }
   // y_{n+1} = x - ss joins the ring
   __device__ void push(const double (&x)[R], const double (&ss)[R]) {
-    head = (head + 1) % kRing;
+    head = (head + 1) & (kRing - 1);
 #pragma unroll
     for (int r = 0; r < R; ++r)
       ring[head * (R * kSmallThreads) + r * kSmallThreads + threadIdx.x] = x[r] - ss[r];
@@ -541,9 +542,8 @@ struct StateHistory {
         case 0: g = y(0, r); break;
         case 1: g = fma(2.0, y(0, r), -y(1, r)); break;
         case 2: g = fma(3.0, y(0, r) - y(1, r), y(2, r)); break;
-        case 3: g = fma(4.0, y(0, r) + y(2, r), fma(-6.0, y(1, r), -y(3, r))); break;
-        default:  // 5y_n - 10y_{n-1} + 10y_{n-2} - 5y_{n-3} + y_{n-4}
-          g = fma(5.0, y(0, r) - y(3, r), fma(10.0, y(2, r) - y(1, r), y(4, r)));
+        default:  // 4y_n - 6y_{n-1} + 4y_{n-2} - y_{n-3}
+          g = fma(4.0, y(0, r) + y(2, r), fma(-6.0, y(1, r), -y(3, r)));
           break;
       }
       x[r] = g + ss[r];
@@ -776,7 +776,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   int code = MLMCP_ST_OK;
   int fail_step = 0;
   double acc = 0.0;
-  StateHistory<R> hist(sh.ring, no_extrap ? 0 : (pred ? 3 : kMaxOrder));
+  StateHistory<R> hist(sh.ring, no_extrap ? 0 : kMaxOrder);
   {
     double s0 = 0.0, c0 = 0.0;
     if (pred) sincos(__dmul_rn(a.omega, grid_time(t.t_base, t.k0, t.dt)), &s0, &c0);
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
       if (v) U[(a.k - 1) * N + i] = x[r];
     }
   }
-  StateHistory<R> hist(sh.ring, pred ? 3 : kMaxOrder);
+  StateHistory<R> hist(sh.ring, kMaxOrder);
   double ss[R], an[R];
   double sf = 0.0, cf = 0.0;
   if (a.k < a.m) {
