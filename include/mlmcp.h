@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 4
+#define MLMCP_ABI_VERSION 7
 
 /* return codes */
 #define MLMCP_OK 0
@@ -225,6 +225,60 @@ int mlmcp_parareal_defect(mlmcp_ctx* ctx, int S, int k, int m, int k_max,
 int mlmcp_parareal_finalize(mlmcp_ctx* ctx, int S, int m, double* U_d,
                             const double* F_d, const int32_t* k_used_d,
                             void* stream);
+
+/* ---- fused estimate launch (SM-resident path) ---------------------------- */
+/* A batch of independent sequential tasks (mlmcp_propagate semantics) and/or
+ * a Parareal batch (mlmcp_parareal_coarse / propagate / defect / finalize
+ * semantics, parareal.py:121-220) run by ONE persistent launch with a
+ * device-side scheduler: each Parareal sample's chain (coarse slice n ->
+ * fine slice n+1, ..., defect, next iteration) advances as soon as its own
+ * inputs are ready, its ready steps take priority over the sequential tasks,
+ * and the sequential tasks fill all other SM slots.  Results are identical to
+ * the separate launches.  Every task kind addresses the SAME arrays: */
+typedef struct mlmcp_task_arrays {
+  int n_seq;                  /* sequential tasks seq_tasks_d[0 .. n_seq)        */
+  const mlmcp_task* seq_tasks_d;
+  const double* xss_d;        /* periodic steady states, row = task.ss_slot     */
+  double* xbuf_d;             /* states of every task (task offsets)            */
+  double* qoi_d;              /* task.qoi_slot                                  */
+  int32_t* iters_d;           /* task.slot: PCG iterations (summed)             */
+  int32_t* status_d;          /* task.slot: 4 ints                              */
+  int32_t* active_d;          /* task.group (Parareal sample), 1 on entry       */
+  int64_t* elapsed_ns_d;      /* task.slot (optional)                           */
+} mlmcp_task_arrays;
+
+typedef struct mlmcp_parareal_batch {
+  int S;                      /* samples (0: no Parareal)                       */
+  int row0;                   /* their operators: M/K rows row0 .. row0+S-1     */
+  int m;                      /* sub-intervals                                  */
+  int k_max;
+  double tol;
+  double dt_c;
+  double t0;
+  const int64_t* slice_k0_d;  /* [m] coarse grid offsets                        */
+  const int32_t* slice_steps_d; /* [m] coarse steps per slice                   */
+  const mlmcp_task* fine_tasks_d; /* [S*m]: fine slice (s, n) at s*m + n-1,
+                                     sample = row0 + s, group = s             */
+  int64_t u_off;              /* U [S][m+1][N] at xbuf_d + u_off, F follows U   */
+  int64_t c_tmp_off;          /* S*N scratch in xbuf_d (coarse results)         */
+  double* C_d;                /* [S][m][N] previous coarse values               */
+  int coarse_slot;            /* iters/status/elapsed slot of sample s's coarse
+                                 solves: coarse_slot + s (status: interval n,
+                                 iteration k, parareal.py:151-152)             */
+  int coarse_ss;              /* steady-state row at dt_c: coarse_ss + s (-1)   */
+  int32_t* k_used_d;          /* [S]                                            */
+  double* defects_d;          /* [S][k_max]                                     */
+} mlmcp_parareal_batch;
+
+size_t mlmcp_fused_workspace_bytes(int S_parareal, int m, int k_max);
+/* grid_ctas > 0 caps the persistent grid (e.g. a Parareal-only launch on
+ * grid_ctas SM slots next to a separate sequential launch); 0: all resident
+ * slots. */
+int mlmcp_run_fused(mlmcp_ctx* ctx, int S, const double* M_d, const double* K_d,
+                    const double* profile_d, double omega, double rtol,
+                    int max_it, const mlmcp_task_arrays* arrays,
+                    const mlmcp_parareal_batch* pr, int grid_ctas, void* ws_d,
+                    size_t ws_bytes, void* stream);
 
 /* ---- sample draws ------------------------------------------------------ */
 /* Uniform parameters for the sample keys (seed, level, k), k = k_first ..

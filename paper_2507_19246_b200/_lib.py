@@ -35,7 +35,7 @@ STATUS_INTS = 4
 
 QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2, 3, 4
 TASK_NO_EXTRAPOLATION = 1
-ABI_VERSION = 4
+ABI_VERSION = 7
 DIRECT_MAX_ROWS = 4
 
 # mlmcp_task (96 bytes, natural alignment)
@@ -48,6 +48,29 @@ TASK_DTYPE = np.dtype([
 ], align=True)
 assert TASK_DTYPE.itemsize == 96
 
+
+
+class TaskArrays(ctypes.Structure):
+    """mlmcp_task_arrays (include/mlmcp.h)."""
+    _fields_ = [("n_seq", ctypes.c_int), ("seq_tasks_d", ctypes.c_void_p),
+                ("xss_d", ctypes.c_void_p), ("xbuf_d", ctypes.c_void_p),
+                ("qoi_d", ctypes.c_void_p), ("iters_d", ctypes.c_void_p),
+                ("status_d", ctypes.c_void_p), ("active_d", ctypes.c_void_p),
+                ("elapsed_ns_d", ctypes.c_void_p)]
+
+
+class PararealBatch(ctypes.Structure):
+    """mlmcp_parareal_batch (include/mlmcp.h)."""
+    _fields_ = [("S", ctypes.c_int), ("row0", ctypes.c_int), ("m", ctypes.c_int),
+                ("k_max", ctypes.c_int), ("tol", ctypes.c_double), ("dt_c", ctypes.c_double),
+                ("t0", ctypes.c_double), ("slice_k0_d", ctypes.c_void_p),
+                ("slice_steps_d", ctypes.c_void_p), ("fine_tasks_d", ctypes.c_void_p),
+                ("u_off", ctypes.c_int64), ("c_tmp_off", ctypes.c_int64),
+                ("C_d", ctypes.c_void_p), ("coarse_slot", ctypes.c_int),
+                ("coarse_ss", ctypes.c_int), ("k_used_d", ctypes.c_void_p),
+                ("defects_d", ctypes.c_void_p)]
+
+
 # every symbol include/mlmcp.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "mlmcp_abi_version", "mlmcp_last_error", "mlmcp_launch_count",
@@ -55,7 +78,7 @@ EXPORTS = (
     "mlmcp_ctx_set_path", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
     "mlmcp_propagate", "mlmcp_periodic_state", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
     "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce", "mlmcp_draw_uniform",
-    "mlmcp_draw_uniform_host",
+    "mlmcp_draw_uniform_host", "mlmcp_fused_workspace_bytes", "mlmcp_run_fused",
 )
 
 _lock = threading.Lock()
@@ -92,6 +115,9 @@ _SIGS = {
     "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, P, F64, P, P, P, P]),
     "mlmcp_parareal_finalize": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+    "mlmcp_fused_workspace_bytes": (SZ, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
+    "mlmcp_run_fused": (ctypes.c_int, [P, ctypes.c_int, P, P, P, F64, F64, ctypes.c_int, P, P,
+                                       ctypes.c_int, P, SZ, P]),
     "mlmcp_draw_uniform": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, I64, ctypes.c_int,
                                           ctypes.c_int, P, P, P, P]),
     "mlmcp_draw_uniform_host": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, I64,

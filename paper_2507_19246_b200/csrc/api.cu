@@ -476,6 +476,34 @@ int mlmcp_periodic_state(mlmcp_ctx* c, int n, const int32_t* sample, const doubl
                         (cudaStream_t)stream);
 }
 
+size_t mlmcp_fused_workspace_bytes(int S, int m, int k_max) {
+  if (S < 0 || m < 0 || k_max < 0) return 0;
+  return fused_workspace_bytes(S, std::max(m, 1), std::max(k_max, 1));
+}
+
+int mlmcp_run_fused(mlmcp_ctx* c, int S, const double* M, const double* K, const double* profile,
+                    double omega, double rtol, int max_it, const mlmcp_task_arrays* ar,
+                    const mlmcp_parareal_batch* pr, int grid_ctas, void* ws, size_t ws_bytes,
+                    void* stream) {
+  if (c == nullptr || ar == nullptr || pr == nullptr) return einval("null fused argument");
+  if (grid_ctas < 0) return einval("grid_ctas must be >= 0");
+  if (S < 1 || !M || !K || !profile) return einval("null or empty operator arrays");
+  if (!(rtol > 0.0) || max_it < 1) return einval("rtol must be > 0 and max_it >= 1");
+  if (use_direct(c) || !use_small(c)) return einval("the fused launch needs the SM-resident path");
+  if (ar->n_seq < 0 || !ar->xbuf_d || (ar->n_seq > 0 && !ar->seq_tasks_d))
+    return einval("bad task arrays");
+  if (pr->S < 0 || (pr->S > 0 && (pr->m < 1 || pr->k_max < 1 || pr->k_max > pr->m ||
+                                  pr->row0 < 0 || pr->row0 + pr->S > S || !pr->fine_tasks_d ||
+                                  !pr->C_d || !pr->slice_k0_d || !pr->slice_steps_d ||
+                                  !ar->active_d || !ar->status_d || !pr->k_used_d ||
+                                  !pr->defects_d || pr->u_off < 0 || pr->c_tmp_off < 0 ||
+                                  pr->coarse_slot < 0 || !(pr->dt_c > 0.0))))
+    return einval("bad Parareal batch");
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  return small_run_fused(c, S, M, K, profile, omega, rtol, max_it, *ar, *pr, grid_ctas, ws,
+                         ws_bytes, (cudaStream_t)stream);
+}
+
 int mlmcp_draw_uniform(uint64_t seed, uint64_t level, int64_t k_first, int n, int P,
                        const double* lo, const double* range, double* out, void* stream) {
   if (n < 0 || P < 1 || k_first < 0 || (n > 0 && (!lo || !range || !out)))

@@ -156,6 +156,12 @@ int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double
                     const int32_t* active, int64_t* elapsed, const double* xss,
                     cudaStream_t stream);
 
+size_t fused_workspace_bytes(int S, int m, int k_max);
+int small_run_fused(Ctx* ctx, int S, const double* M, const double* K, const double* profile,
+                    double omega, double rtol, int max_it, const mlmcp_task_arrays& ar,
+                    const mlmcp_parareal_batch& pr, int grid_ctas, void* ws, size_t ws_bytes,
+                    cudaStream_t stream);
+
 int small_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
                    const double* K, const double* profile, double omega, double rtol,
                    int max_it, double* X, int32_t* iters, cudaStream_t stream);

@@ -30,6 +30,8 @@
 // model: one CTA per sample walks slices k..M-1 sequentially, the state stays
 // in registers between slices.
 #include <math.h>
+#include <stdio.h>
+#include <algorithm>
 #include <stdlib.h>
 
 #include "mlmcp_internal.cuh"
@@ -739,23 +741,12 @@ __device__ __forceinline__ void load_steady(const double* __restrict__ X, const 
   }
 }
 
-template <class Op, int OCC>
-__global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(SmallArgs a) {
+// One propagation task on the calling CTA (shared memory already carved).
+template <class Op>
+__device__ __forceinline__ void run_task(const SmallArgs& a, const mlmcp_task& t, SmallShared& sh,
+                                         int64_t t_start, int interval) {
   constexpr int R = Op::R;
-  extern __shared__ __align__(16) double smem[];
-  const mlmcp_task t = a.tasks[blockIdx.x];
-  const int64_t t_start = global_ns();
-  {
-    // another CTA of the same group may clear active[] concurrently (on a
-    // failure): decide once per block so the barriers below never diverge
-    __shared__ int skip;
-    if (threadIdx.x == 0)
-      skip = (a.active != nullptr && t.group >= 0 && a.active[t.group] == 0) ? 1 : 0;
-    __syncthreads();
-    if (skip) return;
-  }
   const PatternArgs& pa = a.pa;
-  SmallShared sh = setup_shared<R>(smem, a.buf_doubles);
   const double* Ms = a.M + (int64_t)t.sample * a.nnz;
   const double* Ks = a.K + (int64_t)t.sample * a.nnz;
   Op op;
@@ -769,7 +760,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   for (int r = 0; r < R; ++r) {
     const bool v = Op::ok(r, pa);
     const int rw = v ? Op::row(r, pa) : 0;
-    x[r] = v ? a.xbuf[t.x_in + rw] : 0.0;
+    x[r] = v ? __ldcg(a.xbuf + t.x_in + rw) : 0.0;   // L2: may come from another CTA
     if (t.traj >= 0 && v) a.xbuf[t.traj + rw] = x[r];
   }
   int iters = 0;
@@ -835,13 +826,35 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   if (threadIdx.x == 0) {
     if (t.qoi_slot >= 0 && t.qoi_mode != MLMCP_QOI_NONE && t.qoi_mode != MLMCP_QOI_ELECTRICAL)
       a.qoi[t.qoi_slot] = acc;
-    if (a.iters != nullptr && t.slot >= 0) a.iters[t.slot] = iters;
+    if (a.iters != nullptr && t.slot >= 0) atomicAdd(a.iters + t.slot, iters);  // sums re-solves
     add_elapsed(a.elapsed, t.slot, t_start);
     if (code != MLMCP_ST_OK) {
-      write_status(a.status, t.slot, code, fail_step, t.tag, t.tag);
+      write_status(a.status, t.slot, code, fail_step, interval, t.tag);
       if (a.active != nullptr && t.group >= 0) a.active[t.group] = 0;
     }
   }
+}
+
+// Block-uniform "is this task's group still active" (another CTA of the same
+// group may clear active[] concurrently on a failure: decide once per block so
+// the barriers of the task never diverge).
+__device__ __forceinline__ bool group_active(const int32_t* active, int group) {
+  __shared__ int live;
+  __syncthreads();
+  if (threadIdx.x == 0)
+    live = (active == nullptr || group < 0) ? 1 : *((volatile const int32_t*)active + group) != 0;
+  __syncthreads();
+  return live != 0;
+}
+
+template <class Op, int OCC>
+__global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(SmallArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  const mlmcp_task t = a.tasks[blockIdx.x];
+  const int64_t t_start = global_ns();
+  if (!group_active(a.active, t.group)) return;
+  SmallShared sh = setup_shared<Op::R>(smem, a.buf_doubles);
+  run_task<Op>(a, t, sh, t_start, t.tag);   // PropagatorError(k, k) quirk, parareal.py:189-192
 }
 
 struct CoarseArgs {
@@ -870,15 +883,12 @@ struct CoarseArgs {
 // steady-state predictor) run across slices: for k = 1 the sweep is one
 // implicit-Euler trajectory; for k >= 2 each slice restarts from the corrected
 // U_n, which replaces the newest history entry.
-template <class Op, int OCC>
-__global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(CoarseArgs a) {
+// The coarse/update sweep of one sample on the calling CTA.
+template <class Op>
+__device__ __forceinline__ void run_coarse(const CoarseArgs& a, int s, SmallShared& sh,
+                                        int64_t t_start) {
   constexpr int R = Op::R;
-  extern __shared__ __align__(16) double smem[];
-  const int s = blockIdx.x;
-  const int64_t t_start = global_ns();
-  if (a.active[s] == 0) return;
   const PatternArgs& pa = a.pa;
-  SmallShared sh = setup_shared<R>(smem, a.buf_doubles);
   const double* Ms = a.M + (int64_t)s * a.nnz;
   const double* Ks = a.K + (int64_t)s * a.nnz;
   Op op;
@@ -897,9 +907,9 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
     const bool v = Op::ok(r, pa);
     const int i = v ? Op::row(r, pa) : 0;
     if (a.k == 1) {
-      x[r] = v ? U[i] : 0.0;
+      x[r] = v ? __ldcg(U + i) : 0.0;
     } else {
-      x[r] = v ? F[(a.k - 1) * N + i] : 0.0;  // freeze U_{k-1} = F_{k-1}
+      x[r] = v ? __ldcg(F + (a.k - 1) * N + i) : 0.0;  // freeze U_{k-1} = F_{k-1}
       if (v) U[(a.k - 1) * N + i] = x[r];
     }
   }
@@ -944,7 +954,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
         C[(n - 1) * N + i] = x[r];
       } else {
         const double c_new = x[r];
-        const double un = (F[n * N + i] + c_new) - C[(n - 1) * N + i];
+        const double un = (__ldcg(F + n * N + i) + c_new) - __ldcg(C + (n - 1) * N + i);
         U[n * N + i] = un;
         C[(n - 1) * N + i] = c_new;
         x[r] = un;
@@ -957,7 +967,7 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
     for (int r = 0; r < R; ++r)
       if (Op::ok(r, pa)) {
         const int i = Op::row(r, pa);
-        U[a.m * N + i] = F[a.m * N + i];
+        U[a.m * N + i] = __ldcg(F + a.m * N + i);
       }
   }
   if (threadIdx.x == 0) {
@@ -965,6 +975,300 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(Coarse
     add_elapsed(a.elapsed, s, t_start);
   }
   (void)Ks;
+}
+
+template <class Op, int OCC>
+__global__ void __launch_bounds__(kSmallThreads, OCC) small_coarse_kernel(CoarseArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  const int s = blockIdx.x;
+  const int64_t t_start = global_ns();
+  if (a.active[s] == 0) return;
+  SmallShared sh = setup_shared<Op::R>(smem, a.buf_doubles);
+  run_coarse<Op>(a, s, sh, t_start);
+}
+
+// ---------------------------------------------------------------- fused scheduler
+// One persistent launch runs the sequential tasks of every level and/or the
+// finest level's Parareal.  Each Parareal sample is a dependency chain, here
+// pipelined at slice granularity (results identical to the reference order):
+//   iteration k:  COARSE(s,k,n), n = k..M-1, one after another (the update
+//                 U_n = F_n + G(U_{n-1}) - C_{n-1} of parareal.py:173-178)
+//                 FINE(s,k,n),  n = k..M, as soon as U_{n-1} is final
+//                 defect / stop test (parareal.py:198-207) once every fine
+//                 slice of the iteration is done, then iteration k+1.
+// Ready chain steps sit in a device-side FIFO and take priority over the
+// independent sequential tasks, which fill every other SM slot.  All three
+// task kinds run through ONE instance of run_task (same per-task code as the
+// separate launches, and one register allocation — a kernel holding several
+// inlined task bodies spills in the PCG loop and runs ~30% slower); the
+// coarse slice is a propagate task followed by a short update loop.
+enum : int { kJobExit = 0, kJobWait = 1, kJobSeq = 2, kJobCoarse = 3, kJobFine = 4 };
+enum : int { kCtrReserve = 0, kCtrClaim = 1, kCtrSeq = 2, kCtrRemain = 3, kCtrWords = 8 };
+
+struct FusedArgs {
+  SmallArgs t;            // shared arrays of every task kind (xbuf, qoi, iters, status, ...)
+  int n_seq;              // t.tasks[0 .. n_seq) are the sequential tasks
+  // Parareal batch
+  int S, m, k_max, row0;
+  double tol, dt_c, t0;
+  const int64_t* slice_k0;
+  const int32_t* slice_steps;
+  const mlmcp_task* fine; // [S*m]
+  int64_t u_off, c_tmp_off;
+  double* C;
+  int coarse_slot, coarse_ss;
+  int32_t* k_used;
+  double* defects;
+  // scheduler state (workspace)
+  int* ctr;               // kCtrWords counters
+  int* fine_left;         // [S]
+  int4* queue;            // [qcap] (kind, s, k, n)
+  int* qready;            // [qcap]
+  int qcap;
+  int reserve;            // CTAs blockIdx < reserve serve only Parareal jobs while a chain is live
+  // set by dispatch
+  PatternArgs pa;
+  int buf_doubles;
+};
+
+__device__ __forceinline__ int ld_volatile(const int* p) { return *((volatile const int*)p); }
+
+__device__ void fused_push(const FusedArgs& a, int4 job) {
+  const int pos = atomicAdd(a.ctr + kCtrReserve, 1);
+  a.queue[pos] = job;
+  __threadfence();
+  atomicExch(a.qready + pos, 1);
+}
+
+__device__ int4 fused_pop(const FusedArgs& a, bool reserved) {
+  for (;;) {
+    const int c = ld_volatile(a.ctr + kCtrClaim);
+    const int r = ld_volatile(a.ctr + kCtrReserve);
+    if (c >= r) break;
+    if (atomicCAS(a.ctr + kCtrClaim, c, c + 1) == c) {
+      while (ld_volatile(a.qready + c) == 0) __nanosleep(64);
+      __threadfence();
+      const volatile int* q = reinterpret_cast<const volatile int*>(a.queue + c);
+      return make_int4(q[0], q[1], q[2], q[3]);
+    }
+  }
+  const bool pr_live = ld_volatile(a.ctr + kCtrRemain) != 0;
+  if (reserved && pr_live) return make_int4(kJobWait, 0, 0, 0);
+  if (ld_volatile(a.ctr + kCtrSeq) < a.n_seq) {
+    const int i = atomicAdd(a.ctr + kCtrSeq, 1);
+    if (i < a.n_seq) return make_int4(kJobSeq, i, 0, 0);
+  }
+  return make_int4(pr_live ? kJobWait : kJobExit, 0, 0, 0);
+}
+
+__device__ __forceinline__ double* fused_U(const FusedArgs& a, int s) {
+  return a.t.xbuf + a.u_off + (int64_t)s * (a.m + 1) * a.pa.N;
+}
+__device__ __forceinline__ double* fused_F(const FusedArgs& a, int s) {
+  return a.t.xbuf + a.u_off + (int64_t)a.S * (a.m + 1) * a.pa.N +
+         (int64_t)s * (a.m + 1) * a.pa.N;
+}
+
+// start of iteration k of sample s (thread 0 pushes): freeze U_{k-1} = F_{k-1}
+// (k >= 2, by the whole CTA), then the first coarse slice and fine slice k.
+__device__ void fused_start_iteration(const FusedArgs& a, int s, int k) {
+  const int64_t N = a.pa.N;
+  if (k > 1) {
+    double* U = fused_U(a, s);
+    const double* F = fused_F(a, s);
+    for (int64_t i = threadIdx.x; i < N; i += kSmallThreads)
+      U[(int64_t)(k - 1) * N + i] = __ldcg(F + (int64_t)(k - 1) * N + i);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    a.fine_left[s] = a.m - k + 1;
+    __threadfence();
+    if (k < a.m) fused_push(a, make_int4(kJobCoarse, s, k, k));
+    fused_push(a, make_int4(kJobFine, s, k, k));
+  }
+}
+
+// the end of sample s's chain: U[n] = F[n] for n >= k_used (parareal.py:209-210)
+__device__ void fused_finish(const FusedArgs& a, int s) {
+  const int64_t N = a.pa.N;
+  const int ku = *((volatile const int32_t*)a.k_used + s);
+  double* U = fused_U(a, s);
+  const double* F = fused_F(a, s);
+  for (int64_t i = (int64_t)ku * N + threadIdx.x; i < (int64_t)(a.m + 1) * N; i += kSmallThreads)
+    U[i] = __ldcg(F + i);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicSub(a.ctr + kCtrRemain, 1);
+  }
+}
+
+// parareal.py:198-207 after every fine slice of iteration k (whole CTA)
+template <class Op>
+__device__ void fused_defect(const FusedArgs& a, int s, int k, SmallShared& sh) {
+  const int64_t N = a.pa.N;
+  const int m = a.m;
+  const double* U = fused_U(a, s);
+  const double* F = fused_F(a, s);
+  __shared__ int go_on;
+  const bool live = ld_volatile(a.t.active + s) != 0;
+  if (live) {
+    double d = 0.0;
+    for (int n = k; n < m; ++n) {
+      double jj = 0.0, ff = 0.0;
+      for (int64_t i = threadIdx.x; i < N; i += kSmallThreads) {
+        const double f = __ldcg(F + n * N + i);
+        const double diff = f - __ldcg(U + n * N + i);
+        jj = fma(diff, diff, jj);
+        ff = fma(f, f, ff);
+      }
+      double v[2] = {jj, ff};
+      cta_allsum<2>(v, sh.red, sh.par);
+      const double ratio = sqrt(v[0]) / fmax(sqrt(v[1]), 1e-30);
+      if (isnan(ratio) || isnan(d)) d = NAN;   // np.max propagates NaN
+      else d = fmax(d, ratio);
+    }
+    if (threadIdx.x == 0) {
+      a.defects[(int64_t)s * a.k_max + (k - 1)] = d;
+      a.k_used[s] = k;
+      const bool conv = d <= a.tol;
+      if (conv) a.t.active[s] = 0;
+      go_on = (!conv && k < a.k_max) ? 1 : 0;
+    }
+  } else if (threadIdx.x == 0) {
+    go_on = 0;
+  }
+  __syncthreads();
+  if (go_on) fused_start_iteration(a, s, k + 1);
+  else fused_finish(a, s);
+}
+
+// coarse slice n of iteration k: U_n (and C_{n-1}) from c_new = G(U_{n-1})
+__device__ void fused_coarse_update(const FusedArgs& a, int s, int k, int n) {
+  const int64_t N = a.pa.N;
+  double* U = fused_U(a, s);
+  const double* F = fused_F(a, s);
+  double* C = a.C + (int64_t)s * a.m * N;
+  const double* cn = a.t.xbuf + a.c_tmp_off + (int64_t)s * N;
+  for (int64_t i = threadIdx.x; i < N; i += kSmallThreads) {
+    const double c_new = __ldcg(cn + i);
+    if (k == 1) {
+      U[(int64_t)n * N + i] = c_new;
+    } else {
+      U[(int64_t)n * N + i] =
+          (__ldcg(F + (int64_t)n * N + i) + c_new) - __ldcg(C + (int64_t)(n - 1) * N + i);
+    }
+    C[(int64_t)(n - 1) * N + i] = c_new;
+  }
+}
+
+template <class Op, int OCC>
+__global__ void __launch_bounds__(kSmallThreads, OCC) fused_kernel(FusedArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int4 job;
+  __shared__ mlmcp_task task;
+  __shared__ int last;
+  SmallShared sh = setup_shared<Op::R>(smem, a.buf_doubles);
+  for (;;) {
+    if (threadIdx.x == 0) {
+      const int4 jb = fused_pop(a, (int)blockIdx.x < a.reserve);
+      job = jb;
+      if (jb.x == kJobSeq) {
+        task = a.t.tasks[jb.y];
+      } else if (jb.x == kJobFine) {
+        task = a.fine[(int64_t)jb.y * a.m + (jb.w - 1)];
+        task.tag = jb.z;
+      } else if (jb.x == kJobCoarse) {
+        // the coarse propagation of slice n as a propagate task
+        const int s = jb.y, k = jb.z, n = jb.w;
+        mlmcp_task t{};
+        t.sample = a.row0 + s;
+        t.n_steps = a.slice_steps[n - 1];
+        t.k0 = a.slice_k0[n - 1];
+        t.dt = a.dt_c;
+        t.t_base = a.t0;
+        t.x_in = a.u_off + ((int64_t)s * (a.m + 1) + (n - 1)) * a.pa.N;
+        t.x_out = a.c_tmp_off + (int64_t)s * a.pa.N;
+        t.traj = -1;
+        t.qoi_slot = -1;
+        t.qoi_mode = MLMCP_QOI_NONE;
+        t.qoi_from = 0;
+        t.group = s;
+        t.slot = a.coarse_slot + s;
+        t.tag = k;
+        t.flags = 0;
+        t.qoi_index = n;            // interval of a coarse failure (PropagatorError(n, k))
+        t.ss_slot = a.coarse_ss >= 0 ? a.coarse_ss + s : -1;
+        task = t;
+      }
+    }
+    __syncthreads();
+    const int kind = job.x;
+    if (kind == kJobExit) break;
+    if (kind == kJobWait) {
+      if (threadIdx.x == 0) __nanosleep(1000);
+      __syncthreads();
+      continue;
+    }
+    if (group_active(a.t.active, kind == kJobSeq ? -1 : job.y)) {
+      const mlmcp_task t = task;
+      run_task<Op>(a.t, t, sh, global_ns(), kind == kJobCoarse ? t.qoi_index : t.tag);
+    }
+    __syncthreads();
+    if (kind == kJobCoarse) {
+      const int s = job.y, k = job.z, n = job.w;
+      const bool live = ld_volatile(a.t.active + s) != 0;
+      if (live) fused_coarse_update(a, s, k, n);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        if (live) {
+          if (n + 1 < a.m) fused_push(a, make_int4(kJobCoarse, s, k, n + 1));
+          fused_push(a, make_int4(kJobFine, s, k, n + 1));
+        } else {
+          // failed: the fine slices n+1 .. m of this iteration never run
+          last = atomicSub(a.fine_left + s, a.m - n) == a.m - n ? 1 : 0;
+        }
+      }
+      __syncthreads();
+      if (!live && last) fused_defect<Op>(a, s, k, sh);
+    } else if (kind == kJobFine) {
+      const int s = job.y, k = job.z;
+      if (threadIdx.x == 0) {
+        __threadfence();
+        last = atomicSub(a.fine_left + s, 1) == 1 ? 1 : 0;
+        if (last) __threadfence();
+      }
+      __syncthreads();
+      if (last) fused_defect<Op>(a, s, k, sh);
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void fused_init_kernel(FusedArgs a) {
+  // queue: FINE(s,1,1) and COARSE(s,1,1) of every sample (U_0 = x0 is ready)
+  const int S = a.S;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < a.qcap; i += gridDim.x * blockDim.x) {
+    int4 q = make_int4(0, 0, 0, 0);
+    int ready = 0;
+    if (i < S) {
+      q = make_int4(a.m > 1 ? kJobCoarse : kJobFine, i, 1, 1);
+      ready = 1;
+    } else if (i < 2 * S && a.m > 1) {
+      q = make_int4(kJobFine, i - S, 1, 1);
+      ready = 1;
+    }
+    a.queue[i] = q;
+    a.qready[i] = ready;
+  }
+  for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < S; s += gridDim.x * blockDim.x)
+    a.fine_left[s] = a.m;
+  if (blockIdx.x == 0 && threadIdx.x < kCtrWords) {
+    const int pushed = a.m > 1 ? 2 * S : S;
+    a.ctr[threadIdx.x] =
+        threadIdx.x == kCtrReserve ? pushed : (threadIdx.x == kCtrRemain ? S : 0);
+  }
 }
 
 struct PeriodicArgs {
@@ -1213,7 +1517,106 @@ struct LaunchPeriodic {
   }
 };
 
+template <class Op, int OCC>
+struct LaunchFused {
+  static int run(FusedArgs& a, unsigned grid_hint, int nt, size_t smem, cudaStream_t st) {
+    a.t.pa = a.pa;
+    a.t.buf_doubles = a.buf_doubles;
+    if (smem > 48 * 1024)
+      cudaFuncSetAttribute(fused_kernel<Op, OCC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fused_kernel<Op, OCC>, nt, smem);
+    if (per_sm < 1) {
+      set_error("fused scheduler kernel does not fit on an SM");
+      return MLMCP_EINVAL;
+    }
+    const unsigned grid = (unsigned)std::max(1, std::min((int)grid_hint, per_sm * sms));
+    // CTAs reserved for the Parareal chains while any is live (default none;
+    // MLMCP_FUSED_RESERVE overrides, for measurements)
+    static const int env_reserve = [] {
+      const char* e = getenv("MLMCP_FUSED_RESERVE");
+      return e ? atoi(e) : 0;
+    }();
+    a.reserve = a.S == 0 ? 0 : std::min(env_reserve, (int)grid);
+    fused_init_kernel<<<std::max(1, std::min(64, (a.qcap + 255) / 256)), 256, 0, st>>>(a);
+    MLMCP_LAUNCH_CHECK("fused_init_kernel");
+    fused_kernel<Op, OCC><<<grid, nt, smem, st>>>(a);
+    MLMCP_LAUNCH_CHECK("fused_kernel");
+    return MLMCP_OK;
+  }
+};
+
 }  // namespace
+
+size_t fused_workspace_bytes(int S, int m, int k_max) {
+  const size_t qcap = (size_t)S * ((size_t)k_max * (2 * m + 1) + 2) + 1;
+  return 256 + ((sizeof(int) * (size_t)(S + 1) + 255) & ~(size_t)255) +
+         ((sizeof(int) * qcap + 255) & ~(size_t)255) + sizeof(int4) * qcap;
+}
+
+int small_run_fused(Ctx* ctx, int S, const double* M, const double* K, const double* profile,
+                    double omega, double rtol, int max_it, const mlmcp_task_arrays& ar,
+                    const mlmcp_parareal_batch& pr, int grid_ctas, void* ws, size_t ws_bytes,
+                    cudaStream_t stream) {
+  const int Sp = pr.S;
+  if (ar.n_seq == 0 && Sp == 0) return MLMCP_OK;
+  const int m = std::max(pr.m, 1), kmax = std::max(pr.k_max, 1);
+  const size_t need = fused_workspace_bytes(Sp, m, kmax);
+  if (ws == nullptr || ws_bytes < need) {
+    set_error("fused launch: workspace too small (mlmcp_fused_workspace_bytes)");
+    return MLMCP_ENOMEM;
+  }
+  FusedArgs a{};
+  a.t.tasks = ar.seq_tasks_d;
+  a.t.n_tasks = ar.n_seq;
+  a.t.nnz = ctx->nnz;
+  a.t.M = M;
+  a.t.K = K;
+  a.t.profile = profile;
+  a.t.omega = omega;
+  a.t.rtol2 = rtol * rtol;
+  a.t.max_it = max_it;
+  a.t.xbuf = ar.xbuf_d;
+  a.t.qoi = ar.qoi_d;
+  a.t.iters = ar.iters_d;
+  a.t.status = ar.status_d;
+  a.t.active = ar.active_d;
+  a.t.elapsed = ar.elapsed_ns_d;
+  a.t.xss = ar.xss_d;
+  a.n_seq = ar.n_seq;
+  a.S = Sp;
+  a.m = m;
+  a.k_max = kmax;
+  a.row0 = pr.row0;
+  a.tol = pr.tol;
+  a.dt_c = pr.dt_c;
+  a.t0 = pr.t0;
+  a.slice_k0 = pr.slice_k0_d;
+  a.slice_steps = pr.slice_steps_d;
+  a.fine = pr.fine_tasks_d;
+  a.u_off = pr.u_off;
+  a.c_tmp_off = pr.c_tmp_off;
+  a.C = pr.C_d;
+  a.coarse_slot = pr.coarse_slot;
+  a.coarse_ss = pr.coarse_ss;
+  a.k_used = pr.k_used_d;
+  a.defects = pr.defects_d;
+  char* w = static_cast<char*>(ws);
+  a.ctr = reinterpret_cast<int*>(w);
+  w += 256;
+  a.fine_left = reinterpret_cast<int*>(w);
+  w += (sizeof(int) * (size_t)(Sp + 1) + 255) & ~(size_t)255;
+  a.qcap = (int)((size_t)Sp * ((size_t)kmax * (2 * m + 1) + 2) + 1);
+  a.qready = reinterpret_cast<int*>(w);
+  w += (sizeof(int) * (size_t)a.qcap + 255) & ~(size_t)255;
+  a.queue = reinterpret_cast<int4*>(w);
+  unsigned hint = (unsigned)(ar.n_seq + Sp * (m + 1));
+  if (grid_ctas > 0) hint = std::min(hint, (unsigned)grid_ctas);
+  return dispatch<LaunchFused>(ctx, a, hint, stream);
+}
 
 int small_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
                    const double* K, const double* profile, double omega, double rtol,

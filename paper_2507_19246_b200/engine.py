@@ -88,6 +88,7 @@ class DeviceSystem:
                                                   np_ptr(celem), np_ptr(cmw), np_ptr(ckw)),
                   "mlmcp_ctx_set_assembly")
         self._ws = None
+        self._fused_ws = {}
 
     # ------------------------------------------------------------ lifecycle
     def close(self):
@@ -174,6 +175,22 @@ class DeviceSystem:
             ptr(slice_k0), ptr(slice_steps), float(rtol), int(max_it), ptr(U), ptr(F), ptr(C),
             ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(xss), ptr(ws),
             0 if ws is None else ws.numel(), stream_handle(stream)), "mlmcp_parareal_coarse")
+
+    # ------------------------------------------------------------ fused launch
+    def run_fused(self, M, K, profile, omega, rtol, max_it, arrays, batch, S_pr, m, k_max,
+                  stream=None, grid_ctas: int = 0):
+        """mlmcp_run_fused with ctypes ``_lib.TaskArrays`` / ``_lib.PararealBatch``."""
+        nbytes = int(self.lib.mlmcp_fused_workspace_bytes(S_pr, m, k_max))
+        key = stream.cuda_stream if stream is not None else torch.cuda.current_stream().cuda_stream
+        ws = self._fused_ws.get(key)
+        if ws is None or ws.numel() < nbytes:
+            ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._fused_ws[key] = ws
+        check(self.lib.mlmcp_run_fused(self.ctx, M.shape[0], ptr(M), ptr(K), ptr(profile),
+                                       float(omega), float(rtol), int(max_it),
+                                       ctypes.byref(arrays), ctypes.byref(batch), int(grid_ctas),
+                                       ptr(ws), ws.numel(), stream_handle(stream)),
+              "mlmcp_run_fused")
 
     # ------------------------------------------------------------ predictor
     def periodic_state(self, sample_idx: torch.Tensor, dts: torch.Tensor, M, K, profile,

@@ -203,14 +203,18 @@ class _BatchedFamily:
 
     # ------------------------------------------------------------ batched
     def run_levels(self, draws, parareal_cfg: PararealConfig | None = None, levels=None,
-                   concurrent: bool = True, params_dev=None) -> list[CoupledBatch]:
+                   concurrent: bool = True, params_dev=None,
+                   fused: bool | None = None) -> list[CoupledBatch]:
         """Coupled (Q_l, Q_{l-1}) for every level at once.
 
         draws[i]: [N_i, P] parameters of level ``levels[i]`` (default 0..L).
-        All levels' operators are assembled in one launch; every sequential
-        solve of every level goes into one batched launch (longest first);
-        the finest level's Parareal runs concurrently on a second stream.
-        Returns device tensors (no host sync)."""
+        All levels' operators are assembled up front.  On the SM-resident path
+        (``fused``, default) every sequential solve of every level and the
+        finest level's Parareal run in ONE persistent launch whose device-side
+        scheduler advances each Parareal chain as soon as its inputs are ready
+        (mlmcp_run_fused); otherwise the sequential solves go into one batched
+        launch (longest first) and the Parareal runs concurrently on a
+        high-priority second stream.  Returns device tensors (no host sync)."""
         import torch
         sol = self.solver
         levels = list(range(len(draws))) if levels is None else list(levels)
@@ -237,6 +241,11 @@ class _BatchedFamily:
             for i, lvl in enumerate(levels):
                 if lvl == top and sizes[i] > 0:
                     pr_level = i
+        if fused is None:
+            fused = concurrent and sol.sys.sm_resident and not sol.sys.direct
+        if fused:
+            return self._run_levels_fused(levels, sizes, offs, M, K, assemble_level, pr_level,
+                                          parareal_cfg)
         main = torch.cuda.current_stream()
         pr = None
         side = main
@@ -259,6 +268,17 @@ class _BatchedFamily:
         for i in range(len(levels)):
             if i != pr_level:
                 assemble_level(i)
+        jobs, where = self._level_jobs(levels, offs, pr_level)
+        res = sol.run_sequential(M, K, jobs) if jobs else []
+        if pr is not None and side is not main:
+            main.wait_stream(side)
+            for t in (pr.qoi, pr.k_used, pr.defects):
+                t.record_stream(main)
+        self._last = (res, pr, M, K)
+        return self._collect(levels, sizes, where, res, pr_level, pr,
+                             pr_q if pr is not None else None)
+
+    def _level_jobs(self, levels, offs, pr_level):
         jobs, where = [], []
         for i, lvl in enumerate(levels):
             rows = np.arange(offs[i], offs[i + 1])
@@ -272,11 +292,11 @@ class _BatchedFamily:
                 dtm = self.hierarchy[lvl - 1].dt
                 jobs.append(self._seq_job(rows, dtm))
                 where.append((i, "lo", dtm))
-        res = sol.run_sequential(M, K, jobs) if jobs else []
-        if pr is not None and side is not main:
-            main.wait_stream(side)
-            for t in (pr.qoi, pr.k_used, pr.defects):
-                t.record_stream(main)
+        return jobs, where
+
+    def _collect(self, levels, sizes, where, res, pr_level, pr, pr_q):
+        import torch
+        sol = self.solver
         out = []
         for i, lvl in enumerate(levels):
             S = sizes[i]
@@ -305,8 +325,68 @@ class _BatchedFamily:
                 if pr.elapsed is not None:
                     elapsed.extend(pr.elapsed)
             out.append(CoupledBatch(lvl, ql, qm, ku, its, defects=defects, elapsed=elapsed))
-        self._last = (res, pr, M, K)
         return out
+
+    def _pr_ctas(self, jobs, pr_spec) -> int:
+        """SM slots for the Parareal chains: the share of the resident CTA
+        slots proportional to the Parareal batch's expected step work (K ~ 3)
+        against the sequential batch's (MLMCP_PR_CTAS overrides)."""
+        import os
+
+        import torch
+        env = os.environ.get("MLMCP_PR_CTAS")
+        slots = 2 * torch.cuda.get_device_properties(self.solver.device).multi_processor_count
+        if env:
+            return max(1, min(int(env), slots))
+        from .timeint import step_count
+        w_seq = sum(len(j.rows) * j.n_steps for j in jobs)
+        m = pr_spec["m"]
+        k_est = min(3, pr_spec["k_max"])
+        fine_steps = step_count(0.0, pr_spec["t1"], pr_spec["dt_fine"]) // m
+        w_pr = pr_spec["S"] * sum(m - k + 1 for k in range(1, k_est + 1)) * fine_steps
+        share = w_pr / max(1, w_pr + w_seq)
+        return int(min(slots - 32, max(pr_spec["S"], round(slots * share))))
+
+    def _run_levels_fused(self, levels, sizes, offs, M, K, assemble_level, pr_level,
+                          parareal_cfg):
+        """The sequential batch as one launch on the current stream and the
+        finest level's Parareal as a persistent device-scheduled launch
+        (mlmcp_run_fused) holding a fixed share of the SM slots on a second
+        stream, launched first: every Parareal chain step starts as soon as its
+        own inputs are ready instead of waiting for slots held by long
+        sequential tasks (MLMCP_FUSED=all: both batches in one scheduled
+        launch)."""
+        import os
+
+        import torch
+        sol = self.solver
+        for i in range(len(levels)):
+            assemble_level(i)
+        jobs, where = self._level_jobs(levels, offs, pr_level)
+        pr_spec = None
+        cfg = None
+        if pr_level is not None:
+            cfg = parareal_cfg.with_dt_fine(self.hierarchy[levels[pr_level]].dt)
+            pr_spec = dict(row0=int(offs[pr_level]), S=int(sizes[pr_level]), t0=0.0,
+                           t1=self.horizon, m=cfg.num_subintervals, dt_fine=cfg.dt_fine,
+                           dt_coarse=cfg.dt_coarse, tol=cfg.tolerance, k_max=cfg.k_max,
+                           **self._pr_qoi(cfg.dt_fine))
+        if pr_spec is None or os.environ.get("MLMCP_FUSED") == "all":
+            res, pr = sol.run_fused(M, K, jobs, pr_spec)
+        else:
+            main = torch.cuda.current_stream()
+            side = self._pr_stream(sol.device)
+            side.wait_stream(main)
+            with torch.cuda.stream(side):
+                _, pr = sol.run_fused(M, K, [], pr_spec, stream=side,
+                                      grid_ctas=self._pr_ctas(jobs, pr_spec))
+            res = sol.run_sequential(M, K, jobs) if jobs else []
+            main.wait_stream(side)
+            for t in (pr.qoi, pr.k_used, pr.defects):
+                t.record_stream(main)
+        pr_q = self._finish_q(pr.qoi, cfg.dt_fine) if pr is not None else None
+        self._last = (res, pr, M, K)
+        return self._collect(levels, sizes, where, res, pr_level, pr, pr_q)
 
     def check_status(self):
         """Raise SingularSystemError / PropagatorError for failed samples of the

@@ -23,6 +23,7 @@ import numpy as np
 import torch
 
 from . import _lib, fe
+from ._lib import ptr
 from .engine import DeviceSystem, F64, I32, kl_sigma, new_tasks, tasks_to_device
 from .timeint import SingularSystemError, step_count
 
@@ -119,6 +120,9 @@ class BatchSolver:
     # ------------------------------------------------------------ sequential
     def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
         return _run_sequential(self, M, K, jobs, stream, keep_traj)
+
+    def run_fused(self, M, K, jobs: list[SeqJob], pr=None, stream=None, grid_ctas: int = 0):
+        return _run_fused(self, M, K, jobs, pr, stream, grid_ctas)
 
     def run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
                      dt_coarse: float, tol: float, k_max: int, stream=None,
@@ -223,9 +227,10 @@ class FESolver(BatchSolver):
 
 
 # ------------------------------------------------------------ sequential
-def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
-    """All jobs in one batched launch (SM-resident path) or one launch per
-    dt (streaming path).  Returns one SeqResult per job (device tensors)."""
+def _seq_setup(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+    """Task table (longest first), buffers and predictor states of a batch of
+    sequential jobs."""
+    from types import SimpleNamespace
     sizes = [len(j.rows) for j in jobs]
     T = int(sum(sizes))
     N = self.N
@@ -247,7 +252,6 @@ def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool
     tasks["x_out"] = idx * N
     tasks["qoi_slot"] = idx
     tasks["slot"] = idx
-    traj = None
     if keep_traj:
         steps = tasks["n_steps"].astype(np.int64)
         base = T * N
@@ -256,55 +260,73 @@ def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool
         xbuf = torch.zeros(int(base + np.sum((steps + 1) * N)), dtype=F64, device=self.device)
     else:
         xbuf = torch.zeros(T * N, dtype=F64, device=self.device)
-    qoi = torch.zeros(T, dtype=F64, device=self.device)
-    iters = torch.zeros(T, dtype=I32, device=self.device)
-    status = torch.zeros((T, _lib.STATUS_INTS), dtype=I32, device=self.device)
-    elapsed = torch.zeros(T, dtype=torch.int64, device=self.device) if self.timing else None
-    if self.sys.sm_resident:
-        xss = None
+    st = SimpleNamespace(jobs=jobs, T=T, tasks=tasks, xbuf=xbuf, xss=None, td=None,
+                         qoi=torch.zeros(T, dtype=F64, device=self.device),
+                         iters=torch.zeros(T, dtype=I32, device=self.device),
+                         status=torch.zeros((T, _lib.STATUS_INTS), dtype=I32, device=self.device),
+                         elapsed=(torch.zeros(T, dtype=torch.int64, device=self.device)
+                                  if self.timing else None))
+    if self.sys.sm_resident and T:
         if self.use_predictor():
             tasks["ss_slot"] = idx
-            xss = self.steady_states(tasks["sample"], tasks["dt"], M, K, stream)
+            st.xss = self.steady_states(tasks["sample"], tasks["dt"], M, K, stream)
         order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
         key = (tasks.tobytes(), N)
         td = self._task_cache.get(key)
         if td is None:
             td = tasks_to_device(tasks[order], self.device)
             self._task_cache[key] = td
-        if self.events is not None:
-            self.events[0].record(stream if stream is not None else torch.cuda.current_stream())
-        self.sys.propagate(tasks[order], M, K, self.profile, self.omega, self.step_rtol(),
-                           self.max_it, xbuf, qoi, iters, status, None, stream, tasks_dev=td,
-                           elapsed=elapsed, xss=xss)
-        if self.events is not None:
-            self.events[1].record(stream if stream is not None else torch.cuda.current_stream())
-    else:
-        for dt in sorted(set(tasks["dt"].tolist())):
-            sel = tasks[tasks["dt"] == dt]
-            self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it,
-                               xbuf, qoi, iters, status, None, stream, elapsed=elapsed)
+        st.td = td
+        st.order = order
+    return st
+
+
+def _seq_results(self, st):
     out = []
     off = 0
-    for j in jobs:
+    for j in st.jobs:
         sl = slice(off, off + len(j.rows))
-        out.append(SeqResult(qoi[sl], iters[sl], status[sl],
-                             None if elapsed is None else elapsed[sl]))
+        out.append(SeqResult(st.qoi[sl], st.iters[sl], st.status[sl],
+                             None if st.elapsed is None else st.elapsed[sl]))
         off += len(j.rows)
-    self._last_xbuf = xbuf
-    self._last_tasks = tasks
+    self._last_xbuf = st.xbuf
+    self._last_tasks = st.tasks
     return out
 
 
+def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+    """All jobs in one batched launch (SM-resident path) or one launch per
+    dt (streaming path).  Returns one SeqResult per job (device tensors)."""
+    st = _seq_setup(self, M, K, jobs, stream, keep_traj)
+    if st.T == 0:
+        return _seq_results(self, st)
+    cur = stream if stream is not None else torch.cuda.current_stream()
+    if self.sys.sm_resident:
+        if self.events is not None:
+            self.events[0].record(cur)
+        self.sys.propagate(st.tasks[st.order], M, K, self.profile, self.omega, self.step_rtol(),
+                           self.max_it, st.xbuf, st.qoi, st.iters, st.status, None, stream,
+                           tasks_dev=st.td, elapsed=st.elapsed, xss=st.xss)
+        if self.events is not None:
+            self.events[1].record(cur)
+    else:
+        for dt in sorted(set(st.tasks["dt"].tolist())):
+            sel = st.tasks[st.tasks["dt"] == dt]
+            self.sys.propagate(sel, M, K, self.profile, self.omega, self.rtol, self.max_it,
+                               st.xbuf, st.qoi, st.iters, st.status, None, stream,
+                               elapsed=st.elapsed)
+    return _seq_results(self, st)
+
+
 # ------------------------------------------------------------ Parareal
-def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
-                  dt_coarse: float, tol: float, k_max: int, stream=None,
-                  keep_traj: bool = False, qoi_mode: int | None = None,
-                  qoi_index: int = 0, qoi_from: int = -1) -> PararealBatchResult:
-    """parareal_solve for the S samples whose operators are M/K rows 0..S-1
-    (slice the level's M/K to pass a sub-batch), from the zero state."""
+def _pr_setup(self, M, K, S: int, row0: int, t0: float, t1: float, m: int, dt_fine: float,
+              dt_coarse: float, k_max: int, stream=None, keep_traj: bool = False,
+              qoi_mode: int | None = None, qoi_index: int = 0, qoi_from: int = -1):
+    """Buffers, fine task tables and predictor states of a Parareal batch whose
+    operators are M/K rows row0 .. row0+S-1."""
+    from types import SimpleNamespace
     if not 1 <= k_max <= m:
         raise ValueError(f"max_iterations must lie in [1, M={m}], got {k_max}")
-    S = M.shape[0]
     N = self.N
     dev = self.device
     bounds, fk0, fst, ck0, cst = parareal_grid(t0, t1, m, dt_fine, dt_coarse)
@@ -312,26 +334,27 @@ def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
     traj_steps = int(fst.max()) + 1
     traj_size = S * m * traj_steps * N if keep_traj else 0
     buf = torch.zeros(2 * uf_size + traj_size, dtype=F64, device=dev)
-    U = buf[:uf_size].view(S, m + 1, N)
-    F = buf[uf_size:2 * uf_size].view(S, m + 1, N)
-    C = torch.zeros((S, m, N), dtype=F64, device=dev)
-    active = torch.ones(S, dtype=I32, device=dev)
-    k_used = torch.zeros(S, dtype=I32, device=dev)
-    defects = torch.full((S, k_max), float("nan"), dtype=F64, device=dev)
-    status = torch.zeros((S, _lib.STATUS_INTS), dtype=I32, device=dev)
-    fine_status = torch.zeros((S * m, _lib.STATUS_INTS), dtype=I32, device=dev)
-    fine_iters = torch.zeros(S * m, dtype=I32, device=dev)
-    coarse_iters = torch.zeros(S, dtype=I32, device=dev)
-    ck0_d, cst_d = self._grid_tensors(ck0, cst)
-    pr_elapsed_c = pr_elapsed_f = None
+    st = SimpleNamespace(S=S, row0=row0, m=m, k_max=k_max, t0=t0, dt_coarse=dt_coarse,
+                         uf_size=uf_size, traj_steps=traj_steps, buf=buf, keep_traj=keep_traj,
+                         U=buf[:uf_size].view(S, m + 1, N),
+                         F=buf[uf_size:2 * uf_size].view(S, m + 1, N),
+                         C=torch.zeros((S, m, N), dtype=F64, device=dev),
+                         active=torch.ones(S, dtype=I32, device=dev),
+                         k_used=torch.zeros(S, dtype=I32, device=dev),
+                         defects=torch.full((S, k_max), float("nan"), dtype=F64, device=dev),
+                         status=torch.zeros((S, _lib.STATUS_INTS), dtype=I32, device=dev),
+                         fine_status=torch.zeros((S * m, _lib.STATUS_INTS), dtype=I32, device=dev),
+                         fine_iters=torch.zeros(S * m, dtype=I32, device=dev),
+                         coarse_iters=torch.zeros(S, dtype=I32, device=dev),
+                         elapsed_c=None, elapsed_f=None, slice_qoi=None, xss_f=None, xss_c=None)
+    st.ck0_d, st.cst_d = self._grid_tensors(ck0, cst)
     if self.timing:                   # executor ledger: per-sample coarse / per-slice fine ns
-        pr_elapsed_c = torch.zeros(S, dtype=torch.int64, device=dev)
-        pr_elapsed_f = torch.zeros(S * m, dtype=torch.int64, device=dev)
-    # fine task tables: one per iteration k (intervals k..m of every sample)
+        st.elapsed_c = torch.zeros(S, dtype=torch.int64, device=dev)
+        st.elapsed_f = torch.zeros(S * m, dtype=torch.int64, device=dev)
     s_idx, n_idx = np.meshgrid(np.arange(S), np.arange(1, m + 1), indexing="ij")
     s_idx, n_idx = s_idx.ravel(), n_idx.ravel()
     all_tasks = new_tasks(S * m)
-    all_tasks["sample"] = s_idx
+    all_tasks["sample"] = row0 + s_idx
     all_tasks["n_steps"] = fst[n_idx - 1]
     all_tasks["k0"] = fk0[n_idx - 1]
     all_tasks["dt"] = dt_fine
@@ -342,7 +365,6 @@ def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
         all_tasks["traj"] = 2 * uf_size + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
     all_tasks["group"] = s_idx
     all_tasks["slot"] = s_idx * m + (n_idx - 1)
-    slice_qoi = None
     if qoi_mode is not None and qoi_mode != _lib.QOI_FINAL_ENERGY:
         # time-accumulated QoI over the fine trajectory (parareal.py:212 concatenates
         # the last fine solve of every slice): each fine solve of slice n
@@ -352,57 +374,208 @@ def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
         all_tasks["qoi_mode"] = qoi_mode
         all_tasks["qoi_from"] = qoi_from
         all_tasks["qoi_index"] = qoi_index
-        slice_qoi = torch.zeros(S * m, dtype=F64, device=dev)
-    xss_f = xss_c = None
+        st.slice_qoi = torch.zeros(S * m, dtype=F64, device=dev)
     if self.use_predictor():
         # periodic steady states at dt_fine (rows 0..S-1) and dt_coarse (S..2S-1)
         all_tasks["ss_slot"] = s_idx
-        X = self.steady_states(np.concatenate([np.arange(S), np.arange(S)]),
+        rows = row0 + np.arange(S)
+        X = self.steady_states(np.concatenate([rows, rows]),
                                np.concatenate([np.full(S, dt_fine), np.full(S, dt_coarse)]),
                                M, K, stream)
-        xss_f, xss_c = X[:S], X[S:]
+        st.xss_f, st.xss_c = X[:S], X[S:]
         if os.environ.get("MLMCP_PREDICTOR") == "fine":
-            xss_c = None
-    key = ("pr", all_tasks.tobytes(), k_max)
+            st.xss_c = None
+    st.all_tasks, st.n_idx = all_tasks, n_idx
+    return st
+
+
+def _pr_result(self, st, K, stream=None) -> PararealBatchResult:
+    S, m, N = st.S, st.m, self.N
+    dev = self.device
+    ekey = ("energy", S, m, N, st.row0)
+    ev = self._task_cache.get(ekey)
+    if ev is None:
+        ev = (torch.arange(st.row0, st.row0 + S, dtype=I32, device=dev),
+              torch.tensor((st.uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64),
+                           device=dev))
+        self._task_cache[ekey] = ev
+    if st.slice_qoi is not None:
+        qoi = st.slice_qoi.view(S, m).sum(dim=1)
+    else:
+        qoi = self.sys.energy(ev[0], ev[1], st.buf, K, stream)
+    traj = None
+    if st.keep_traj:
+        traj = st.buf[2 * st.uf_size:].view(S, m, st.traj_steps, N)
+    return PararealBatchResult(qoi, st.k_used, st.defects, st.status, st.fine_status, st.U, st.F,
+                               traj, st.fine_iters, st.coarse_iters,
+                               (st.elapsed_c, st.elapsed_f) if self.timing else None)
+
+
+def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
+                  dt_coarse: float, tol: float, k_max: int, stream=None,
+                  keep_traj: bool = False, qoi_mode: int | None = None,
+                  qoi_index: int = 0, qoi_from: int = -1) -> PararealBatchResult:
+    """parareal_solve for the S samples whose operators are M/K rows 0..S-1
+    (slice the level's M/K to pass a sub-batch), from the zero state:
+    K_max rounds of [coarse sweep, fine slices, defect] launches."""
+    S = M.shape[0]
+    st = _pr_setup(self, M, K, S, 0, t0, t1, m, dt_fine, dt_coarse, k_max, stream, keep_traj,
+                   qoi_mode, qoi_index, qoi_from)
+    dev = self.device
+    key = ("pr", st.all_tasks.tobytes(), k_max)
     tables = self._task_cache.get(key)
     if tables is None:
         tables = []
         for k in range(1, k_max + 1):
-            sel = all_tasks[n_idx >= k].copy()
+            sel = st.all_tasks[st.n_idx >= k].copy()
             sel["tag"] = k
             tables.append(tasks_to_device(sel, dev))
         self._task_cache[key] = tables
     for k in range(1, k_max + 1):
         self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
-                                 ck0_d, cst_d, self.step_rtol(), self.max_it, U, F, C,
-                                 coarse_iters, status, active, stream, elapsed=pr_elapsed_c, xss=xss_c)
-        tk = tables[k - 1]
-        n_tk = tk.numel() // _lib.TASK_DTYPE.itemsize
-        sel = all_tasks[n_idx >= k]
+                                 st.ck0_d, st.cst_d, self.step_rtol(), self.max_it, st.U, st.F,
+                                 st.C, st.coarse_iters, st.status, st.active, stream,
+                                 elapsed=st.elapsed_c, xss=st.xss_c)
+        sel = st.all_tasks[st.n_idx >= k]
         self.sys.propagate(sel, M, K, self.profile, self.omega, self.step_rtol(), self.max_it,
-                           buf, slice_qoi, fine_iters, fine_status, active, stream, tasks_dev=tk,
-                           elapsed=pr_elapsed_f, xss=xss_f)
-        assert n_tk == len(sel)
-        self.sys.parareal_defect(S, k, m, k_max, U, F, tol, active, k_used, defects, stream)
-    self.sys.parareal_finalize(S, m, U, F, k_used, stream)
-    ekey = ("energy", S, m, N)
-    ev = self._task_cache.get(ekey)
-    if ev is None:
-        ev = (torch.arange(S, dtype=I32, device=dev),
-              torch.tensor((uf_size + (np.arange(S) * (m + 1) + m) * N).astype(np.int64),
-                           device=dev))
-        self._task_cache[ekey] = ev
-    if slice_qoi is not None:
-        qoi = slice_qoi.view(S, m).sum(dim=1)
-    else:
-        qoi = self.sys.energy(ev[0], ev[1], buf, K, stream)
-    traj = None
-    if keep_traj:
-        traj = buf[2 * uf_size:].view(S, m, traj_steps, N)
+                           st.buf, st.slice_qoi, st.fine_iters, st.fine_status, st.active, stream,
+                           tasks_dev=tables[k - 1], elapsed=st.elapsed_f, xss=st.xss_f)
+        self.sys.parareal_defect(S, k, m, k_max, st.U, st.F, tol, st.active, st.k_used,
+                                 st.defects, stream)
+    self.sys.parareal_finalize(S, m, st.U, st.F, st.k_used, stream)
     self._keep = tables
-    return PararealBatchResult(qoi, k_used, defects, status, fine_status, U, F, traj,
-                               fine_iters, coarse_iters,
-                               (pr_elapsed_c, pr_elapsed_f) if self.timing else None)
+    return _pr_result(self, st, K, stream)
+
+
+def _run_fused(self, M, K, jobs: list[SeqJob], pr=None, stream=None, grid_ctas: int = 0):
+    """Sequential jobs and/or one Parareal batch in ONE persistent launch with
+    the device-side scheduler (mlmcp_run_fused).  ``pr`` = dict(row0, S, t0,
+    t1, m, dt_fine, dt_coarse, tol, k_max, qoi_mode, qoi_index, qoi_from).
+    Every task kind addresses one set of arrays (states, QoI, iteration,
+    status and timer slots, steady states), laid out [sequential | Parareal
+    fine | Parareal coarse].  Returns (list of SeqResult, PararealBatchResult
+    or None)."""
+    from types import SimpleNamespace
+    N = self.N
+    dev = self.device
+    pred = self.use_predictor()
+    # ---- sequential part (slots 0 .. T-1)
+    T = int(sum(len(j.rows) for j in jobs))
+    tasks = new_tasks(T)
+    off = 0
+    for j in jobs:
+        sl = slice(off, off + len(j.rows))
+        tasks["sample"][sl] = j.rows
+        tasks["n_steps"][sl] = j.n_steps
+        tasks["dt"][sl] = j.dt
+        tasks["qoi_mode"][sl] = j.qoi_mode
+        tasks["qoi_from"][sl] = j.qoi_from
+        tasks["qoi_index"][sl] = j.qoi_index
+        off += len(j.rows)
+    idx = np.arange(T)
+    tasks["x_in"] = idx * N
+    tasks["x_out"] = idx * N
+    tasks["qoi_slot"] = idx
+    tasks["slot"] = idx
+    if pred:
+        tasks["ss_slot"] = idx
+    order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
+    # ---- Parareal part
+    S = int(pr["S"]) if pr is not None else 0
+    m = int(pr["m"]) if S else 1
+    k_max = int(pr["k_max"]) if S else 1
+    n_fine = S * m
+    n_slots = T + n_fine + S
+    u_off = T * N
+    uf = S * (m + 1) * N
+    c_tmp_off = u_off + 2 * uf
+    xbuf = torch.zeros(c_tmp_off + S * N, dtype=F64, device=dev)
+    qoi = torch.zeros(T + n_fine, dtype=F64, device=dev)
+    iters = torch.zeros(n_slots, dtype=I32, device=dev)
+    status = torch.zeros((n_slots, _lib.STATUS_INTS), dtype=I32, device=dev)
+    elapsed = torch.zeros(n_slots, dtype=torch.int64, device=dev) if self.timing else None
+    active = torch.ones(max(S, 1), dtype=I32, device=dev)
+    batch = _lib.PararealBatch()
+    pst = None
+    ss_samples = [tasks["sample"]] if pred else []
+    ss_dts = [tasks["dt"]] if pred else []
+    if S:
+        bounds, fk0, fst, ck0, cst = parareal_grid(pr["t0"], pr["t1"], m, pr["dt_fine"],
+                                                   pr["dt_coarse"])
+        s_idx, n_idx = np.meshgrid(np.arange(S), np.arange(1, m + 1), indexing="ij")
+        s_idx, n_idx = s_idx.ravel(), n_idx.ravel()
+        ft = new_tasks(n_fine)
+        ft["sample"] = pr["row0"] + s_idx
+        ft["n_steps"] = fst[n_idx - 1]
+        ft["k0"] = fk0[n_idx - 1]
+        ft["dt"] = pr["dt_fine"]
+        ft["t_base"] = pr["t0"]
+        ft["x_in"] = u_off + (s_idx * (m + 1) + (n_idx - 1)) * N
+        ft["x_out"] = u_off + uf + (s_idx * (m + 1) + n_idx) * N
+        ft["group"] = s_idx
+        ft["slot"] = T + s_idx * m + (n_idx - 1)
+        qm = pr.get("qoi_mode")
+        slice_q = qm is not None and qm != _lib.QOI_FINAL_ENERGY
+        if slice_q:
+            ft["qoi_slot"] = T + s_idx * m + (n_idx - 1)
+            ft["qoi_mode"] = qm
+            ft["qoi_from"] = pr.get("qoi_from", -1)
+            ft["qoi_index"] = pr.get("qoi_index", 0)
+        if pred:
+            ft["ss_slot"] = T + s_idx
+            rows = pr["row0"] + np.arange(S)
+            ss_samples += [rows, rows]
+            ss_dts += [np.full(S, pr["dt_fine"]), np.full(S, pr["dt_coarse"])]
+        key = ("fused-fine", ft.tobytes())
+        ftd = self._task_cache.get(key)
+        if ftd is None:
+            ftd = tasks_to_device(ft, dev)
+            self._task_cache[key] = ftd
+        ck0_d, cst_d = self._grid_tensors(ck0, cst)
+        C = torch.zeros((S, m, N), dtype=F64, device=dev)
+        k_used = torch.zeros(S, dtype=I32, device=dev)
+        defects = torch.full((S, k_max), float("nan"), dtype=F64, device=dev)
+        batch = _lib.PararealBatch(S, int(pr["row0"]), m, k_max, float(pr["tol"]),
+                                   float(pr["dt_coarse"]), float(pr["t0"]), ptr(ck0_d),
+                                   ptr(cst_d), ptr(ftd), u_off, c_tmp_off, ptr(C), T + n_fine,
+                                   T + S if pred else -1, ptr(k_used), ptr(defects))
+        pst = SimpleNamespace(S=S, m=m, k_max=k_max, row0=int(pr["row0"]), uf_size=uf,
+                              buf=xbuf[u_off:u_off + 2 * uf], C=C, active=active[:S],
+                              k_used=k_used, defects=defects, keep_traj=False,
+                              status=status[T + n_fine:], fine_status=status[T:T + n_fine],
+                              fine_iters=iters[T:T + n_fine], coarse_iters=iters[T + n_fine:],
+                              elapsed_c=None if elapsed is None else elapsed[T + n_fine:],
+                              elapsed_f=None if elapsed is None else elapsed[T:T + n_fine],
+                              slice_qoi=qoi[T:] if slice_q else None, traj_steps=0, t0=pr["t0"],
+                              dt_coarse=pr["dt_coarse"])
+        pst.U = pst.buf[:uf].view(S, m + 1, N)
+        pst.F = pst.buf[uf:].view(S, m + 1, N)
+    xss = None
+    if pred and (T or S):
+        xss = self.steady_states(np.concatenate(ss_samples), np.concatenate(ss_dts), M, K, stream)
+    td = None
+    if T:
+        key = (tasks.tobytes(), N)
+        td = self._task_cache.get(key)
+        if td is None:
+            td = tasks_to_device(tasks[order], dev)
+            self._task_cache[key] = td
+    arrays = _lib.TaskArrays(T, ptr(td) if td is not None else None, ptr(xss), ptr(xbuf),
+                             ptr(qoi), ptr(iters), ptr(status), ptr(active), ptr(elapsed))
+    cur = stream if stream is not None else torch.cuda.current_stream()
+    if self.events is not None:
+        self.events[0].record(cur)
+    if T or S:
+        self.sys.run_fused(M, K, self.profile, self.omega, self.step_rtol(), self.max_it, arrays,
+                           batch, S, m, k_max, stream, grid_ctas)
+    if self.events is not None:
+        self.events[1].record(cur)
+    sq = SimpleNamespace(jobs=jobs, qoi=qoi[:T], iters=iters[:T], status=status[:T],
+                         elapsed=None if elapsed is None else elapsed[:T], xbuf=xbuf[:T * N],
+                         tasks=tasks)
+    res = _seq_results(self, sq)
+    self._keep_fused = (arrays, batch, td, xss)
+    return res, (_pr_result(self, pst, K, stream) if pst is not None else None)
 
 
 def raise_on_status(status: torch.Tensor, what: str):

@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_counters():
     lib = _lib.load()
-    assert lib.mlmcp_abi_version() == _lib.ABI_VERSION == 4
+    assert lib.mlmcp_abi_version() == _lib.ABI_VERSION == 7
     assert _lib.launch_count() >= 0
 
 
@@ -101,3 +101,14 @@ def _load_fresh(path):
         return _lib.load(path)
     finally:
         _lib._lib = saved
+
+
+@pytest.mark.parametrize("name,cls", [("mlmcp_task_arrays", "TaskArrays"),
+                                      ("mlmcp_parareal_batch", "PararealBatch")])
+def test_batch_struct_layout_matches_header(name, cls):
+    src = open(os.path.join(ROOT, "include", "mlmcp.h")).read()
+    body = src[src.index("typedef struct %s {" % name):src.index("} %s;" % name)]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"(\w+)\s*;", body)
+    st = getattr(_lib, cls)
+    assert [f[0] for f in st._fields_] == fields
