@@ -563,12 +563,13 @@ def _run_fused(self, M, K, jobs: list[SeqJob], pr=None, stream=None, grid_ctas: 
     arrays = _lib.TaskArrays(T, ptr(td) if td is not None else None, ptr(xss), ptr(xbuf),
                              ptr(qoi), ptr(iters), ptr(status), ptr(active), ptr(elapsed))
     cur = stream if stream is not None else torch.cuda.current_stream()
-    if self.events is not None:
+    timed = self.events is not None and T > 0     # events bracket launches with sequential tasks
+    if timed:
         self.events[0].record(cur)
     if T or S:
         self.sys.run_fused(M, K, self.profile, self.omega, self.step_rtol(), self.max_it, arrays,
                            batch, S, m, k_max, stream, grid_ctas)
-    if self.events is not None:
+    if timed:
         self.events[1].record(cur)
     sq = SimpleNamespace(jobs=jobs, qoi=qoi[:T], iters=iters[:T], status=status[:T],
                          elapsed=None if elapsed is None else elapsed[:T], xbuf=xbuf[:T * N],
