@@ -149,7 +149,9 @@ class BatchSolver:
             v = (torch.tensor(samples.astype(np.int32), device=self.device),
                  torch.tensor(dts.astype(np.float64), device=self.device))
             self._task_cache[key] = v
-        return self.sys.periodic_state(v[0], v[1], M, K, self.profile, self.omega, stream=stream)
+        return self.sys.periodic_state(v[0], v[1], M, K, self.profile, self.omega,
+                                       rtol=float(os.environ.get("MLMCP_SS_RTOL", "1e-8")),
+                                       stream=stream)
 
     def _grid_tensors(self, ck0, cst):
         key = ("grid", ck0.tobytes(), cst.tobytes())
