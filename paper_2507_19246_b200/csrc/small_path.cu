@@ -1306,6 +1306,7 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_periodic_kernel(Period
   const double* Ks = a.K + (int64_t)s * a.nnz;
   Op op;
   op.load(pa, Ms, Ks, dt);
+  op.load_mass(pa, Ms, sh.mm);          // GridOp: M in smem (no global loads per iteration)
   double sn, c;
   sincos(__dmul_rn(a.omega, dt), &sn, &c);
   double ir[R], ii[R], xr[R], xi[R], rr[R], ri[R], pr[R], pi[R];
@@ -1342,8 +1343,8 @@ __global__ void __launch_bounds__(kSmallThreads, 1) small_periodic_kernel(Period
       double apr[R], api[R], mpr[R], mpi[R];
       op.apply(pr, sh.bufA, pa, apr);
       op.apply(pi, sh.bufB, pa, api);
-      op.apply_vals(Ms, pr, sh.bufA, pa, mpr);
-      op.apply_vals(Ms, pi, sh.bufB, pa, mpi);
+      op.apply_mass(Ms, sh.mm, pr, sh.bufA, pa, mpr);
+      op.apply_mass(Ms, sh.mm, pi, sh.bufB, pa, mpi);
       double qr[R], qi[R];
       double sg[2] = {0.0, 0.0};
 #pragma unroll

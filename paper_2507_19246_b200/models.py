@@ -349,13 +349,14 @@ class _BatchedFamily:
 
     def _run_levels_fused(self, levels, sizes, offs, M, K, assemble_level, pr_level,
                           parareal_cfg):
-        """The sequential batch as one launch on the current stream and the
-        finest level's Parareal as a persistent device-scheduled launch
-        (mlmcp_run_fused) holding a fixed share of the SM slots on a second
-        stream, launched first: every Parareal chain step starts as soon as its
-        own inputs are ready instead of waiting for slots held by long
-        sequential tasks (MLMCP_FUSED=all: both batches in one scheduled
-        launch)."""
+        """Every sequential solve and the finest level's Parareal in ONE
+        persistent device-scheduled launch (mlmcp_run_fused): each Parareal
+        chain step starts as soon as its own inputs are ready instead of
+        waiting for SM slots held by long sequential tasks, and sequential
+        tasks fill the rest.  MLMCP_FUSED=split: the sequential batch as its
+        own launch and the Parareal as a persistent launch on a fixed share of
+        the slots on a second stream (sensitive to which launch the hardware
+        dispatches first)."""
         import os
 
         import torch
@@ -371,7 +372,7 @@ class _BatchedFamily:
                            t1=self.horizon, m=cfg.num_subintervals, dt_fine=cfg.dt_fine,
                            dt_coarse=cfg.dt_coarse, tol=cfg.tolerance, k_max=cfg.k_max,
                            **self._pr_qoi(cfg.dt_fine))
-        if pr_spec is None or os.environ.get("MLMCP_FUSED") == "all":
+        if pr_spec is None or os.environ.get("MLMCP_FUSED", "all") != "split":
             res, pr = sol.run_fused(M, K, jobs, pr_spec)
         else:
             main = torch.cuda.current_stream()
