@@ -239,6 +239,11 @@ def _dist():
     return None
 
 
+def torch_device_type(device) -> str:
+    import torch
+    return torch.device(device).type
+
+
 def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
     """Slot buffer -> all-reduce -> fixed-order K7 reduction."""
     import torch
@@ -305,14 +310,33 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
         slots, sums = _reduce_level(batch, counts[lvl], a, b, dist, dev)
         all_slots.append(slots)
         sums_dev.append(sums)
-    if hasattr(family, "check_status"):
-        family.check_status()
-    host = [s.cpu().numpy() for s in sums_dev]
+    top = len(hierarchy) - 1
+    want_k = parareal_cfg is not None
+    flag = family.status_flag() if hasattr(family, "status_flag") else None
+    if dev is not None and torch_device_type(dev) == "cuda":
+        # one device->host read for the level sums, the Parareal K slots and the
+        # failure flag (the detailed status check only runs when a task failed)
+        import torch
+        parts = [s.to(torch.float64) for s in sums_dev]
+        if want_k:
+            parts.append(all_slots[top][:, 2])
+        if flag is not None:
+            parts.append(flag.to(torch.float64).reshape(1))
+        pack = torch.cat([p.reshape(-1) for p in parts]).cpu().numpy()
+        if flag is not None and pack[-1] != 0.0:
+            family.check_status()
+        host = [pack[4 * i:4 * i + 4] for i in range(len(sums_dev))]
+        ks_host = pack[4 * len(sums_dev):4 * len(sums_dev) + counts[top]] if want_k else None
+    else:
+        if hasattr(family, "check_status"):
+            family.check_status()
+        host = [s.cpu().numpy() for s in sums_dev]
+        ks_host = all_slots[top][:, 2].cpu().numpy() if want_k else None
     wall = time.perf_counter() - t_start
     for lvl, sums in enumerate(host):
         ks = None
-        if parareal_cfg is not None and lvl == len(hierarchy) - 1:
-            ks = all_slots[lvl][:, 2].cpu().numpy().astype(int).tolist()
+        if want_k and lvl == top:
+            ks = ks_host.astype(int).tolist()
         per_level.append(LevelStats(lvl, counts[lvl], float(sums[0]), float(sums[1]),
                                     wall / max(1, sum(counts)), ks))
     expectation = float(sum(st.mean_y for st in per_level))

@@ -389,9 +389,23 @@ class _BatchedFamily:
         self._last = (res, pr, M, K)
         return self._collect(levels, sizes, where, res, pr_level, pr, pr_q)
 
+    def status_flag(self):
+        """0-d device tensor: any failed task in the last run (no host sync)."""
+        import torch
+        if getattr(self, "_last", None) is None:
+            return None
+        res, pr, _, _ = self._last
+        sts = [r.status for r in res]
+        if pr is not None:
+            sts += [pr.status, pr.fine_status]
+        sts = [st for st in sts if st.numel()]
+        if not sts:
+            return None
+        return torch.stack([(st[:, 0] != 0).any() for st in sts]).any()
+
     def check_status(self):
         """Raise SingularSystemError / PropagatorError for failed samples of the
-        last run (one host sync)."""
+        last run."""
         from .parareal import raise_parareal_status
         from .solver import raise_on_status
         if getattr(self, "_last", None) is None:
