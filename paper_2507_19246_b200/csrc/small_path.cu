@@ -508,6 +508,10 @@ constexpr int kMaxOrder = 3;
 constexpr int kRing = kMaxOrder + 1;   // power of two: slot arithmetic is a mask
 static_assert((kRing & (kRing - 1)) == 0, "ring size must be a power of two");
 
+// extrapolation order of the transient (MLMCP_ORDER, measurements; default 3)
+__constant__ int c_order = kMaxOrder;
+__device__ __forceinline__ int order_pref() { return c_order; }
+
 template <int R>
 struct StateHistory {
   double* ring;   // [kRing][R*256]: y_n, y_{n-1}, ... (ring, head = y_n)
@@ -767,7 +771,7 @@ __device__ __forceinline__ void run_task(const SmallArgs& a, const mlmcp_task& t
   int code = MLMCP_ST_OK;
   int fail_step = 0;
   double acc = 0.0;
-  StateHistory<R> hist(sh.ring, no_extrap ? 0 : kMaxOrder);
+  StateHistory<R> hist(sh.ring, no_extrap ? 0 : order_pref());
   {
     double s0 = 0.0, c0 = 0.0;
     if (pred) sincos(__dmul_rn(a.omega, grid_time(t.t_base, t.k0, t.dt)), &s0, &c0);
@@ -913,7 +917,7 @@ __device__ __forceinline__ void run_coarse(const CoarseArgs& a, int s, SmallShar
       if (v) U[(a.k - 1) * N + i] = x[r];
     }
   }
-  StateHistory<R> hist(sh.ring, kMaxOrder);
+  StateHistory<R> hist(sh.ring, order_pref());
   double ss[R], an[R];
   double sf = 0.0, cf = 0.0;
   if (a.k < a.m) {
@@ -1552,6 +1556,17 @@ struct LaunchFused {
 
 }  // namespace
 
+static void set_order_once() {
+  static bool done = false;
+  if (done) return;
+  done = true;
+  const char* e = getenv("MLMCP_ORDER");
+  if (e) {
+    int o = std::max(0, std::min(atoi(e), kMaxOrder));
+    cudaMemcpyToSymbol(c_order, &o, sizeof(int));
+  }
+}
+
 size_t fused_workspace_bytes(int S, int m, int k_max) {
   const size_t qcap = (size_t)S * ((size_t)k_max * (2 * m + 1) + 2) + 1;
   return 256 + ((sizeof(int) * (size_t)(S + 1) + 255) & ~(size_t)255) +
@@ -1564,6 +1579,7 @@ int small_run_fused(Ctx* ctx, int S, const double* M, const double* K, const dou
                     cudaStream_t stream) {
   const int Sp = pr.S;
   if (ar.n_seq == 0 && Sp == 0) return MLMCP_OK;
+  set_order_once();
   const int m = std::max(pr.m, 1), kmax = std::max(pr.k_max, 1);
   const size_t need = fused_workspace_bytes(Sp, m, kmax);
   if (ws == nullptr || ws_bytes < need) {
@@ -1645,6 +1661,7 @@ int small_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double
                     const int32_t* active, int64_t* elapsed, const double* xss,
                     cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
+  set_order_once();
   SmallArgs a{};
   a.elapsed = elapsed;
   a.xss = xss;
