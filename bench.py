@@ -260,8 +260,16 @@ def main():
     b_it = 8 * nnz + 56 * N                                   # SURVEY §8(d) bytes / PCG iteration
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)   # > 126 MB L2
 
-    def one_step(rec):
-        batches = fam.run_levels(draws, pcfg, params_dev=params_dev)
+    graph_launches = [0]
+
+    def one_step(rec, graphed=True):
+        # the estimate's launch sequence replays as a captured CUDA graph
+        # (libmlmcp kernels counted at capture: graph_launches)
+        if graphed:
+            batches = fam.run_levels_graphed(draws, pcfg, params_dev=params_dev)
+            graph_launches[0] += fam._graph_launches
+        else:
+            batches = fam.run_levels(draws, pcfg, params_dev=params_dev)
         sums = []
         for lvl, (b, (a, e)) in enumerate(zip(batches, ranges)):
             slots = torch.zeros((counts[lvl], 4), dtype=torch.float64, device=dev)
@@ -281,10 +289,10 @@ def main():
     fam.check_status()
     seq_start = torch.cuda.Event(enable_timing=True)
     seq_end = torch.cuda.Event(enable_timing=True)
-    sol.events = (seq_start, seq_end)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     seq_ms, batches_rec = [], []
+    graph_launches[0] = 0
     clocks = ClockSampler()
     if world > 1:
         dist.barrier()
@@ -298,15 +306,22 @@ def main():
         one_step(batches_rec)
         ev[s][1].record()
         torch.cuda.synchronize()
-        seq_ms.append(seq_start.elapsed_time(seq_end))
     torch.cuda.synchronize()
     wall = time.perf_counter() - wall0
-    launches = (_lib.launch_count() - l0) // max(1, args.steps)
+    launches = (_lib.launch_count() - l0 + graph_launches[0]) // max(1, args.steps)
     if world > 1:
         dist.barrier()
     clk = clocks.stop(local)
-    sol.events = None
     fam.check_status()
+    # roofline: the estimate launch timed with events on its stream (eager runs,
+    # same work as a replay)
+    sol.events = (seq_start, seq_end)
+    for _ in range(3):
+        flush.zero_()
+        one_step(None, graphed=False)
+        torch.cuda.synchronize()
+        seq_ms.append(seq_start.elapsed_time(seq_end))
+    sol.events = None
     step_ms = [a.elapsed_time(b) for a, b in ev]
     ms_local = float(np.mean(step_ms))
     ms = torch.tensor([ms_local], dtype=torch.float64, device=dev)

@@ -297,7 +297,10 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
     if sol is not None:
         sol.timing = True
     try:
-        batches = family.run_levels(draws, parareal_cfg)
+        if hasattr(family, "run_levels_graphed"):
+            batches = family.run_levels_graphed(draws, parareal_cfg)
+        else:
+            batches = family.run_levels(draws, parareal_cfg)
     finally:
         if sol is not None:
             sol.timing = False

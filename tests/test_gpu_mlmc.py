@@ -257,3 +257,26 @@ def test_fused_launch_matches_separate_launches(cuda, cfg_id, counts):
             np.testing.assert_allclose(x.q_l.cpu().numpy(), y.q_l.cpu().numpy(), rtol=1e-10)
             np.testing.assert_allclose(x.defects.cpu().numpy(), y.defects.cpu().numpy(),
                                        rtol=1e-6, atol=1e-11)
+
+
+def test_graph_replay_matches_eager(cuda):
+    """mlmc_estimate's CUDA-graph replay (run_levels_graphed) gives the same
+    per-level sums as the eager launch sequence, across repeated estimates
+    with different draws (seeds)."""
+    from paper_2507_19246_b200.configs import get_config
+    from paper_2507_19246_b200.mlmc import draw_level
+    from paper_2507_19246_b200.models import eddy_current_family
+    fam = eddy_current_family(1, device="cuda:0")
+    pcfg = get_config(1).parareal_config()
+    counts = (20, 10, 6)
+    for seed in (0, 1, 0):
+        draws = [draw_level(fam.uncertain, seed, lvl, range(1, n + 1))
+                 for lvl, n in enumerate(counts)]
+        g = fam.run_levels_graphed(draws, pcfg)
+        gq = [(b.q_l.cpu().numpy().copy(), b.q_lm1.cpu().numpy().copy(), b.k_used.cpu().numpy().copy())
+              for b in g]
+        e = fam.run_levels(draws, pcfg)
+        for (ql, qm, ku), b in zip(gq, e):
+            np.testing.assert_array_equal(ql, b.q_l.cpu().numpy())
+            np.testing.assert_array_equal(qm, b.q_lm1.cpu().numpy())
+            np.testing.assert_array_equal(ku, b.k_used.cpu().numpy())
