@@ -244,18 +244,51 @@ def torch_device_type(device) -> str:
     return torch.device(device).type
 
 
-def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
-    """Slot buffer -> all-reduce -> fixed-order K7 reduction."""
+def _fill_slots(slots, batch, a: int, b: int):
     import torch
-    on_gpu = device is not None and torch.device(device).type == "cuda"
-    dev = device if on_gpu else "cpu"
-    slots = torch.zeros((n_global, 4), dtype=torch.float64, device=dev)
+    dev = slots.device
     if b > a:
         slots[a:b, 0] = batch.q_l.to(dev, torch.float64)
         slots[a:b, 1] = batch.q_lm1.to(dev, torch.float64)
         slots[a:b, 2] = batch.k_used.to(dev, torch.float64)
         if batch.iters is not None:
             slots[a:b, 3] = batch.iters.to(dev, torch.float64)
+
+
+def _run_chunked(family, ranges, counts, cap: int, seed: int, parareal_cfg, dev):
+    """Evaluate the rank's sample ranges in run_levels calls of <= cap samples
+    (level by level, keys unchanged) into per-level slot buffers."""
+    import torch
+    slots = [torch.zeros((n, 4), dtype=torch.float64, device=dev) for n in counts]
+    last = None
+    for lvl, (a, b) in enumerate(ranges):
+        for c0 in range(a, b, cap):
+            c1 = min(b, c0 + cap)
+            draws = [np.zeros((0, 1)) for _ in ranges]
+            draws[lvl] = draw_level(family.uncertain, seed, lvl, range(c0 + 1, c1 + 1))
+            out = family.run_levels(draws, parareal_cfg)
+            if hasattr(family, "check_status"):
+                family.check_status()
+            _fill_slots(slots[lvl], out[lvl], c0, c1)
+            last = out
+    return slots, last
+
+
+def _reduce_slots(slots, dist, device):
+    import torch
+    if dist is not None and dist.get_world_size() > 1:
+        dist.all_reduce(slots, op=dist.ReduceOp.SUM)
+    from .engine import level_reduce
+    return level_reduce(slots[:, 0].contiguous(), slots[:, 1].contiguous())
+
+
+def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
+    """Slot buffer -> all-reduce -> fixed-order K7 reduction."""
+    import torch
+    on_gpu = device is not None and torch.device(device).type == "cuda"
+    dev = device if on_gpu else "cpu"
+    slots = torch.zeros((n_global, 4), dtype=torch.float64, device=dev)
+    _fill_slots(slots, batch, a, b)
     if dist is not None and dist.get_world_size() > 1:
         dist.all_reduce(slots, op=dist.ReduceOp.SUM)
     if on_gpu:
@@ -293,26 +326,35 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
         draws = [LazyDraw(b - a, (lambda lvl=lvl, a=a, b=b: draw_level(
             family.uncertain, seed, lvl, range(a + 1, b + 1))))
             for lvl, (a, b) in enumerate(ranges)]
-    sol = getattr(family, "solver", None) if timing else None
-    if sol is not None:
-        sol.timing = True
-    try:
-        if hasattr(family, "run_levels_graphed"):
-            batches = family.run_levels_graphed(draws, parareal_cfg)
-        else:
-            batches = family.run_levels(draws, parareal_cfg)
-    finally:
-        if sol is not None:
-            sol.timing = False
     dev = device
     if dev is None and hasattr(family, "solver"):
         dev = family.solver.device
-    per_level, all_slots = [], []
-    sums_dev = []
-    for lvl, (batch, (a, b)) in enumerate(zip(batches, ranges)):
-        slots, sums = _reduce_level(batch, counts[lvl], a, b, dist, dev)
-        all_slots.append(slots)
-        sums_dev.append(sums)
+    sol = None
+    cap = (family.max_samples_per_call(parareal_cfg)
+           if hasattr(family, "max_samples_per_call") else None)
+    if cap is not None and sum(b - a for a, b in ranges) > cap:
+        # full-size streaming configs: the rank's samples in calls of <= cap
+        # samples, filling the per-sample slot buffers (same keys, same result)
+        all_slots, batches = _run_chunked(family, ranges, counts, cap, seed, parareal_cfg, dev)
+        sums_dev = [_reduce_slots(slots, dist, dev) for slots in all_slots]
+    else:
+        sol = getattr(family, "solver", None) if timing else None
+        if sol is not None:
+            sol.timing = True
+        try:
+            if hasattr(family, "run_levels_graphed"):
+                batches = family.run_levels_graphed(draws, parareal_cfg)
+            else:
+                batches = family.run_levels(draws, parareal_cfg)
+        finally:
+            if sol is not None:
+                sol.timing = False
+        all_slots, sums_dev = [], []
+        for lvl, (batch, (a, b)) in enumerate(zip(batches, ranges)):
+            slots, sums = _reduce_level(batch, counts[lvl], a, b, dist, dev)
+            all_slots.append(slots)
+            sums_dev.append(sums)
+    per_level = []
     top = len(hierarchy) - 1
     want_k = parareal_cfg is not None
     flag = family.status_flag() if hasattr(family, "status_flag") else None

@@ -573,6 +573,24 @@ class EddyCurrentFamily(_BatchedFamily):
             return acc * dt / self.avg_window
         return acc
 
+    def max_samples_per_call(self, parareal_cfg=None):
+        """Samples one run_levels call may hold on this GPU: None on the
+        SM-resident path (a config-1 estimate needs ~0.2 GB); on the streaming
+        path (128^2..512^2, up to 29 MB of operators per sample plus the
+        per-task workspace) 40% of the free HBM divided by the per-sample
+        footprint, so full-size configs 2-4 run as a sequence of calls."""
+        import torch
+        sol = self.solver
+        if sol.sys.sm_resident:
+            return None
+        free, _ = torch.cuda.mem_get_info(sol.device)
+        lib = sol.sys.lib
+        per = 16 * sol.nnz + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, 2, 1))
+        if parareal_cfg is not None:
+            m = parareal_cfg.num_subintervals
+            per += (3 * m + 2) * sol.N * 8 + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, m, 1))
+        return max(1, int(0.4 * free // max(per, 1)))
+
     def _n_params(self) -> int:
         return fe.n_params(self.layout)
 

@@ -280,3 +280,22 @@ def test_graph_replay_matches_eager(cuda):
             np.testing.assert_array_equal(ql, b.q_l.cpu().numpy())
             np.testing.assert_array_equal(qm, b.q_lm1.cpu().numpy())
             np.testing.assert_array_equal(ku, b.k_used.cpu().numpy())
+
+
+def test_chunked_estimate_bitwise(cuda, monkeypatch):
+    """Full-size streaming configs run the rank's samples in several
+    run_levels calls (max_samples_per_call); per-sample results do not depend
+    on the batch composition, so the chunked estimate is bitwise the single-
+    call one (forced here with a cap of 5 samples on a small mesh)."""
+    from paper_2507_19246_b200.mlmc import FixedSamples, mlmc_estimate
+    from paper_2507_19246_b200.parareal import PararealConfig
+    fam = small_family()
+    pr = PararealConfig(4, T / 128, T / 16, 1e-8, 4)
+    counts = (12, 7, 5)
+    ref = mlmc_estimate(fam, policy=FixedSamples(counts), parareal_cfg=pr, seed=3)
+    monkeypatch.setattr(type(fam), "max_samples_per_call", lambda self, cfg=None: 5)
+    got = mlmc_estimate(fam, policy=FixedSamples(counts), parareal_cfg=pr, seed=3)
+    assert got.expectation == ref.expectation
+    for a, b in zip(got.per_level, ref.per_level):
+        assert (a.sum_y, a.sum_y2) == (b.sum_y, b.sum_y2)
+    assert got.per_level[-1].parareal_k == ref.per_level[-1].parareal_k
