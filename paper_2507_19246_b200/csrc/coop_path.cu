@@ -310,7 +310,7 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         res = b - ax;
         u = sl.dinv[r] * res;
         double* acc = (t == t_lo) ? lo4 : hi4;
-        acc[3] += b * b;
+        acc[3] += b * sl.dinv[r] * b;          // Jacobi-weighted norm of b
       }
       sl.r[r] = res;
       if (t >= 0) *xrow(a, a.Ub, t, sl.row[r]) = u;
@@ -344,8 +344,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
       const double bb = tot[t * 4 + 3];
       st.tol2 = a.rtol2 * bb;
       if (bb == 0.0) { st.zero = 1; continue; }          // b == 0 exactly: a = 0
-      if (rho <= st.tol2) continue;
-      if (!isfinite(rho)) { st.code = MLMCP_ST_NONFINITE; st.fail_step = step; st.live = 0; continue; }
+      if (gamma <= st.tol2) continue;                     // r.D^-1.r <= rtol^2 b.D^-1.b
+      if (!isfinite(gamma) || !isfinite(rho)) { st.code = MLMCP_ST_NONFINITE; st.fail_step = step; st.live = 0; continue; }
       if (!(delta > 0.0)) { st.code = MLMCP_ST_BREAKDOWN; st.fail_step = step; st.live = 0; continue; }
       st.done = 0;
       st.inv_g = fast_rcp(gamma);
@@ -398,8 +398,8 @@ __global__ void __launch_bounds__(kCoopThreads, 1) coop_kernel(CoopArgs a) {
         TaskState& st = ts[t];
         if (st.done) continue;
         const double gnew = tot[t * 4 + 0], delta = tot[t * 4 + 1], rho = tot[t * 4 + 2];
-        if (rho <= st.tol2) { st.done = 1; continue; }
-        if (!isfinite(rho)) { st.code = MLMCP_ST_NONFINITE; st.fail_step = step; st.live = 0; st.done = 1; continue; }
+        if (gnew <= st.tol2) { st.done = 1; continue; }
+        if (!isfinite(gnew) || !isfinite(rho)) { st.code = MLMCP_ST_NONFINITE; st.fail_step = step; st.live = 0; st.done = 1; continue; }
         if (st.it_step >= a.max_it) { st.code = MLMCP_ST_NOCONV; st.fail_step = step; st.live = 0; st.done = 1; continue; }
         const double beta = gnew * st.inv_g;
         const double den = fma(-(gnew * gnew), st.c, delta);

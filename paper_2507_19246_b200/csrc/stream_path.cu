@@ -2,8 +2,9 @@
 // interior system does not fit one SM (128^2 .. 512^2: configs 2, 3, 4).
 //
 // Same numerical method and step semantics as small_path.cu (reference:
-// timeint.py:88-128), but every PCG iteration is two grid-wide launches over
-// all live (task, row-block) pairs:
+// timeint.py:88-128: extrapolated initial guesses, Jacobi-weighted stopping
+// rule), but every PCG iteration is two grid-wide launches over all live
+// (task, row-block) pairs:
 //   K_spmv   w = A (D^-1 r) with the operator in a per-sample ELL layout
 //            [S][W][N] (coalesced, built once per call from the CSR M/K
 //            values), partial (r.u, w.u, r.r) per block; the last block of a
@@ -32,7 +33,10 @@ enum : int { D_BB = 0, D_GAMMA, D_ALPHA, D_BETA, D_ACC, D_SF, kTD };
 // task int layout
 enum : int { I_STATE = 0, I_IT_STEP, I_IT_TOTAL, I_CODE, I_FAILSTEP, I_FIRST, kTI };
 
+constexpr int kRingS = 4;   // past states a_{n-1..n-4} (order <= 4 extrapolation)
+
 struct Work {
+  double* ring;    // [kRingS][T][N]
   double* A;       // [S][W][N]
   double* dinv;    // [S][N]
   double* X;       // [T][N]
@@ -50,7 +54,7 @@ struct Work {
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t off[12];
+  size_t off[13];
   size_t total;
 };
 
@@ -58,12 +62,12 @@ Layout make_layout(const Ctx* ctx, int T, int S) {
   // operator slots: ELL width, or the stencil width for the cooperative path
   const size_t N = ctx->n, W = std::max(ctx->max_row_nnz, ctx->stencil_w), T_ = T, S_ = S;
   const size_t nblk = (N + kThreads - 1) / kThreads;
-  size_t sizes[12] = {S_ * W * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
+  size_t sizes[13] = {S_ * W * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
                       T_ * N * 8,     T_ * N * 8, T_ * nblk * 4 * 8, T_ * kTD * 8,
-                      T_ * kTI * 4,   T_ * 4,     64};
+                      T_ * kTI * 4,   T_ * 4,     64, kRingS * T_ * N * 8};
   Layout L;
   size_t o = 0;
-  for (int i = 0; i < 12; ++i) {
+  for (int i = 0; i < 13; ++i) {
     L.off[i] = o;
     o += align_up(sizes[i]);
   }
@@ -86,6 +90,7 @@ Work carve(void* ws, const Layout& L) {
   w.ti = reinterpret_cast<int32_t*>(b + L.off[9]);
   w.arrive = reinterpret_cast<int32_t*>(b + L.off[10]);
   w.counters = reinterpret_cast<int32_t*>(b + L.off[11]);
+  w.ring = reinterpret_cast<double*>(b + L.off[12]);
   return w;
 }
 
@@ -198,7 +203,30 @@ __global__ void copy_in_kernel(SArgs a) {
   }
 }
 
-// rhs b = M x + dt*sf*prof, r = b - A x, partial b.b
+// Initial guess of the step: polynomial extrapolation (order <= 4) of the
+// task's last states, a_n itself for MLMCP_TASK_NO_EXTRAPOLATION (the
+// reference's one-step semantics).  a_n moves to ring[step & 3] (the rhs reads
+// it there), X becomes the guess.
+__global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step) {
+  const int t = blockIdx.y;
+  const mlmcp_task tk = a.tasks[t];
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N || step >= tk.n_steps) return;
+  const int64_t TN = (int64_t)a.T * a.N, o = (int64_t)t * a.N + i;
+  const double an = a.w.X[o];
+  const int p = (tk.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : min(step, kRingS);
+  auto past = [&](int k) { return a.w.ring[(int64_t)((step - k) & (kRingS - 1)) * TN + o]; };
+  double g = an;
+  if (p == 1) g = fma(2.0, an, -past(1));
+  else if (p == 2) g = fma(3.0, an - past(1), past(2));
+  else if (p == 3) g = fma(4.0, an + past(2), fma(-6.0, past(1), -past(3)));
+  else if (p >= 4) g = fma(5.0, an - past(3), fma(10.0, past(2) - past(1), past(4)));
+  a.w.ring[(int64_t)(step & (kRingS - 1)) * TN + o] = an;
+  a.w.X[o] = g;
+}
+
+// rhs b = M a_n + dt*sf*prof, r = b - A x0, partial b.D^-1.b (Jacobi-weighted
+// norm of the stopping rule, as the SM-resident path)
 __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) {
   __shared__ double red[2 * 4 * 32];
   const int t = blockIdx.y;
@@ -211,17 +239,18 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) 
   double bb = 0.0;
   if (i < a.N) {
     const double* X = a.w.X + (int64_t)t * a.N;
+    const double* An = a.w.ring + (int64_t)(step & (kRingS - 1)) * a.T * a.N + (int64_t)t * a.N;
     const double* Ms = a.M + (int64_t)s * a.nnz;
     const double* As = a.w.A + (int64_t)s * a.W * a.N;
     double mx = 0.0;
     const int q0 = a.row_ptr[i], q1 = a.row_ptr[i + 1];
-    for (int q = q0; q < q1; ++q) mx = fma(Ms[q], X[a.col[q]], mx);
+    for (int q = q0; q < q1; ++q) mx = fma(Ms[q], An[a.col[q]], mx);
     double ax = 0.0;
     for (int j = 0; j < a.W; ++j)
       ax = fma(As[(int64_t)j * a.N + i], X[a.ell_col[j * a.N + i]], ax);
     const double b = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, a.profile[i])));
     a.w.R[(int64_t)t * a.N + i] = b - ax;
-    bb = b * b;
+    bb = b * a.w.dinv[(int64_t)s * a.N + i] * b;
   }
   double v[1] = {bb};
   if (task_reduce<1>(v, a, t, red) && threadIdx.x == 0) {
@@ -268,12 +297,12 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(SArgs a) {
   if (task_reduce<3>(v, a, t, red) && threadIdx.x == 0) {
     double* td = a.w.td + t * kTD;
     int32_t* ti = a.w.ti + t * kTI;
-    const double gamma = v[0], delta = v[1], rho = v[2];
+    const double gamma = v[0], delta = v[1];
     int code = MLMCP_ST_OK;
     bool stop = false;
-    if (rho <= a.rtol2 * td[D_BB]) {
+    if (gamma <= a.rtol2 * td[D_BB]) {   // r.D^-1.r <= rtol^2 b.D^-1.b
       stop = true;
-    } else if (!isfinite(rho)) {
+    } else if (!isfinite(gamma)) {
       code = MLMCP_ST_NONFINITE;
     } else if (ti[I_IT_STEP] >= a.max_it) {
       code = MLMCP_ST_NOCONV;
@@ -406,6 +435,8 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   int chunk = 4;
   for (int step = 0; step < n_steps_max; ++step) {
     MLMCP_CUDA_CHECK(cudaMemsetAsync(a.w.counters, 0, 2 * sizeof(int32_t), stream));
+    guess_kernel<<<grid_rows, blk, 0, stream>>>(a, step);
+    MLMCP_LAUNCH_CHECK("guess_kernel");
     step_init_kernel<<<grid_rows, blk, 0, stream>>>(a, step);
     MLMCP_LAUNCH_CHECK("step_init_kernel");
     int done_iters = 0;
