@@ -299,3 +299,29 @@ def test_chunked_estimate_bitwise(cuda, monkeypatch):
     for a, b in zip(got.per_level, ref.per_level):
         assert (a.sum_y, a.sum_y2) == (b.sum_y, b.sum_y2)
     assert got.per_level[-1].parareal_k == ref.per_level[-1].parareal_k
+
+
+def test_fused_scheduler_coarse_failure_ends_chains(cuda):
+    """A Parareal batch whose coarse solves cannot converge (max_it below the
+    coarse step's PCG count): every chain ends at its first coarse slice with
+    the reference's PropagatorError(interval=1, iteration=1) status, the
+    scheduler terminates, and no fine slice beyond the failure runs."""
+    import torch
+
+    from paper_2507_19246_b200 import _lib
+    from paper_2507_19246_b200.parareal import PropagatorError, raise_parareal_status
+    fam = small_family(n=32, max_it=20)
+    sol = fam.solver
+    P = np.array([mo.draw(mo.CONFIGS[1], 0, 2, k) for k in range(1, 5)])
+    M, K = sol.assemble(torch.from_numpy(P).cuda())
+    spec = dict(row0=0, S=4, t0=0.0, t1=T, m=16, dt_fine=T / 1024, dt_coarse=T / 16,
+                tol=1e-8, k_max=5, qoi_mode=_lib.QOI_FINAL_ENERGY)
+    _, pr = sol.run_fused(M, K, [], spec)
+    st = pr.status.cpu().numpy()
+    assert (st[:, 0] == _lib.ST_NOCONV).all()
+    assert (st[:, 2] == 1).all() and (st[:, 3] == 1).all()      # interval 1, iteration 1
+    fi = pr.fine_iters.cpu().numpy().reshape(4, 16)
+    assert (fi[:, 0] > 0).all() and (fi[:, 1:] == 0).all()
+    with pytest.raises(PropagatorError) as ei:
+        raise_parareal_status(st, pr.fine_status.cpu().numpy())
+    assert (ei.value.interval, ei.value.iteration) == (1, 1)
