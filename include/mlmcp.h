@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 7
+#define MLMCP_ABI_VERSION 8
 
 /* return codes */
 #define MLMCP_OK 0
@@ -187,12 +187,17 @@ int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
  * ss_slot = i then start every PCG solve from ss_{g} + the polynomial
  * extrapolation of a - ss (fewer iterations; the per-step stopping rule and
  * accuracy are unchanged).  COCG to rtol (loose, e.g. 1e-8); iters_d[i] =
- * COCG iterations (optional).  EINVAL on the streaming / direct paths. */
+ * COCG iterations (optional).  SM-resident path: one CTA per item, no
+ * workspace; streaming path (meshes > 1024 rows): grid-wide COCG kernels in
+ * ws_d (mlmcp_periodic_workspace_bytes), host-synchronous like
+ * mlmcp_propagate.  EINVAL on the direct path. */
+size_t mlmcp_periodic_workspace_bytes(const mlmcp_ctx* ctx, int n);
 int mlmcp_periodic_state(mlmcp_ctx* ctx, int n, const int32_t* sample_d,
                          const double* dt_d, int S, const double* M_d,
                          const double* K_d, const double* profile_d,
                          double omega, double rtol, int max_it, double* X_d,
-                         int32_t* iters_d, void* stream);
+                         int32_t* iters_d, void* ws_d, size_t ws_bytes,
+                         void* stream);
 
 /* ---- K5: Parareal ------------------------------------------------------ */
 /* Coarse/update sweep of iteration k (1-based) for S samples.

@@ -431,8 +431,8 @@ int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, c
   if (use_small(c))
     return small_propagate(c, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                            iters, status, active, elapsed, xss, (cudaStream_t)stream);
-  return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xbuf, qoi,
-                          iters, status, active, ws, ws_bytes, (cudaStream_t)stream);
+  return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xss, xbuf,
+                          qoi, iters, status, active, ws, ws_bytes, (cudaStream_t)stream);
 }
 
 int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, const double* K,
@@ -461,19 +461,27 @@ int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, co
                                 ws_bytes, (cudaStream_t)stream);
 }
 
+size_t mlmcp_periodic_workspace_bytes(const mlmcp_ctx* c, int n) {
+  if (c == nullptr || n <= 0 || use_small(c) || use_direct(c)) return 0;
+  return stream_periodic_workspace_bytes(c, n);
+}
+
 int mlmcp_periodic_state(mlmcp_ctx* c, int n, const int32_t* sample, const double* dt, int S,
                          const double* M, const double* K, const double* profile, double omega,
-                         double rtol, int max_it, double* X, int32_t* iters, void* stream) {
+                         double rtol, int max_it, double* X, int32_t* iters, void* ws,
+                         size_t ws_bytes, void* stream) {
   if (c == nullptr) return einval("null context");
   if (n < 0 || S < 1 || !sample || !dt || !M || !K || !profile || !X)
     return einval("null or empty periodic-state argument");
   if (!(rtol > 0.0) || max_it < 1) return einval("rtol must be > 0 and max_it >= 1");
-  if (use_direct(c) || !use_small(c))
-    return einval("periodic steady states are computed on the SM-resident path only");
+  if (use_direct(c)) return einval("periodic steady states: not on the direct path");
   if (n == 0) return MLMCP_OK;
   MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
-  return small_periodic(c, n, sample, dt, M, K, profile, omega, rtol, max_it, X, iters,
-                        (cudaStream_t)stream);
+  if (use_small(c))
+    return small_periodic(c, n, sample, dt, M, K, profile, omega, rtol, max_it, X, iters,
+                          (cudaStream_t)stream);
+  return stream_periodic(c, n, sample, dt, M, K, profile, omega, rtol, max_it, X, iters, ws,
+                         ws_bytes, (cudaStream_t)stream);
 }
 
 size_t mlmcp_fused_workspace_bytes(int S, int m, int k_max) {

@@ -191,11 +191,17 @@ void draw_uniform_cpu(uint64_t seed, uint64_t level, int64_t k_first, int n, int
                       const double* lo, const double* range, double* out);
 
 size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S);
+size_t stream_periodic_workspace_bytes(const Ctx* ctx, int n);
+int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
+                    const double* K, const double* profile, double omega, double rtol,
+                    int max_it, double* X, int32_t* iters, void* ws, size_t ws_bytes,
+                    cudaStream_t stream);
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                      const double* K, const double* profile, double omega, double rtol,
-                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                     const int32_t* active, void* ws, size_t ws_bytes, cudaStream_t stream);
+                     int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
+                     int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
+                     cudaStream_t stream);
 
 int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
                            const double* profile, double omega, double dt_c, double t0,

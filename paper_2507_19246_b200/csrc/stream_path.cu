@@ -112,6 +112,7 @@ struct SArgs {
   int32_t* iters;
   int32_t* status;
   int32_t* active;
+  const double* xss;   // [slots][2][N] periodic steady states (task.ss_slot) or null
   Work w;
 };
 
@@ -203,26 +204,47 @@ __global__ void copy_in_kernel(SArgs a) {
   }
 }
 
-// Initial guess of the step: polynomial extrapolation (order <= 4) of the
-// task's last states, a_n itself for MLMCP_TASK_NO_EXTRAPOLATION (the
-// reference's one-step semantics).  a_n moves to ring[step & 3] (the rhs reads
-// it there), X becomes the guess.
+// Initial guess of the step (as the SM-resident path): with a periodic steady
+// state X (task.ss_slot >= 0) the guess is ss_{n+1} + the order-3
+// extrapolation of the transients y = a - ss; without, the order-4
+// extrapolation of the states; a_n itself for MLMCP_TASK_NO_EXTRAPOLATION
+// (the reference's one-step semantics).  The ring keeps y (= a when ss = 0),
+// a_n moves to Wv (the rhs reads it there), X becomes the guess.
 __global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step) {
+  __shared__ double sc[4];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
+  const bool pred = a.xss != nullptr && tk.ss_slot >= 0 &&
+                    !(tk.flags & MLMCP_TASK_NO_EXTRAPOLATION);
+  if (threadIdx.x == 0 && pred) {
+    const int64_t g = tk.k0 + step + 1;
+    sincos(__dmul_rn(a.omega, grid_time(tk.t_base, g, tk.dt)), &sc[0], &sc[1]);
+    sincos(__dmul_rn(a.omega, grid_time(tk.t_base, g - 1, tk.dt)), &sc[2], &sc[3]);
+  }
+  __syncthreads();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N || step >= tk.n_steps) return;
   const int64_t TN = (int64_t)a.T * a.N, o = (int64_t)t * a.N + i;
   const double an = a.w.X[o];
-  const int p = (tk.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : min(step, kRingS);
+  double sst = 0.0, ssn = 0.0;
+  if (pred) {
+    const double* Xs = a.xss + (int64_t)tk.ss_slot * 2 * a.N;
+    const double xr = Xs[i], xi = Xs[a.N + i];
+    sst = fma(xr, sc[0], xi * sc[1]);
+    ssn = fma(xr, sc[2], xi * sc[3]);
+  }
+  const double yn = an - ssn;
+  const int pmax = pred ? 3 : kRingS;
+  const int p = (tk.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : min(step, pmax);
   auto past = [&](int k) { return a.w.ring[(int64_t)((step - k) & (kRingS - 1)) * TN + o]; };
-  double g = an;
-  if (p == 1) g = fma(2.0, an, -past(1));
-  else if (p == 2) g = fma(3.0, an - past(1), past(2));
-  else if (p == 3) g = fma(4.0, an + past(2), fma(-6.0, past(1), -past(3)));
-  else if (p >= 4) g = fma(5.0, an - past(3), fma(10.0, past(2) - past(1), past(4)));
-  a.w.ring[(int64_t)(step & (kRingS - 1)) * TN + o] = an;
-  a.w.X[o] = g;
+  double g = yn;
+  if (p == 1) g = fma(2.0, yn, -past(1));
+  else if (p == 2) g = fma(3.0, yn - past(1), past(2));
+  else if (p == 3) g = fma(4.0, yn + past(2), fma(-6.0, past(1), -past(3)));
+  else if (p >= 4) g = fma(5.0, yn - past(3), fma(10.0, past(2) - past(1), past(4)));
+  a.w.ring[(int64_t)(step & (kRingS - 1)) * TN + o] = yn;
+  a.w.Wv[o] = an;
+  a.w.X[o] = g + sst;
 }
 
 // rhs b = M a_n + dt*sf*prof, r = b - A x0, partial b.D^-1.b (Jacobi-weighted
@@ -239,7 +261,7 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) 
   double bb = 0.0;
   if (i < a.N) {
     const double* X = a.w.X + (int64_t)t * a.N;
-    const double* An = a.w.ring + (int64_t)(step & (kRingS - 1)) * a.T * a.N + (int64_t)t * a.N;
+    const double* An = a.w.Wv + (int64_t)t * a.N;      // a_n (guess_kernel)
     const double* Ms = a.M + (int64_t)s * a.nnz;
     const double* As = a.w.A + (int64_t)s * a.W * a.N;
     double mx = 0.0;
@@ -492,6 +514,7 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   a.iters = iters;
   a.status = status;
   a.active = const_cast<int32_t*>(active);
+  a.xss = nullptr;
   a.w = w;
   return a;
 }
@@ -538,6 +561,233 @@ __global__ void coarse_status_kernel(int S, int k, int n, const int32_t* tstatus
   }
 }
 
+
+// ---------------------------------------------------------------- steady states
+// Periodic steady state X of the implicit-Euler iteration for meshes that do
+// not fit one SM (the streaming counterpart of small_periodic_kernel):
+// (Zr + i Zi) X = dt profile with Zr = (1 - cos w dt) M + dt K, Zi = sin(w dt) M,
+// by COCG with the complex Jacobi preconditioner, one (sample, dt) item per
+// blockIdx.y, the operator applied from the CSR values on the fly.  Per item
+// workspace: x, r, p, z, q (complex) and D^-1 (complex) = 12 N doubles.
+struct PArgs {
+  int T, N, nblk;
+  int64_t nnz;
+  const int32_t* row_ptr;
+  const int32_t* col;
+  const int32_t* sample;
+  const double* dt;
+  const double* M;
+  const double* K;
+  const double* profile;
+  double omega, rtol2;
+  int max_it;
+  double* vec;       // [T][12][N]
+  double* partial;   // [T][nblk][4]
+  double* td;        // [T][8]: rho_r, rho_i, bb, alpha_r, alpha_i, beta_r, beta_i, -
+  int32_t* ti;       // [T][4]: state, iters
+  int32_t* arrive;   // [T]
+  int32_t* counters; // [0] live, [1] done
+  double* X;         // [T][2][N] output
+};
+
+enum : int { PV_XR = 0, PV_XI, PV_RR, PV_RI, PV_PR, PV_PI, PV_ZR, PV_ZI, PV_QR, PV_QI, PV_DR,
+             PV_DI, kPV };
+
+__device__ __forceinline__ double* pvec(const PArgs& a, int t, int k) {
+  return a.vec + ((int64_t)t * kPV + k) * a.N;
+}
+
+template <int NV>
+__device__ __forceinline__ bool ptask_reduce(double (&v)[NV], const PArgs& a, int t, double* red) {
+  __shared__ bool last;
+  int par = 0;
+  block_allsum<NV>(v, red, par);
+  if (threadIdx.x == 0) {
+    double* dst = a.partial + ((int64_t)t * a.nblk + blockIdx.x) * 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) dst[k] = v[k];
+    __threadfence();
+    last = atomicAdd(a.arrive + t, 1) == a.nblk - 1;
+  }
+  __syncthreads();
+  if (!last) return false;
+  __threadfence();
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (int b = threadIdx.x; b < a.nblk; b += blockDim.x) {
+    const double* src = a.partial + ((int64_t)t * a.nblk + b) * 4;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) acc[k] += __ldcg(src + k);
+  }
+  block_allsum<NV>(acc, red, par);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = acc[k];
+  if (threadIdx.x == 0) a.arrive[t] = 0;
+  return true;
+}
+
+__device__ __forceinline__ void item_cs(const PArgs& a, int t, double& c1, double& sn,
+                                        double& dt) {
+  dt = a.dt[t];
+  double c;
+  sincos(__dmul_rn(a.omega, dt), &sn, &c);
+  c1 = 1.0 - c;
+}
+
+__global__ void __launch_bounds__(kThreads) pinit_kernel(PArgs a) {
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double c1, sn, dt;
+  item_cs(a, t, c1, sn, dt);
+  double v[3] = {0.0, 0.0, 0.0};
+  if (i < a.N) {
+    const int s = a.sample[t];
+    const double* Ms = a.M + (int64_t)s * a.nnz;
+    const double* Ks = a.K + (int64_t)s * a.nnz;
+    double m = 0.0, k = 0.0;
+    for (int q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q)
+      if (a.col[q] == i) {
+        m = Ms[q];
+        k = Ks[q];
+      }
+    const double dr = fma(c1, m, dt * k), di = sn * m, den = dr * dr + di * di;
+    const double ir = den > 0.0 ? dr / den : 0.0, ii = den > 0.0 ? -di / den : 0.0;
+    const double b = dt * a.profile[i];
+    pvec(a, t, PV_DR)[i] = ir;
+    pvec(a, t, PV_DI)[i] = ii;
+    pvec(a, t, PV_XR)[i] = 0.0;
+    pvec(a, t, PV_XI)[i] = 0.0;
+    pvec(a, t, PV_RR)[i] = b;
+    pvec(a, t, PV_RI)[i] = 0.0;
+    pvec(a, t, PV_PR)[i] = ir * b;     // p = z = D^-1 r (r real)
+    pvec(a, t, PV_PI)[i] = ii * b;
+    v[0] = b * ir * b;                 // rho = r^T z (unconjugated)
+    v[1] = b * ii * b;
+    v[2] = b * b;
+  }
+  if (ptask_reduce<3>(v, a, t, red) && threadIdx.x == 0) {
+    double* td = a.td + t * 8;
+    td[0] = v[0];
+    td[1] = v[1];
+    td[2] = v[2];
+    a.ti[t * 4 + 0] = v[2] > 0.0 ? 1 : 0;
+    a.ti[t * 4 + 1] = 0;
+    atomicAdd(a.counters + 0, 1);
+    if (!(v[2] > 0.0)) atomicAdd(a.counters + 1, 1);
+  }
+}
+
+// q = Z p, sigma = p^T q; last block: alpha = rho / sigma
+__global__ void __launch_bounds__(kThreads) pspmv_kernel(PArgs a) {
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  if (!block_uniform(a.ti[t * 4] == 1)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  double c1, sn, dt;
+  item_cs(a, t, c1, sn, dt);
+  double v[2] = {0.0, 0.0};
+  if (i < a.N) {
+    const int s = a.sample[t];
+    const double* Ms = a.M + (int64_t)s * a.nnz;
+    const double* Ks = a.K + (int64_t)s * a.nnz;
+    const double* pr = pvec(a, t, PV_PR);
+    const double* pi = pvec(a, t, PV_PI);
+    double mr = 0.0, mi = 0.0, kr = 0.0, ki = 0.0;
+    for (int q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q) {
+      const int c = a.col[q];
+      const double xr = pr[c], xi = pi[c];
+      mr = fma(Ms[q], xr, mr);
+      mi = fma(Ms[q], xi, mi);
+      kr = fma(Ks[q], xr, kr);
+      ki = fma(Ks[q], xi, ki);
+    }
+    // Zr p = c1 M p + dt K p;  Zi p = sn M p;  q = Zr p + i Zi p
+    const double zr_r = fma(c1, mr, dt * kr), zr_i = fma(c1, mi, dt * ki);
+    const double qr = zr_r - sn * mi, qi = zr_i + sn * mr;
+    pvec(a, t, PV_QR)[i] = qr;
+    pvec(a, t, PV_QI)[i] = qi;
+    v[0] = pr[i] * qr - pi[i] * qi;
+    v[1] = pr[i] * qi + pi[i] * qr;
+  }
+  if (ptask_reduce<2>(v, a, t, red) && threadIdx.x == 0) {
+    double* td = a.td + t * 8;
+    const double den = v[0] * v[0] + v[1] * v[1];
+    if (!(den > 0.0)) {
+      a.ti[t * 4] = 2;                 // breakdown: keep the current X
+      atomicAdd(a.counters + 1, 1);
+    } else {
+      td[3] = (td[0] * v[0] + td[1] * v[1]) / den;
+      td[4] = (td[1] * v[0] - td[0] * v[1]) / den;
+    }
+  }
+}
+
+// x += alpha p; r -= alpha q; z = D^-1 r; rho' = r^T z, |r|^2; last block: beta / stop
+__global__ void __launch_bounds__(kThreads) pupdate_kernel(PArgs a) {
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  if (!block_uniform(a.ti[t * 4] == 1)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const double* td = a.td + t * 8;
+  const double ar = td[3], ai = td[4];
+  double v[3] = {0.0, 0.0, 0.0};
+  if (i < a.N) {
+    const double pr = pvec(a, t, PV_PR)[i], pi = pvec(a, t, PV_PI)[i];
+    const double qr = pvec(a, t, PV_QR)[i], qi = pvec(a, t, PV_QI)[i];
+    pvec(a, t, PV_XR)[i] += ar * pr - ai * pi;
+    pvec(a, t, PV_XI)[i] += ar * pi + ai * pr;
+    const double rr = pvec(a, t, PV_RR)[i] - (ar * qr - ai * qi);
+    const double ri = pvec(a, t, PV_RI)[i] - (ar * qi + ai * qr);
+    pvec(a, t, PV_RR)[i] = rr;
+    pvec(a, t, PV_RI)[i] = ri;
+    const double dr = pvec(a, t, PV_DR)[i], di = pvec(a, t, PV_DI)[i];
+    const double zr = dr * rr - di * ri, zi = dr * ri + di * rr;
+    pvec(a, t, PV_ZR)[i] = zr;
+    pvec(a, t, PV_ZI)[i] = zi;
+    v[0] = rr * zr - ri * zi;
+    v[1] = rr * zi + ri * zr;
+    v[2] = rr * rr + ri * ri;
+  }
+  if (ptask_reduce<3>(v, a, t, red) && threadIdx.x == 0) {
+    double* tdw = a.td + t * 8;
+    int32_t* ti = a.ti + t * 4;
+    ti[1] += 1;
+    const double rden = tdw[0] * tdw[0] + tdw[1] * tdw[1];
+    if (v[2] <= a.rtol2 * tdw[2] || !isfinite(v[2]) || ti[1] >= a.max_it || !(rden > 0.0)) {
+      ti[0] = 2;
+      atomicAdd(a.counters + 1, 1);
+    } else {
+      tdw[5] = (v[0] * tdw[0] + v[1] * tdw[1]) / rden;
+      tdw[6] = (v[1] * tdw[0] - v[0] * tdw[1]) / rden;
+      tdw[0] = v[0];
+      tdw[1] = v[1];
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) ppupd_kernel(PArgs a) {
+  const int t = blockIdx.y;
+  if (a.ti[t * 4] != 1) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const double br = a.td[t * 8 + 5], bi = a.td[t * 8 + 6];
+  const double pr = pvec(a, t, PV_PR)[i], pi = pvec(a, t, PV_PI)[i];
+  pvec(a, t, PV_PR)[i] = pvec(a, t, PV_ZR)[i] + (br * pr - bi * pi);
+  pvec(a, t, PV_PI)[i] = pvec(a, t, PV_ZI)[i] + (br * pi + bi * pr);
+}
+
+__global__ void pfinal_kernel(PArgs a) {
+  const int t = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const double xr = pvec(a, t, PV_XR)[i], xi = pvec(a, t, PV_XI)[i];
+  const bool fin = isfinite(xr) && isfinite(xi);
+  a.X[((int64_t)t * 2) * a.N + i] = fin ? xr : 0.0;
+  a.X[((int64_t)t * 2 + 1) * a.N + i] = fin ? xi : 0.0;
+}
+
 }  // namespace
 
 size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S) {
@@ -548,8 +798,9 @@ size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S) {
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                      const double* K, const double* profile, double omega, double rtol,
-                     int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                     const int32_t* active, void* ws, size_t ws_bytes, cudaStream_t stream) {
+                     int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
+                     int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
+                     cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
   const Layout L = make_layout(ctx, n_tasks, S);
   if (ws == nullptr || ws_bytes < L.total) {
@@ -580,7 +831,10 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
   Work w = carve(ws, L);
   SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                       iters, status, active, w);
-  if (coop_usable(ctx, n_tasks)) {
+  a.xss = xss;
+  bool any_ss = false;
+  for (const auto& t : h) any_ss |= (t.ss_slot >= 0 && !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION));
+  if (coop_usable(ctx, n_tasks) && !(any_ss && xss != nullptr)) {
     // grid-resident path: form the ELL operator once, then one cooperative launch
     // per chunk of tasks runs every step (coop_path.cu)
     const dim3 grid_form((a.N + kThreads - 1) / kThreads, a.S);
@@ -677,6 +931,80 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
     freeze_kernel<<<grid, 256, 0, stream>>>(S, m, (int)N, m, m, U, F, act);
     MLMCP_LAUNCH_CHECK("freeze_kernel");
   }
+  (void)iters;
+  return MLMCP_OK;
+}
+
+size_t stream_periodic_workspace_bytes(const Ctx* ctx, int n) {
+  const size_t N = ctx->n, T = n, nblk = (N + kThreads - 1) / kThreads;
+  return align_up(T * kPV * N * 8) + align_up(T * nblk * 4 * 8) + align_up(T * 8 * 8) +
+         align_up(T * 4 * 4) + align_up(T * 4) + 64;
+}
+
+int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
+                    const double* K, const double* profile, double omega, double rtol,
+                    int max_it, double* X, int32_t* iters, void* ws, size_t ws_bytes,
+                    cudaStream_t stream) {
+  if (n == 0) return MLMCP_OK;
+  const size_t need = stream_periodic_workspace_bytes(ctx, n);
+  if (ws == nullptr || ws_bytes < need) {
+    set_error("steady-state workspace too small: need " + std::to_string(need) + " bytes");
+    return MLMCP_ENOMEM;
+  }
+  PArgs a{};
+  a.T = n;
+  a.N = ctx->n;
+  a.nblk = (ctx->n + kThreads - 1) / kThreads;
+  a.nnz = ctx->nnz;
+  a.row_ptr = ctx->row_ptr;
+  a.col = ctx->col;
+  a.sample = sample;
+  a.dt = dt;
+  a.M = M;
+  a.K = K;
+  a.profile = profile;
+  a.omega = omega;
+  a.rtol2 = rtol * rtol;
+  a.max_it = max_it;
+  a.X = X;
+  char* b = static_cast<char*>(ws);
+  const size_t N = ctx->n, T = n, nblk = a.nblk;
+  a.vec = reinterpret_cast<double*>(b);
+  b += align_up(T * kPV * N * 8);
+  a.partial = reinterpret_cast<double*>(b);
+  b += align_up(T * nblk * 4 * 8);
+  a.td = reinterpret_cast<double*>(b);
+  b += align_up(T * 8 * 8);
+  a.ti = reinterpret_cast<int32_t*>(b);
+  b += align_up(T * 4 * 4);
+  a.arrive = reinterpret_cast<int32_t*>(b);
+  b += align_up(T * 4);
+  a.counters = reinterpret_cast<int32_t*>(b);
+  MLMCP_CUDA_CHECK(cudaMemsetAsync(a.arrive, 0, sizeof(int32_t) * T, stream));
+  MLMCP_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, 2 * sizeof(int32_t), stream));
+  const dim3 grid((a.N + kThreads - 1) / kThreads, n);
+  pinit_kernel<<<grid, kThreads, 0, stream>>>(a);
+  MLMCP_LAUNCH_CHECK("pinit_kernel");
+  int32_t* hc = ctx->host_counters;
+  int done_iters = 0;
+  while (done_iters < max_it) {
+    const int chunk = done_iters == 0 ? 16 : 4;
+    for (int c = 0; c < chunk; ++c) {
+      pspmv_kernel<<<grid, kThreads, 0, stream>>>(a);
+      MLMCP_LAUNCH_CHECK("pspmv_kernel");
+      pupdate_kernel<<<grid, kThreads, 0, stream>>>(a);
+      MLMCP_LAUNCH_CHECK("pupdate_kernel");
+      ppupd_kernel<<<grid, kThreads, 0, stream>>>(a);
+      MLMCP_LAUNCH_CHECK("ppupd_kernel");
+    }
+    done_iters += chunk;
+    MLMCP_CUDA_CHECK(cudaMemcpyAsync(hc, a.counters, 2 * sizeof(int32_t), cudaMemcpyDeviceToHost,
+                                     stream));
+    MLMCP_CUDA_CHECK(cudaStreamSynchronize(stream));
+    if (hc[1] >= hc[0]) break;
+  }
+  pfinal_kernel<<<grid, kThreads, 0, stream>>>(a);
+  MLMCP_LAUNCH_CHECK("pfinal_kernel");
   (void)iters;
   return MLMCP_OK;
 }

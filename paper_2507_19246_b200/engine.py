@@ -200,10 +200,14 @@ class DeviceSystem:
         n = len(sample_idx)
         X = torch.empty((n, 2, self.n_rows), dtype=F64, device=self.device)
         if n:
+            nbytes = int(self.lib.mlmcp_periodic_workspace_bytes(self.ctx, n))
+            ws = None
+            if nbytes:     # streaming path: grid-wide COCG in a workspace
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             check(self.lib.mlmcp_periodic_state(self.ctx, n, ptr(sample_idx), ptr(dts),
                                                 M.shape[0], ptr(M), ptr(K), ptr(profile),
                                                 float(omega), float(rtol), int(max_it), ptr(X),
-                                                None, stream_handle(stream)),
+                                                None, ptr(ws), nbytes, stream_handle(stream)),
                   "mlmcp_periodic_state")
         return X
 

@@ -585,7 +585,8 @@ class EddyCurrentFamily(_BatchedFamily):
             return None
         free, _ = torch.cuda.mem_get_info(sol.device)
         lib = sol.sys.lib
-        per = 16 * sol.nnz + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, 2, 1))
+        per = (16 * sol.nnz + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, 2, 1))
+               + int(lib.mlmcp_periodic_workspace_bytes(sol.sys.ctx, 2)) + 32 * sol.N)
         if parareal_cfg is not None:
             m = parareal_cfg.num_subintervals
             per += (3 * m + 2) * sol.N * 8 + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, m, 1))

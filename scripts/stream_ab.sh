@@ -1,6 +1,8 @@
-for impl in 1 2; do
-  echo "== MLMCP_STREAM_IMPL=$impl (1 two-launch, 2 cooperative)"
-  MLMCP_STREAM_IMPL=$impl timeout 300 python scripts/microbench_stream.py 3 16 16
-  MLMCP_STREAM_IMPL=$impl timeout 300 python scripts/microbench_stream.py 2 4 16
-  MLMCP_STREAM_IMPL=$impl timeout 300 python scripts/microbench_stream.py 4 1 8
+# A/B of the steady-state predictor on the streaming path (configs 2-4):
+# default (extrapolation only) vs MLMCP_PREDICTOR=all (periodic COCG + ss guess)
+for pred in 1 all; do
+  echo "== MLMCP_PREDICTOR=$pred"
+  MLMCP_PREDICTOR=$pred timeout 300 python scripts/microbench_stream.py 3 256 16
+  MLMCP_PREDICTOR=$pred timeout 300 python scripts/microbench_stream.py 2 64 16
+  MLMCP_PREDICTOR=$pred timeout 300 python scripts/microbench_stream.py 4 16 8
 done
