@@ -292,7 +292,37 @@ int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
       gpos.swap(g);
     }
   }
+  // the same detection for grids up to 256 x 256 (the cluster path), when the
+  // pattern is too large for the single-SM kernel
+  std::vector<int32_t> cpos;
+  for (int wd = 2; wd <= 256 && c->cl_wd == 0 && n_rows > kSmallMaxRows; ++wd) {
+    if (n_rows % wd != 0 || n_rows / wd > 256) continue;
+    std::vector<int32_t> g((size_t)7 * n_rows, -1);
+    bool ok = true;
+    for (int i = 0; i < n_rows && ok; ++i) {
+      const int x = i % wd, y = i / wd;
+      for (int q = row_ptr[i]; q < row_ptr[i + 1] && ok; ++q) {
+        const int j = col[q], dx = j % wd - x, dy = j / wd - y;
+        int slot = -1;
+        if (dx == -1 && dy == -1) slot = 0;
+        else if (dx == 0 && dy == -1) slot = 1;
+        else if (dx == -1 && dy == 0) slot = 2;
+        else if (dx == 0 && dy == 0) slot = 3;
+        else if (dx == 1 && dy == 0) slot = 4;
+        else if (dx == 0 && dy == 1) slot = 5;
+        else if (dx == 1 && dy == 1) slot = 6;
+        if (slot < 0) ok = false;
+        else g[(size_t)slot * n_rows + i] = q;
+      }
+    }
+    if (ok) {
+      c->cl_wd = wd;
+      c->cl_h = n_rows / wd;
+      cpos.swap(g);
+    }
+  }
   int rc = upload(&c->row_ptr, row_ptr, (size_t)n_rows + 1);
+  if (!rc && c->cl_wd) rc = upload(&c->cl_pos, cpos.data(), cpos.size());
   if (!rc && c->stencil_w) rc = upload(&c->stencil_pos, spos.data(), spos.size());
   if (!rc && c->grid_wd) rc = upload(&c->grid_pos, gpos.data(), gpos.size());
   if (!rc) rc = upload(&c->col, col, (size_t)nnz);
@@ -324,6 +354,7 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->ell_pos);
   cudaFree(c->stencil_pos);
   cudaFree(c->grid_pos);
+  cudaFree(c->cl_pos);
   cudaFree(c->grid_bar);
   cudaFree(c->cptr);
   cudaFree(c->celem);
@@ -432,7 +463,8 @@ int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, c
     return small_propagate(c, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                            iters, status, active, elapsed, xss, (cudaStream_t)stream);
   return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xss, xbuf,
-                          qoi, iters, status, active, ws, ws_bytes, (cudaStream_t)stream);
+                          qoi, iters, status, active, elapsed, ws, ws_bytes,
+                          (cudaStream_t)stream);
 }
 
 int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, const double* K,

@@ -49,6 +49,10 @@ struct Ctx {
   int grid_wd = 0;
   int grid_h = 0;
   int32_t* grid_pos = nullptr;     // device [7][n] in order SW,S,W,C,E,N,NE: CSR position or -1
+  // the same 2D grid view for larger grids (wd, gh <= 256): the cluster path
+  int cl_wd = 0;
+  int cl_h = 0;
+  int32_t* cl_pos = nullptr;       // device [7][n], as grid_pos
   // assembly gather map
   int n_elem = 0;
   int n_contrib = 0;
@@ -200,8 +204,8 @@ int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, co
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                      const double* K, const double* profile, double omega, double rtol,
                      int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
-                     int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
-                     cudaStream_t stream);
+                     int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
+                     size_t ws_bytes, cudaStream_t stream);
 
 int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
                            const double* profile, double omega, double dt_c, double t0,
@@ -212,6 +216,12 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
 
 size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks);
 bool coop_usable(const Ctx* ctx, int n_tasks);
+// cluster path (one thread-block cluster per task, grids up to 128 x 128)
+bool cluster_usable(const Ctx* ctx);
+int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
+                      const double* K, const double* profile, double omega, double rtol,
+                      int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
+                      const int32_t* active, int64_t* elapsed, cudaStream_t stream);
 int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                    const std::vector<mlmcp_task>& h, int S, const double* A,
                    const double* dinv, const double* M, const double* K,

@@ -799,14 +799,10 @@ size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S) {
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                      const double* K, const double* profile, double omega, double rtol,
                      int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
-                     int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
-                     cudaStream_t stream) {
+                     int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
+                     size_t ws_bytes, cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
   const Layout L = make_layout(ctx, n_tasks, S);
-  if (ws == nullptr || ws_bytes < L.total) {
-    set_error("streaming workspace too small: need " + std::to_string(L.total) + " bytes");
-    return MLMCP_ENOMEM;
-  }
   // the streaming path needs one dt per call (one ELL operator per sample)
   std::vector<mlmcp_task> h(n_tasks);
   MLMCP_CUDA_CHECK(cudaMemcpyAsync(h.data(), tasks, sizeof(mlmcp_task) * n_tasks,
@@ -828,12 +824,22 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
     }
     steps_max = std::max(steps_max, t.n_steps);
   }
+  bool any_ss = false;
+  for (const auto& t : h) any_ss |= (t.ss_slot >= 0 && !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION));
+  // one thread-block cluster per task when a sample's grid fits a cluster
+  // (cluster_path.cu); it predicts by extrapolation only, so batches that
+  // carry periodic steady states stay on the kernels below
+  if (cluster_usable(ctx) && !(any_ss && xss != nullptr))
+    return cluster_propagate(ctx, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
+                             iters, status, active, elapsed, stream);
+  if (ws == nullptr || ws_bytes < L.total) {
+    set_error("streaming workspace too small: need " + std::to_string(L.total) + " bytes");
+    return MLMCP_ENOMEM;
+  }
   Work w = carve(ws, L);
   SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                       iters, status, active, w);
   a.xss = xss;
-  bool any_ss = false;
-  for (const auto& t : h) any_ss |= (t.ss_slot >= 0 && !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION));
   if (coop_usable(ctx, n_tasks) && !(any_ss && xss != nullptr)) {
     // grid-resident path: form the ELL operator once, then one cooperative launch
     // per chunk of tasks runs every step (coop_path.cu)
