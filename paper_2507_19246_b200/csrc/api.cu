@@ -292,11 +292,12 @@ int mlmcp_ctx_create(int device, int n_rows, int nnz, const int32_t* row_ptr,
       gpos.swap(g);
     }
   }
-  // the same detection for grids up to 256 x 256 (the cluster path), when the
-  // pattern is too large for the single-SM kernel
+  // the same detection for larger grids (the cluster path up to 128 x 128, the
+  // tile path of the streaming kernels beyond), when the pattern is too large
+  // for the single-SM kernel
   std::vector<int32_t> cpos;
-  for (int wd = 2; wd <= 256 && c->cl_wd == 0 && n_rows > kSmallMaxRows; ++wd) {
-    if (n_rows % wd != 0 || n_rows / wd > 256) continue;
+  for (int wd = 2; wd <= 4096 && c->cl_wd == 0 && n_rows > kSmallMaxRows; ++wd) {
+    if (n_rows % wd != 0 || n_rows / wd > 4096) continue;
     std::vector<int32_t> g((size_t)7 * n_rows, -1);
     bool ok = true;
     for (int i = 0; i < n_rows && ok; ++i) {
@@ -361,6 +362,9 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->cmw);
   cudaFree(c->ckw);
   if (c->host_counters) cudaFreeHost(c->host_counters);
+  if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  for (cudaStream_t s : c->cap_stream)
+    if (s) cudaStreamDestroy(s);
   delete c;
   return MLMCP_OK;
 }

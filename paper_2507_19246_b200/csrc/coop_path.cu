@@ -575,10 +575,10 @@ int launch_coop(CoopArgs& a, int grid, cudaStream_t stream) {
 size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks) { return coop_plan(ctx, n_tasks).bytes; }
 
 bool coop_usable(const Ctx* ctx, int n_tasks) {
-  // MLMCP_STREAM_IMPL: 1 two-launch kernels, 2 cooperative, default auto
+  // MLMCP_STREAM_IMPL: 1 two-launch kernels, 2 cooperative, 4 tile, default auto
   const char* e = getenv("MLMCP_STREAM_IMPL");
   const int impl = e ? atoi(e) : 0;
-  if (impl == 1 || ctx->stencil_w == 0) return false;
+  if (impl == 1 || impl == 4 || ctx->stencil_w == 0) return false;
   const CoopPlan p = coop_plan(ctx, n_tasks);
   if (p.R == 0) return false;
   // auto: the grid-resident kernel is barrier-latency bound (~16 us per PCG

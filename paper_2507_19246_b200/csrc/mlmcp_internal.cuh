@@ -64,6 +64,10 @@ struct Ctx {
   int32_t* host_counters = nullptr;
   // grid-barrier words of the cooperative path (zeroed at creation)
   unsigned int* grid_bar = nullptr;
+  // graph-driven step loop of the streaming path: capture streams and the
+  // executable graph (updated in place from call to call)
+  cudaStream_t cap_stream[3] = {nullptr, nullptr, nullptr};
+  cudaGraphExec_t step_exec = nullptr;
 };
 
 void set_error(const std::string& msg);

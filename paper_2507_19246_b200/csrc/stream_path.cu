@@ -15,6 +15,7 @@
 // The host loop launches chunks of iterations sized by the previous step's
 // count and reads one pinned 8-byte counter per chunk (the only host sync).
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <vector>
@@ -44,6 +45,9 @@ struct Work {
   double* P;
   double* Sv;
   double* Wv;
+  double* R1;      // tile path: second buffers of r, w, s (ping-pong by iteration parity)
+  double* W1;
+  double* S1;
   double* partial; // [T][nblk][4]
   double* td;      // [T][kTD]
   int32_t* ti;     // [T][kTI]
@@ -54,7 +58,7 @@ struct Work {
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t off[13];
+  size_t off[16];
   size_t total;
 };
 
@@ -62,12 +66,13 @@ Layout make_layout(const Ctx* ctx, int T, int S) {
   // operator slots: ELL width, or the stencil width for the cooperative path
   const size_t N = ctx->n, W = std::max(ctx->max_row_nnz, ctx->stencil_w), T_ = T, S_ = S;
   const size_t nblk = (N + kThreads - 1) / kThreads;
-  size_t sizes[13] = {S_ * W * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
+  size_t sizes[16] = {S_ * W * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
                       T_ * N * 8,     T_ * N * 8, T_ * nblk * 4 * 8, T_ * kTD * 8,
-                      T_ * kTI * 4,   T_ * 4,     64, kRingS * T_ * N * 8};
+                      T_ * kTI * 4,   T_ * 4,     64, kRingS * T_ * N * 8,
+                      T_ * N * 8,     T_ * N * 8, T_ * N * 8};
   Layout L;
   size_t o = 0;
-  for (int i = 0; i < 13; ++i) {
+  for (int i = 0; i < 16; ++i) {
     L.off[i] = o;
     o += align_up(sizes[i]);
   }
@@ -91,6 +96,9 @@ Work carve(void* ws, const Layout& L) {
   w.arrive = reinterpret_cast<int32_t*>(b + L.off[10]);
   w.counters = reinterpret_cast<int32_t*>(b + L.off[11]);
   w.ring = reinterpret_cast<double*>(b + L.off[12]);
+  w.R1 = reinterpret_cast<double*>(b + L.off[13]);
+  w.W1 = reinterpret_cast<double*>(b + L.off[14]);
+  w.S1 = reinterpret_cast<double*>(b + L.off[15]);
   return w;
 }
 
@@ -113,6 +121,14 @@ struct SArgs {
   int32_t* status;
   int32_t* active;
   const double* xss;   // [slots][2][N] periodic steady states (task.ss_slot) or null
+  // tile path (structured wd x gh grid): operator [S][4][N] (C, E, N, NE) in w.A
+  int tile;            // 1: tile path
+  int wd, gh, ntx, ntile;
+  const int32_t* gpos; // [7][N] CSR position of SW,S,W,C,E,N,NE or -1
+  // graph-driven step loop: the PCG while-node's condition, cleared by the
+  // iteration in which the last live task of the step stops
+  cudaGraphConditionalHandle it_cond;
+  int use_cond;
   Work w;
 };
 
@@ -121,17 +137,19 @@ struct SArgs {
 // (all threads), with totals in v.
 template <int NV>
 __device__ __forceinline__ bool task_reduce(double (&v)[NV], const SArgs& a, int t,
-                                            double* red) {
+                                            double* red, int nb = -1, int slot = -1) {
   __shared__ bool last;
   int par = 0;
+  if (nb < 0) nb = a.nblk;
+  if (slot < 0) slot = blockIdx.x;
   block_allsum<NV>(v, red, par);
   if (threadIdx.x == 0) {
-    double* dst = a.w.partial + ((int64_t)t * a.nblk + blockIdx.x) * 4;
+    double* dst = a.w.partial + ((int64_t)t * a.nblk + slot) * 4;
 #pragma unroll
     for (int k = 0; k < NV; ++k) dst[k] = v[k];
     __threadfence();
     const int prev = atomicAdd(a.w.arrive + t, 1);
-    last = (prev == a.nblk - 1);
+    last = (prev == nb - 1);
   }
   __syncthreads();
   if (!last) return false;
@@ -139,7 +157,7 @@ __device__ __forceinline__ bool task_reduce(double (&v)[NV], const SArgs& a, int
   double acc[NV];
 #pragma unroll
   for (int k = 0; k < NV; ++k) acc[k] = 0.0;
-  for (int b = threadIdx.x; b < a.nblk; b += blockDim.x) {
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) {
     const double* src = a.w.partial + ((int64_t)t * a.nblk + b) * 4;
 #pragma unroll
     for (int k = 0; k < NV; ++k) acc[k] += __ldcg(src + k);
@@ -166,6 +184,54 @@ __device__ __forceinline__ bool block_uniform(bool v) {
   const bool out = flag != 0;
   __syncthreads();
   return out;
+}
+
+
+// Last block of a task's PCG iteration (spmv / tile kernels): stopping rule
+// r.D^-1.r <= rtol^2 b.D^-1.b, failure codes, and the Chronopoulos-Gear
+// scalars alpha, beta of the update that follows.
+__device__ __forceinline__ void cg_scalars(const SArgs& a, int t, double gamma, double delta) {
+  double* td = a.w.td + t * kTD;
+  int32_t* ti = a.w.ti + t * kTI;
+  int code = MLMCP_ST_OK;
+  bool stop = false;
+  if (gamma <= a.rtol2 * td[D_BB]) {
+    stop = true;
+  } else if (!isfinite(gamma)) {
+    code = MLMCP_ST_NONFINITE;
+  } else if (ti[I_IT_STEP] >= a.max_it) {
+    code = MLMCP_ST_NOCONV;
+  } else if (ti[I_IT_STEP] == 0) {
+    if (!(delta > 0.0)) code = MLMCP_ST_BREAKDOWN;
+    else {
+      td[D_ALPHA] = gamma / delta;
+      td[D_BETA] = 0.0;
+      td[D_GAMMA] = gamma;
+    }
+  } else {
+    const double beta = gamma / td[D_GAMMA];
+    const double den = delta - beta * gamma / td[D_ALPHA];
+    if (!(den > 0.0)) code = MLMCP_ST_BREAKDOWN;
+    else {
+      td[D_ALPHA] = gamma / den;
+      td[D_BETA] = beta;
+      td[D_GAMMA] = gamma;
+    }
+  }
+  if (code != MLMCP_ST_OK) {
+    ti[I_CODE] = code;
+    stop = true;
+  }
+  if (stop) {
+    ti[I_STATE] = ST_DONE;
+    const int done = atomicAdd(a.w.counters + 1, 1) + 1;
+    if (a.use_cond && done >= *(volatile const int32_t*)(a.w.counters + 0))
+      cudaGraphSetConditional(a.it_cond, 0);
+  } else {
+    ti[I_FIRST] = (ti[I_IT_STEP] == 0);
+    ti[I_IT_STEP] += 1;
+    ti[I_IT_TOTAL] += 1;
+  }
 }
 
 __global__ void form_ell_kernel(SArgs a, double dt) {
@@ -210,7 +276,8 @@ __global__ void copy_in_kernel(SArgs a) {
 // extrapolation of the states; a_n itself for MLMCP_TASK_NO_EXTRAPOLATION
 // (the reference's one-step semantics).  The ring keeps y (= a when ss = 0),
 // a_n moves to Wv (the rhs reads it there), X becomes the guess.
-__global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step) {
+__global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step_arg) {
+  const int step = step_arg >= 0 ? step_arg : *(volatile const int32_t*)(a.w.counters + 2);
   __shared__ double sc[4];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
@@ -249,7 +316,8 @@ __global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step) {
 
 // rhs b = M a_n + dt*sf*prof, r = b - A x0, partial b.D^-1.b (Jacobi-weighted
 // norm of the stopping rule, as the SM-resident path)
-__global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) {
+__global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step_arg) {
+  const int step = step_arg >= 0 ? step_arg : *(volatile const int32_t*)(a.w.counters + 2);
   __shared__ double red[2 * 4 * 32];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
@@ -268,8 +336,13 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step) 
     const int q0 = a.row_ptr[i], q1 = a.row_ptr[i + 1];
     for (int q = q0; q < q1; ++q) mx = fma(Ms[q], An[a.col[q]], mx);
     double ax = 0.0;
-    for (int j = 0; j < a.W; ++j)
-      ax = fma(As[(int64_t)j * a.N + i], X[a.ell_col[j * a.N + i]], ax);
+    if (a.tile) {   // A = M + dt K from the CSR values (w.A holds the tile layout)
+      const double* Ks = a.K + (int64_t)s * a.nnz;
+      for (int q = q0; q < q1; ++q) ax = fma(op_entry(Ms[q], Ks[q], tk.dt), X[a.col[q]], ax);
+    } else {
+      for (int j = 0; j < a.W; ++j)
+        ax = fma(As[(int64_t)j * a.N + i], X[a.ell_col[j * a.N + i]], ax);
+    }
     const double b = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, a.profile[i])));
     a.w.R[(int64_t)t * a.N + i] = b - ax;
     bb = b * a.w.dinv[(int64_t)s * a.N + i] * b;
@@ -316,48 +389,7 @@ __global__ void __launch_bounds__(kThreads) spmv_kernel(SArgs a) {
     rr = r * r;
   }
   double v[3] = {ru, wu, rr};
-  if (task_reduce<3>(v, a, t, red) && threadIdx.x == 0) {
-    double* td = a.w.td + t * kTD;
-    int32_t* ti = a.w.ti + t * kTI;
-    const double gamma = v[0], delta = v[1];
-    int code = MLMCP_ST_OK;
-    bool stop = false;
-    if (gamma <= a.rtol2 * td[D_BB]) {   // r.D^-1.r <= rtol^2 b.D^-1.b
-      stop = true;
-    } else if (!isfinite(gamma)) {
-      code = MLMCP_ST_NONFINITE;
-    } else if (ti[I_IT_STEP] >= a.max_it) {
-      code = MLMCP_ST_NOCONV;
-    } else if (ti[I_IT_STEP] == 0) {
-      if (!(delta > 0.0)) code = MLMCP_ST_BREAKDOWN;
-      else {
-        td[D_ALPHA] = gamma / delta;
-        td[D_BETA] = 0.0;
-        td[D_GAMMA] = gamma;
-      }
-    } else {
-      const double beta = gamma / td[D_GAMMA];
-      const double den = delta - beta * gamma / td[D_ALPHA];
-      if (!(den > 0.0)) code = MLMCP_ST_BREAKDOWN;
-      else {
-        td[D_ALPHA] = gamma / den;
-        td[D_BETA] = beta;
-        td[D_GAMMA] = gamma;
-      }
-    }
-    if (code != MLMCP_ST_OK) {
-      ti[I_CODE] = code;
-      stop = true;
-    }
-    if (stop) {
-      ti[I_STATE] = ST_DONE;
-      atomicAdd(a.w.counters + 1, 1);
-    } else {
-      ti[I_FIRST] = (ti[I_IT_STEP] == 0);
-      ti[I_IT_STEP] += 1;
-      ti[I_IT_TOTAL] += 1;
-    }
-  }
+  if (task_reduce<3>(v, a, t, red) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
 }
 
 __global__ void __launch_bounds__(kThreads) update_kernel(SArgs a) {
@@ -386,9 +418,482 @@ __global__ void __launch_bounds__(kThreads) update_kernel(SArgs a) {
   a.w.R[o] = fma(-alpha, s, r);
 }
 
+// ------------------------------------------------------------------ tile path
+// Structured wd x gh grids too large for one cluster (256^2, 512^2: configs
+// 2, 4): ONE launch per PCG iteration over all live (task, tile) pairs.  A
+// tile is kTW x kTH grid points; each thread a column strip of kTR rows.
+// Launch k (k = PCG iterations done in this step) fuses the update of
+// iteration k-1 with the operator apply of iteration k:
+//   p = u + beta p, s = w + beta s, x += alpha p, r -= alpha s   (own points)
+//   u = D^-1 r on the tile and its one-point halo (halo values recomputed
+//   from the previous iterates of the neighbouring tiles), w = A u from the
+//   shared-memory u, partial (r.u, w.u); the last tile of the task computes
+//   the scalars (cg_scalars).
+// r, w, s alternate between two buffers by iteration parity, so a launch reads
+// only buffers no tile of the same launch writes.  The operator is the
+// symmetric half (C, E, N, NE) per point, [S][4][N]; W, S, SW are the E, N, NE
+// coefficients of the west / south / south-west neighbour.
+// HBM streams per point and iteration: read x r w s p D^-1 + 4 operator
+// values, write x r w s p = 120 B (B_it = 8 nnz + 56 N counts 112 B).
+constexpr int kTW = 64;
+constexpr int kTLD = kTW + 2;
+
+__global__ void form_tile_kernel(SArgs a, double dt) {
+  const int s = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= a.N) return;
+  const double* Ms = a.M + (int64_t)s * a.nnz;
+  const double* Ks = a.K + (int64_t)s * a.nnz;
+  double* As = a.w.A + (int64_t)s * 4 * a.N;
+  double c = 1.0;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int q = a.gpos[(int64_t)(3 + j) * a.N + i];
+    const double v = q >= 0 ? op_entry(Ms[q], Ks[q], dt) : 0.0;
+    if (j == 0 && q >= 0) c = v;
+    As[(int64_t)j * a.N + i] = v;
+  }
+  a.w.dinv[(int64_t)s * a.N + i] = 1.0 / c;
+}
+
+__device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
+               "r"(ok ? 8 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+__device__ __forceinline__ int bcast_int(int v) {
+  __shared__ int val;
+  if (threadIdx.x == 0) val = v;
+  __syncthreads();
+  const int out = val;
+  __syncthreads();
+  return out;
+}
+
+// r_k of a point from the previous iterates (identical arithmetic for the
+// owner and for the neighbours that recompute it as halo)
+__device__ __forceinline__ double tile_s(bool first, double beta, double wo, double so) {
+  return first ? wo : fma(beta, so, wo);
+}
+
+template <int kTH, int kTR, int kMinB>
+__global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SArgs a) {
+  constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
+  static_assert(kTHalo <= kTW * (kTH / kTR), "one halo point per thread");
+  constexpr int kTCL = kTW + 1;                 // operator tile: columns -1..kTW-1
+  constexpr int kTCN = (kTH + 1) * kTCL;        //                rows -1..kTH-1
+  __shared__ double U[(kTH + 2) * kTLD];
+  __shared__ double Ac[4 * kTCN];               // C, E, N, NE (cp.async-staged)
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  const mlmcp_task tk = a.tasks[t];
+  const int32_t* ti = a.w.ti + t * kTI;
+  int mode = 0;   // 0 skip, 1 run, 2 zero solution
+  if (threadIdx.x == 0 && task_live(a, tk, t)) {
+    const int st = ti[I_STATE];
+    mode = st == ST_RUN ? 1 : (st == ST_ZERO ? 2 : 0);
+  }
+  mode = bcast_int(mode);
+  if (mode == 0) return;
+  const int k = ti[I_IT_STEP];
+  const int64_t N = a.N, o = (int64_t)t * N;
+  const int tx0 = (blockIdx.x % a.ntx) * kTW, ty0 = (blockIdx.x / a.ntx) * kTH;
+  const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
+  const int gx = tx0 + cx;
+  const int gy0 = ty0 + sy * kTR;
+  const bool colok = gx < a.wd;
+  double* X = a.w.X + o;
+  if (mode == 2) {
+#pragma unroll
+    for (int r = 0; r < kTR; ++r)
+      if (colok && gy0 + r < a.gh) X[(int64_t)(gy0 + r) * a.wd + gx] = 0.0;
+    return;
+  }
+  const double* Di = a.w.dinv + (int64_t)tk.sample * N;
+  const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
+  // operator of the tile and of its west column / south row: asynchronous
+  // copies into shared memory, overlapped with the vector loads below
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const int ly = sy * kTR + r;
+    const bool ok = colok && gy0 + r < a.gh;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + (ly + 1) * kTCL + cx + 1], As + j * N + i, ok);
+  }
+  if (threadIdx.x < kTH + 1 + kTW) {
+    const int h = threadIdx.x;
+    const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) cp8(&Ac[q * kTCN + (ly + 1) * kTCL + lx + 1], As + q * N + j, ok);
+  }
+  cp_commit();
+  const bool odd = k & 1, upd = k > 0, first = k == 1;
+  const double* td = a.w.td + t * kTD;
+  const double alpha = upd ? td[D_ALPHA] : 0.0, beta = upd ? td[D_BETA] : 0.0;
+  // parity buffers: r_j in R[j&1], w_j in W[j&1], s_j in S[j&1] (buffer 0 = R, Wv, Sv)
+  const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;   // r_{k-1} (k == 0: r_0)
+  const double* Wo = odd ? a.w.Wv + o : a.w.W1 + o;            // w_{k-1}
+  const double* So = odd ? a.w.S1 + o : a.w.Sv + o;            // s_{k-2}
+  double* Rn = odd ? a.w.R1 + o : a.w.R + o;
+  double* Sn = odd ? a.w.Sv + o : a.w.S1 + o;
+  double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
+
+  // halo frame: u at the neighbouring tiles' points (0 outside the grid)
+  if (threadIdx.x < kTHalo) {
+    const int h = threadIdx.x;
+    int lx, ly;
+    if (h < kTW + 2) { lx = h - 1; ly = -1; }
+    else if (h < 2 * (kTW + 2)) { lx = h - (kTW + 2) - 1; ly = kTH; }
+    else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
+    else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    double u = 0.0;
+    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
+      const int64_t j = (int64_t)hy * a.wd + hx;
+      double r = __ldcg(Ro + j);
+      if (upd) r = fma(-alpha, tile_s(first, beta, __ldcg(Wo + j), first ? 0.0 : __ldcg(So + j)), r);
+      u = __ldg(Di + j) * r;
+    }
+    U[(ly + 1) * kTLD + lx + 1] = u;
+  }
+  // own points: update of iteration k-1, u_k
+  double gam = 0.0;
+  {
+    double rv[kTR], dv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+      rv[r] = ok ? __ldcg(Ro + i) : 0.0;
+      dv[r] = ok ? __ldg(Di + i) : 0.0;
+      if (upd) {
+        wv[r] = ok ? __ldcg(Wo + i) : 0.0;
+        sv[r] = (ok && !first) ? __ldcg(So + i) : 0.0;
+        pv[r] = (ok && !first) ? __ldcg(a.w.P + o + i) : 0.0;
+        xv[r] = ok ? __ldcg(X + i) : 0.0;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+      double rk = rv[r];
+      if (upd) {
+        const double uo = dv[r] * rv[r];
+        const double p = first ? uo : fma(beta, pv[r], uo);
+        const double s = tile_s(first, beta, wv[r], sv[r]);
+        rk = fma(-alpha, s, rv[r]);
+        if (ok) {
+          a.w.P[o + i] = p;
+          Sn[i] = s;
+          X[i] = fma(alpha, p, xv[r]);
+          Rn[i] = rk;
+        }
+      }
+      const double u = dv[r] * rk;
+      U[(sy * kTR + r + 1) * kTLD + cx + 1] = u;
+      gam = fma(rk, u, gam);
+    }
+  }
+  cp_wait_all();
+  __syncthreads();
+  // w_k = A u_k (W, S, SW coefficients = E, N, NE of the west / south / south-west point)
+  double del = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const int gy = gy0 + r;
+    if (!(colok && gy < a.gh)) continue;
+    const int64_t i = (int64_t)gy * a.wd + gx;
+    const int b = (sy * kTR + r + 1) * kTLD + cx + 1;
+    const int lc = (sy * kTR + r + 1) * kTCL + cx + 1;
+    const double c = Ac[lc], e = Ac[kTCN + lc], nn = Ac[2 * kTCN + lc], ne = Ac[3 * kTCN + lc];
+    const double cw = Ac[kTCN + lc - 1];
+    const double cs = Ac[2 * kTCN + lc - kTCL];
+    const double csw = Ac[3 * kTCN + lc - kTCL - 1];
+    const double uc = U[b];
+    double acc0 = c * uc, acc1 = csw * U[b - kTLD - 1];
+    acc0 = fma(cs, U[b - kTLD], acc0);
+    acc1 = fma(cw, U[b - 1], acc1);
+    acc0 = fma(e, U[b + 1], acc0);
+    acc1 = fma(nn, U[b + kTLD], acc1);
+    acc0 = fma(ne, U[b + kTLD + 1], acc0);
+    const double w = acc0 + acc1;
+    Wn[i] = w;
+    del = fma(w, uc, del);
+  }
+  double v[2] = {gam, del};
+  if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
+}
+
+// Pipelined persistent variant of the tile kernel: one CTA per SM walks the
+// (task, tile) items of the launch with a stride of the grid size; while it
+// computes item q, the cp.async copies of item q + grid (own points, halo
+// frame, operator with its west / south neighbours) are in flight into the
+// other shared-memory stage, so every SM keeps ~87 KB of loads outstanding
+// and the memory system streams without per-CTA round-trip gaps.  Tiles are
+// 64 x 16 points (4 rows per thread); arithmetic is the tile kernel's.
+constexpr int kPW = 64, kPH = 16, kPR = 4;
+constexpr int kPThreads = kPW * (kPH / kPR);        // 256
+constexpr int kPN = kPW * kPH;                      // 1024 points
+constexpr int kPHalo = 2 * (kPW + 2) + 2 * kPH;     // 164 frame points of u
+constexpr int kPCL = kPW + 1;                       // operator tile row stride: columns -1..63
+constexpr int kPCN = (kPH + 1) * kPCL;              // rows -1..15
+constexpr int kPCH = (kPH + 1) + kPW;               // operator halo: column -1 (rows -1..15), row -1
+constexpr int kPULD = kPW + 2;
+constexpr int kPMaxTasks = 4096;
+static_assert(kPHalo <= kPThreads && kPCH <= kPThreads, "one halo point per thread");
+
+struct PStage {
+  double r[kPN], w[kPN], s[kPN], p[kPN], x[kPN], d[kPN], c[kPN];
+  double e[kPCN], n[kPCN], ne[kPCN];
+  double hr[kPHalo], hw[kPHalo], hs[kPHalo], hd[kPHalo];
+};
+constexpr size_t kPSmem = 2 * sizeof(PStage) + sizeof(double) * ((kPH + 2) * kPULD + 2 * 4 * 32) +
+                          sizeof(int2) * kPMaxTasks;
+
+// frame point h of the u halo -> tile-local (lx, ly), lx in -1..kPW, ly in -1..kPH
+__device__ __forceinline__ void p_frame(int h, int& lx, int& ly) {
+  if (h < kPW + 2) { lx = h - 1; ly = -1; }
+  else if (h < 2 * (kPW + 2)) { lx = h - (kPW + 2) - 1; ly = kPH; }
+  else if (h < 2 * (kPW + 2) + kPH) { lx = -1; ly = h - 2 * (kPW + 2); }
+  else { lx = kPW; ly = h - 2 * (kPW + 2) - kPH; }
+}
+
+struct PItem {
+  int t, mode, k, sample, tx0, ty0;
+};
+
+__device__ __forceinline__ PItem p_item(const SArgs& a, const int2* tab, int q) {
+  PItem it;
+  it.t = q / a.ntile;
+  const int j = q - it.t * a.ntile;
+  const int2 e = tab[it.t];
+  it.mode = e.x & 3;
+  it.k = e.x >> 2;
+  it.sample = e.y;
+  it.tx0 = (j % a.ntx) * kPW;
+  it.ty0 = (j / a.ntx) * kPH;
+  return it;
+}
+
+__device__ __forceinline__ void p_prefetch(const SArgs& a, const PItem& it, PStage& S,
+                                           double& alpha, double& beta) {
+  if (it.mode != 1) return;
+  const int64_t N = a.N, o = (int64_t)it.t * N;
+  const bool odd = it.k & 1, upd = it.k > 0, first = it.k == 1;
+  if (upd) {
+    const double* td = a.w.td + it.t * kTD;
+    alpha = td[D_ALPHA];
+    beta = td[D_BETA];
+  } else {
+    alpha = beta = 0.0;
+  }
+  const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;
+  const double* Wo = odd ? a.w.Wv + o : a.w.W1 + o;
+  const double* So = odd ? a.w.S1 + o : a.w.Sv + o;
+  const double* Di = a.w.dinv + (int64_t)it.sample * N;
+  const double* As = a.w.A + (int64_t)it.sample * 4 * N;
+  const int cx = threadIdx.x % kPW, sy = threadIdx.x / kPW;
+  const int gx = it.tx0 + cx;
+#pragma unroll
+  for (int rr = 0; rr < kPR; ++rr) {
+    const int ly = sy * kPR + rr, gy = it.ty0 + ly;
+    const bool ok = gx < a.wd && gy < a.gh;
+    const int64_t i = ok ? (int64_t)gy * a.wd + gx : 0;
+    const int l = ly * kPW + cx, lc = (ly + 1) * kPCL + cx + 1;
+    cp8(&S.r[l], Ro + i, ok);
+    cp8(&S.d[l], Di + i, ok);
+    cp8(&S.c[l], As + i, ok);
+    cp8(&S.e[lc], As + N + i, ok);
+    cp8(&S.n[lc], As + 2 * N + i, ok);
+    cp8(&S.ne[lc], As + 3 * N + i, ok);
+    if (upd) {
+      cp8(&S.w[l], Wo + i, ok);
+      cp8(&S.x[l], a.w.X + o + i, ok);
+      if (!first) {
+        cp8(&S.s[l], So + i, ok);
+        cp8(&S.p[l], a.w.P + o + i, ok);
+      }
+    }
+  }
+  if (threadIdx.x < kPHalo) {
+    const int h = threadIdx.x;
+    int lx, ly;
+    p_frame(h, lx, ly);
+    const int hx = it.tx0 + lx, hy = it.ty0 + ly;
+    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+    cp8(&S.hr[h], Ro + j, ok);
+    cp8(&S.hd[h], Di + j, ok);
+    if (upd) {
+      cp8(&S.hw[h], Wo + j, ok);
+      if (!first) cp8(&S.hs[h], So + j, ok);
+    }
+  }
+  if (threadIdx.x < kPCH) {   // E / N / NE of column -1 and row -1
+    const int h = threadIdx.x;
+    const int lx = h <= kPH ? -1 : h - (kPH + 1);
+    const int ly = h <= kPH ? h - 1 : -1;
+    const int hx = it.tx0 + lx, hy = it.ty0 + ly;
+    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+    const int lc = (ly + 1) * kPCL + lx + 1;
+    cp8(&S.e[lc], As + N + j, ok);
+    cp8(&S.n[lc], As + 2 * N + j, ok);
+    cp8(&S.ne[lc], As + 3 * N + j, ok);
+  }
+}
+
+__device__ __forceinline__ void p_compute(const SArgs& a, const PItem& it, const PStage& S,
+                                          double alpha, double beta, double* U, double* red) {
+  if (it.mode == 0) return;
+  const int64_t N = a.N, o = (int64_t)it.t * N;
+  const int cx = threadIdx.x % kPW, sy = threadIdx.x / kPW;
+  const int gx = it.tx0 + cx;
+  double* X = a.w.X + o;
+  if (it.mode == 2) {
+#pragma unroll
+    for (int rr = 0; rr < kPR; ++rr) {
+      const int gy = it.ty0 + sy * kPR + rr;
+      if (gx < a.wd && gy < a.gh) X[(int64_t)gy * a.wd + gx] = 0.0;
+    }
+    return;
+  }
+  const bool odd = it.k & 1, upd = it.k > 0, first = it.k == 1;
+  double* Rn = odd ? a.w.R1 + o : a.w.R + o;
+  double* Sn = odd ? a.w.Sv + o : a.w.S1 + o;
+  double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
+  if (threadIdx.x < kPHalo) {
+    const int h = threadIdx.x;
+    int lx, ly;
+    p_frame(h, lx, ly);
+    double r = S.hr[h];
+    if (upd) r = fma(-alpha, tile_s(first, beta, S.hw[h], first ? 0.0 : S.hs[h]), r);
+    U[(ly + 1) * kPULD + lx + 1] = S.hd[h] * r;   // zero-filled outside the grid
+  }
+  double gam = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < kPR; ++rr) {
+    const int ly = sy * kPR + rr, gy = it.ty0 + ly;
+    const bool ok = gx < a.wd && gy < a.gh;
+    const int64_t i = (int64_t)gy * a.wd + gx;
+    const int l = ly * kPW + cx;
+    const double ro = S.r[l], dv = S.d[l];
+    double rk = ro;
+    if (upd) {
+      const double uo = dv * ro;
+      const double p = first ? uo : fma(beta, S.p[l], uo);
+      const double s = tile_s(first, beta, S.w[l], first ? 0.0 : S.s[l]);
+      rk = fma(-alpha, s, ro);
+      if (ok) {
+        a.w.P[o + i] = p;
+        Sn[i] = s;
+        X[i] = fma(alpha, p, S.x[l]);
+        Rn[i] = rk;
+      }
+    }
+    const double u = dv * rk;
+    U[(ly + 1) * kPULD + cx + 1] = u;
+    gam = fma(rk, u, gam);
+  }
+  __syncthreads();
+  double del = 0.0;
+#pragma unroll
+  for (int rr = 0; rr < kPR; ++rr) {
+    const int ly = sy * kPR + rr, gy = it.ty0 + ly;
+    const int b = (ly + 1) * kPULD + cx + 1;
+    const int lc = (ly + 1) * kPCL + cx + 1;
+    const double uc = U[b];
+    double acc0 = S.c[ly * kPW + cx] * uc, acc1 = S.ne[lc - kPCL - 1] * U[b - kPULD - 1];
+    acc0 = fma(S.n[lc - kPCL], U[b - kPULD], acc0);
+    acc1 = fma(S.e[lc - 1], U[b - 1], acc1);
+    acc0 = fma(S.e[lc], U[b + 1], acc0);
+    acc1 = fma(S.n[lc], U[b + kPULD], acc1);
+    acc0 = fma(S.ne[lc], U[b + kPULD + 1], acc0);
+    const double w = acc0 + acc1;
+    if (gx < a.wd && gy < a.gh) Wn[(int64_t)gy * a.wd + gx] = w;
+    del = fma(w, uc, del);
+  }
+  double v[2] = {gam, del};
+  const int j = (it.ty0 / kPH) * a.ntx + it.tx0 / kPW;
+  if (task_reduce<2>(v, a, it.t, red, a.ntile, j) && threadIdx.x == 0)
+    cg_scalars(a, it.t, v[0], v[1]);
+}
+
+__global__ void __launch_bounds__(kPThreads, 1) tile_pipe_kernel(SArgs a) {
+  extern __shared__ __align__(16) double psm[];
+  PStage* stg = reinterpret_cast<PStage*>(psm);
+  double* U = psm + 2 * (sizeof(PStage) / sizeof(double));
+  double* red = U + (kPH + 2) * kPULD;
+  int2* tab = reinterpret_cast<int2*>(red + 2 * 4 * 32);
+  for (int t = threadIdx.x; t < a.T; t += kPThreads) {
+    const mlmcp_task tk = a.tasks[t];
+    const int32_t* ti = a.w.ti + t * kTI;
+    int mode = 0;
+    if (task_live(a, tk, t)) {
+      const int st = ti[I_STATE];
+      mode = st == ST_RUN ? 1 : (st == ST_ZERO ? 2 : 0);
+    }
+    tab[t] = make_int2(mode | (ti[I_IT_STEP] << 2), tk.sample);
+  }
+  __syncthreads();
+  const int n_items = a.T * a.ntile;
+  int q = blockIdx.x;
+  if (q >= n_items) return;
+  double alpha_n = 0.0, beta_n = 0.0;
+  PItem nxt = p_item(a, tab, q);
+  p_prefetch(a, nxt, stg[0], alpha_n, beta_n);
+  cp_commit();
+  for (int it = 0; q < n_items; ++it, q += gridDim.x) {
+    const PItem cur = nxt;
+    const double alpha = alpha_n, beta = beta_n;
+    cp_wait_all();
+    __syncthreads();
+    const int qn = q + gridDim.x;
+    if (qn < n_items) {
+      nxt = p_item(a, tab, qn);
+      p_prefetch(a, nxt, stg[(it + 1) & 1], alpha_n, beta_n);
+    }
+    cp_commit();
+    p_compute(a, cur, stg[it & 1], alpha, beta, U, red);
+  }
+}
+
+int tile_pipe_grid() {
+  static int g = 0;
+  if (g == 0) {
+    int dev = 0, sms = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaFuncSetAttribute(tile_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kPSmem);
+    g = sms > 0 ? sms : 148;
+  }
+  return g;
+}
+
+int tile_cfg() {
+  const char* e = getenv("MLMCP_TILE_CFG");
+  return e ? std::max(1, std::min(3, atoi(e))) : 1;
+}
+
+bool tile_pipe_on(const SArgs& a) {
+  const char* e = getenv("MLMCP_TILE_PIPE");
+  return a.T <= kPMaxTasks && e && atoi(e) == 1;   // off by default (measured slower)
+}
+
 // mode 0: per-step (trajectory store + SUM_ENERGY accumulation);
 // mode 1: finalize (x_out, FINAL_ENERGY / SUM write-out, iters, status)
-__global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step, int mode) {
+__global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step_arg, int mode) {
+  const int step = step_arg >= 0 ? step_arg : *(volatile const int32_t*)(a.w.counters + 2);
   __shared__ double red[2 * 4 * 32];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
@@ -435,7 +940,8 @@ __global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step, i
 }
 
 // records the failing step of tasks that failed in this step
-__global__ void mark_fail_kernel(SArgs a, int step) {
+__global__ void mark_fail_kernel(SArgs a, int step_arg) {
+  const int step = step_arg >= 0 ? step_arg : *(volatile const int32_t*)(a.w.counters + 2);
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= a.T) return;
   int32_t* ti = a.w.ti + t * kTI;
@@ -443,16 +949,209 @@ __global__ void mark_fail_kernel(SArgs a, int step) {
   if (ti[I_CODE] == MLMCP_ST_OK) ti[I_FAILSTEP] = -1;
 }
 
+// control kernels of the graph-driven step loop (counters[2] = current step)
+__global__ void steps_begin_kernel(int32_t* counters) { counters[2] = 0; }
+
+// PCG while-node condition at the start of a step: run while live tasks remain
+__global__ void iter_begin_kernel(int32_t* counters, cudaGraphConditionalHandle h) {
+  cudaGraphSetConditional(h, counters[1] < counters[0] ? 1 : 0);
+}
+
+__global__ void step_next_kernel(int32_t* counters, int n_steps, cudaGraphConditionalHandle h) {
+  const int s = counters[2] + 1;
+  counters[2] = s;
+  cudaGraphSetConditional(h, s < n_steps ? 1 : 0);
+}
+
+// MLMCP_STREAM_IMPL: 1 two-launch ELL kernels, 2 cooperative, 3 cluster,
+// 4 tile; default auto
+int stream_impl() {
+  const char* e = getenv("MLMCP_STREAM_IMPL");
+  return e ? atoi(e) : 0;
+}
+
+bool tile_usable(const Ctx* ctx) {
+  const int impl = stream_impl();
+  if (impl == 1 || impl == 2) return false;
+  if (ctx->cl_wd == 0 || ctx->n < kTW) return false;
+  const int ntile = ((ctx->cl_wd + 63) / 64) * ((ctx->cl_h + 15) / 16);   // finest tiling
+  return ntile <= (ctx->n + kThreads - 1) / kThreads;   // partial-sum slots
+}
+
+// MLMCP_STREAM_GRAPH=1: device-driven step loop (conditional graph nodes);
+// measured on par with the host loop below (whose syncs overlap nothing
+// costly), which stays the default because ncu can profile its kernels
+bool graph_steps() {
+  const char* e = getenv("MLMCP_STREAM_GRAPH");
+  return e && atoi(e) == 1;
+}
+
+// three private non-blocking streams for building the step graph by capture
+int capture_streams(Ctx* ctx, cudaStream_t (&cs)[3]) {
+  for (int i = 0; i < 3; ++i) {
+    if (ctx->cap_stream[i] == nullptr) {
+      cudaError_t e = cudaStreamCreateWithFlags(&ctx->cap_stream[i], cudaStreamNonBlocking);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaStreamCreateWithFlags");
+    }
+    cs[i] = ctx->cap_stream[i];
+  }
+  return MLMCP_OK;
+}
+
+// instantiate (or update the cached executable graph in place) and launch
+int launch_exec(Ctx* ctx, cudaGraph_t g, cudaStream_t stream) {
+  if (ctx->step_exec != nullptr) {
+    cudaGraphExecUpdateResultInfo info;
+    if (cudaGraphExecUpdate(ctx->step_exec, g, &info) != cudaSuccess) {
+      cudaGetLastError();
+      cudaGraphExecDestroy(ctx->step_exec);
+      ctx->step_exec = nullptr;
+    }
+  }
+  if (ctx->step_exec == nullptr) {
+    cudaError_t e = cudaGraphInstantiate(&ctx->step_exec, g, 0);
+    if (e != cudaSuccess) {
+      ctx->step_exec = nullptr;
+      return cuda_fail(e, "cudaGraphInstantiate(step loop)");
+    }
+  }
+  MLMCP_CUDA_CHECK(cudaGraphLaunch(ctx->step_exec, stream));
+  return MLMCP_OK;
+}
+
 int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t stream) {
   const dim3 blk(kThreads);
   const dim3 grid_rows((a.N + kThreads - 1) / kThreads, a.T);
   const dim3 grid_form((a.N + kThreads - 1) / kThreads, a.S);
-  form_ell_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
-  MLMCP_LAUNCH_CHECK("form_ell_kernel");
+  if (a.tile) {
+    form_tile_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
+    MLMCP_LAUNCH_CHECK("form_tile_kernel");
+  } else {
+    form_ell_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
+    MLMCP_LAUNCH_CHECK("form_ell_kernel");
+  }
+  const bool pipe = a.tile && tile_pipe_on(a);
+  if (a.tile) {   // the pipelined kernel uses the 64 x 16 tiling
+    a.ntx = pipe ? (a.wd + kPW - 1) / kPW : (a.wd + kTW - 1) / kTW;
+    a.ntile = a.ntx * ((a.gh + kPH - 1) / kPH);
+  }
+  const dim3 grid_pipe(a.tile ? tile_pipe_grid() : 1);
+  const int tcfg = tile_cfg();
+  if (a.tile && !pipe) {
+    const int th = tcfg == 3 ? 8 : 16;
+    a.ntile = a.ntx * ((a.gh + th - 1) / th);
+  }
+  const dim3 grid_tiles2(a.tile ? a.ntile : 1, a.T);
   copy_in_kernel<<<grid_rows, blk, 0, stream>>>(a);
   MLMCP_LAUNCH_CHECK("copy_in_kernel");
   mark_fail_kernel<<<(a.T + 255) / 256, 256, 0, stream>>>(a, 0);
   MLMCP_LAUNCH_CHECK("mark_fail_kernel");
+  auto launch_iteration = [&](cudaStream_t s) -> int {
+    if (pipe) {
+      tile_pipe_kernel<<<grid_pipe, kPThreads, kPSmem, s>>>(a);
+      MLMCP_LAUNCH_CHECK("tile_pipe_kernel");
+    } else if (a.tile) {
+      if (tcfg == 1) tile_iter_kernel<16, 4, 3><<<grid_tiles2, 256, 0, s>>>(a);
+      else if (tcfg == 2) tile_iter_kernel<16, 4, 4><<<grid_tiles2, 256, 0, s>>>(a);
+      else tile_iter_kernel<8, 2, 4><<<grid_tiles2, 256, 0, s>>>(a);
+      MLMCP_LAUNCH_CHECK("tile_iter_kernel");
+    } else {
+      spmv_kernel<<<grid_rows, blk, 0, s>>>(a);
+      MLMCP_LAUNCH_CHECK("spmv_kernel");
+      update_kernel<<<grid_rows, blk, 0, s>>>(a);
+      MLMCP_LAUNCH_CHECK("update_kernel");
+    }
+    return MLMCP_OK;
+  };
+  if (graph_steps()) {
+    // Device-driven step loop: one CUDA graph with a while-node over the steps
+    // whose body runs the step's kernels and a nested while-node over PCG
+    // iterations; the iteration in which the last task stops clears the inner
+    // condition (cg_scalars).  No host synchronisation per step or iteration.
+    if (n_steps_max <= 0) {
+      step_end_kernel<<<grid_rows, blk, 0, stream>>>(a, 0, 1);
+      MLMCP_LAUNCH_CHECK("step_end_kernel(final)");
+      return MLMCP_OK;
+    }
+    cudaStream_t cs[3];
+    if (const int rc0 = capture_streams(ctx, cs)) return rc0;
+    cudaGraph_t g;
+    MLMCP_CUDA_CHECK(cudaGraphCreate(&g, 0));
+    cudaGraphConditionalHandle h_step, h_it;
+    MLMCP_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h_step, g, 1, cudaGraphCondAssignDefault));
+    // the step loop (body graph b_step)
+    cudaGraphNodeParams ps = {};
+    ps.type = cudaGraphNodeTypeConditional;
+    ps.conditional.handle = h_step;
+    ps.conditional.type = cudaGraphCondTypeWhile;
+    ps.conditional.size = 1;
+    cudaGraphNode_t n_step;
+    MLMCP_CUDA_CHECK(cudaGraphAddNode(&n_step, g, nullptr, 0, &ps));
+    cudaGraph_t b_step = ps.conditional.phGraph_out[0];
+    MLMCP_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h_it, b_step, 0, 0));
+    a.it_cond = h_it;
+    a.use_cond = 1;
+    // body of the step loop: guess, rhs, the PCG loop, step end, advance
+    MLMCP_CUDA_CHECK(cudaStreamBeginCaptureToGraph(cs[1], b_step, nullptr, nullptr, 0,
+                                                   cudaStreamCaptureModeThreadLocal));
+    int rc = MLMCP_OK;
+    do {
+      if (cudaMemsetAsync(a.w.counters, 0, 2 * sizeof(int32_t), cs[1]) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
+        break;
+      }
+      guess_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1);
+      step_init_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1);
+      iter_begin_kernel<<<1, 1, 0, cs[1]>>>(a.w.counters, h_it);
+      cudaStreamCaptureStatus st;
+      const cudaGraphNode_t* deps = nullptr;
+      size_t nd = 0;
+      cudaGraph_t cap;
+      if (cudaStreamGetCaptureInfo(cs[1], &st, nullptr, &cap, &deps, &nd) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError(), "cudaStreamGetCaptureInfo");
+        break;
+      }
+      cudaGraphNodeParams pi = {};
+      pi.type = cudaGraphNodeTypeConditional;
+      pi.conditional.handle = h_it;
+      pi.conditional.type = cudaGraphCondTypeWhile;
+      pi.conditional.size = 1;
+      cudaGraphNode_t n_it;
+      if (cudaGraphAddNode(&n_it, cap, deps, nd, &pi) != cudaSuccess ||
+          cudaStreamUpdateCaptureDependencies(cs[1], &n_it, 1,
+                                              cudaStreamSetCaptureDependencies) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError(), "conditional node");
+        break;
+      }
+      cudaGraph_t b_it = pi.conditional.phGraph_out[0];
+      if (cudaStreamBeginCaptureToGraph(cs[2], b_it, nullptr, nullptr, 0,
+                                        cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+        rc = cuda_fail(cudaGetLastError(), "capture (iteration body)");
+        break;
+      }
+      rc = launch_iteration(cs[2]);
+      cudaGraph_t b_it_out;
+      const cudaError_t e2 = cudaStreamEndCapture(cs[2], &b_it_out);
+      if (rc == MLMCP_OK && e2 != cudaSuccess) rc = cuda_fail(e2, "end capture (iteration body)");
+      if (rc != MLMCP_OK) break;
+      mark_fail_kernel<<<(a.T + 255) / 256, 256, 0, cs[1]>>>(a, -1);
+      step_end_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1, 0);
+      step_next_kernel<<<1, 1, 0, cs[1]>>>(a.w.counters, n_steps_max, h_step);
+    } while (false);
+    cudaGraph_t b_step_out;
+    const cudaError_t e1 = cudaStreamEndCapture(cs[1], &b_step_out);
+    if (rc == MLMCP_OK && e1 != cudaSuccess) rc = cuda_fail(e1, "end capture (step body)");
+    if (rc == MLMCP_OK) {
+      steps_begin_kernel<<<1, 1, 0, stream>>>(a.w.counters);
+      rc = launch_exec(ctx, g, stream);
+    }
+    cudaGraphDestroy(g);
+    if (rc != MLMCP_OK) return rc;
+    MLMCP_LAUNCH_CHECK("graph step loop");
+    step_end_kernel<<<grid_rows, blk, 0, stream>>>(a, 0, 1);
+    MLMCP_LAUNCH_CHECK("step_end_kernel(final)");
+    return MLMCP_OK;
+  }
   int32_t* hc = ctx->host_counters;
   int chunk = 4;
   for (int step = 0; step < n_steps_max; ++step) {
@@ -464,10 +1163,8 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     int done_iters = 0;
     for (;;) {
       for (int c = 0; c < chunk; ++c) {
-        spmv_kernel<<<grid_rows, blk, 0, stream>>>(a);
-        MLMCP_LAUNCH_CHECK("spmv_kernel");
-        update_kernel<<<grid_rows, blk, 0, stream>>>(a);
-        MLMCP_LAUNCH_CHECK("update_kernel");
+        const int rc = launch_iteration(stream);
+        if (rc != MLMCP_OK) return rc;
       }
       done_iters += chunk;
       MLMCP_CUDA_CHECK(cudaMemcpyAsync(hc, a.w.counters, 2 * sizeof(int32_t),
@@ -515,6 +1212,14 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   a.status = status;
   a.active = const_cast<int32_t*>(active);
   a.xss = nullptr;
+  a.tile = tile_usable(ctx) ? 1 : 0;
+  a.wd = ctx->cl_wd;
+  a.gh = ctx->cl_h;
+  a.ntx = a.tile ? (a.wd + kTW - 1) / kTW : 0;
+  a.ntile = a.tile ? a.ntx * ((a.gh + 15) / 16) : 0;   // set per kernel in run_steps
+  a.gpos = ctx->cl_pos;
+  a.it_cond = 0;
+  a.use_cond = 0;
   a.w = w;
   return a;
 }

@@ -180,17 +180,21 @@ def test_cfg4_512_level0(cuda):
     assert abs(out.q_l[0].item() - q) <= 1e-8 * abs(q)
 
 
-@pytest.mark.parametrize("impl", ["coop", "twolaunch"])
+@pytest.mark.parametrize("impl", ["auto", "twolaunch", "coop", "cluster", "tile"])
 def test_streaming_64_mesh_vs_oracle(cuda, impl, monkeypatch):
-    """64x64 mesh (3969 rows) forced onto the streaming path: the grid-resident
-    cooperative kernel (default) and the two-launch kernels, sequential and
+    """64x64 mesh (3969 rows) forced onto the streaming path: every kernel
+    family of it (MLMCP_STREAM_IMPL: two-launch ELL kernels, grid-resident
+    cooperative, thread-block cluster, fused tile kernel), sequential and
     Parareal, vs the splu oracle."""
     from paper_2507_19246_b200 import fe
     from paper_2507_19246_b200.models import (EddyCurrentFamily, ParameterVector, QoIKind,
                                               UncertainInput, make_hierarchy)
     from paper_2507_19246_b200.parareal import PararealConfig
-    if impl == "twolaunch":
-        pytest.skip("MLMCP_STREAM_IMPL is read once per process; covered by the coop run")
+    code = {"auto": None, "twolaunch": "1", "coop": "2", "cluster": "3", "tile": "4"}[impl]
+    if code is None:
+        monkeypatch.delenv("MLMCP_STREAM_IMPL", raising=False)
+    else:
+        monkeypatch.setenv("MLMCP_STREAM_IMPL", code)   # read by libmlmcp on every call
     nominal = np.array([fe.NU0] * 4 + [fe.SIGMA0] * 4)
     fam = EddyCurrentFamily("quad4", UncertainInput(ParameterVector("quad4", nominal), 0.1),
                             make_hierarchy([T / 64, T / 128]), T, 64, "quad4",
