@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--config", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="skip the e2e leg (profiling runs)")
+    ap.add_argument("--no-streaming", action="store_true",
+                    help="skip the HBM-streaming roofline legs (configs 2 and 4)")
     ap.add_argument("--cpu-seconds", type=float, default=6.0,
                     help="target wall seconds of the bounded CPU-baseline sample")
     return ap.parse_args()
@@ -223,6 +225,50 @@ def ncu_traffic():
         return d.get("dram_bytes_per_launch")
     except Exception:
         return None
+
+
+def streaming_roofline(dev, peak, flush):
+    """HBM roofline of the streaming path (meshes > 1024 rows, where the batch's
+    working set is far larger than L2): one level-0 batch of config 2 (256^2)
+    and of config 4 (512^2), timed with CUDA events on the launching stream.
+    achieved = PCG iterations x B_it / time of the whole propagate call
+    (step starts, guesses and QoI included)."""
+    import torch
+
+    from paper_2507_19246_b200.mlmc import draw_level
+    from paper_2507_19246_b200.models import eddy_current_family
+    out = []
+    for cfg_i, S, steps in ((2, 512, 8), (4, 128, 4)):
+        fam = eddy_current_family(cfg_i, device=dev)
+        sol = fam.solver
+        p = draw_level(fam.uncertain, 0, 0, range(1, S + 1))
+        M, K = sol.assemble(torch.from_numpy(p).to(dev))
+        job = fam._seq_job(np.arange(S), fam.hierarchy[0].dt)
+        job.n_steps = steps
+        times = []
+        for r in range(3):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            res = sol.run_sequential(M, K, [job])[0]
+            e1.record()
+            torch.cuda.synchronize()
+            if r:
+                times.append(e0.elapsed_time(e1) / 1000.0)
+        its = int(res.iters.to(torch.int64).sum().item())
+        b_it = 8 * sol.mesh.nnz + 56 * sol.N
+        t = float(np.mean(times))
+        ach = its * b_it / t / 1e9
+        out.append({"workload": f"cfg{cfg_i} level-0 batch: {S} samples x {steps} implicit-Euler "
+                                f"steps, {sol.n}x{sol.n} mesh (N={sol.N})",
+                    "kernel": "tile_iter_kernel<16,4,3> (one fused launch per PCG iteration) + "
+                              "tile_init / guess / step_end per step",
+                    "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                    "pcg_iterations": its, "ms": 1000 * t,
+                    "algorithmic_bytes": f"{its} PCG iterations x (8 nnz + 56 N) = {its} x {b_it} B"})
+        del M, K, res, sol, fam
+        torch.cuda.empty_cache()
+    return out
 
 
 def main():
@@ -406,6 +452,8 @@ def main():
            "detail": {"pcg_iterations_sequential": its, "pcg_iterations_parareal_fine": pr_fine_its,
                       "pcg_iterations_parareal_coarse": pr_coarse_its,
                       "host_wall_ms_per_step": 1000 * wall / args.steps}}
+    if rank == 0 and not args.no_streaming:
+        out["roofline"]["streaming"] = streaming_roofline(dev, peak, flush)
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         os.environ["OPENBLAS_NUM_THREADS"] = "1"
         cores = os.cpu_count() or 1

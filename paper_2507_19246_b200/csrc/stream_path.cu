@@ -66,7 +66,7 @@ Layout make_layout(const Ctx* ctx, int T, int S) {
   // operator slots: ELL width, or the stencil width for the cooperative path
   const size_t N = ctx->n, W = std::max(ctx->max_row_nnz, ctx->stencil_w), T_ = T, S_ = S;
   const size_t nblk = (N + kThreads - 1) / kThreads;
-  size_t sizes[16] = {S_ * W * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
+  size_t sizes[16] = {S_ * std::max(W, (size_t)8) * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
                       T_ * N * 8,     T_ * N * 8, T_ * nblk * 4 * 8, T_ * kTD * 8,
                       T_ * kTI * 4,   T_ * 4,     64, kRingS * T_ * N * 8,
                       T_ * N * 8,     T_ * N * 8, T_ * N * 8};
@@ -314,6 +314,22 @@ __global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step_arg) 
   a.w.X[o] = g + sst;
 }
 
+// Last block of a task's step start: b.D^-1.b of the stopping rule, state
+__device__ __forceinline__ void step_scalars(const SArgs& a, int t, double bb) {
+  double* td = a.w.td + t * kTD;
+  int32_t* ti = a.w.ti + t * kTI;
+  td[D_BB] = bb;
+  ti[I_IT_STEP] = 0;
+  ti[I_FIRST] = 1;
+  atomicAdd(a.w.counters + 0, 1);
+  if (bb == 0.0) {
+    ti[I_STATE] = ST_ZERO;
+    atomicAdd(a.w.counters + 1, 1);
+  } else {
+    ti[I_STATE] = ST_RUN;
+  }
+}
+
 // rhs b = M a_n + dt*sf*prof, r = b - A x0, partial b.D^-1.b (Jacobi-weighted
 // norm of the stopping rule, as the SM-resident path)
 __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step_arg) {
@@ -348,20 +364,7 @@ __global__ void __launch_bounds__(kThreads) step_init_kernel(SArgs a, int step_a
     bb = b * a.w.dinv[(int64_t)s * a.N + i] * b;
   }
   double v[1] = {bb};
-  if (task_reduce<1>(v, a, t, red) && threadIdx.x == 0) {
-    double* td = a.w.td + t * kTD;
-    int32_t* ti = a.w.ti + t * kTI;
-    td[D_BB] = v[0];
-    ti[I_IT_STEP] = 0;
-    ti[I_FIRST] = 1;
-    atomicAdd(a.w.counters + 0, 1);
-    if (v[0] == 0.0) {
-      ti[I_STATE] = ST_ZERO;
-      atomicAdd(a.w.counters + 1, 1);
-    } else {
-      ti[I_STATE] = ST_RUN;
-    }
-  }
+  if (task_reduce<1>(v, a, t, red) && threadIdx.x == 0) step_scalars(a, t, v[0]);
 }
 
 __global__ void __launch_bounds__(kThreads) spmv_kernel(SArgs a) {
@@ -445,6 +448,7 @@ __global__ void form_tile_kernel(SArgs a, double dt) {
   const double* Ms = a.M + (int64_t)s * a.nnz;
   const double* Ks = a.K + (int64_t)s * a.nnz;
   double* As = a.w.A + (int64_t)s * 4 * a.N;
+  double* Ms4 = a.w.A + ((int64_t)a.S + s) * 4 * a.N;   // mass, same layout
   double c = 1.0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
@@ -452,6 +456,7 @@ __global__ void form_tile_kernel(SArgs a, double dt) {
     const double v = q >= 0 ? op_entry(Ms[q], Ks[q], dt) : 0.0;
     if (j == 0 && q >= 0) c = v;
     As[(int64_t)j * a.N + i] = v;
+    Ms4[(int64_t)j * a.N + i] = q >= 0 ? Ms[q] : 0.0;
   }
   a.w.dinv[(int64_t)s * a.N + i] = 1.0 / c;
 }
@@ -631,6 +636,119 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   }
   double v[2] = {gam, del};
   if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
+}
+
+// Step start on the tile layout: b = M a_n + dt sf profile, r_0 = b - A x_0,
+// partial b.D^-1.b.  a_n (Wv) and x_0 (X) are staged with their one-point
+// halo, the symmetric halves of A and M with their west column / south row,
+// all by cp.async; the stencil sums run in the CSR column order
+// (SW, S, W, C, E, N, NE) of the per-row kernel.
+template <int kTH, int kTR, int kMinB>
+__global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SArgs a, int step_arg) {
+  const int step = step_arg >= 0 ? step_arg : *(volatile const int32_t*)(a.w.counters + 2);
+  constexpr int kTCL = kTW + 1, kTCN = (kTH + 1) * kTCL, kTV = (kTH + 2) * kTLD;
+  constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
+  static_assert(kTHalo <= kTW * (kTH / kTR), "one halo point per thread");
+  extern __shared__ __align__(16) double ism[];
+  double* Ac = ism;                 // [4][kTCN]
+  double* Mc = Ac + 4 * kTCN;       // [4][kTCN]
+  double* XV = Mc + 4 * kTCN;       // x_0 with halo
+  double* AV = XV + kTV;            // a_n with halo
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  const mlmcp_task tk = a.tasks[t];
+  if (!block_uniform(step < tk.n_steps && task_live(a, tk, t))) return;
+  const int64_t N = a.N, o = (int64_t)t * N;
+  const int tx0 = (blockIdx.x % a.ntx) * kTW, ty0 = (blockIdx.x / a.ntx) * kTH;
+  const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
+  const int gx = tx0 + cx, gy0 = ty0 + sy * kTR;
+  const bool colok = gx < a.wd;
+  const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
+  const double* Ms = a.w.A + ((int64_t)a.S + tk.sample) * 4 * N;
+  const double* X = a.w.X + o;
+  const double* An = a.w.Wv + o;
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const int ly = sy * kTR + r;
+    const bool ok = colok && gy0 + r < a.gh;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+    const int lc = (ly + 1) * kTCL + cx + 1, lv = (ly + 1) * kTLD + cx + 1;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
+      cp8(&Mc[j * kTCN + lc], Ms + j * N + i, ok);
+    }
+    cp8(&XV[lv], X + i, ok);
+    cp8(&AV[lv], An + i, ok);
+  }
+  if (threadIdx.x < kTH + 1 + kTW) {
+    const int h = threadIdx.x;
+    const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+    const int lc = (ly + 1) * kTCL + lx + 1;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) {
+      cp8(&Ac[q * kTCN + lc], As + q * N + j, ok);
+      cp8(&Mc[q * kTCN + lc], Ms + q * N + j, ok);
+    }
+  }
+  if (threadIdx.x < kTHalo) {
+    int lx, ly;
+    const int h = threadIdx.x;
+    if (h < kTW + 2) { lx = h - 1; ly = -1; }
+    else if (h < 2 * (kTW + 2)) { lx = h - (kTW + 2) - 1; ly = kTH; }
+    else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
+    else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+    const int lv = (ly + 1) * kTLD + lx + 1;
+    cp8(&XV[lv], X + j, ok);
+    cp8(&AV[lv], An + j, ok);
+  }
+  cp_commit();
+  const int64_t g = tk.k0 + step + 1;
+  const double sf = sin(__dmul_rn(a.omega, grid_time(tk.t_base, g, tk.dt)));
+  double prof[kTR], dv[kTR];
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const bool ok = colok && gy0 + r < a.gh;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+    prof[r] = ok ? __ldg(a.profile + i) : 0.0;
+    dv[r] = ok ? __ldg(a.w.dinv + (int64_t)tk.sample * N + i) : 0.0;
+  }
+  cp_wait_all();
+  __syncthreads();
+  double bb = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const int ly = sy * kTR + r, gy = gy0 + r;
+    if (!(colok && gy < a.gh)) continue;
+    const int64_t i = (int64_t)gy * a.wd + gx;
+    const int lc = (ly + 1) * kTCL + cx + 1, b = (ly + 1) * kTLD + cx + 1;
+    // coefficient of direction SW, S, W, C, E, N, NE
+    const int cofs[7] = {3 * kTCN + lc - kTCL - 1, 2 * kTCN + lc - kTCL, kTCN + lc - 1, lc,
+                         kTCN + lc, 2 * kTCN + lc, 3 * kTCN + lc};
+    const int vofs[7] = {b - kTLD - 1, b - kTLD, b - 1, b, b + 1, b + kTLD, b + kTLD + 1};
+    double mx = 0.0, ax = 0.0;
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+      mx = fma(Mc[cofs[d]], AV[vofs[d]], mx);
+      ax = fma(Ac[cofs[d]], XV[vofs[d]], ax);
+    }
+    const double bv = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, prof[r])));
+    a.w.R[o + i] = bv - ax;
+    bb += bv * dv[r] * bv;
+  }
+  double v[1] = {bb};
+  if (task_reduce<1>(v, a, t, red, a.ntile) && threadIdx.x == 0) step_scalars(a, t, v[0]);
+}
+
+template <int kTH, int kTR>
+constexpr size_t tile_init_smem() {
+  return sizeof(double) * (8 * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
 }
 
 // Pipelined persistent variant of the tile kernel: one CTA per SM walks the
@@ -1046,6 +1164,31 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   MLMCP_LAUNCH_CHECK("copy_in_kernel");
   mark_fail_kernel<<<(a.T + 255) / 256, 256, 0, stream>>>(a, 0);
   MLMCP_LAUNCH_CHECK("mark_fail_kernel");
+  auto launch_init = [&](cudaStream_t s, int step) -> int {
+    if (a.tile && !pipe && tcfg == 3) {
+      tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(), s>>>(a, step);
+      MLMCP_LAUNCH_CHECK("tile_init_kernel");
+    } else if (a.tile) {
+      tile_init_kernel<16, 4, 2><<<grid_tiles2, 256, tile_init_smem<16, 4>(), s>>>(a, step);
+      MLMCP_LAUNCH_CHECK("tile_init_kernel");
+    } else {
+      step_init_kernel<<<grid_rows, blk, 0, s>>>(a, step);
+      MLMCP_LAUNCH_CHECK("step_init_kernel");
+    }
+    return MLMCP_OK;
+  };
+  if (a.tile) {
+    static bool attr = false;
+    if (!attr) {
+      MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<8, 2, 4>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)tile_init_smem<8, 2>()));
+      MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<16, 4, 2>,
+                                            cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                            (int)tile_init_smem<16, 4>()));
+      attr = true;
+    }
+  }
   auto launch_iteration = [&](cudaStream_t s) -> int {
     if (pipe) {
       tile_pipe_kernel<<<grid_pipe, kPThreads, kPSmem, s>>>(a);
@@ -1101,7 +1244,8 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
         break;
       }
       guess_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1);
-      step_init_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1);
+      rc = launch_init(cs[1], -1);
+      if (rc != MLMCP_OK) break;
       iter_begin_kernel<<<1, 1, 0, cs[1]>>>(a.w.counters, h_it);
       cudaStreamCaptureStatus st;
       const cudaGraphNode_t* deps = nullptr;
@@ -1158,8 +1302,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     MLMCP_CUDA_CHECK(cudaMemsetAsync(a.w.counters, 0, 2 * sizeof(int32_t), stream));
     guess_kernel<<<grid_rows, blk, 0, stream>>>(a, step);
     MLMCP_LAUNCH_CHECK("guess_kernel");
-    step_init_kernel<<<grid_rows, blk, 0, stream>>>(a, step);
-    MLMCP_LAUNCH_CHECK("step_init_kernel");
+    if (const int rc = launch_init(stream, step)) return rc;
     int done_iters = 0;
     for (;;) {
       for (int c = 0; c < chunk; ++c) {
