@@ -329,3 +329,44 @@ def test_fused_scheduler_coarse_failure_ends_chains(cuda):
     with pytest.raises(PropagatorError) as ei:
         raise_parareal_status(st, pr.fine_status.cpu().numpy())
     assert (ei.value.interval, ei.value.iteration) == (1, 1)
+
+
+@pytest.mark.parametrize("n,env", [
+    (40, {"MLMCP_STREAM_IMPL": "4"}),                               # one ragged tile column
+    (72, {"MLMCP_STREAM_IMPL": "4"}),                               # 64 + 7 columns
+    (72, {"MLMCP_STREAM_IMPL": "4", "MLMCP_TILE_CFG": "3"}),        # 8-row tiles
+    (72, {"MLMCP_STREAM_IMPL": "4", "MLMCP_TILE_CFG": "4"}),        # TMA-staged variant
+    (72, {"MLMCP_STREAM_IMPL": "4", "MLMCP_STREAM_GRAPH": "1"}),    # device-driven step loop
+    (72, {"MLMCP_STREAM_IMPL": "1", "MLMCP_STREAM_GRAPH": "1"}),
+])
+def test_tile_path_ragged_grids_vs_oracle(cuda, n, env, monkeypatch):
+    """The tile kernels on grids whose width / height are not multiples of the
+    tile (edge tiles, halo clamping), every variant and the graph-driven step
+    loop: sequential and Parareal vs the splu oracle (QoI 1e-8, K equal)."""
+    from paper_2507_19246_b200 import fe
+    from paper_2507_19246_b200.models import (EddyCurrentFamily, ParameterVector, QoIKind,
+                                              UncertainInput, make_hierarchy)
+    from paper_2507_19246_b200.parareal import PararealConfig
+    for k in ("MLMCP_STREAM_IMPL", "MLMCP_TILE_CFG", "MLMCP_STREAM_GRAPH"):
+        monkeypatch.delenv(k, raising=False)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    nominal = np.array([fe.NU0] * 8 + [fe.SIGMA0] * 8)
+    fam = EddyCurrentFamily("blocks8", UncertainInput(ParameterVector("blocks8", nominal), 0.1),
+                            make_hierarchy([T / 32, T / 64]), T, n, "blocks8",
+                            QoIKind.MAGNETIC_ENERGY_T, device="cuda:0", path="stream")
+    cfg = mo.OracleConfig(f"t{n}", n, "blocks8", T, (T / 32, T / 64), (3, 1), "energy_T",
+                          parareal=(4, T / 4, 1e-8, 3))
+    prob = mo.FEProblem(n, "blocks8")
+    p = np.array([mo.draw(cfg, 0, 0, k) for k in (1, 2, 3)])
+    out = fam.run_levels([p], levels=[0])[0]
+    fam.check_status()
+    for i in range(3):
+        q = mo.evaluate(prob, cfg, p[i], T / 32, False, dense=False).q
+        assert abs(out.q_l[i].item() - q) <= 1e-8 * abs(q)
+    pp = np.array([mo.draw(cfg, 0, 1, 1)])
+    b = fam.run_levels([pp], PararealConfig(4, T / 64, T / 4, 1e-8, 3), levels=[1])[0]
+    fam.check_status()
+    rec = mo.evaluate(prob, cfg, pp[0], T / 64, True, dense=False)
+    assert int(b.k_used[0].item()) == rec.k_used
+    assert abs(b.q_l[0].item() - rec.q) <= 1e-8 * abs(rec.q)
