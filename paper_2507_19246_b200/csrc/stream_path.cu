@@ -751,262 +751,6 @@ constexpr size_t tile_init_smem() {
   return sizeof(double) * (8 * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
 }
 
-// Pipelined persistent variant of the tile kernel: one CTA per SM walks the
-// (task, tile) items of the launch with a stride of the grid size; while it
-// computes item q, the cp.async copies of item q + grid (own points, halo
-// frame, operator with its west / south neighbours) are in flight into the
-// other shared-memory stage, so every SM keeps ~87 KB of loads outstanding
-// and the memory system streams without per-CTA round-trip gaps.  Tiles are
-// 64 x 16 points (4 rows per thread); arithmetic is the tile kernel's.
-constexpr int kPW = 64, kPH = 16, kPR = 4;
-constexpr int kPThreads = kPW * (kPH / kPR);        // 256
-constexpr int kPN = kPW * kPH;                      // 1024 points
-constexpr int kPHalo = 2 * (kPW + 2) + 2 * kPH;     // 164 frame points of u
-constexpr int kPCL = kPW + 1;                       // operator tile row stride: columns -1..63
-constexpr int kPCN = (kPH + 1) * kPCL;              // rows -1..15
-constexpr int kPCH = (kPH + 1) + kPW;               // operator halo: column -1 (rows -1..15), row -1
-constexpr int kPULD = kPW + 2;
-constexpr int kPMaxTasks = 4096;
-static_assert(kPHalo <= kPThreads && kPCH <= kPThreads, "one halo point per thread");
-
-struct PStage {
-  double r[kPN], w[kPN], s[kPN], p[kPN], x[kPN], d[kPN], c[kPN];
-  double e[kPCN], n[kPCN], ne[kPCN];
-  double hr[kPHalo], hw[kPHalo], hs[kPHalo], hd[kPHalo];
-};
-constexpr size_t kPSmem = 2 * sizeof(PStage) + sizeof(double) * ((kPH + 2) * kPULD + 2 * 4 * 32) +
-                          sizeof(int2) * kPMaxTasks;
-
-// frame point h of the u halo -> tile-local (lx, ly), lx in -1..kPW, ly in -1..kPH
-__device__ __forceinline__ void p_frame(int h, int& lx, int& ly) {
-  if (h < kPW + 2) { lx = h - 1; ly = -1; }
-  else if (h < 2 * (kPW + 2)) { lx = h - (kPW + 2) - 1; ly = kPH; }
-  else if (h < 2 * (kPW + 2) + kPH) { lx = -1; ly = h - 2 * (kPW + 2); }
-  else { lx = kPW; ly = h - 2 * (kPW + 2) - kPH; }
-}
-
-struct PItem {
-  int t, mode, k, sample, tx0, ty0;
-};
-
-__device__ __forceinline__ PItem p_item(const SArgs& a, const int2* tab, int q) {
-  PItem it;
-  it.t = q / a.ntile;
-  const int j = q - it.t * a.ntile;
-  const int2 e = tab[it.t];
-  it.mode = e.x & 3;
-  it.k = e.x >> 2;
-  it.sample = e.y;
-  it.tx0 = (j % a.ntx) * kPW;
-  it.ty0 = (j / a.ntx) * kPH;
-  return it;
-}
-
-__device__ __forceinline__ void p_prefetch(const SArgs& a, const PItem& it, PStage& S,
-                                           double& alpha, double& beta) {
-  if (it.mode != 1) return;
-  const int64_t N = a.N, o = (int64_t)it.t * N;
-  const bool odd = it.k & 1, upd = it.k > 0, first = it.k == 1;
-  if (upd) {
-    const double* td = a.w.td + it.t * kTD;
-    alpha = td[D_ALPHA];
-    beta = td[D_BETA];
-  } else {
-    alpha = beta = 0.0;
-  }
-  const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;
-  const double* Wo = odd ? a.w.Wv + o : a.w.W1 + o;
-  const double* So = odd ? a.w.S1 + o : a.w.Sv + o;
-  const double* Di = a.w.dinv + (int64_t)it.sample * N;
-  const double* As = a.w.A + (int64_t)it.sample * 4 * N;
-  const int cx = threadIdx.x % kPW, sy = threadIdx.x / kPW;
-  const int gx = it.tx0 + cx;
-#pragma unroll
-  for (int rr = 0; rr < kPR; ++rr) {
-    const int ly = sy * kPR + rr, gy = it.ty0 + ly;
-    const bool ok = gx < a.wd && gy < a.gh;
-    const int64_t i = ok ? (int64_t)gy * a.wd + gx : 0;
-    const int l = ly * kPW + cx, lc = (ly + 1) * kPCL + cx + 1;
-    cp8(&S.r[l], Ro + i, ok);
-    cp8(&S.d[l], Di + i, ok);
-    cp8(&S.c[l], As + i, ok);
-    cp8(&S.e[lc], As + N + i, ok);
-    cp8(&S.n[lc], As + 2 * N + i, ok);
-    cp8(&S.ne[lc], As + 3 * N + i, ok);
-    if (upd) {
-      cp8(&S.w[l], Wo + i, ok);
-      cp8(&S.x[l], a.w.X + o + i, ok);
-      if (!first) {
-        cp8(&S.s[l], So + i, ok);
-        cp8(&S.p[l], a.w.P + o + i, ok);
-      }
-    }
-  }
-  if (threadIdx.x < kPHalo) {
-    const int h = threadIdx.x;
-    int lx, ly;
-    p_frame(h, lx, ly);
-    const int hx = it.tx0 + lx, hy = it.ty0 + ly;
-    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
-    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
-    cp8(&S.hr[h], Ro + j, ok);
-    cp8(&S.hd[h], Di + j, ok);
-    if (upd) {
-      cp8(&S.hw[h], Wo + j, ok);
-      if (!first) cp8(&S.hs[h], So + j, ok);
-    }
-  }
-  if (threadIdx.x < kPCH) {   // E / N / NE of column -1 and row -1
-    const int h = threadIdx.x;
-    const int lx = h <= kPH ? -1 : h - (kPH + 1);
-    const int ly = h <= kPH ? h - 1 : -1;
-    const int hx = it.tx0 + lx, hy = it.ty0 + ly;
-    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
-    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
-    const int lc = (ly + 1) * kPCL + lx + 1;
-    cp8(&S.e[lc], As + N + j, ok);
-    cp8(&S.n[lc], As + 2 * N + j, ok);
-    cp8(&S.ne[lc], As + 3 * N + j, ok);
-  }
-}
-
-__device__ __forceinline__ void p_compute(const SArgs& a, const PItem& it, const PStage& S,
-                                          double alpha, double beta, double* U, double* red) {
-  if (it.mode == 0) return;
-  const int64_t N = a.N, o = (int64_t)it.t * N;
-  const int cx = threadIdx.x % kPW, sy = threadIdx.x / kPW;
-  const int gx = it.tx0 + cx;
-  double* X = a.w.X + o;
-  if (it.mode == 2) {
-#pragma unroll
-    for (int rr = 0; rr < kPR; ++rr) {
-      const int gy = it.ty0 + sy * kPR + rr;
-      if (gx < a.wd && gy < a.gh) X[(int64_t)gy * a.wd + gx] = 0.0;
-    }
-    return;
-  }
-  const bool odd = it.k & 1, upd = it.k > 0, first = it.k == 1;
-  double* Rn = odd ? a.w.R1 + o : a.w.R + o;
-  double* Sn = odd ? a.w.Sv + o : a.w.S1 + o;
-  double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
-  if (threadIdx.x < kPHalo) {
-    const int h = threadIdx.x;
-    int lx, ly;
-    p_frame(h, lx, ly);
-    double r = S.hr[h];
-    if (upd) r = fma(-alpha, tile_s(first, beta, S.hw[h], first ? 0.0 : S.hs[h]), r);
-    U[(ly + 1) * kPULD + lx + 1] = S.hd[h] * r;   // zero-filled outside the grid
-  }
-  double gam = 0.0;
-#pragma unroll
-  for (int rr = 0; rr < kPR; ++rr) {
-    const int ly = sy * kPR + rr, gy = it.ty0 + ly;
-    const bool ok = gx < a.wd && gy < a.gh;
-    const int64_t i = (int64_t)gy * a.wd + gx;
-    const int l = ly * kPW + cx;
-    const double ro = S.r[l], dv = S.d[l];
-    double rk = ro;
-    if (upd) {
-      const double uo = dv * ro;
-      const double p = first ? uo : fma(beta, S.p[l], uo);
-      const double s = tile_s(first, beta, S.w[l], first ? 0.0 : S.s[l]);
-      rk = fma(-alpha, s, ro);
-      if (ok) {
-        a.w.P[o + i] = p;
-        Sn[i] = s;
-        X[i] = fma(alpha, p, S.x[l]);
-        Rn[i] = rk;
-      }
-    }
-    const double u = dv * rk;
-    U[(ly + 1) * kPULD + cx + 1] = u;
-    gam = fma(rk, u, gam);
-  }
-  __syncthreads();
-  double del = 0.0;
-#pragma unroll
-  for (int rr = 0; rr < kPR; ++rr) {
-    const int ly = sy * kPR + rr, gy = it.ty0 + ly;
-    const int b = (ly + 1) * kPULD + cx + 1;
-    const int lc = (ly + 1) * kPCL + cx + 1;
-    const double uc = U[b];
-    double acc0 = S.c[ly * kPW + cx] * uc, acc1 = S.ne[lc - kPCL - 1] * U[b - kPULD - 1];
-    acc0 = fma(S.n[lc - kPCL], U[b - kPULD], acc0);
-    acc1 = fma(S.e[lc - 1], U[b - 1], acc1);
-    acc0 = fma(S.e[lc], U[b + 1], acc0);
-    acc1 = fma(S.n[lc], U[b + kPULD], acc1);
-    acc0 = fma(S.ne[lc], U[b + kPULD + 1], acc0);
-    const double w = acc0 + acc1;
-    if (gx < a.wd && gy < a.gh) Wn[(int64_t)gy * a.wd + gx] = w;
-    del = fma(w, uc, del);
-  }
-  double v[2] = {gam, del};
-  const int j = (it.ty0 / kPH) * a.ntx + it.tx0 / kPW;
-  if (task_reduce<2>(v, a, it.t, red, a.ntile, j) && threadIdx.x == 0)
-    cg_scalars(a, it.t, v[0], v[1]);
-}
-
-__global__ void __launch_bounds__(kPThreads, 1) tile_pipe_kernel(SArgs a) {
-  extern __shared__ __align__(16) double psm[];
-  PStage* stg = reinterpret_cast<PStage*>(psm);
-  double* U = psm + 2 * (sizeof(PStage) / sizeof(double));
-  double* red = U + (kPH + 2) * kPULD;
-  int2* tab = reinterpret_cast<int2*>(red + 2 * 4 * 32);
-  for (int t = threadIdx.x; t < a.T; t += kPThreads) {
-    const mlmcp_task tk = a.tasks[t];
-    const int32_t* ti = a.w.ti + t * kTI;
-    int mode = 0;
-    if (task_live(a, tk, t)) {
-      const int st = ti[I_STATE];
-      mode = st == ST_RUN ? 1 : (st == ST_ZERO ? 2 : 0);
-    }
-    tab[t] = make_int2(mode | (ti[I_IT_STEP] << 2), tk.sample);
-  }
-  __syncthreads();
-  const int n_items = a.T * a.ntile;
-  int q = blockIdx.x;
-  if (q >= n_items) return;
-  double alpha_n = 0.0, beta_n = 0.0;
-  PItem nxt = p_item(a, tab, q);
-  p_prefetch(a, nxt, stg[0], alpha_n, beta_n);
-  cp_commit();
-  for (int it = 0; q < n_items; ++it, q += gridDim.x) {
-    const PItem cur = nxt;
-    const double alpha = alpha_n, beta = beta_n;
-    cp_wait_all();
-    __syncthreads();
-    const int qn = q + gridDim.x;
-    if (qn < n_items) {
-      nxt = p_item(a, tab, qn);
-      p_prefetch(a, nxt, stg[(it + 1) & 1], alpha_n, beta_n);
-    }
-    cp_commit();
-    p_compute(a, cur, stg[it & 1], alpha, beta, U, red);
-  }
-}
-
-int tile_pipe_grid() {
-  static int g = 0;
-  if (g == 0) {
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(tile_pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kPSmem);
-    g = sms > 0 ? sms : 148;
-  }
-  return g;
-}
-
-int tile_cfg() {
-  const char* e = getenv("MLMCP_TILE_CFG");
-  return e ? std::max(1, std::min(4, atoi(e))) : 1;
-}
-
-bool tile_pipe_on(const SArgs& a) {
-  const char* e = getenv("MLMCP_TILE_PIPE");
-  return a.T <= kPMaxTasks && e && atoi(e) == 1;   // off by default (measured slower)
-}
 
 // ------------------------------------------------------ TMA-staged tile kernel
 // Warp-specialised persistent variant of tile_iter_kernel (one CTA per SM,
@@ -1450,6 +1194,13 @@ bool tile_usable(const Ctx* ctx) {
   return ntile <= (ctx->n + kThreads - 1) / kThreads;   // partial-sum slots
 }
 
+// MLMCP_TILE_CFG: 1 tile_iter_kernel<16,4,3> (default), 2 <16,4,4>, 3 <8,2,4>,
+// 4 the TMA-staged warp-specialised kernel (experimental)
+int tile_cfg() {
+  const char* e = getenv("MLMCP_TILE_CFG");
+  return e ? std::max(1, std::min(4, atoi(e))) : 1;
+}
+
 // MLMCP_STREAM_GRAPH=1: device-driven step loop (conditional graph nodes);
 // measured on par with the host loop below (whose syncs overlap nothing
 // costly), which stays the default because ncu can profile its kernels
@@ -1502,16 +1253,11 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     form_ell_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
     MLMCP_LAUNCH_CHECK("form_ell_kernel");
   }
-  const bool pipe = a.tile && tile_pipe_on(a);
-  if (a.tile) {   // the pipelined kernel uses the 64 x 16 tiling
-    a.ntx = pipe ? (a.wd + kPW - 1) / kPW : (a.wd + kTW - 1) / kTW;
-    a.ntile = a.ntx * ((a.gh + kPH - 1) / kPH);
-  }
-  const dim3 grid_pipe(a.tile ? tile_pipe_grid() : 1);
   const int tcfg = tile_cfg();
   const dim3 grid_tma(a.tile && tcfg == 4 ? tile_tma_grid() : 1);
-  if (a.tile && !pipe) {
-    const int th = (tcfg == 3 || tcfg == 4) ? 8 : 16;
+  if (a.tile) {   // 64-column tiles of 16 rows (variants 3, 4: 8 rows)
+    const int th = (tcfg >= 3) ? 8 : 16;
+    a.ntx = (a.wd + kTW - 1) / kTW;
     a.ntile = a.ntx * ((a.gh + th - 1) / th);
   }
   const dim3 grid_tiles2(a.tile ? a.ntile : 1, a.T);
@@ -1520,7 +1266,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   mark_fail_kernel<<<(a.T + 255) / 256, 256, 0, stream>>>(a, 0);
   MLMCP_LAUNCH_CHECK("mark_fail_kernel");
   auto launch_init = [&](cudaStream_t s, int step) -> int {
-    if (a.tile && !pipe && (tcfg == 3 || tcfg == 4)) {
+    if (a.tile && tcfg >= 3) {
       tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else if (a.tile) {
@@ -1545,10 +1291,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     }
   }
   auto launch_iteration = [&](cudaStream_t s) -> int {
-    if (pipe) {
-      tile_pipe_kernel<<<grid_pipe, kPThreads, kPSmem, s>>>(a);
-      MLMCP_LAUNCH_CHECK("tile_pipe_kernel");
-    } else if (a.tile) {
+    if (a.tile) {
       if (tcfg == 4) tile_tma_kernel<<<grid_tma, kXThreads, kXSmem, s>>>(a);
       else if (tcfg == 1) tile_iter_kernel<16, 4, 3><<<grid_tiles2, 256, 0, s>>>(a);
       else if (tcfg == 2) tile_iter_kernel<16, 4, 4><<<grid_tiles2, 256, 0, s>>>(a);
