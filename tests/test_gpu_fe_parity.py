@@ -123,3 +123,51 @@ def test_empty_batch(cuda):
     fam = family(8, "quad4", [0.02 / 32, 0.02 / 64], 0.02)
     out = fam.run_levels([np.zeros((0, 8)), np.zeros((0, 8))])
     assert all(len(b.q_l) == 0 for b in out)
+
+
+@pytest.mark.parametrize("impl", ["1", "4"])
+def test_streaming_batch_invariance_bitwise(cuda, impl, monkeypatch):
+    """Streaming paths (two-launch ELL, tile): per-task reductions in fixed
+    order, so a sample's result is bitwise independent of the batch it runs in
+    (full 256x256 config-2 mesh, 6 steps)."""
+    import torch
+    from paper_2507_19246_b200.mlmc import draw_level
+    from paper_2507_19246_b200.models import eddy_current_family
+    monkeypatch.setenv("MLMCP_STREAM_IMPL", impl)
+    fam = eddy_current_family(2, device="cuda:0")
+    sol = fam.solver
+    p = draw_level(fam.uncertain, 0, 0, range(1, 4))
+    dt = fam.hierarchy[0].dt
+
+    def run(params):
+        M, K = sol.assemble(torch.from_numpy(params).to(sol.device))
+        job = fam._seq_job(np.arange(len(params)), dt)
+        job.n_steps = 6
+        r = sol.run_sequential(M, K, [job])[0]
+        return (sol._last_xbuf.view(len(params), -1).cpu().numpy().copy(),
+                r.iters.cpu().numpy().copy())
+
+    x3, it3 = run(p)
+    x1, it1 = run(p[1:2])
+    assert np.array_equal(x3[1], x1[0]) and it3[1] == it1[0]
+
+
+def test_streaming_paths_agree_full_mesh(cuda, monkeypatch):
+    """Two-launch ELL kernels and the tile kernel on the full 512x512 config-4
+    mesh: same iterates to the PCG tolerance (states within 1e-10 of max|x|)."""
+    import torch
+    from paper_2507_19246_b200.mlmc import draw_level
+    from paper_2507_19246_b200.models import eddy_current_family
+    fam = eddy_current_family(4, device="cuda:0")
+    sol = fam.solver
+    p = draw_level(fam.uncertain, 0, 0, range(1, 3))
+    M, K = sol.assemble(torch.from_numpy(p).to(sol.device))
+    out = {}
+    for impl in ("1", "4"):
+        monkeypatch.setenv("MLMCP_STREAM_IMPL", impl)
+        job = fam._seq_job(np.arange(2), fam.hierarchy[0].dt)
+        job.n_steps = 4
+        sol.run_sequential(M, K, [job])
+        out[impl] = sol._last_xbuf.view(2, -1).cpu().numpy().copy()
+    scale = np.max(np.abs(out["1"]))
+    assert scale > 0 and np.max(np.abs(out["1"] - out["4"])) <= 1e-10 * scale
