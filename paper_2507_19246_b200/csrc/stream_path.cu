@@ -436,8 +436,9 @@ __global__ void __launch_bounds__(kThreads) update_kernel(SArgs a) {
 // only buffers no tile of the same launch writes.  The operator is the
 // symmetric half (C, E, N, NE) per point, [S][4][N]; W, S, SW are the E, N, NE
 // coefficients of the west / south / south-west neighbour.
-// HBM streams per point and iteration: read x r w s p D^-1 + 4 operator
-// values, write x r w s p = 120 B (B_it = 8 nnz + 56 N counts 112 B).
+// HBM streams per point and iteration: read x r w s p + 4 operator values,
+// write x r w s p = 112 B (D^-1 = 1/C recomputed; B_it = 8 nnz + 56 N also
+// counts 112 B).
 constexpr int kTW = 64;
 constexpr int kTLD = kTW + 2;
 
@@ -488,7 +489,7 @@ __device__ __forceinline__ double tile_s(bool first, double beta, double wo, dou
 template <int kTH, int kTR, int kMinB>
 __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SArgs a) {
   constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
-  static_assert(kTHalo <= kTW * (kTH / kTR), "one halo point per thread");
+  constexpr int kNT = kTW * (kTH / kTR);
   constexpr int kTCL = kTW + 1;                 // operator tile: columns -1..kTW-1
   constexpr int kTCN = (kTH + 1) * kTCL;        //                rows -1..kTH-1
   __shared__ double U[(kTH + 2) * kTLD];
@@ -530,8 +531,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
 #pragma unroll
     for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + (ly + 1) * kTCL + cx + 1], As + j * N + i, ok);
   }
-  if (threadIdx.x < kTH + 1 + kTW) {
-    const int h = threadIdx.x;
+  for (int h = threadIdx.x; h < kTH + 1 + kTW; h += kNT) {
     const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
     const int hx = tx0 + lx, hy = ty0 + ly;
     const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
@@ -552,8 +552,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
 
   // halo frame: u at the neighbouring tiles' points (0 outside the grid)
-  if (threadIdx.x < kTHalo) {
-    const int h = threadIdx.x;
+  for (int h = threadIdx.x; h < kTHalo; h += kNT) {
     int lx, ly;
     if (h < kTW + 2) { lx = h - 1; ly = -1; }
     else if (h < 2 * (kTW + 2)) { lx = h - (kTW + 2) - 1; ly = kTH; }
@@ -578,13 +577,21 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
       const bool ok = colok && gy0 + r < a.gh;
       const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
       rv[r] = ok ? __ldcg(Ro + i) : 0.0;
-      dv[r] = ok ? __ldg(Di + i) : 0.0;
       if (upd) {
         wv[r] = ok ? __ldcg(Wo + i) : 0.0;
         sv[r] = (ok && !first) ? __ldcg(So + i) : 0.0;
         pv[r] = (ok && !first) ? __ldcg(a.w.P + o + i) : 0.0;
         xv[r] = ok ? __ldcg(X + i) : 0.0;
       }
+    }
+    // D^-1 of the own points from the staged diagonal (this thread's own
+    // copies: no barrier needed), the same correctly rounded 1/C as
+    // form_tile_kernel's stored D^-1 (one 8-byte stream less per iteration)
+    cp_wait_all();
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      dv[r] = ok ? 1.0 / Ac[(sy * kTR + r + 1) * kTCL + cx + 1] : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < kTR; ++r) {
