@@ -126,6 +126,15 @@ def cpu_model():
     return "unknown"
 
 
+def workload_name(cfg_i, cfg, counts, pcfg):
+    """The workload string both arms report (config.workload)."""
+    par = ("Parareal M=%d K<=%d tol=%g" % (pcfg.num_subintervals, pcfg.k_max, pcfg.tolerance)
+           if pcfg else "no Parareal")
+    return (f"cfg{cfg_i}: {cfg.n}x{cfg.n} P1 eddy-current, levels "
+            f"dt=T/{round(cfg.horizon / cfg.dts[0])}..T/{round(cfg.horizon / cfg.dts[-1])}, "
+            f"N_l={list(counts)} ({par}), full MLMC estimate per step")
+
+
 def reference_arm(args):
     """--impl reference: the reference algorithm (oracle port; the reference is
     pure Python and cannot travel) on all host cores."""
@@ -152,7 +161,11 @@ def reference_arm(args):
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{args.config}-subset", "mesh": f"{cfg.n}x{cfg.n}"},
+            "config": {"workload": workload_name(args.config, cfg, [n * args.gpus for n in cfg.samples],
+                                                 cfg.parareal_config()),
+                       "seq_equiv_sample_timesteps": cfg.seq_equiv_steps(args.gpus),
+                       "sampled_per_step": f"N_l={counts} of it (bounded CPU sample, rate extrapolated)",
+                       "parallelism": f"{cores} host processes"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -426,9 +439,7 @@ def main():
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": {"workload": f"cfg{args.config}: {cfg.n}x{cfg.n} P1 eddy-current, levels "
-                                  f"dt=T/{round(cfg.horizon / cfg.dts[0])}..T/{round(cfg.horizon / cfg.dts[-1])}, "
-                                  f"N_l={list(counts)} ({'Parareal M=%d K<=%d tol=%g' % (pcfg.num_subintervals, pcfg.k_max, pcfg.tolerance) if pcfg else 'no Parareal'}), full MLMC estimate per step",
+           "config": {"workload": workload_name(args.config, cfg, counts, pcfg),
                       "seq_equiv_sample_timesteps": total_steps, "mlmc_parareal_wall_ms": ms,
                       "pcg_rtol": sol.step_rtol(), "predictor": sol.use_predictor(), "parareal_k": sorted(set(k_used)),
                       "l2": "flushed between steps (512 MiB write)", "parallelism": f"samples x{world}"},
