@@ -230,6 +230,23 @@ def measured_peak():
         return FALLBACK_HBM, "fallback"
 
 
+def ncu_sm_internal():
+    """SM-internal utilisation of the top kernel from the committed ncu capture
+    (the bound of the SM-resident config-1 kernel: fp64 pipe / issue slots)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_top_kernel.json")) as fh:
+            src = json.load(fh).get("source")
+        with open(os.path.join(ROOT, src)) as fh:
+            d = json.load(fh)
+        d = d["kernels"][0] if "kernels" in d else d
+        f = lambda k: float(d[k]["value"]) / 100.0
+        return {"fp64_pipe_active": f("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                "issue_active": f("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                "source": src}
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     """dram bytes per launch of the top kernel from the committed ncu capture."""
     try:
@@ -452,6 +469,7 @@ def main():
                                    "persistent device-scheduled launch)"),
                         "algorithmic_bytes": f"{kern_its} PCG iterations x (8 nnz + 56 N) = {kern_its} x {b_it} B",
                         "kernel_ms": seq_kernel_ms, "peak_kind": peak_kind,
+                        "sm_internal": ncu_sm_internal(),
                         "note": "32x32 operators live in registers/SMEM (SM-resident CTA per task): "
                                 "frac > 1 means the kernel runs faster than streaming its algorithmic "
                                 "bytes from HBM would allow; ncu dram bytes are the actual traffic"},
