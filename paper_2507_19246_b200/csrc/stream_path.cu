@@ -495,6 +495,11 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   __shared__ double U[(kTH + 2) * kTLD];
   __shared__ double Ac[4 * kTCN];               // C, E, N, NE (cp.async-staged)
   __shared__ double red[2 * 4 * 32];
+  // programmatic dependent launch: this grid may be scheduled while the
+  // previous iteration's grid drains; wait for it (and its memory) before
+  // reading anything, and let the next iteration's grid be scheduled early
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
   const int32_t* ti = a.w.ti + t * kTI;
@@ -1208,6 +1213,13 @@ int tile_cfg() {
   return e ? std::max(1, std::min(4, atoi(e))) : 1;
 }
 
+// MLMCP_TILE_PDL=0 disables programmatic dependent launch of the tile
+// iterations (back-to-back launches then drain fully before the next starts)
+bool pdl_on() {
+  const char* e = getenv("MLMCP_TILE_PDL");
+  return !(e && atoi(e) == 0);
+}
+
 // MLMCP_STREAM_GRAPH=1: device-driven step loop (conditional graph nodes);
 // measured on par with the host loop below (whose syncs overlap nothing
 // costly), which stays the default because ncu can profile its kernels
@@ -1300,7 +1312,22 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   auto launch_iteration = [&](cudaStream_t s) -> int {
     if (a.tile) {
       if (tcfg == 4) tile_tma_kernel<<<grid_tma, kXThreads, kXSmem, s>>>(a);
-      else if (tcfg == 1) tile_iter_kernel<16, 4, 3><<<grid_tiles2, 256, 0, s>>>(a);
+      else if (tcfg == 1) {
+        if (pdl_on()) {
+          cudaLaunchConfig_t lc = {};
+          lc.gridDim = grid_tiles2;
+          lc.blockDim = dim3(256);
+          lc.stream = s;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          lc.attrs = at;
+          lc.numAttrs = 1;
+          MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_kernel<16, 4, 3>, a));
+        } else {
+          tile_iter_kernel<16, 4, 3><<<grid_tiles2, 256, 0, s>>>(a);
+        }
+      }
       else if (tcfg == 2) tile_iter_kernel<16, 4, 4><<<grid_tiles2, 256, 0, s>>>(a);
       else tile_iter_kernel<8, 2, 4><<<grid_tiles2, 256, 0, s>>>(a);
       MLMCP_LAUNCH_CHECK("tile_iter_kernel");
