@@ -23,19 +23,25 @@ def run(cfg_i):
     fam = eddy_current_family(cfg_i, device="cuda:0")
     mlmc_estimate(fam, policy=FixedSamples(tuple(min(n, 2) for n in cfg.samples)),
                   parareal_cfg=pcfg, seed=cfg.seed)
-    torch.cuda.synchronize()
-    t = time.perf_counter()
-    res = mlmc_estimate(fam, policy=FixedSamples(tuple(cfg.samples)), parareal_cfg=pcfg,
-                        seed=cfg.seed)
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t
+    walls = []
+    while True:   # configs that finish in seconds: a second (warm) call is the one reported
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        res = mlmc_estimate(fam, policy=FixedSamples(tuple(cfg.samples)), parareal_cfg=pcfg,
+                            seed=cfg.seed)
+        torch.cuda.synchronize()
+        walls.append(time.perf_counter() - t)
+        if len(walls) == 2 or walls[0] > 5.0:
+            break
+    wall = walls[-1]
     steps = cfg.seq_equiv_steps(1)
     ks = sorted({int(k) for lv in res.per_level for k in (getattr(lv, "parareal_k", None) or [])})
     return {"config": cfg_i, "mesh": f"{cfg.n}x{cfg.n}", "N_l": list(cfg.samples),
             "parareal": list(cfg.parareal) if cfg.parareal else None,
             "expectation": res.expectation, "rmse_estimate": res.rmse_estimate,
             "wall_s": wall, "seq_equiv_sample_timesteps": steps,
-            "sample_timesteps_per_s": steps / wall, "parareal_k_values": ks, "gpus": 1}
+            "sample_timesteps_per_s": steps / wall, "parareal_k_values": ks,
+            "calls_s": walls, "gpus": 1}
 
 
 if __name__ == "__main__":
