@@ -492,8 +492,9 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   constexpr int kNT = kTW * (kTH / kTR);
   constexpr int kTCL = kTW + 1;                 // operator tile: columns -1..kTW-1
   constexpr int kTCN = (kTH + 1) * kTCL;        //                rows -1..kTH-1
-  __shared__ double U[(kTH + 2) * kTLD];
-  __shared__ double Ac[4 * kTCN];               // C, E, N, NE (cp.async-staged)
+  extern __shared__ __align__(16) double tsm[];
+  double* U = tsm;                              // (kTH + 2) * kTLD
+  double* Ac = U + (kTH + 2) * kTLD;            // C, E, N, NE (cp.async-staged)
   __shared__ double red[2 * 4 * 32];
   // programmatic dependent launch: this grid may be scheduled while the
   // previous iteration's grid drains; wait for it (and its memory) before
@@ -648,6 +649,37 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   }
   double v[2] = {gam, del};
   if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
+}
+
+template <int kTH, int kTR>
+constexpr size_t tile_iter_smem() {
+  return sizeof(double) * ((kTH + 2) * kTLD + 4 * (kTH + 1) * (kTW + 1));
+}
+
+// launch one tile iteration (programmatic dependent launch unless disabled)
+template <int kTH, int kTR, int kMinB>
+int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
+  constexpr int nt = kTW * (kTH / kTR);
+  constexpr size_t smem = tile_iter_smem<kTH, kTR>();
+  static bool attr = false;
+  if (!attr) {
+    MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_kernel<kTH, kTR, kMinB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
+  }
+  cudaLaunchConfig_t lc = {};
+  lc.gridDim = grid;
+  lc.blockDim = dim3(nt);
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = pdl ? 1 : 0;
+  MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_kernel<kTH, kTR, kMinB>, a));
+  MLMCP_LAUNCH_CHECK("tile_iter_kernel");
+  return MLMCP_OK;
 }
 
 // Step start on the tile layout: b = M a_n + dt sf profile, r_0 = b - A x_0,
@@ -1207,7 +1239,8 @@ bool tile_usable(const Ctx* ctx) {
 }
 
 // MLMCP_TILE_CFG: 1 tile_iter_kernel<16,4,3> (default), 2 <16,4,4>, 3 <8,2,4>,
-// 4 the TMA-staged warp-specialised kernel (experimental)
+// 4 the TMA-staged warp-specialised kernel (experimental); 64x32 tiles at
+// 2 CTAs/SM measured 11% slower than the default
 int tile_cfg() {
   const char* e = getenv("MLMCP_TILE_CFG");
   return e ? std::max(1, std::min(4, atoi(e))) : 1;
@@ -1275,7 +1308,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   const int tcfg = tile_cfg();
   const dim3 grid_tma(a.tile && tcfg == 4 ? tile_tma_grid() : 1);
   if (a.tile) {   // 64-column tiles of 16 rows (variants 3, 4: 8 rows)
-    const int th = (tcfg >= 3) ? 8 : 16;
+    const int th = tcfg >= 3 ? 8 : 16;
     a.ntx = (a.wd + kTW - 1) / kTW;
     a.ntile = a.ntx * ((a.gh + th - 1) / th);
   }
@@ -1311,26 +1344,16 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   }
   auto launch_iteration = [&](cudaStream_t s) -> int {
     if (a.tile) {
-      if (tcfg == 4) tile_tma_kernel<<<grid_tma, kXThreads, kXSmem, s>>>(a);
-      else if (tcfg == 1) {
-        if (pdl_on()) {
-          cudaLaunchConfig_t lc = {};
-          lc.gridDim = grid_tiles2;
-          lc.blockDim = dim3(256);
-          lc.stream = s;
-          cudaLaunchAttribute at[1];
-          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-          at[0].val.programmaticStreamSerializationAllowed = 1;
-          lc.attrs = at;
-          lc.numAttrs = 1;
-          MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_kernel<16, 4, 3>, a));
-        } else {
-          tile_iter_kernel<16, 4, 3><<<grid_tiles2, 256, 0, s>>>(a);
-        }
+      if (tcfg == 4) {
+        tile_tma_kernel<<<grid_tma, kXThreads, kXSmem, s>>>(a);
+        MLMCP_LAUNCH_CHECK("tile_tma_kernel");
+      } else if (tcfg == 1) {
+        if (const int rc = launch_tile_iter<16, 4, 3>(a, grid_tiles2, s, pdl_on())) return rc;
+      } else if (tcfg == 2) {
+        if (const int rc = launch_tile_iter<16, 4, 4>(a, grid_tiles2, s, pdl_on())) return rc;
+      } else {
+        if (const int rc = launch_tile_iter<8, 2, 4>(a, grid_tiles2, s, pdl_on())) return rc;
       }
-      else if (tcfg == 2) tile_iter_kernel<16, 4, 4><<<grid_tiles2, 256, 0, s>>>(a);
-      else tile_iter_kernel<8, 2, 4><<<grid_tiles2, 256, 0, s>>>(a);
-      MLMCP_LAUNCH_CHECK("tile_iter_kernel");
     } else {
       spmv_kernel<<<grid_rows, blk, 0, s>>>(a);
       MLMCP_LAUNCH_CHECK("spmv_kernel");
