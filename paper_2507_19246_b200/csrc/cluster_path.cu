@@ -551,6 +551,106 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_propagate_kernel(ClArg
   cl_sync();   // no CTA leaves while another may still address its shared memory
 }
 
+
+// Parareal coarse sweep on the cluster path (parareal.py:168-178): one
+// cluster per Parareal sample walks the slices n = k .. m-1 of iteration k:
+// propagate U_{n-1} over slice n with the coarse step (the operator at dt_c
+// stays in registers for the whole sweep), then
+//   k == 1: U_n = C_{n-1} = c;   k >= 2: U_n = (F_n + c) - C_{n-1}, C_{n-1} = c
+// (the arithmetic of correct_kernel).  A failed coarse solve records
+// (code, step, interval n, iteration k) and deactivates the sample, as the
+// streaming sweep's coarse_status_kernel.  Replaces ~30 launches per slice of
+// the streaming sweep with one launch per sweep.
+struct ClCoarse {
+  int k, m;
+  double dt_c, t0;
+  const int64_t* slice_k0;
+  const int32_t* slice_steps;
+  double* U;          // [S][m+1][N]
+  const double* F;    // [S][m+1][N]
+  double* C;          // [S][m][N]
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a, ClCoarse cc) {
+  constexpr int R = C::R;
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int live;
+  cg::cluster_group cl = cg::this_cluster();
+  Thr<C> th;
+  th.rank = (int)cl.block_rank();
+  th.x = threadIdx.x % C::TX;
+  th.k = threadIdx.x / C::TX;
+  th.gy0 = th.rank * C::HB + th.k * R;
+  const int s = blockIdx.x / C::CS;
+  ClShared<C> sh;
+  sh.VA = smem;
+  sh.VB = sh.VA + C::kV;
+  sh.VC = sh.VB + C::kV;
+  sh.mm = sh.VC + C::kV;
+  sh.mmb = sh.mm + 4 * C::kSlots;
+  sh.ring = sh.mmb + 2 * C::TX;
+  sh.red = sh.ring + C::kRing * C::kSlots;
+  sh.par = 0;
+  for (int i = threadIdx.x; i < 3 * C::kV; i += C::kThreads) smem[i] = 0.0;
+  if (th.rank == 0 && threadIdx.x == 0) {
+    const int lv = *((volatile const int32_t*)a.active + s) != 0;
+    for (int c = 0; c < C::CS; ++c) *cl.map_shared_rank(&live, c) = lv;
+  }
+  cl_sync();
+  if (!live) return;
+  const int64_t N = a.N;
+  const double* Ms = a.M + (int64_t)s * a.nnz;
+  const double* Ks = a.K + (int64_t)s * a.nnz;
+  ClOp<C> op;
+  op.load(th, a, Ms, Ks, cc.dt_c);
+  ClOp<C>::load_mass(th, a, Ms, sh.mm, sh.mmb);
+  double* Us = cc.U + (int64_t)s * (cc.m + 1) * N;
+  const double* Fs = cc.F + (int64_t)s * (cc.m + 1) * N;
+  double* Cs = cc.C + (int64_t)s * cc.m * N;
+  double x[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    x[r] = th.ok(r, a) ? __ldcg(Us + (int64_t)(cc.k - 1) * N + th.row(r, a)) : 0.0;
+  int iters = 0;
+  for (int n = cc.k; n < cc.m; ++n) {
+    const int n_steps = cc.slice_steps[n - 1];
+    const int64_t k0 = cc.slice_k0[n - 1];
+    int code = MLMCP_ST_OK, fail_step = 0;
+    for (int step = 0; step < n_steps; ++step) {
+      const int64_t g = k0 + step + 1;
+      const double sf = sin(__dmul_rn(a.omega, grid_time(cc.t0, g, cc.dt_c)));
+      double an[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) an[r] = x[r];
+      cl_guess<C>(th, x, sh.ring, step, min(step, a.order));
+#pragma unroll
+      for (int r = 0; r < R; ++r) sh.ring[(step & (C::kRing - 1)) * C::kSlots + th.slot(r)] = an[r];
+      code = cl_ie_step<C>(op, th, a, x, an, sf, cc.dt_c, sh, cl, iters);
+      if (code != MLMCP_ST_OK) { fail_step = step; break; }
+    }
+    if (code != MLMCP_ST_OK) {   // cluster-uniform (scalars are identical in every CTA)
+      if (th.rank == 0 && threadIdx.x == 0) {
+        if (a.status[(int64_t)s * kStatusInts] == MLMCP_ST_OK)
+          write_status(a.status, s, code, fail_step, n, cc.k);
+        const_cast<int32_t*>(a.active)[s] = 0;
+      }
+      break;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (!th.ok(r, a)) continue;
+      const int64_t i = th.row(r, a);
+      const double c = x[r];
+      const double u = cc.k == 1 ? c : (Fs[(int64_t)n * N + i] + c) - Cs[(int64_t)(n - 1) * N + i];
+      Us[(int64_t)n * N + i] = u;
+      Cs[(int64_t)(n - 1) * N + i] = c;
+      x[r] = u;
+    }
+  }
+  cl_sync();   // no CTA leaves while another may still address its shared memory
+}
+
 // 128 column threads x 4 strips of 4 rows, 8 CTAs: grids up to 128 x 128
 using Cfg128 = Cfg<4, 128, 4, 8>;
 
@@ -624,6 +724,54 @@ int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const doub
   a.active = active;
   a.elapsed = elapsed;
   return launch<Cfg128>(a, n_tasks, stream);
+}
+
+
+int cluster_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
+                            const double* profile, double omega, double dt_c, double t0,
+                            const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
+                            int max_it, double* U, const double* F, double* C, int32_t* status,
+                            const int32_t* active, cudaStream_t stream) {
+  if (S == 0 || k >= m) return MLMCP_OK;
+  using Cf = Cfg128;
+  ClArgs a{};
+  a.N = ctx->n;
+  a.wd = ctx->cl_wd;
+  a.gh = ctx->cl_h;
+  a.nnz = ctx->nnz;
+  a.gpos = ctx->cl_pos;
+  a.M = M;
+  a.K = K;
+  a.profile = profile;
+  a.omega = omega;
+  a.rtol2 = rtol * rtol;
+  a.max_it = max_it;
+  a.order = order_pref();
+  a.status = status;
+  a.active = active;
+  ClCoarse cc{k, m, dt_c, t0, slice_k0, slice_steps, U, F, C};
+  const size_t smem = sizeof(double) * Cf::kSmemDoubles;
+  static bool attr_done = false;
+  if (!attr_done) {
+    MLMCP_CUDA_CHECK(cudaFuncSetAttribute(cluster_coarse_kernel<Cf>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr_done = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(S * Cf::CS));
+  cfg.blockDim = dim3(Cf::kThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = Cf::CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, cluster_coarse_kernel<Cf>, a, cc));
+  MLMCP_LAUNCH_CHECK("cluster_coarse_kernel");
+  return MLMCP_OK;
 }
 
 }  // namespace mlmcp

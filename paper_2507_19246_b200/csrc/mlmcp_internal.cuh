@@ -226,6 +226,11 @@ int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const doub
                       const double* K, const double* profile, double omega, double rtol,
                       int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
                       const int32_t* active, int64_t* elapsed, cudaStream_t stream);
+int cluster_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
+                            const double* profile, double omega, double dt_c, double t0,
+                            const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
+                            int max_it, double* U, const double* F, double* C, int32_t* status,
+                            const int32_t* active, cudaStream_t stream);
 int coop_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                    const std::vector<mlmcp_task>& h, int S, const double* A,
                    const double* dinv, const double* M, const double* K,

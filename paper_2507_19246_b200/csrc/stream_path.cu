@@ -1885,6 +1885,24 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
   mlmcp_task* dtasks = reinterpret_cast<mlmcp_task*>(base + tasks_off);
   double* cval = reinterpret_cast<double*>(base + cval_off);
   int32_t* tstatus = reinterpret_cast<int32_t*>(base + tst_off);
+  if (cluster_usable(ctx)) {   // one launch for the whole sweep (cluster_path.cu)
+    int32_t* act = const_cast<int32_t*>(active);
+    const dim3 grid((unsigned)((N + 255) / 256), S);
+    if (k > 1) {
+      freeze_kernel<<<grid, 256, 0, stream>>>(S, m, (int)N, k - 1, k - 1, U, F, act);
+      MLMCP_LAUNCH_CHECK("freeze_kernel");
+    }
+    const int rc = cluster_parareal_coarse(ctx, S, k, m, M, K, profile, omega, dt_c, t0,
+                                           slice_k0, slice_steps, rtol, max_it, U, F, C, status,
+                                           active, stream);
+    if (rc != MLMCP_OK) return rc;
+    if (k > 1) {
+      freeze_kernel<<<grid, 256, 0, stream>>>(S, m, (int)N, m, m, U, F, act);
+      MLMCP_LAUNCH_CHECK("freeze_kernel");
+    }
+    (void)iters;
+    return MLMCP_OK;
+  }
   std::vector<int64_t> hk0(m);
   std::vector<int32_t> hsteps(m);
   MLMCP_CUDA_CHECK(cudaMemcpyAsync(hk0.data(), slice_k0, sizeof(int64_t) * m,
@@ -1898,6 +1916,7 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
     freeze_kernel<<<grid, 256, 0, stream>>>(S, m, (int)N, k - 1, k - 1, U, F, act);
     MLMCP_LAUNCH_CHECK("freeze_kernel");
   }
+
   std::vector<mlmcp_task> h(S);
   Work w = carve(ws, L);
   for (int n = k; n < m; ++n) {
