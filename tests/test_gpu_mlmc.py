@@ -370,3 +370,27 @@ def test_tile_path_ragged_grids_vs_oracle(cuda, n, env, monkeypatch):
     rec = mo.evaluate(prob, cfg, pp[0], T / 64, True, dense=False)
     assert int(b.k_used[0].item()) == rec.k_used
     assert abs(b.q_l[0].item() - rec.q) <= 1e-8 * abs(rec.q)
+
+
+@pytest.mark.parametrize("impl", ["3", "4"])
+def test_streaming_coarse_failure_maps_to_propagator_error(cuda, impl, monkeypatch):
+    """Coarse solves that cannot converge within max_it on the cluster sweep
+    (impl 3) and on the tile path (impl 4): the sample is deactivated with the
+    reference's PropagatorError(interval=1, iteration=1) (parareal.py:151-152)."""
+    from paper_2507_19246_b200 import fe
+    from paper_2507_19246_b200.models import (EddyCurrentFamily, ParameterVector, QoIKind,
+                                              UncertainInput, make_hierarchy)
+    from paper_2507_19246_b200.parareal import PararealConfig, PropagatorError
+    monkeypatch.setenv("MLMCP_STREAM_IMPL", impl)
+    nominal = np.array([fe.NU0] * 8 + [fe.SIGMA0] * 8)
+    fam = EddyCurrentFamily("blocks8", UncertainInput(ParameterVector("blocks8", nominal), 0.1),
+                            make_hierarchy([T / 32]), T, 64, "blocks8",
+                            QoIKind.MAGNETIC_ENERGY_T, device="cuda:0", path="stream",
+                            max_it=12)
+    cfg = mo.OracleConfig("t64f", 64, "blocks8", T, (T / 32,), (2,), "energy_T",
+                          parareal=(4, T / 4, 1e-8, 3))
+    pp = np.array([mo.draw(cfg, 0, 0, k) for k in (1, 2)])
+    fam.run_levels([pp], PararealConfig(4, T / 32, T / 4, 1e-8, 3), levels=[0])
+    with pytest.raises(PropagatorError) as ei:
+        fam.check_status()
+    assert (ei.value.interval, ei.value.iteration) == (1, 1)
