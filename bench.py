@@ -271,6 +271,7 @@ def streaming_roofline(dev, peak, flush):
     for cfg_i, S, steps in ((2, 512, 8), (4, 128, 4)):
         fam = eddy_current_family(cfg_i, device=dev)
         sol = fam.solver
+        sol.predictor = False   # the PCG kernels alone (no steady-state COCG solves)
         p = draw_level(fam.uncertain, 0, 0, range(1, S + 1))
         M, K = sol.assemble(torch.from_numpy(p).to(dev))
         job = fam._seq_job(np.arange(S), fam.hierarchy[0].dt)

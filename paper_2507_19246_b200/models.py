@@ -554,6 +554,7 @@ class EddyCurrentFamily(_BatchedFamily):
             from .solver import FESolver
             self._solver = FESolver(self.n, self.layout, self.device, self.rtol, self.max_it,
                                     self.path)
+            self._solver.periods = self.horizon * self._solver.omega / (2.0 * np.pi)
         return self._solver
 
     def _seq_job(self, rows, dt):

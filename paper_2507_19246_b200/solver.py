@@ -116,6 +116,7 @@ class BatchSolver:
         # MLMCP_PREDICTOR=0 disables it (A/B measurements)
         self.predictor = os.environ.get("MLMCP_PREDICTOR", "1") != "0"
         self.omega = 2.0 * np.pi * frequency       # same rounding as np.sin(2.0*np.pi*f*t)
+        self.periods = 1.0    # forcing periods in the family's horizon (set by the family)
 
     # ------------------------------------------------------------ sequential
     def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
@@ -137,14 +138,19 @@ class BatchSolver:
     def use_predictor(self) -> bool:
         """The steady-state predictor pays where the forced periodic response
         dominates the step-to-step change — the sigma = 0 (quasi-static) regions
-        of configs 0/1: PCG iterations per step 29.7 -> 11.4.  On the streaming
-        configs 2-4 every region conducts, the skin depth (~2e-3) is below the
-        mesh width and the solution over one period is the initial transient
-        itself: measured no gain (cfg3 14.1 vs 14.2 iterations per step), so
-        the streaming path keeps plain extrapolation unless MLMCP_PREDICTOR=all."""
+        of configs 0/1 (PCG iterations per step 29.7 -> 11.4; estimate 37.1 ->
+        15.6 ms), and on the streaming meshes once the horizon spans several
+        periods, so that the initial transient has decayed in the later ones
+        (config 2, 4 periods: 42.5 -> 32.8 s per estimate).  Over a single
+        period (configs 3, 4) the solution is the transient itself: measured no
+        gain (config 3: 14.1 vs 14.2 iterations per step), and on grids up to
+        128^2 the predictor would move the batch off the cluster kernel.
+        MLMCP_PREDICTOR=all forces it on, =0 off."""
         if not self.predictor or self.sys.direct or self.omega == 0.0:
             return False
-        return self.sys.sm_resident or os.environ.get("MLMCP_PREDICTOR") == "all"
+        if self.sys.sm_resident or os.environ.get("MLMCP_PREDICTOR") == "all":
+            return True
+        return self.periods >= 2.0 and self.N > 127 * 127
 
     def step_rtol(self) -> float:
         return min(self.rtol, PREDICTOR_RTOL) if self.use_predictor() else self.rtol
