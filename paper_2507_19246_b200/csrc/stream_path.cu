@@ -34,7 +34,18 @@ enum : int { D_BB = 0, D_GAMMA, D_ALPHA, D_BETA, D_ACC, D_SF, kTD };
 // task int layout
 enum : int { I_STATE = 0, I_IT_STEP, I_IT_TOTAL, I_CODE, I_FAILSTEP, I_FIRST, kTI };
 
-constexpr int kRingS = 4;   // past states a_{n-1..n-4} (order <= 4 extrapolation)
+constexpr int kRingS = 8;   // past states a_{n-1..n-8} (extrapolation order <= 7)
+
+// extrapolation weights: a_{n+1} ~ sum_j c[p][j] a_{n-j}, c[p][j] = (-1)^j C(p+1, j+1)
+__constant__ double c_extrap[8][8] = {
+    {1, 0, 0, 0, 0, 0, 0, 0},
+    {2, -1, 0, 0, 0, 0, 0, 0},
+    {3, -3, 1, 0, 0, 0, 0, 0},
+    {4, -6, 4, -1, 0, 0, 0, 0},
+    {5, -10, 10, -5, 1, 0, 0, 0},
+    {6, -15, 20, -15, 6, -1, 0, 0},
+    {7, -21, 35, -35, 21, -7, 1, 0},
+    {8, -28, 56, -70, 56, -28, 8, -1}};
 
 struct Work {
   double* ring;    // [kRingS][T][N]
@@ -125,6 +136,7 @@ struct SArgs {
   int tile;            // 1: tile path
   int wd, gh, ntx, ntile;
   const int32_t* gpos; // [7][N] CSR position of SW,S,W,C,E,N,NE or -1
+  int order;           // extrapolation order of the initial guess (<= kRingS - 1)
   // graph-driven step loop: the PCG while-node's condition, cleared by the
   // iteration in which the last live task of the step stops
   cudaGraphConditionalHandle it_cond;
@@ -301,14 +313,15 @@ __global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step_arg) 
     ssn = fma(xr, sc[2], xi * sc[3]);
   }
   const double yn = an - ssn;
-  const int pmax = pred ? 3 : kRingS;
-  const int p = (tk.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : min(step, pmax);
+  const int p = (tk.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : min(step, a.order);
   auto past = [&](int k) { return a.w.ring[(int64_t)((step - k) & (kRingS - 1)) * TN + o]; };
+  // polynomial extrapolation of order p through y_n .. y_{n-p} (high orders pay:
+  // the states are smooth in time)
   double g = yn;
-  if (p == 1) g = fma(2.0, yn, -past(1));
-  else if (p == 2) g = fma(3.0, yn - past(1), past(2));
-  else if (p == 3) g = fma(4.0, yn + past(2), fma(-6.0, past(1), -past(3)));
-  else if (p >= 4) g = fma(5.0, yn - past(3), fma(10.0, past(2) - past(1), past(4)));
+  if (p > 0) {
+    g = c_extrap[p][0] * yn;
+    for (int j = 1; j <= p; ++j) g = fma(c_extrap[p][j], past(j), g);
+  }
   a.w.ring[(int64_t)(step & (kRingS - 1)) * TN + o] = yn;
   a.w.Wv[o] = an;
   a.w.X[o] = g + sst;
@@ -1223,6 +1236,13 @@ __global__ void step_next_kernel(int32_t* counters, int n_steps, cudaGraphCondit
   cudaGraphSetConditional(h, s < n_steps ? 1 : 0);
 }
 
+// extrapolation order of the streaming paths' initial guesses (MLMCP_STREAM_ORDER)
+int stream_order() {
+  const char* e = getenv("MLMCP_STREAM_ORDER");
+  const int o = e ? atoi(e) : 4;
+  return std::max(0, std::min(o, kRingS - 1));
+}
+
 // MLMCP_STREAM_IMPL: 1 two-launch ELL kernels, 2 cooperative, 3 cluster,
 // 4 tile; default auto
 int stream_impl() {
@@ -1519,6 +1539,7 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   a.gpos = ctx->cl_pos;
   a.it_cond = 0;
   a.use_cond = 0;
+  a.order = stream_order();
   a.w = w;
   return a;
 }
