@@ -66,10 +66,10 @@ struct Cfg {
   static constexpr int LD = TX + 2;              // exchange-buffer row stride
   static constexpr int kV = (HB + 2) * LD;       // one exchange buffer (+ halo rows, pad columns)
   static constexpr int kSlots = HB * TX;         // per-CTA (row, column) slots
-  static constexpr int kRing = 4;                // past states a_{n-1..n-4}
+  static constexpr int kRing = 8;                // past states a_{n-1..n-8}
   static constexpr int kRedVals = 4;
   static constexpr int kRed = 2 * kRedVals * CS * kWarps;
-  static constexpr int kSmemDoubles = 3 * kV + 4 * kSlots + 2 * TX + kRing * kSlots + kRed;
+  static constexpr int kSmemDoubles = 3 * kV + kRing * kSlots + kRed;
   static_assert(TX % 32 == 0, "column threads must fill warps");
   static_assert((CS * kWarps) % 32 == 0 || CS * kWarps < 32, "reduction layout");
 };
@@ -319,8 +319,7 @@ struct ClShared {
   double* VA;    // exchange: a_n (rhs), x (energy)
   double* VB;    // exchange: initial guess
   double* VC;    // exchange: u (PCG iterations)
-  double* mm;    // [4][kSlots] mass C, E, N, NE
-  double* mmb;   // [2][TX] band-first-row S, SW mass coefficients
+  const double* Ms;   // per-sample CSR mass values (M a_n once per step, from L2)
   double* ring;  // [kRing][kSlots] past states
   double* red;   // [2][kRedVals][CS][kWarps]
   int par;
@@ -358,7 +357,7 @@ __device__ __forceinline__ int cl_ie_step(const ClOp<C>& op, const Thr<C>& th, c
   double red3[3] = {0.0, 0.0, 0.0};
   {
     double mx[R], ax[R], bv[R];
-    ClOp<C>::apply_mass(th, A, sh.mm, sh.mmb, an, sh.VA, mx);
+    ClOp<C>::apply_vals(th, A, sh.Ms, an, sh.VA, mx);
     op.apply(th, x, sh.VB, ax);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -444,22 +443,28 @@ __device__ __forceinline__ int cl_ie_step(const ClOp<C>& op, const Thr<C>& th, c
   return MLMCP_ST_OK;
 }
 
+// extrapolation weights: a_{n+1} ~ sum_j c[p][j] a_{n-j}, c[p][j] = (-1)^j C(p+1, j+1)
+__constant__ double c_cl_extrap[8][8] = {
+    {1, 0, 0, 0, 0, 0, 0, 0},
+    {2, -1, 0, 0, 0, 0, 0, 0},
+    {3, -3, 1, 0, 0, 0, 0, 0},
+    {4, -6, 4, -1, 0, 0, 0, 0},
+    {5, -10, 10, -5, 1, 0, 0, 0},
+    {6, -15, 20, -15, 6, -1, 0, 0},
+    {7, -21, 35, -35, 21, -7, 1, 0},
+    {8, -28, 56, -70, 56, -28, 8, -1}};
+
 // x <- order-p extrapolation of a_n (x on entry) and the past states in the ring
 template <class C>
 __device__ __forceinline__ void cl_guess(const Thr<C>& th, double (&x)[C::R], const double* ring,
                                          int step, int p) {
   constexpr int kR = C::kRing;
-  auto past = [&](int i, int r) {   // a_{n-i}, i >= 1
-    return ring[((step - i) & (kR - 1)) * C::kSlots + th.slot(r)];
-  };
+  if (p <= 0) return;
 #pragma unroll
   for (int r = 0; r < C::R; ++r) {
-    const double yn = x[r];
-    double g = yn;
-    if (p == 1) g = fma(2.0, yn, -past(1, r));
-    else if (p == 2) g = fma(3.0, yn - past(1, r), past(2, r));
-    else if (p == 3) g = fma(4.0, yn + past(2, r), fma(-6.0, past(1, r), -past(3, r)));
-    else if (p >= 4) g = fma(5.0, yn - past(3, r), fma(10.0, past(2, r) - past(1, r), past(4, r)));
+    double g = c_cl_extrap[p][0] * x[r];
+    for (int j = 1; j <= p; ++j)
+      g = fma(c_cl_extrap[p][j], ring[((step - j) & (kR - 1)) * C::kSlots + th.slot(r)], g);
     x[r] = g;
   }
 }
@@ -481,9 +486,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_propagate_kernel(ClArg
   sh.VA = smem;
   sh.VB = sh.VA + C::kV;
   sh.VC = sh.VB + C::kV;
-  sh.mm = sh.VC + C::kV;
-  sh.mmb = sh.mm + 4 * C::kSlots;
-  sh.ring = sh.mmb + 2 * C::TX;
+  sh.ring = sh.VC + C::kV;
   sh.red = sh.ring + C::kRing * C::kSlots;
   sh.par = 0;
   for (int i = threadIdx.x; i < 3 * C::kV; i += C::kThreads) smem[i] = 0.0;
@@ -500,7 +503,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_propagate_kernel(ClArg
   const double* Ks = a.K + (int64_t)t.sample * a.nnz;
   ClOp<C> op;
   op.load(th, a, Ms, Ks, t.dt);
-  ClOp<C>::load_mass(th, a, Ms, sh.mm, sh.mmb);
+  sh.Ms = Ms;
   double x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -587,9 +590,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a
   sh.VA = smem;
   sh.VB = sh.VA + C::kV;
   sh.VC = sh.VB + C::kV;
-  sh.mm = sh.VC + C::kV;
-  sh.mmb = sh.mm + 4 * C::kSlots;
-  sh.ring = sh.mmb + 2 * C::TX;
+  sh.ring = sh.VC + C::kV;
   sh.red = sh.ring + C::kRing * C::kSlots;
   sh.par = 0;
   for (int i = threadIdx.x; i < 3 * C::kV; i += C::kThreads) smem[i] = 0.0;
@@ -604,7 +605,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a
   const double* Ks = a.K + (int64_t)s * a.nnz;
   ClOp<C> op;
   op.load(th, a, Ms, Ks, cc.dt_c);
-  ClOp<C>::load_mass(th, a, Ms, sh.mm, sh.mmb);
+  sh.Ms = Ms;
   double* Us = cc.U + (int64_t)s * (cc.m + 1) * N;
   const double* Fs = cc.F + (int64_t)s * (cc.m + 1) * N;
   double* Cs = cc.C + (int64_t)s * cc.m * N;
@@ -682,8 +683,8 @@ int launch(const ClArgs& a, int n_tasks, cudaStream_t stream) {
 
 int order_pref() {
   const char* e = getenv("MLMCP_CLUSTER_ORDER");
-  const int o = e ? atoi(e) : 4;
-  return std::max(0, std::min(o, 4));
+  const int o = e ? atoi(e) : 7;   // higher orders pay: smooth states in time
+  return std::max(0, std::min(o, 7));
 }
 
 }  // namespace
