@@ -10,8 +10,10 @@
 //   * CTA c of the cluster owns the band of grid rows [c*HB, (c+1)*HB) of the
 //     wd x gh interior grid; each thread a column strip of R rows;
 //   * A = M + dt K (7 coefficients per row, the S one implied by symmetry) and
-//     the strip's L D L^T factors stay in registers for the whole task, the
-//     mass matrix's symmetric half in shared memory (per-step rhs M a_n);
+//     the strip's L D L^T factors stay in registers for the whole task; the
+//     per-step rhs M a_n reads the per-sample CSR mass values (L2), which
+//     leaves shared memory for a ring of 8 past states (order-7 extrapolated
+//     initial guesses);
 //   * neighbour values go through a shared-memory exchange buffer; a band's
 //     first and last grid rows are also stored straight into the neighbouring
 //     CTAs' buffers (DSMEM), made visible by one cluster barrier;
@@ -191,58 +193,7 @@ struct ClOp {
       out[r] = acc0 + acc1;
     }
   }
-  // mass matrix, symmetric half (C, E, N, NE of every slot) in smem; the
-  // band's first row keeps its own S / SW coefficients (their owners live in
-  // the CTA below)
-  __device__ static void load_mass(const Thr<C>& th, const ClArgs& A, const double* __restrict__ Ms,
-                                   double* mm, double* mmb) {
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const bool v = th.ok(r, A);
-      const int rw = v ? th.row(r, A) : 0;
-      const int sl = th.slot(r);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int q = v ? __ldg(A.gpos + (int64_t)(3 + j) * A.N + rw) : -1;
-        mm[j * C::kSlots + sl] = q >= 0 ? __ldg(Ms + q) : 0.0;
-      }
-    }
-    if (th.k == 0) {
-      const bool v = th.ok(0, A);
-      const int rw = v ? th.row(0, A) : 0;
-      const int qs = v ? __ldg(A.gpos + (int64_t)1 * A.N + rw) : -1;
-      const int qsw = v ? __ldg(A.gpos + rw) : -1;
-      mmb[th.x] = qs >= 0 ? __ldg(Ms + qs) : 0.0;
-      mmb[C::TX + th.x] = qsw >= 0 ? __ldg(Ms + qsw) : 0.0;
-    }
-  }
-  __device__ static void apply_mass(const Thr<C>& th, const ClArgs& A, const double* mm,
-                                    const double* mmb, const double (&v)[R], const double* V,
-                                    double (&out)[R]) {
-    double nb[R][7];
-    neighbours(th, v, V, nb);
-    constexpr int L = C::kSlots;
-#pragma unroll
-    for (int r = 0; r < R; ++r) {
-      const int sl = th.slot(r);
-      const bool first = (r == 0 && th.k == 0);
-      const double mw = th.x > 0 ? mm[1 * L + sl - 1] : 0.0;
-      const double msn = first ? mmb[th.x] : mm[2 * L + sl - C::TX];
-      const double msw = first ? mmb[C::TX + th.x] : (th.x > 0 ? mm[3 * L + sl - C::TX - 1] : 0.0);
-      double acc = 0.0;
-      if (th.ok(r, A)) {
-        acc = fma(msw, nb[r][0], acc);
-        acc = fma(msn, nb[r][1], acc);
-        acc = fma(mw, nb[r][2], acc);
-        acc = fma(mm[0 * L + sl], nb[r][3], acc);
-        acc = fma(mm[1 * L + sl], nb[r][4], acc);
-        acc = fma(mm[2 * L + sl], nb[r][5], acc);
-        acc = fma(mm[3 * L + sl], nb[r][6], acc);
-      }
-      out[r] = acc;
-    }
-  }
-  // out = B v for per-sample CSR values B (energy)
+  // out = B v for per-sample CSR values B (the energy, and M a_n once per step)
   __device__ static void apply_vals(const Thr<C>& th, const ClArgs& A,
                                     const double* __restrict__ vals, const double (&v)[R],
                                     const double* V, double (&out)[R]) {
