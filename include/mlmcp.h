@@ -143,6 +143,11 @@ int mlmcp_ctx_set_assembly(mlmcp_ctx* ctx, int n_elem, int n_contrib,
  * MLMCP_DIRECT_MAX_ROWS, SM-resident up to small_max_rows, else streaming. */
 #define MLMCP_DIRECT_MAX_ROWS 4
 int mlmcp_ctx_set_path(mlmcp_ctx* ctx, int path);
+/* Device time of the streaming paths' PCG-iteration launches (measurement;
+ * no reference counterpart): mode 1 resets and starts accumulating (CUDA
+ * events around each host-loop chunk of iteration launches), 0 stops; both
+ * return the totals so far in *ms and *launches (either may be NULL). */
+int mlmcp_stream_timing(mlmcp_ctx* ctx, int mode, double* ms, int64_t* launches);
 
 /* ---- K1: assembly ------------------------------------------------------ */
 /* sigma(s, e) = sigma_d[s*sigma_stride + (sigma_index_d ? sigma_index_d[e] : e)]

@@ -75,7 +75,7 @@ class PararealBatch(ctypes.Structure):
 EXPORTS = (
     "mlmcp_abi_version", "mlmcp_last_error", "mlmcp_launch_count",
     "mlmcp_ctx_create", "mlmcp_ctx_destroy", "mlmcp_ctx_info", "mlmcp_ctx_set_assembly",
-    "mlmcp_ctx_set_path", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
+    "mlmcp_ctx_set_path", "mlmcp_stream_timing", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
     "mlmcp_propagate", "mlmcp_periodic_workspace_bytes", "mlmcp_periodic_state", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
     "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce", "mlmcp_draw_uniform",
     "mlmcp_draw_uniform_host", "mlmcp_fused_workspace_bytes", "mlmcp_run_fused",
@@ -97,6 +97,8 @@ _SIGS = {
     "mlmcp_ctx_create": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
                                         ctypes.POINTER(P)]),
     "mlmcp_ctx_destroy": (ctypes.c_int, [P]),
+    "mlmcp_stream_timing": (ctypes.c_int, [P, ctypes.c_int, ctypes.POINTER(F64),
+                                           ctypes.POINTER(I64)]),
     "mlmcp_ctx_info": (ctypes.c_int, [P, ctypes.POINTER(ctypes.c_int),
                                       ctypes.POINTER(ctypes.c_int)]),
     "mlmcp_ctx_set_assembly": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),

@@ -363,6 +363,8 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->ckw);
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
+  for (cudaEvent_t e : c->iter_ev)
+    if (e) cudaEventDestroy(e);
   for (cudaStream_t s : c->cap_stream)
     if (s) cudaStreamDestroy(s);
   delete c;
@@ -385,6 +387,22 @@ int mlmcp_ctx_set_path(mlmcp_ctx* c, int path) {
   if (path == 3 && c->n > MLMCP_DIRECT_MAX_ROWS)
     return einval("direct path holds at most MLMCP_DIRECT_MAX_ROWS rows");
   c->path = path;
+  return MLMCP_OK;
+}
+
+int mlmcp_stream_timing(mlmcp_ctx* c, int mode, double* ms, int64_t* launches) {
+  if (c == nullptr) return einval("null context");
+  if (mode != 0 && mode != 1) return einval("mode must be 0 (stop) or 1 (reset and start)");
+  if (mode == 1) {
+    MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+    for (auto& e : c->iter_ev)
+      if (e == nullptr) MLMCP_CUDA_CHECK(cudaEventCreate(&e));
+    c->iter_ms = 0.0;
+    c->iter_launches = 0;
+  }
+  c->time_iters = mode;
+  if (ms) *ms = c->iter_ms;
+  if (launches) *launches = c->iter_launches;
   return MLMCP_OK;
 }
 

@@ -68,6 +68,11 @@ struct Ctx {
   // executable graph (updated in place from call to call)
   cudaStream_t cap_stream[3] = {nullptr, nullptr, nullptr};
   cudaGraphExec_t step_exec = nullptr;
+  // mlmcp_stream_timing: device time of the PCG-iteration launches
+  int time_iters = 0;
+  double iter_ms = 0.0;
+  int64_t iter_launches = 0;
+  cudaEvent_t iter_ev[2] = {nullptr, nullptr};
 };
 
 void set_error(const std::string& msg);

@@ -1481,14 +1481,22 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     if (const int rc = launch_init(stream, step)) return rc;
     int done_iters = 0;
     for (;;) {
+      if (ctx->time_iters) MLMCP_CUDA_CHECK(cudaEventRecord(ctx->iter_ev[0], stream));
       for (int c = 0; c < chunk; ++c) {
         const int rc = launch_iteration(stream);
         if (rc != MLMCP_OK) return rc;
       }
+      if (ctx->time_iters) MLMCP_CUDA_CHECK(cudaEventRecord(ctx->iter_ev[1], stream));
       done_iters += chunk;
       MLMCP_CUDA_CHECK(cudaMemcpyAsync(hc, a.w.counters, 2 * sizeof(int32_t),
                                        cudaMemcpyDeviceToHost, stream));
       MLMCP_CUDA_CHECK(cudaStreamSynchronize(stream));
+      if (ctx->time_iters) {
+        float ms = 0.0f;
+        MLMCP_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->iter_ev[0], ctx->iter_ev[1]));
+        ctx->iter_ms += ms;
+        ctx->iter_launches += chunk;
+      }
       if (hc[1] >= hc[0]) break;
       chunk = 2;
     }

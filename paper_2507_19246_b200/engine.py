@@ -108,6 +108,15 @@ class DeviceSystem:
         check(self.lib.mlmcp_ctx_set_path(self.ctx, code), "mlmcp_ctx_set_path")
         self._path = code
 
+    def stream_timing(self, mode: int) -> tuple[float, int]:
+        """mlmcp_stream_timing: (ms, launches) of the streaming PCG-iteration
+        launches; mode 1 resets and starts, 0 stops."""
+        ms = ctypes.c_double()
+        n = ctypes.c_int64()
+        check(self.lib.mlmcp_stream_timing(self.ctx, int(mode), ctypes.byref(ms), ctypes.byref(n)),
+              "mlmcp_stream_timing")
+        return float(ms.value), int(n.value)
+
     @property
     def direct(self) -> bool:
         return self._path == 3 or (self._path == 0 and self.n_rows <= _lib.DIRECT_MAX_ROWS)
