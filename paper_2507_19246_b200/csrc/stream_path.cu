@@ -708,8 +708,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   static_assert(kTHalo <= kTW * (kTH / kTR), "one halo point per thread");
   extern __shared__ __align__(16) double ism[];
   double* Ac = ism;                 // [4][kTCN]
-  double* Mc = Ac + 4 * kTCN;       // [4][kTCN]
-  double* XV = Mc + 4 * kTCN;       // x_0 with halo
+  double* XV = Ac + 4 * kTCN;       // x_0 with halo
   double* AV = XV + kTV;            // a_n with halo
   __shared__ double red[2 * 4 * 32];
   const int t = blockIdx.y;
@@ -731,10 +730,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
     const int lc = (ly + 1) * kTCL + cx + 1, lv = (ly + 1) * kTLD + cx + 1;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
-      cp8(&Mc[j * kTCN + lc], Ms + j * N + i, ok);
-    }
+    for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
     cp8(&XV[lv], X + i, ok);
     cp8(&AV[lv], An + i, ok);
   }
@@ -746,10 +742,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
     const int lc = (ly + 1) * kTCL + lx + 1;
 #pragma unroll
-    for (int q = 1; q < 4; ++q) {
-      cp8(&Ac[q * kTCN + lc], As + q * N + j, ok);
-      cp8(&Mc[q * kTCN + lc], Ms + q * N + j, ok);
-    }
+    for (int q = 1; q < 4; ++q) cp8(&Ac[q * kTCN + lc], As + q * N + j, ok);
   }
   if (threadIdx.x < kTHalo) {
     int lx, ly;
@@ -785,14 +778,21 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     if (!(colok && gy < a.gh)) continue;
     const int64_t i = (int64_t)gy * a.wd + gx;
     const int lc = (ly + 1) * kTCL + cx + 1, b = (ly + 1) * kTLD + cx + 1;
-    // coefficient of direction SW, S, W, C, E, N, NE
+    // coefficient of direction SW, S, W, C, E, N, NE (A staged; M from global:
+    // own C, E, N, NE and the E, N, NE of the west / south / south-west points)
     const int cofs[7] = {3 * kTCN + lc - kTCL - 1, 2 * kTCN + lc - kTCL, kTCN + lc - 1, lc,
                          kTCN + lc, 2 * kTCN + lc, 3 * kTCN + lc};
     const int vofs[7] = {b - kTLD - 1, b - kTLD, b - 1, b, b + 1, b + kTLD, b + kTLD + 1};
+    const bool w_ = gx > 0, s_ = gy > 0;
+    const double mco[7] = {(w_ && s_) ? __ldg(Ms + 3 * N + i - a.wd - 1) : 0.0,
+                           s_ ? __ldg(Ms + 2 * N + i - a.wd) : 0.0,
+                           w_ ? __ldg(Ms + N + i - 1) : 0.0,
+                           __ldg(Ms + i), __ldg(Ms + N + i), __ldg(Ms + 2 * N + i),
+                           __ldg(Ms + 3 * N + i)};
     double mx = 0.0, ax = 0.0;
 #pragma unroll
     for (int d = 0; d < 7; ++d) {
-      mx = fma(Mc[cofs[d]], AV[vofs[d]], mx);
+      mx = fma(mco[d], AV[vofs[d]], mx);
       ax = fma(Ac[cofs[d]], XV[vofs[d]], ax);
     }
     const double bv = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, prof[r])));
@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
 
 template <int kTH, int kTR>
 constexpr size_t tile_init_smem() {
-  return sizeof(double) * (8 * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
+  return sizeof(double) * (4 * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
 }
 
 
@@ -1342,7 +1342,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
       tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else if (a.tile) {
-      tile_init_kernel<16, 4, 2><<<grid_tiles2, 256, tile_init_smem<16, 4>(), s>>>(a, step);
+      tile_init_kernel<16, 4, 3><<<grid_tiles2, 256, tile_init_smem<16, 4>(), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else {
       step_init_kernel<<<grid_rows, blk, 0, s>>>(a, step);
@@ -1356,7 +1356,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<8, 2, 4>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)tile_init_smem<8, 2>()));
-      MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<16, 4, 2>,
+      MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<16, 4, 3>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)tile_init_smem<16, 4>()));
       attr = true;

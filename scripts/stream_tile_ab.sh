@@ -1,7 +1,6 @@
-for l in 0 1 0 1; do
-  MLMCP_LSGUESS=$l timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-streaming --no-e2e > gpurun_out/bench_ls$l.log 2>/dev/null
-  echo ls=$l; tail -1 gpurun_out/bench_ls$l.log | python -c "import json,sys; d=json.loads(sys.stdin.read()); print(d['ms_per_step'], d['value'], d['detail'], d['config']['parareal_k'])"
-done
-timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo pytest=$?
-tail -2 gpurun_out/pytest_gpu.log
-python scripts/defect_parity.py 2>&1 | tail -4
+timeout 900 python -m pytest tests/test_gpu_mlmc.py tests/test_gpu_fe_parity.py -x -q -k "streaming or stream or cfg2 or cfg4 or ragged or agree" > gpurun_out/pt_stream1.log 2>&1; echo pytest=$?
+tail -2 gpurun_out/pt_stream1.log
+export MLMCP_STREAM_IMPL=4
+timeout 300 python scripts/microbench_stream.py 2 64 64 2
+timeout 300 python scripts/microbench_stream.py 4 16 32 2
+ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/stream_launches_v15.csv python scripts/microbench_stream.py 2 64 8 0 > /dev/null 2>&1; echo l=$?
