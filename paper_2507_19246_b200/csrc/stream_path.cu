@@ -46,6 +46,13 @@ __constant__ double c_extrap[8][8] = {
     {6, -15, 20, -15, 6, -1, 0, 0},
     {7, -21, 35, -35, 21, -7, 1, 0},
     {8, -28, 56, -70, 56, -28, 8, -1}};
+// least-squares degree-6 fit through y_n .. y_{n-7}, extrapolated one step:
+// with the steady-state predictor (rtol 1e-14) it beats the exact order-7
+// polynomial (sum |w| 69 vs 255), numpy model of config 2: 4.4 -> 3.6
+// iterations per step
+__constant__ int c_ls_on = 1;   // MLMCP_LSGUESS=0 disables (A/B)
+__constant__ double c_ls68[8] = {49.0 / 8, -119.0 / 8, 133.0 / 8, -35.0 / 8,
+                                 -77.0 / 8, 91.0 / 8, -41.0 / 8, 7.0 / 8};
 
 struct Work {
   double* ring;    // [kRingS][T][N]
@@ -318,7 +325,10 @@ __global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step_arg) 
   // polynomial extrapolation of order p through y_n .. y_{n-p} (high orders pay:
   // the states are smooth in time)
   double g = yn;
-  if (p > 0) {
+  if (pred && p >= 7 && c_ls_on) {
+    g = c_ls68[0] * yn;
+    for (int j = 1; j < 8; ++j) g = fma(c_ls68[j], past(j), g);
+  } else if (p > 0) {
     g = c_extrap[p][0] * yn;
     for (int j = 1; j <= p; ++j) g = fma(c_extrap[p][j], past(j), g);
   }
@@ -1548,6 +1558,15 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   a.it_cond = 0;
   a.use_cond = 0;
   a.order = stream_order();
+  static bool ls_set = false;
+  if (!ls_set) {
+    const char* l = getenv("MLMCP_LSGUESS");
+    if (l) {
+      const int v = atoi(l) != 0;
+      cudaMemcpyToSymbol(c_ls_on, &v, sizeof(int));
+    }
+    ls_set = true;
+  }
   a.w = w;
   return a;
 }
