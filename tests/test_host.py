@@ -167,3 +167,17 @@ def test_toy_estimator_constant_qoi():
     fam = toy_family(make_hierarchy([0.1, 0.05]), nominal=2.0, halfwidth=0.0)
     res = mlmc_estimate(fam, policy=FixedSamples((5, 5)), seed=0)
     assert abs(res.expectation - 2.0 * 1.05) <= 1e-15 * 2.1 and res.rmse_estimate == 0.0
+
+
+def test_bench_reports_one_workload_for_both_arms_and_sm_internal_roofline():
+    """bench.py: the reference arm and the GPU arm name the same workload;
+    the SM-internal utilisation of the headline kernel comes from the
+    committed ncu summary that profiles/ncu_top_kernel.json points to."""
+    import bench
+    from paper_2507_19246_b200.configs import get_config
+    cfg = get_config(1)
+    w = bench.workload_name(1, cfg, list(cfg.samples), cfg.parareal_config())
+    assert w.startswith("cfg1: 32x32") and "N_l=[512, 128, 32]" in w and "Parareal M=16" in w
+    sm = bench.ncu_sm_internal()
+    assert sm is not None and 0.0 < sm["fp64_pipe_active"] < 1.0 and 0.0 < sm["issue_active"] < 1.0
+    assert bench.ncu_traffic() > 0
