@@ -280,6 +280,7 @@ __global__ void copy_in_kernel(SArgs a) {
   if (i < a.N) {
     const double x = a.xbuf[tk.x_in + i];
     a.w.X[(int64_t)t * a.N + i] = x;
+    a.w.Wv[(int64_t)t * a.N + i] = x;   // a_0 for the tile path's step start
     if (tk.traj >= 0) a.xbuf[tk.traj + i] = x;
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -731,8 +732,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   const bool colok = gx < a.wd;
   const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
   const double* Ms = a.w.A + ((int64_t)a.S + tk.sample) * 4 * N;
-  const double* X = a.w.X + o;
-  const double* An = a.w.Wv + o;
+  const double* An = a.w.Wv + o;   // a_n (step_end / copy_in)
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const int ly = sy * kTR + r;
@@ -741,7 +741,6 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const int lc = (ly + 1) * kTCL + cx + 1, lv = (ly + 1) * kTLD + cx + 1;
 #pragma unroll
     for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
-    cp8(&XV[lv], X + i, ok);
     cp8(&AV[lv], An + i, ok);
   }
   if (threadIdx.x < kTH + 1 + kTW) {
@@ -765,10 +764,51 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
     const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
     const int lv = (ly + 1) * kTLD + lx + 1;
-    cp8(&XV[lv], X + j, ok);
     cp8(&AV[lv], An + j, ok);
   }
   cp_commit();
+  // initial guess x_0 (the guess kernel's arithmetic, folded in) for the own
+  // points and the halo frame; a_n comes from Wv (written by step_end / copy_in),
+  // so no tile reads what another tile writes (X, ring slot step & 7)
+  __shared__ double sc[4];
+  const bool pred = a.xss != nullptr && tk.ss_slot >= 0 &&
+                    !(tk.flags & MLMCP_TASK_NO_EXTRAPOLATION);
+  if (threadIdx.x == 0 && pred) {
+    const int64_t gg = tk.k0 + step + 1;
+    sincos(__dmul_rn(a.omega, grid_time(tk.t_base, gg, tk.dt)), &sc[0], &sc[1]);
+    sincos(__dmul_rn(a.omega, grid_time(tk.t_base, gg - 1, tk.dt)), &sc[2], &sc[3]);
+  }
+  __syncthreads();
+  const int pord = (tk.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : min(step, a.order);
+  const int64_t TN = (int64_t)a.T * N;
+  const double* Xs = pred ? a.xss + (int64_t)tk.ss_slot * 2 * N : nullptr;
+  // x_0 at task point j from a_n (an); y_n joins the ring when `own`
+  auto guess_at = [&](int64_t j, double an, bool own) {
+    double sst = 0.0, ssn = 0.0;
+    if (pred) {
+      const double xr = __ldg(Xs + j), xi = __ldg(Xs + N + j);
+      sst = fma(xr, sc[0], xi * sc[1]);
+      ssn = fma(xr, sc[2], xi * sc[3]);
+    }
+    const double yn = an - ssn;
+    double pv[kRingS];   // past transients, loaded together (independent loads)
+#pragma unroll
+    for (int q = 1; q < kRingS; ++q)
+      pv[q] = q <= pord ? __ldcg(a.w.ring + (int64_t)((step - q) & (kRingS - 1)) * TN + o + j) : 0.0;
+    double gv = yn;
+    if (pred && pord >= 7 && c_ls_on) {
+      gv = c_ls68[0] * yn;
+#pragma unroll
+      for (int q = 1; q < 8; ++q) gv = fma(c_ls68[q], pv[q], gv);
+    } else if (pord > 0) {
+      gv = c_extrap[pord][0] * yn;
+#pragma unroll
+      for (int q = 1; q < kRingS; ++q)
+        if (q <= pord) gv = fma(c_extrap[pord][q], pv[q], gv);
+    }
+    if (own) a.w.ring[(int64_t)(step & (kRingS - 1)) * TN + o + j] = yn;
+    return gv + sst;
+  };
   const int64_t g = tk.k0 + step + 1;
   const double sf = sin(__dmul_rn(a.omega, grid_time(tk.t_base, g, tk.dt)));
   double prof[kTR], dv[kTR];
@@ -779,7 +819,34 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     prof[r] = ok ? __ldg(a.profile + i) : 0.0;
     dv[r] = ok ? __ldg(a.w.dinv + (int64_t)tk.sample * N + i) : 0.0;
   }
-  cp_wait_all();
+  cp_wait_all();   // own and halo a_n were copied by this thread
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const int ly = sy * kTR + r;
+    const bool ok = colok && gy0 + r < a.gh;
+    const int lv = (ly + 1) * kTLD + cx + 1;
+    double x0 = 0.0;
+    if (ok) {
+      const int64_t i = (int64_t)(gy0 + r) * a.wd + gx;
+      x0 = guess_at(i, AV[lv], true);
+      a.w.X[o + i] = x0;
+    }
+    XV[lv] = x0;
+  }
+  if (threadIdx.x < kTHalo) {
+    int lx, ly;
+    const int h = threadIdx.x;
+    if (h < kTW + 2) { lx = h - 1; ly = -1; }
+    else if (h < 2 * (kTW + 2)) { lx = h - (kTW + 2) - 1; ly = kTH; }
+    else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
+    else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    const int lv = (ly + 1) * kTLD + lx + 1;
+    double x0 = 0.0;
+    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh)
+      x0 = guess_at((int64_t)hy * a.wd + hx, AV[lv], false);
+    XV[lv] = x0;
+  }
   __syncthreads();
   double bb = 0.0;
 #pragma unroll
@@ -1193,6 +1260,7 @@ __global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step_ar
   if (mode == 0) {
     if (step >= tk.n_steps || code_now) return;
     if (tk.traj >= 0 && i < a.N) a.xbuf[tk.traj + (int64_t)(step + 1) * a.N + i] = X[i];
+    if (a.tile && i < a.N) a.w.Wv[(int64_t)t * a.N + i] = X[i];   // a_n of the next step
     const int64_t g = tk.k0 + step + 1;
     energy = tk.qoi_mode == MLMCP_QOI_SUM_ENERGY && g > tk.qoi_from && tk.qoi_slot >= 0;
   } else {
@@ -1429,7 +1497,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
         rc = cuda_fail(cudaGetLastError(), "cudaMemsetAsync");
         break;
       }
-      guess_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1);
+      if (!a.tile) guess_kernel<<<grid_rows, blk, 0, cs[1]>>>(a, -1);
       rc = launch_init(cs[1], -1);
       if (rc != MLMCP_OK) break;
       iter_begin_kernel<<<1, 1, 0, cs[1]>>>(a.w.counters, h_it);
@@ -1486,8 +1554,10 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   int chunk = 4;
   for (int step = 0; step < n_steps_max; ++step) {
     MLMCP_CUDA_CHECK(cudaMemsetAsync(a.w.counters, 0, 2 * sizeof(int32_t), stream));
-    guess_kernel<<<grid_rows, blk, 0, stream>>>(a, step);
-    MLMCP_LAUNCH_CHECK("guess_kernel");
+    if (!a.tile) {   // the tile path's step start computes the guess itself
+      guess_kernel<<<grid_rows, blk, 0, stream>>>(a, step);
+      MLMCP_LAUNCH_CHECK("guess_kernel");
+    }
     if (const int rc = launch_init(stream, step)) return rc;
     int done_iters = 0;
     for (;;) {
