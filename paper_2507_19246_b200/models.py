@@ -220,6 +220,9 @@ class _BatchedFamily:
         levels = list(range(len(draws))) if levels is None else list(levels)
         top = len(self.hierarchy) - 1
         sizes = [len(d) for d in draws]
+        cap = self.max_samples_per_call(parareal_cfg)
+        if params_dev is None and cap is not None and sum(sizes) > cap:
+            return self._run_levels_chunked(draws, levels, parareal_cfg, cap)
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         nnz = sol.nnz
         M = torch.empty((int(offs[-1]), nnz), dtype=torch.float64, device=sol.device)
@@ -388,6 +391,30 @@ class _BatchedFamily:
         pr_q = self._finish_q(pr.qoi, cfg.dt_fine) if pr is not None else None
         self._last = (res, pr, M, K)
         return self._collect(levels, sizes, where, res, pr_level, pr, pr_q)
+
+    def _run_levels_chunked(self, draws, levels, parareal_cfg, cap: int):
+        """run_levels over batches larger than HBM holds: each level in calls of
+        <= cap samples (per-sample results are bitwise independent of the
+        batch), statuses checked per call, results concatenated."""
+        import torch
+        out = []
+        for d, lvl in zip(draws, levels):
+            parts = []
+            for c0 in range(0, len(d), cap):
+                parts.append(self.run_levels([d[c0:c0 + cap]], parareal_cfg, levels=[lvl])[0])
+                self.check_status()
+            if not parts:
+                parts.append(self.run_levels([d], parareal_cfg, levels=[lvl])[0])
+            cat = lambda xs: (torch.cat(xs) if all(isinstance(x, torch.Tensor) for x in xs)
+                              else xs[-1])
+            out.append(CoupledBatch(
+                level=lvl, q_l=cat([b.q_l for b in parts]), q_lm1=cat([b.q_lm1 for b in parts]),
+                k_used=cat([b.k_used for b in parts]),
+                iters=cat([b.iters for b in parts]) if parts[0].iters is not None else None,
+                wall_s=sum(b.wall_s for b in parts),
+                defects=cat([b.defects for b in parts]) if parts[0].defects is not None else None,
+                elapsed=[e for b in parts for e in b.elapsed]))
+        return out
 
     def run_levels_graphed(self, draws, parareal_cfg: PararealConfig | None = None,
                            params_dev=None):
