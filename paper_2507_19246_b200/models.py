@@ -220,8 +220,9 @@ class _BatchedFamily:
         levels = list(range(len(draws))) if levels is None else list(levels)
         top = len(self.hierarchy) - 1
         sizes = [len(d) for d in draws]
-        cap = self.max_samples_per_call(parareal_cfg)
-        if params_dev is None and cap is not None and sum(sizes) > cap:
+        cap_fn = getattr(self, "max_samples_per_call", None)
+        cap = cap_fn(parareal_cfg) if cap_fn is not None and params_dev is None else None
+        if cap is not None and sum(sizes) > cap:
             return self._run_levels_chunked(draws, levels, parareal_cfg, cap)
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         nnz = sol.nnz
