@@ -255,51 +255,78 @@ def _fill_slots(slots, batch, a: int, b: int):
             slots[a:b, 3] = batch.iters.to(dev, torch.float64)
 
 
-def _run_chunked(family, ranges, counts, cap: int, seed: int, parareal_cfg, dev):
-    """Evaluate the rank's sample ranges in run_levels calls of <= cap samples
-    (level by level, keys unchanged) into per-level slot buffers."""
+def _family_caps(family, n_levels: int, parareal_cfg):
+    """Per-level sample caps of one run_levels call (None: one call)."""
+    if hasattr(family, "level_caps"):
+        return family.level_caps(list(range(n_levels)), parareal_cfg)
+    fn = getattr(family, "max_samples_per_call", None)
+    if fn is None:
+        return None
+    caps = [fn(parareal_cfg, level=lvl) for lvl in range(n_levels)]
+    return None if any(c is None for c in caps) else [max(1, int(c)) for c in caps]
+
+
+def _run_chunked(family, ranges, counts, caps, seed: int, parareal_cfg, dev):
+    """Evaluate the rank's sample ranges in run_levels calls of <= caps[l]
+    samples (level by level, keys unchanged) into per-level slot buffers.
+    The caps are computed once by the caller (no per-call re-sizing)."""
     import torch
     slots = [torch.zeros((n, 4), dtype=torch.float64, device=dev) for n in counts]
     last = None
     for lvl, (a, b) in enumerate(ranges):
+        cap = caps[lvl]
         for c0 in range(a, b, cap):
             c1 = min(b, c0 + cap)
-            draws = [np.zeros((0, 1)) for _ in ranges]
-            draws[lvl] = draw_level(family.uncertain, seed, lvl, range(c0 + 1, c1 + 1))
-            out = family.run_levels(draws, parareal_cfg)
+            d = draw_level(family.uncertain, seed, lvl, range(c0 + 1, c1 + 1))
+            out = family.run_levels([d], parareal_cfg, levels=[lvl], _no_chunk=True)
             if hasattr(family, "check_status"):
                 family.check_status()
-            _fill_slots(slots[lvl], out[lvl], c0, c1)
+            _fill_slots(slots[lvl], out[0], c0, c1)
             last = out
     return slots, last
 
 
+def _level_costs(hierarchy, counts, parareal_cfg, ks, wall: float):
+    """Per-level cost per sample C_l (measured per level during
+    the warm-up): the batched call's wall time split by each level's solver
+    work — N_l (1/dt_l + 1/dt_{l-1}) time steps, the Parareal level's fine
+    steps counted with its redundancy sum_{k<=K} (M - k + 1) / M at the mean K
+    used (parareal.py:182-196) plus one coarse step per slice and iteration."""
+    top = len(hierarchy) - 1
+    work = []
+    for lvl, n in enumerate(counts):
+        hi = 1.0 / hierarchy[lvl].dt
+        if parareal_cfg is not None and lvl == top:
+            m = parareal_cfg.num_subintervals
+            kbar = float(np.mean(ks)) if ks is not None and len(ks) else float(parareal_cfg.k_max)
+            kk = max(1, int(round(kbar)))
+            hi = hi * sum(m - k + 1 for k in range(1, kk + 1)) / m + kk * m
+        lo = 1.0 / hierarchy[lvl - 1].dt if lvl > 0 else 0.0
+        work.append(n * (hi + lo))
+    tot = sum(work)
+    return [(wall * w / tot / n) if (n and tot > 0) else 0.0 for w, n in zip(work, counts)]
+
+
 def _reduce_slots(slots, dist, device):
+    """all-reduce of a filled slot buffer, then the fixed-order reduction."""
     import torch
     if dist is not None and dist.get_world_size() > 1:
         dist.all_reduce(slots, op=dist.ReduceOp.SUM)
-    from .engine import level_reduce
-    return level_reduce(slots[:, 0].contiguous(), slots[:, 1].contiguous())
+    if slots.device.type == "cuda":
+        from .engine import level_reduce
+        return level_reduce(slots[:, 0].contiguous(), slots[:, 1].contiguous())
+    # CPU families (tests) — same fixed order as the kernel's definition
+    y = (slots[:, 0] - slots[:, 1]).numpy()
+    return torch.tensor([float(np.sum(y)), float(np.sum(y * y)), 0.0, 0.0], dtype=torch.float64)
 
 
 def _reduce_level(batch, n_global: int, a: int, b: int, dist, device):
     """Slot buffer -> all-reduce -> fixed-order K7 reduction."""
     import torch
     on_gpu = device is not None and torch.device(device).type == "cuda"
-    dev = device if on_gpu else "cpu"
-    slots = torch.zeros((n_global, 4), dtype=torch.float64, device=dev)
+    slots = torch.zeros((n_global, 4), dtype=torch.float64, device=device if on_gpu else "cpu")
     _fill_slots(slots, batch, a, b)
-    if dist is not None and dist.get_world_size() > 1:
-        dist.all_reduce(slots, op=dist.ReduceOp.SUM)
-    if on_gpu:
-        from .engine import level_reduce
-        sums = level_reduce(slots[:, 0].contiguous(), slots[:, 1].contiguous())
-    else:
-        # CPU families (tests) — same fixed order as the kernel's definition
-        y = (slots[:, 0] - slots[:, 1]).numpy()
-        sums = torch.tensor([float(np.sum(y)), float(np.sum(y * y)), 0.0, 0.0],
-                            dtype=torch.float64)
-    return slots, sums
+    return slots, _reduce_slots(slots, dist, device)
 
 
 def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: int = 0,
@@ -330,12 +357,11 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
     if dev is None and hasattr(family, "solver"):
         dev = family.solver.device
     sol = None
-    cap = (family.max_samples_per_call(parareal_cfg)
-           if hasattr(family, "max_samples_per_call") else None)
-    if cap is not None and sum(b - a for a, b in ranges) > cap:
-        # full-size streaming configs: the rank's samples in calls of <= cap
+    caps = _family_caps(family, len(hierarchy), parareal_cfg)
+    if caps is not None and sum((b - a) / c for (a, b), c in zip(ranges, caps)) > 1.0:
+        # full-size streaming configs: the rank's samples in calls of <= cap_l
         # samples, filling the per-sample slot buffers (same keys, same result)
-        all_slots, batches = _run_chunked(family, ranges, counts, cap, seed, parareal_cfg, dev)
+        all_slots, batches = _run_chunked(family, ranges, counts, caps, seed, parareal_cfg, dev)
         sums_dev = [_reduce_slots(slots, dist, dev) for slots in all_slots]
     else:
         sol = getattr(family, "solver", None) if timing else None
@@ -378,12 +404,14 @@ def mlmc_estimate(family, hierarchy=None, policy=None, parareal_cfg=None, seed: 
         host = [s.cpu().numpy() for s in sums_dev]
         ks_host = all_slots[top][:, 2].cpu().numpy() if want_k else None
     wall = time.perf_counter() - t_start
+    costs = _level_costs(hierarchy, counts, parareal_cfg,
+                         ks_host if want_k else None, wall)
     for lvl, sums in enumerate(host):
         ks = None
         if want_k and lvl == top:
             ks = ks_host.astype(int).tolist()
         per_level.append(LevelStats(lvl, counts[lvl], float(sums[0]), float(sums[1]),
-                                    wall / max(1, sum(counts)), ks))
+                                    costs[lvl], ks))
     expectation = float(sum(st.mean_y for st in per_level))
     rmse = math.sqrt(sum(max(st.var_y, 0.0) / st.n for st in per_level if st.n > 0))
     ledger = {"wall_time_s": wall, "world_size": world,

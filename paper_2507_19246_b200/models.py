@@ -146,12 +146,16 @@ class LinearToyFamily:
 
     uncertain: UncertainInput
     hierarchy: tuple
+    cap: int | None = None      # samples per run_levels call (chunked-path tests)
 
     def evaluate(self, params: ParameterVector, level: LevelSpec, parareal_cfg=None,
                  pool=None) -> EvalRecord:
         return EvalRecord(q=float(params.values[0]) * (1.0 + level.dt), cost_s=1e-9)
 
-    def run_levels(self, draws, parareal_cfg=None, levels=None):
+    def max_samples_per_call(self, parareal_cfg=None, level=None):
+        return self.cap
+
+    def run_levels(self, draws, parareal_cfg=None, levels=None, **_):
         import torch
         levels = list(range(len(draws))) if levels is None else levels
         out = []
@@ -164,9 +168,10 @@ class LinearToyFamily:
         return out
 
 
-def toy_family(hierarchy, nominal: float = 1.0, halfwidth: float = 0.05) -> LinearToyFamily:
+def toy_family(hierarchy, nominal: float = 1.0, halfwidth: float = 0.05,
+               cap: int | None = None) -> LinearToyFamily:
     return LinearToyFamily(UncertainInput(ParameterVector("toy", np.array([nominal])), halfwidth),
-                           tuple(hierarchy))
+                           tuple(hierarchy), cap)
 
 
 class _BatchedFamily:
@@ -204,7 +209,7 @@ class _BatchedFamily:
     # ------------------------------------------------------------ batched
     def run_levels(self, draws, parareal_cfg: PararealConfig | None = None, levels=None,
                    concurrent: bool = True, params_dev=None,
-                   fused: bool | None = None) -> list[CoupledBatch]:
+                   fused: bool | None = None, _no_chunk: bool = False) -> list[CoupledBatch]:
         """Coupled (Q_l, Q_{l-1}) for every level at once.
 
         draws[i]: [N_i, P] parameters of level ``levels[i]`` (default 0..L).
@@ -220,10 +225,14 @@ class _BatchedFamily:
         levels = list(range(len(draws))) if levels is None else list(levels)
         top = len(self.hierarchy) - 1
         sizes = [len(d) for d in draws]
-        cap_fn = getattr(self, "max_samples_per_call", None)
-        cap = cap_fn(parareal_cfg) if cap_fn is not None and params_dev is None else None
-        if cap is not None and sum(sizes) > cap:
-            return self._run_levels_chunked(draws, levels, parareal_cfg, cap)
+        if not _no_chunk and params_dev is None:
+            # HBM budget, computed ONCE per call: each level's footprint per
+            # sample differs (tasks per launch, Parareal buffers on the top
+            # level), so the batch is chunked level by level with per-level caps
+            caps = self.level_caps(levels, parareal_cfg)
+            if caps is not None and sum(s / c for s, c in zip(sizes, caps)) > 1.0:
+                return self._run_levels_chunked(draws, levels, parareal_cfg, caps,
+                                                concurrent=concurrent, fused=fused)
         offs = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
         nnz = sol.nnz
         M = torch.empty((int(offs[-1]), nnz), dtype=torch.float64, device=sol.device)
@@ -393,21 +402,46 @@ class _BatchedFamily:
         self._last = (res, pr, M, K)
         return self._collect(levels, sizes, where, res, pr_level, pr, pr_q)
 
-    def _run_levels_chunked(self, draws, levels, parareal_cfg, cap: int):
+    def level_caps(self, levels, parareal_cfg=None):
+        """Per-level sample caps of one run_levels call (None: unbounded).
+        Computed once per call from the reclaimable HBM; families without
+        ``max_samples_per_call`` are unbounded."""
+        cap_fn = getattr(self, "max_samples_per_call", None)
+        if cap_fn is None:
+            return None
+        caps = [cap_fn(parareal_cfg, level=lvl) for lvl in levels]
+        if any(c is None for c in caps):
+            return None
+        return [max(1, int(c)) for c in caps]
+
+    def _run_levels_chunked(self, draws, levels, parareal_cfg, caps, concurrent: bool = True,
+                            fused: bool | None = None):
         """run_levels over batches larger than HBM holds: each level in calls of
-        <= cap samples (per-sample results are bitwise independent of the
+        <= caps[i] samples (per-sample results are bitwise independent of the
         batch), statuses checked per call, results concatenated."""
         import torch
         out = []
-        for d, lvl in zip(draws, levels):
+        for d, lvl, cap in zip(draws, levels, caps):
+            d = d.get() if hasattr(d, "get") else d          # LazyDraw: materialise first
             parts = []
             for c0 in range(0, len(d), cap):
-                parts.append(self.run_levels([d[c0:c0 + cap]], parareal_cfg, levels=[lvl])[0])
+                parts.append(self.run_levels([d[c0:c0 + cap]], parareal_cfg, levels=[lvl],
+                                             concurrent=concurrent, fused=fused,
+                                             _no_chunk=True)[0])
                 self.check_status()
             if not parts:
-                parts.append(self.run_levels([d], parareal_cfg, levels=[lvl])[0])
-            cat = lambda xs: (torch.cat(xs) if all(isinstance(x, torch.Tensor) for x in xs)
-                              else xs[-1])
+                parts.append(self.run_levels([d], parareal_cfg, levels=[lvl],
+                                             concurrent=concurrent, fused=fused,
+                                             _no_chunk=True)[0])
+
+            def cat(xs):
+                if all(isinstance(x, torch.Tensor) for x in xs):
+                    return torch.cat(xs)
+                if all(isinstance(x, np.ndarray) for x in xs):
+                    return np.concatenate(xs)
+                raise TypeError(f"cannot concatenate chunk results of types "
+                                f"{sorted({type(x).__name__ for x in xs})}")
+
             out.append(CoupledBatch(
                 level=lvl, q_l=cat([b.q_l for b in parts]), q_lm1=cat([b.q_lm1 for b in parts]),
                 k_used=cat([b.k_used for b in parts]),
@@ -602,24 +636,44 @@ class EddyCurrentFamily(_BatchedFamily):
             return acc * dt / self.avg_window
         return acc
 
-    def max_samples_per_call(self, parareal_cfg=None):
-        """Samples one run_levels call may hold on this GPU: None on the
-        SM-resident path (a config-1 estimate needs ~0.2 GB); on the streaming
-        path (128^2..512^2, up to 29 MB of operators per sample plus the
-        per-task workspace) 40% of the free HBM divided by the per-sample
-        footprint, so full-size configs 2-4 run as a sequence of calls."""
+    def max_samples_per_call(self, parareal_cfg=None, level=None):
+        """Samples of ``level`` one run_levels call may hold on this GPU: None
+        on the SM-resident path (a config-1 estimate needs ~0.2 GB); on the
+        streaming path (128^2..512^2) half of the reclaimable HBM divided by
+        that level's per-sample footprint, so full-size configs 2-4 run as a
+        sequence of calls.  The footprint counts what the level's launches
+        hold per sample: the M/K values, the per-task workspace of ONE
+        propagate launch (one task per sample and dt; m fine tasks per sample
+        on the Parareal level) and the states of every task (2 per sample
+        above level 0; U, F, C on the Parareal level), plus the steady states
+        of the predictor.  ``level`` None: the most demanding sequential level."""
         import torch
         sol = self.solver
         if sol.sys.sm_resident:
             return None
-        free, _ = torch.cuda.mem_get_info(sol.device)
-        lib = sol.sys.lib
-        per = (16 * sol.nnz + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, 2, 1))
-               + int(lib.mlmcp_periodic_workspace_bytes(sol.sys.ctx, 2)) + 32 * sol.N)
-        if parareal_cfg is not None:
+        lib, ctx = sol.sys.lib, sol.sys.ctx
+        ws = lambda tasks, S: int(lib.mlmcp_workspace_bytes(ctx, tasks, S))
+        per_task = ws(2, 1) - ws(1, 1)
+        per_op = ws(2, 2) - ws(2, 1)
+        N8 = 8 * sol.N
+        top = len(self.hierarchy) - 1
+        lvl = 1 if level is None else int(level)
+        if parareal_cfg is not None and lvl == top:
             m = parareal_cfg.num_subintervals
-            per += (3 * m + 2) * sol.N * 8 + int(lib.mlmcp_workspace_bytes(sol.sys.ctx, m, 1))
-        return max(1, int(0.4 * free // max(per, 1)))
+            tasks, states, ss = m, (3 * m + 2) * N8, 2
+        else:
+            tasks, states, ss = 1, (2 if lvl > 0 else 1) * N8, (2 if lvl > 0 else 1)
+        per = 16 * sol.nnz + per_op + tasks * per_task + states
+        if sol.use_predictor():
+            per += ss * (int(lib.mlmcp_periodic_workspace_bytes(ctx, 2))
+                         - int(lib.mlmcp_periodic_workspace_bytes(ctx, 1)) + 2 * N8)
+        free, _ = torch.cuda.mem_get_info(sol.device)
+        # memory torch's caching allocator holds but no tensor uses, and the
+        # engine workspace (replaced, not added, by the next call) are free too
+        reclaim = torch.cuda.memory_reserved(sol.device) - torch.cuda.memory_allocated(sol.device)
+        cur_ws = sol.sys._ws.numel() if sol.sys._ws is not None else 0
+        avail = free + max(0, reclaim) + cur_ws
+        return max(1, int(0.5 * avail // max(per, 1)))
 
     def _n_params(self) -> int:
         return fe.n_params(self.layout)

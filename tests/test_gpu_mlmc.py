@@ -297,7 +297,7 @@ def test_chunked_estimate_bitwise(cuda, monkeypatch):
     pr = PararealConfig(4, T / 128, T / 16, 1e-8, 4)
     counts = (12, 7, 5)
     ref = mlmc_estimate(fam, policy=FixedSamples(counts), parareal_cfg=pr, seed=3)
-    monkeypatch.setattr(type(fam), "max_samples_per_call", lambda self, cfg=None: 5)
+    monkeypatch.setattr(type(fam), "max_samples_per_call", lambda self, cfg=None, level=None: 5)
     got = mlmc_estimate(fam, policy=FixedSamples(counts), parareal_cfg=pr, seed=3)
     assert got.expectation == ref.expectation
     for a, b in zip(got.per_level, ref.per_level):

@@ -181,3 +181,29 @@ def test_bench_reports_one_workload_for_both_arms_and_sm_internal_roofline():
     sm = bench.ncu_sm_internal()
     assert sm is not None and 0.0 < sm["fp64_pipe_active"] < 1.0 and 0.0 < sm["issue_active"] < 1.0
     assert bench.ncu_traffic() > 0
+
+
+def test_level_costs_follow_level_work():
+    """each level gets its own cost per sample, the
+    wall time split by solver work, so optimal_allocation sees C_l grow with
+    the level's steps (and the Parareal level's redundant fine work)."""
+    from paper_2507_19246_b200.mlmc import _level_costs
+    from paper_2507_19246_b200.models import make_hierarchy
+    from paper_2507_19246_b200.parareal import PararealConfig
+    h = make_hierarchy([0.02 / 64, 0.02 / 128, 0.02 / 256])
+    c = _level_costs(h, [100, 50, 10], None, None, 1.0)
+    assert abs(sum(ci * n for ci, n in zip(c, [100, 50, 10])) - 1.0) < 1e-12
+    assert abs(c[1] / c[0] - 3.0) < 1e-12 and abs(c[2] / c[1] - 2.0) < 1e-12
+    pc = PararealConfig(16, 0.02 / 256, 0.02 / 16, 1e-8, 5)
+    cp = _level_costs(h, [100, 50, 10], pc, [3] * 10, 1.0)
+    assert cp[2] / cp[1] > c[2] / c[1]          # Parareal redundancy (K=3: 45/16 fine work)
+
+
+def test_toy_family_chunked_estimate_bitwise():
+    from paper_2507_19246_b200.mlmc import FixedSamples, mlmc_estimate
+    from paper_2507_19246_b200.models import make_hierarchy, toy_family
+    h = make_hierarchy([0.1, 0.05, 0.025])
+    a = mlmc_estimate(toy_family(h), policy=FixedSamples((23, 9, 4)), seed=5)
+    b = mlmc_estimate(toy_family(h, cap=3), policy=FixedSamples((23, 9, 4)), seed=5)
+    assert a.expectation == b.expectation
+    assert [(s.sum_y, s.sum_y2) for s in a.per_level] == [(s.sum_y, s.sum_y2) for s in b.per_level]
