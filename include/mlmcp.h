@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 8
+#define MLMCP_ABI_VERSION 9
 
 /* return codes */
 #define MLMCP_OK 0
@@ -136,6 +136,29 @@ int mlmcp_ctx_info(const mlmcp_ctx* ctx, int* max_row_nnz, int* small_max_rows);
 int mlmcp_ctx_set_assembly(mlmcp_ctx* ctx, int n_elem, int n_contrib,
                            const int32_t* cptr, const int32_t* elem,
                            const double* mw, const double* kw);
+/* Region-linear operator (HOST arrays, copied; structured 2D grids only):
+ * for a material layout that is constant per region, the operator
+ * coefficients of interior point p are sums over the six triangles around it
+ * (their regions packed 4 bits each in code[p], in increasing element order):
+ *     M_c(p) = sum_e sigma_{r(e)} mw[c][e],  K_c(p) = sum_e nu_{r(e)} kw[c][e]
+ * for c = C (mw[0..5]), E (mw[6..7]: triangles 2, 4), N (mw[8..9]: 3, 5),
+ * NE (mw[10..11]: 4, 5), in the gather map's summation order (the same
+ * doubles mlmcp_assemble writes).  With it the streaming tile kernels compute
+ * A = M + dt K on the fly from the per-sample region parameters passed to
+ * mlmcp_propagate / mlmcp_parareal_coarse instead of streaming the operator
+ * (HBM bytes per PCG iteration 112 -> 80 per point).  n_regions = 0
+ * unregisters.  Replaces the per-sample operator formation models.py:284-286
+ * / timeint.py:65 for region-constant materials. */
+int mlmcp_ctx_set_region_grid(mlmcp_ctx* ctx, int n_regions, const uint32_t* code,
+                              const double* mw, const double* kw);
+/* Per-sample region parameters from drawn parameters params_d[S][2R] =
+ * (nu_0..nu_{R-1}, sigma_0..sigma_{R-1}) (models.py:69-74 keeps them
+ * positive; mask_d[R] zeroes the non-conducting regions after the draw):
+ * sigma_d[S][R] = sigma * mask (for mlmcp_assemble, may be NULL) and
+ * rp_d[S][R][2] = (sigma * mask, nu) (for the region-linear operator, may be
+ * NULL).  Stream-ordered. */
+int mlmcp_region_params(int S, int R, const double* params_d, const double* mask_d,
+                        double* sigma_d, double* rp_d, void* stream);
 /* Force a path: 0 auto, 1 SM-resident (PCG), 2 streaming (PCG), 3 direct
  * (dense LU with partial pivoting per task, one thread per task, n_rows <=
  * MLMCP_DIRECT_MAX_ROWS; the only path for non-symmetric M + dt K, e.g. the
@@ -175,9 +198,12 @@ size_t mlmcp_workspace_bytes(const mlmcp_ctx* ctx, int n_tasks, int S);
  * the streaming path leaves them untouched.  QoI modes ELECTRICAL / JOULE are
  * supported on the SM-resident and direct paths (EINVAL on streaming). */
 
+/* region_params_d (optional, may be NULL): [S][R][2] region parameters of
+ * the S operators (mlmcp_region_params) when the context has a region grid:
+ * the streaming tile kernels then compute the operator on the fly. */
 int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                     int S, const double* M_d, const double* K_d,
-                    const double* profile_d, double omega, double rtol,
+                    const double* region_params_d, const double* profile_d, double omega, double rtol,
                     int max_it, const double* xss_d, double* xbuf_d,
                     double* qoi_d, int32_t* iters_d, int32_t* status_d,
                     const int32_t* active_d, int64_t* elapsed_ns_d,
@@ -215,7 +241,7 @@ int mlmcp_periodic_state(mlmcp_ctx* ctx, int n, const int32_t* sample_d,
  * dt_c (mlmcp_periodic_state) for the initial-guess predictor. */
 int mlmcp_parareal_coarse(mlmcp_ctx* ctx, int S, int k, int m,
                           const double* M_d, const double* K_d,
-                          const double* profile_d, double omega, double dt_c,
+                          const double* region_params_d, const double* profile_d, double omega, double dt_c,
                           double t0, const int64_t* slice_k0_d,
                           const int32_t* slice_steps_d, double rtol,
                           int max_it, double* U_d, const double* F_d,

@@ -66,14 +66,19 @@ def _reference():
     cache = {}
 
     def factorize(model, dt):
+        # keyed by the model OBJECT (kept alive in the entry): an id() alone can
+        # be reused by the next sample's model once the previous one is freed
         key = (id(model), float(dt))
-        lu = cache.get(key)
-        if lu is None:
-            if len(cache) > 8:
-                cache.clear()
-            lu = splu(sp.csc_matrix(model.mass + dt * model.stiffness))
-            cache[key] = lu
+        hit = cache.get(key)
+        if hit is not None and hit[0] is model:
+            return hit[1]
+        if len(cache) > 8:
+            cache.clear()
+        lu = splu(sp.csc_matrix(model.mass + dt * model.stiffness))
+        cache[key] = (model, lu)
         return lu
+
+    _STATE["cache"] = cache
 
     timeint._factorize = factorize
     timeint.lu_solve = lambda lu, rhs: lu.solve(rhs)
@@ -115,6 +120,7 @@ def _coupled_job(args):
     cfg_i, level, k = args
     from oracle import mlmc_oracle as mo
     timeint, parareal = _reference()
+    _STATE["cache"].clear()
     cfg = mo.CONFIGS[cfg_i]
     prob = _problem(cfg)
     p = mo.draw(cfg, 0, level, k)

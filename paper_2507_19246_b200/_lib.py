@@ -35,7 +35,7 @@ STATUS_INTS = 4
 
 QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2, 3, 4
 TASK_NO_EXTRAPOLATION = 1
-ABI_VERSION = 8
+ABI_VERSION = 9
 DIRECT_MAX_ROWS = 4
 
 # mlmcp_task (96 bytes, natural alignment)
@@ -75,7 +75,8 @@ class PararealBatch(ctypes.Structure):
 EXPORTS = (
     "mlmcp_abi_version", "mlmcp_last_error", "mlmcp_launch_count",
     "mlmcp_ctx_create", "mlmcp_ctx_destroy", "mlmcp_ctx_info", "mlmcp_ctx_set_assembly",
-    "mlmcp_ctx_set_path", "mlmcp_stream_timing", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
+    "mlmcp_ctx_set_path", "mlmcp_ctx_set_region_grid", "mlmcp_region_params",
+    "mlmcp_stream_timing", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
     "mlmcp_propagate", "mlmcp_periodic_workspace_bytes", "mlmcp_periodic_state", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
     "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce", "mlmcp_draw_uniform",
     "mlmcp_draw_uniform_host", "mlmcp_fused_workspace_bytes", "mlmcp_run_fused",
@@ -107,13 +108,15 @@ _SIGS = {
     "mlmcp_kl_sigma": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P, F64, F64,
                                       P, P]),
     "mlmcp_workspace_bytes": (SZ, [P, ctypes.c_int, ctypes.c_int]),
-    "mlmcp_propagate": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_int, P, P, P, F64, F64,
+    "mlmcp_propagate": (ctypes.c_int, [P, ctypes.c_int, P, ctypes.c_int, P, P, P, P, F64, F64,
                                        ctypes.c_int, P, P, P, P, P, P, P, P, SZ, P]),
+    "mlmcp_ctx_set_region_grid": (ctypes.c_int, [P, ctypes.c_int, P, P, P]),
+    "mlmcp_region_params": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, P, P, P, P]),
     "mlmcp_periodic_workspace_bytes": (SZ, [P, ctypes.c_int]),
     "mlmcp_periodic_state": (ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_int, P, P, P, F64,
                                             F64, ctypes.c_int, P, P, P, SZ, P]),
     "mlmcp_parareal_coarse": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
-                                             P, F64, F64, F64, P, P, F64, ctypes.c_int, P, P,
+                                             P, P, F64, F64, F64, P, P, F64, ctypes.c_int, P, P,
                                              P, P, P, P, P, P, P, SZ, P]),
     "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, P, F64, P, P, P, P]),

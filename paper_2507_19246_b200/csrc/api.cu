@@ -177,6 +177,19 @@ __global__ void level_reduce_kernel(int n, const double* __restrict__ ql,
   }
 }
 
+// sigma[s][r] = params[s][R + r] * mask[r]; rp[s][r] = (sigma[s][r], params[s][r])
+__global__ void region_params_kernel(int S, int R, const double* __restrict__ params,
+                                     const double* __restrict__ mask, double* sigma, double* rp) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= S * R) return;
+  const int s = i / R, r = i % R;
+  const double sg = __dmul_rn(params[(int64_t)s * 2 * R + R + r], mask ? mask[r] : 1.0);
+  if (sigma) sigma[(int64_t)s * R + r] = sg;
+  if (rp) {
+    rp[((int64_t)s * R + r) * 2] = sg;
+    rp[((int64_t)s * R + r) * 2 + 1] = params[(int64_t)s * 2 * R + r];
+  }
+}
 }  // namespace
 }  // namespace mlmcp
 
@@ -361,6 +374,7 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->celem);
   cudaFree(c->cmw);
   cudaFree(c->ckw);
+  cudaFree(c->rcode);
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   for (cudaEvent_t e : c->iter_ev)
@@ -430,6 +444,49 @@ int mlmcp_ctx_set_assembly(mlmcp_ctx* c, int n_elem, int n_contrib, const int32_
   return rc;
 }
 
+int mlmcp_ctx_set_region_grid(mlmcp_ctx* c, int n_regions, const uint32_t* code,
+                              const double* mw, const double* kw) {
+  if (c == nullptr) return einval("null context");
+  if (n_regions == 0) {   // unregister
+    cudaSetDevice(c->device);
+    cudaFree(c->rcode);
+    c->rcode = nullptr;
+    c->rR = 0;
+    return MLMCP_OK;
+  }
+  if (n_regions < 1 || n_regions > 16 || !code || !mw || !kw)
+    return einval("region grid: need 1..16 regions and code / weight arrays");
+  if (c->cl_wd == 0 || (int64_t)c->cl_wd * c->cl_h != c->n)
+    return einval("region grid: the pattern is not a structured 2D grid");
+  for (int i = 0; i < c->n; ++i)
+    for (int e = 0; e < 6; ++e)
+      if ((int)((code[i] >> (4 * e)) & 15u) >= n_regions)
+        return einval("region grid: triangle region index out of range");
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  cudaFree(c->rcode);
+  c->rcode = nullptr;
+  MLMCP_CUDA_CHECK(cudaMalloc(&c->rcode, sizeof(uint32_t) * (size_t)c->n));
+  MLMCP_CUDA_CHECK(cudaMemcpy(c->rcode, code, sizeof(uint32_t) * (size_t)c->n,
+                              cudaMemcpyHostToDevice));
+  for (int i = 0; i < 12; ++i) {
+    c->rmw[i] = mw[i];
+    c->rkw[i] = kw[i];
+  }
+  c->rR = n_regions;
+  return MLMCP_OK;
+}
+
+
+int mlmcp_region_params(int S, int R, const double* params, const double* mask, double* sigma,
+                        double* rp, void* stream) {
+  if (S < 0 || R < 1 || R > 16 || !params || (!sigma && !rp)) return einval("bad region parameters");
+  if (S == 0) return MLMCP_OK;
+  region_params_kernel<<<(S * R + 255) / 256, 256, 0, (cudaStream_t)stream>>>(S, R, params, mask,
+                                                                            sigma, rp);
+  MLMCP_LAUNCH_CHECK("region_params_kernel");
+  return MLMCP_OK;
+}
+
 int mlmcp_assemble(mlmcp_ctx* c, int S, const double* sigma, int64_t sstride,
                    const int32_t* sidx, const double* nu, int64_t nstride, const int32_t* nidx,
                    double* M, double* K, void* stream) {
@@ -468,7 +525,8 @@ size_t mlmcp_workspace_bytes(const mlmcp_ctx* c, int n_tasks, int S) {
 }
 
 int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
-                    const double* K, const double* profile, double omega, double rtol,
+                    const double* K, const double* rpar, const double* profile, double omega,
+                    double rtol,
                     int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
                     int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
                     size_t ws_bytes, void* stream) {
@@ -484,13 +542,14 @@ int mlmcp_propagate(mlmcp_ctx* c, int n_tasks, const mlmcp_task* tasks, int S, c
   if (use_small(c))
     return small_propagate(c, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                            iters, status, active, elapsed, xss, (cudaStream_t)stream);
-  return stream_propagate(c, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xss, xbuf,
+  return stream_propagate(c, n_tasks, tasks, S, M, K, rpar, profile, omega, rtol, max_it, xss, xbuf,
                           qoi, iters, status, active, elapsed, ws, ws_bytes,
                           (cudaStream_t)stream);
 }
 
 int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, const double* K,
-                          const double* profile, double omega, double dt_c, double t0,
+                          const double* rpar, const double* profile, double omega, double dt_c,
+                          double t0,
                           const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                           int max_it, double* U, const double* F, double* C, int32_t* iters,
                           int32_t* status, const int32_t* active, int64_t* elapsed,
@@ -510,7 +569,7 @@ int mlmcp_parareal_coarse(mlmcp_ctx* c, int S, int k, int m, const double* M, co
     return small_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
                                  slice_steps, rtol, max_it, U, F, C, iters, status, active,
                                  elapsed, xss, (cudaStream_t)stream);
-  return stream_parareal_coarse(c, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0,
+  return stream_parareal_coarse(c, S, k, m, M, K, rpar, profile, omega, dt_c, t0, slice_k0,
                                 slice_steps, rtol, max_it, U, F, C, iters, status, active, ws,
                                 ws_bytes, (cudaStream_t)stream);
 }

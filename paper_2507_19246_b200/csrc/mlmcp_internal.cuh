@@ -60,6 +60,11 @@ struct Ctx {
   int32_t* celem = nullptr;
   double* cmw = nullptr;
   double* ckw = nullptr;
+  // region-linear operator description (mlmcp_ctx_set_region_grid): the tile
+  // kernels compute the operator from per-sample region parameters
+  uint32_t* rcode = nullptr;       // device [n]
+  int rR = 0;
+  double rmw[12] = {0}, rkw[12] = {0};
   // pinned host counters for the streaming path
   int32_t* host_counters = nullptr;
   // grid-barrier words of the cooperative path (zeroed at creation)
@@ -211,13 +216,13 @@ int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, co
                     cudaStream_t stream);
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
-                     const double* K, const double* profile, double omega, double rtol,
+                     const double* K, const double* rpar, const double* profile, double omega, double rtol,
                      int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
                      int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
                      size_t ws_bytes, cudaStream_t stream);
 
 int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
-                           const double* profile, double omega, double dt_c, double t0,
+                           const double* rpar, const double* profile, double omega, double dt_c, double t0,
                            const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                            int max_it, double* U, const double* F, double* C, int32_t* iters,
                            int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,

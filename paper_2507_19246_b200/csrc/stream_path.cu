@@ -148,6 +148,14 @@ struct SArgs {
   // iteration in which the last live task of the step stops
   cudaGraphConditionalHandle it_cond;
   int use_cond;
+  // region-linear operator (mlmcp_ctx_set_region_grid + per-sample region
+  // parameters): the tile kernels compute the operator coefficients from the
+  // six triangles around each point instead of streaming them (rcode null:
+  // the stored [S][4][N] symmetric halves of A and M)
+  const uint32_t* rcode;   // [N] six 4-bit triangle regions per point
+  const double* rpar;      // [S][R][2] (sigma_r masked, nu_r)
+  int R;
+  double rmw[12], rkw[12]; // C0..C5, E0, E1, N0, N1, NE0, NE1
   Work w;
 };
 
@@ -486,6 +494,49 @@ __global__ void form_tile_kernel(SArgs a, double dt) {
   a.w.dinv[(int64_t)s * a.N + i] = 1.0 / c;
 }
 
+// Region-linear operator at interior grid point (gx, gy): the symmetric half
+// (C, E, N, NE) of A = M + dt K (and of M) from the per-sample region
+// parameters sp[r] = (sigma_r, nu_r) of the six triangles around the point,
+// summed in the assembly gather map's element order with assemble_kernel's
+// and op_entry's arithmetic — the same doubles the stored path streams.
+// E / N / NE are 0 where the neighbour is a boundary node.
+__device__ __forceinline__ void region_coef(const SArgs& a, const double2* sp, int gx, int gy,
+                                            double dt, double (&A)[4], double (&Mo)[4]) {
+  const uint32_t code = __ldg(a.rcode + (int64_t)gy * a.wd + gx);
+  double2 p[6];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) p[e] = sp[(code >> (4 * e)) & 15u];
+  double m = 0.0, k = 0.0;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    m = __dadd_rn(m, __dmul_rn(p[e].x, a.rmw[e]));
+    k = __dadd_rn(k, __dmul_rn(p[e].y, a.rkw[e]));
+  }
+  Mo[0] = m;
+  A[0] = op_entry(m, k, dt);
+  const bool e_ok = gx + 1 < a.wd, n_ok = gy + 1 < a.gh;
+  const int e0[3] = {2, 3, 4}, e1[3] = {4, 5, 5};
+  const bool ok[3] = {e_ok, n_ok, e_ok && n_ok};
+#pragma unroll
+  for (int c = 0; c < 3; ++c) {
+    double mm = 0.0, kk = 0.0;
+    if (ok[c]) {
+      mm = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].x, a.rmw[6 + 2 * c])),
+                     __dmul_rn(p[e1[c]].x, a.rmw[7 + 2 * c]));
+      kk = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].y, a.rkw[6 + 2 * c])),
+                     __dmul_rn(p[e1[c]].y, a.rkw[7 + 2 * c]));
+    }
+    Mo[1 + c] = mm;
+    A[1 + c] = ok[c] ? op_entry(mm, kk, dt) : 0.0;
+  }
+}
+
+// the task's region parameters into shared memory (block-wide; caller syncs)
+__device__ __forceinline__ void load_region_params(const SArgs& a, int sample, double2* sp) {
+  if (threadIdx.x < a.R)
+    sp[threadIdx.x] = reinterpret_cast<const double2*>(a.rpar)[(int64_t)sample * a.R + threadIdx.x];
+}
+
 __device__ __forceinline__ void cp8(double* dst, const double* src, bool ok) {
   const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(d), "l"(src),
@@ -551,25 +602,45 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   }
   const double* Di = a.w.dinv + (int64_t)tk.sample * N;
   const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
-  // operator of the tile and of its west column / south row: asynchronous
-  // copies into shared memory, overlapped with the vector loads below
+  const bool region = a.rcode != nullptr;
+  __shared__ double2 sp[16];          // region mode: (sigma_r, nu_r) of the task's sample
+  double dv[kTR];
+  if (region) {
+    // operator of the tile computed from the region parameters (no operator
+    // stream): own points here, the west column / south row in the halo loop
+    load_region_params(a, tk.sample, sp);
+    __syncthreads();
 #pragma unroll
-  for (int r = 0; r < kTR; ++r) {
-    const int ly = sy * kTR + r;
-    const bool ok = colok && gy0 + r < a.gh;
-    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+    for (int r = 0; r < kTR; ++r) {
+      const int ly = sy * kTR + r;
+      const bool ok = colok && gy0 + r < a.gh;
+      double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4];
+      if (ok) region_coef(a, sp, gx, gy0 + r, tk.dt, A4, M4);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + (ly + 1) * kTCL + cx + 1], As + j * N + i, ok);
+      for (int j = 0; j < 4; ++j) Ac[j * kTCN + (ly + 1) * kTCL + cx + 1] = A4[j];
+      dv[r] = ok ? 1.0 / A4[0] : 0.0;
+    }
+  } else {
+    // operator of the tile and of its west column / south row: asynchronous
+    // copies into shared memory, overlapped with the vector loads below
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const int ly = sy * kTR + r;
+      const bool ok = colok && gy0 + r < a.gh;
+      const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + (ly + 1) * kTCL + cx + 1], As + j * N + i, ok);
+    }
+    for (int h = threadIdx.x; h < kTH + 1 + kTW; h += kNT) {
+      const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
+      const int hx = tx0 + lx, hy = ty0 + ly;
+      const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+      const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+#pragma unroll
+      for (int q = 1; q < 4; ++q) cp8(&Ac[q * kTCN + (ly + 1) * kTCL + lx + 1], As + q * N + j, ok);
+    }
+    cp_commit();
   }
-  for (int h = threadIdx.x; h < kTH + 1 + kTW; h += kNT) {
-    const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
-    const int hx = tx0 + lx, hy = ty0 + ly;
-    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
-    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
-#pragma unroll
-    for (int q = 1; q < 4; ++q) cp8(&Ac[q * kTCN + (ly + 1) * kTCL + lx + 1], As + q * N + j, ok);
-  }
-  cp_commit();
   const bool odd = k & 1, upd = k > 0, first = k == 1;
   const double* td = a.w.td + t * kTD;
   const double alpha = upd ? td[D_ALPHA] : 0.0, beta = upd ? td[D_BETA] : 0.0;
@@ -589,19 +660,31 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
     else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
     else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
     const int hx = tx0 + lx, hy = ty0 + ly;
+    const bool in = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
     double u = 0.0;
-    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
+    double A4[4] = {0.0, 0.0, 0.0, 0.0};
+    if (region && in) {
+      double M4[4];
+      region_coef(a, sp, hx, hy, tk.dt, A4, M4);
+    }
+    if (in) {
       const int64_t j = (int64_t)hy * a.wd + hx;
       double r = __ldcg(Ro + j);
       if (upd) r = fma(-alpha, tile_s(first, beta, __ldcg(Wo + j), first ? 0.0 : __ldcg(So + j)), r);
-      u = __ldg(Di + j) * r;
+      u = (region ? 1.0 / A4[0] : __ldg(Di + j)) * r;
     }
     U[(ly + 1) * kTLD + lx + 1] = u;
+    // region mode: E, N, NE of the west column / south row (the W, S, SW
+    // coefficients of the tile's edge points)
+    if (region && ((lx == -1 && ly < kTH) || (ly == -1 && lx < kTW))) {
+#pragma unroll
+      for (int q = 1; q < 4; ++q) Ac[q * kTCN + (ly + 1) * kTCL + lx + 1] = A4[q];
+    }
   }
   // own points: update of iteration k-1, u_k
   double gam = 0.0;
   {
-    double rv[kTR], dv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
+    double rv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
 #pragma unroll
     for (int r = 0; r < kTR; ++r) {
       const bool ok = colok && gy0 + r < a.gh;
@@ -617,11 +700,13 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
     // D^-1 of the own points from the staged diagonal (this thread's own
     // copies: no barrier needed), the same correctly rounded 1/C as
     // form_tile_kernel's stored D^-1 (one 8-byte stream less per iteration)
-    cp_wait_all();
+    if (!region) {
+      cp_wait_all();
 #pragma unroll
-    for (int r = 0; r < kTR; ++r) {
-      const bool ok = colok && gy0 + r < a.gh;
-      dv[r] = ok ? 1.0 / Ac[(sy * kTR + r + 1) * kTCL + cx + 1] : 0.0;
+      for (int r = 0; r < kTR; ++r) {
+        const bool ok = colok && gy0 + r < a.gh;
+        dv[r] = ok ? 1.0 / Ac[(sy * kTR + r + 1) * kTCL + cx + 1] : 0.0;
+      }
     }
 #pragma unroll
     for (int r = 0; r < kTR; ++r) {
@@ -721,7 +806,9 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   double* Ac = ism;                 // [4][kTCN]
   double* XV = Ac + 4 * kTCN;       // x_0 with halo
   double* AV = XV + kTV;            // a_n with halo
+  double* Mc = AV + kTV;            // region mode: E, N, NE of M [3][kTCN]
   __shared__ double red[2 * 4 * 32];
+  __shared__ double2 sp[16];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
   if (!block_uniform(step < tk.n_steps && task_live(a, tk, t))) return;
@@ -730,20 +817,37 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
   const int gx = tx0 + cx, gy0 = ty0 + sy * kTR;
   const bool colok = gx < a.wd;
+  const bool region = a.rcode != nullptr;
   const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
   const double* Ms = a.w.A + ((int64_t)a.S + tk.sample) * 4 * N;
   const double* An = a.w.Wv + o;   // a_n (step_end / copy_in)
+  double mown[kTR], dv[kTR];       // region mode: own C of M, D^-1
+  if (region) {
+    load_region_params(a, tk.sample, sp);
+    __syncthreads();
+  }
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const int ly = sy * kTR + r;
     const bool ok = colok && gy0 + r < a.gh;
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
     const int lc = (ly + 1) * kTCL + cx + 1, lv = (ly + 1) * kTLD + cx + 1;
+    if (region) {
+      double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (ok) region_coef(a, sp, gx, gy0 + r, tk.dt, A4, M4);
 #pragma unroll
-    for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
+      for (int j = 0; j < 4; ++j) Ac[j * kTCN + lc] = A4[j];
+#pragma unroll
+      for (int j = 0; j < 3; ++j) Mc[j * kTCN + lc] = M4[1 + j];
+      mown[r] = M4[0];
+      dv[r] = ok ? 1.0 / A4[0] : 0.0;
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
+    }
     cp8(&AV[lv], An + i, ok);
   }
-  if (threadIdx.x < kTH + 1 + kTW) {
+  if (!region && threadIdx.x < kTH + 1 + kTW) {
     const int h = threadIdx.x;
     const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
     const int hx = tx0 + lx, hy = ty0 + ly;
@@ -765,6 +869,17 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
     const int lv = (ly + 1) * kTLD + lx + 1;
     cp8(&AV[lv], An + j, ok);
+    // region mode: E, N, NE of A and M at the west column / south row
+    if (region && ((lx == -1 && ly < kTH) || (ly == -1 && lx < kTW))) {
+      double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4] = {0.0, 0.0, 0.0, 0.0};
+      if (ok) region_coef(a, sp, hx, hy, tk.dt, A4, M4);
+      const int lc = (ly + 1) * kTCL + lx + 1;
+#pragma unroll
+      for (int q = 1; q < 4; ++q) {
+        Ac[q * kTCN + lc] = A4[q];
+        Mc[(q - 1) * kTCN + lc] = M4[q];
+      }
+    }
   }
   cp_commit();
   // initial guess x_0 (the guess kernel's arithmetic, folded in) for the own
@@ -811,13 +926,13 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   };
   const int64_t g = tk.k0 + step + 1;
   const double sf = sin(__dmul_rn(a.omega, grid_time(tk.t_base, g, tk.dt)));
-  double prof[kTR], dv[kTR];
+  double prof[kTR];
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const bool ok = colok && gy0 + r < a.gh;
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
     prof[r] = ok ? __ldg(a.profile + i) : 0.0;
-    dv[r] = ok ? __ldg(a.w.dinv + (int64_t)tk.sample * N + i) : 0.0;
+    if (!region) dv[r] = ok ? __ldg(a.w.dinv + (int64_t)tk.sample * N + i) : 0.0;
   }
   cp_wait_all();   // own and halo a_n were copied by this thread
 #pragma unroll
@@ -861,11 +976,25 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
                          kTCN + lc, 2 * kTCN + lc, 3 * kTCN + lc};
     const int vofs[7] = {b - kTLD - 1, b - kTLD, b - 1, b, b + 1, b + kTLD, b + kTLD + 1};
     const bool w_ = gx > 0, s_ = gy > 0;
-    const double mco[7] = {(w_ && s_) ? __ldg(Ms + 3 * N + i - a.wd - 1) : 0.0,
-                           s_ ? __ldg(Ms + 2 * N + i - a.wd) : 0.0,
-                           w_ ? __ldg(Ms + N + i - 1) : 0.0,
-                           __ldg(Ms + i), __ldg(Ms + N + i), __ldg(Ms + 2 * N + i),
-                           __ldg(Ms + 3 * N + i)};
+    double mco[7];
+    if (region) {
+      // M's E, N, NE of the west / south / south-west points and the own point
+      mco[0] = Mc[2 * kTCN + lc - kTCL - 1];
+      mco[1] = Mc[kTCN + lc - kTCL];
+      mco[2] = Mc[lc - 1];
+      mco[3] = mown[r];
+      mco[4] = Mc[lc];
+      mco[5] = Mc[kTCN + lc];
+      mco[6] = Mc[2 * kTCN + lc];
+    } else {
+      mco[0] = (w_ && s_) ? __ldg(Ms + 3 * N + i - a.wd - 1) : 0.0;
+      mco[1] = s_ ? __ldg(Ms + 2 * N + i - a.wd) : 0.0;
+      mco[2] = w_ ? __ldg(Ms + N + i - 1) : 0.0;
+      mco[3] = __ldg(Ms + i);
+      mco[4] = __ldg(Ms + N + i);
+      mco[5] = __ldg(Ms + 2 * N + i);
+      mco[6] = __ldg(Ms + 3 * N + i);
+    }
     double mx = 0.0, ax = 0.0;
 #pragma unroll
     for (int d = 0; d < 7; ++d) {
@@ -881,8 +1010,8 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
 }
 
 template <int kTH, int kTR>
-constexpr size_t tile_init_smem() {
-  return sizeof(double) * (4 * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
+constexpr size_t tile_init_smem(bool region = false) {
+  return sizeof(double) * ((region ? 7 : 4) * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
 }
 
 
@@ -1397,8 +1526,10 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   const dim3 grid_rows((a.N + kThreads - 1) / kThreads, a.T);
   const dim3 grid_form((a.N + kThreads - 1) / kThreads, a.S);
   if (a.tile) {
-    form_tile_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
-    MLMCP_LAUNCH_CHECK("form_tile_kernel");
+    if (a.rcode == nullptr) {   // region mode computes the operator in the tile kernels
+      form_tile_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
+      MLMCP_LAUNCH_CHECK("form_tile_kernel");
+    }
   } else {
     form_ell_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
     MLMCP_LAUNCH_CHECK("form_ell_kernel");
@@ -1416,11 +1547,12 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   mark_fail_kernel<<<(a.T + 255) / 256, 256, 0, stream>>>(a, 0);
   MLMCP_LAUNCH_CHECK("mark_fail_kernel");
   auto launch_init = [&](cudaStream_t s, int step) -> int {
+    const bool rg = a.rcode != nullptr;
     if (a.tile && tcfg >= 3) {
-      tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(), s>>>(a, step);
+      tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(rg), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else if (a.tile) {
-      tile_init_kernel<16, 4, 3><<<grid_tiles2, 256, tile_init_smem<16, 4>(), s>>>(a, step);
+      tile_init_kernel<16, 4, 3><<<grid_tiles2, 256, tile_init_smem<16, 4>(rg), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else {
       step_init_kernel<<<grid_rows, blk, 0, s>>>(a, step);
@@ -1433,10 +1565,10 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     if (!attr) {
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<8, 2, 4>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tile_init_smem<8, 2>()));
+                                            (int)tile_init_smem<8, 2>(true)));
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<16, 4, 3>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tile_init_smem<16, 4>()));
+                                            (int)tile_init_smem<16, 4>(true)));
       attr = true;
     }
   }
@@ -1628,6 +1760,10 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   a.it_cond = 0;
   a.use_cond = 0;
   a.order = stream_order();
+  a.rcode = nullptr;
+  a.rpar = nullptr;
+  a.R = 0;
+  for (int i = 0; i < 12; ++i) a.rmw[i] = a.rkw[i] = 0.0;
   static bool ls_set = false;
   if (!ls_set) {
     const char* l = getenv("MLMCP_LSGUESS");
@@ -1639,6 +1775,27 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   }
   a.w = w;
   return a;
+}
+
+// MLMCP_TILE_OPERATOR=stored keeps the streamed [S][4][N] operator (A/B)
+bool region_on() {
+  const char* e = getenv("MLMCP_TILE_OPERATOR");
+  return !(e && e[0] == 's');
+}
+
+// region-linear operator on the tile path when the context has a region grid
+// and the caller passed the per-sample region parameters (the TMA variant
+// keeps the streamed operator)
+void set_region(const Ctx* ctx, SArgs& a, const double* rpar) {
+  if (!a.tile || ctx->rcode == nullptr || rpar == nullptr || tile_cfg() == 4 || !region_on())
+    return;
+  a.rcode = ctx->rcode;
+  a.rpar = rpar;
+  a.R = ctx->rR;
+  for (int i = 0; i < 12; ++i) {
+    a.rmw[i] = ctx->rmw[i];
+    a.rkw[i] = ctx->rkw[i];
+  }
 }
 
 // Parareal correction for the streaming path: (parareal.py:168-178)
@@ -1919,7 +2076,8 @@ size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S) {
 }
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
-                     const double* K, const double* profile, double omega, double rtol,
+                     const double* K, const double* rpar, const double* profile, double omega,
+                     double rtol,
                      int max_it, const double* xss, double* xbuf, double* qoi, int32_t* iters,
                      int32_t* status, const int32_t* active, int64_t* elapsed, void* ws,
                      size_t ws_bytes, cudaStream_t stream) {
@@ -1961,6 +2119,7 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
   Work w = carve(ws, L);
   SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                       iters, status, active, w);
+  set_region(ctx, a, rpar);
   a.xss = xss;
   if (coop_usable(ctx, n_tasks) && !(any_ss && xss != nullptr)) {
     // grid-resident path: form the ELL operator once, then one cooperative launch
@@ -1981,7 +2140,8 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
 }
 
 int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
-                           const double* profile, double omega, double dt_c, double t0,
+                           const double* rpar, const double* profile, double omega, double dt_c,
+                           double t0,
                            const int64_t* slice_k0, const int32_t* slice_steps, double rtol,
                            int max_it, double* U, const double* F, double* C, int32_t* iters,
                            int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
@@ -2065,6 +2225,7 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
     // the work buffer X (task t == sample s), from which cval is taken.
     SArgs a = make_args(ctx, S, S, dtasks, M, K, profile, omega, rtol, max_it, U, nullptr,
                         nullptr, tstatus, act, w);
+    set_region(ctx, a, rpar);
     int rc = run_steps(ctx, a, hsteps[n - 1], dt_c, stream);
     if (rc != MLMCP_OK) return rc;
     MLMCP_CUDA_CHECK(cudaMemcpyAsync(cval, w.X, sizeof(double) * S * N,

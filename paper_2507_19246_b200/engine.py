@@ -89,6 +89,7 @@ class DeviceSystem:
                   "mlmcp_ctx_set_assembly")
         self._ws = None
         self._fused_ws = {}
+        self.region_grid = None
 
     # ------------------------------------------------------------ lifecycle
     def close(self):
@@ -157,16 +158,33 @@ class DeviceSystem:
         return M, K
 
     # ------------------------------------------------------------ K2-K4, K6
+    def set_region_grid(self, rg) -> bool:
+        """Register a fe.RegionGrid (region-linear operator on the tile path)."""
+        if rg is None:
+            check(self.lib.mlmcp_ctx_set_region_grid(self.ctx, 0, None, None, None),
+                  "mlmcp_ctx_set_region_grid")
+            self.region_grid = None
+            return False
+        code = np.ascontiguousarray(rg.code, dtype=np.uint32)
+        mw = np.ascontiguousarray(rg.mw, dtype=np.float64)
+        kw = np.ascontiguousarray(rg.kw, dtype=np.float64)
+        check(self.lib.mlmcp_ctx_set_region_grid(self.ctx, int(rg.n_regions), np_ptr(code),
+                                                 np_ptr(mw), np_ptr(kw)),
+              "mlmcp_ctx_set_region_grid")
+        self.region_grid = rg
+        return True
+
     def propagate(self, tasks: np.ndarray, M, K, profile, omega: float, rtol: float,
                   max_it: int, xbuf, qoi=None, iters=None, status=None, active=None,
-                  stream=None, tasks_dev: torch.Tensor | None = None, elapsed=None, xss=None):
+                  stream=None, tasks_dev: torch.Tensor | None = None, elapsed=None, xss=None,
+                  rp=None):
         n = len(tasks)
         if n == 0:
             return None
         S = M.shape[0]
         td = tasks_dev if tasks_dev is not None else tasks_to_device(tasks, self.device)
         ws = self.workspace(n, S)
-        check(self.lib.mlmcp_propagate(self.ctx, n, ptr(td), S, ptr(M), ptr(K), ptr(profile),
+        check(self.lib.mlmcp_propagate(self.ctx, n, ptr(td), S, ptr(M), ptr(K), ptr(rp), ptr(profile),
                                        float(omega), float(rtol), int(max_it), ptr(xss),
                                        ptr(xbuf), ptr(qoi),
                                        ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(ws),
@@ -177,10 +195,10 @@ class DeviceSystem:
     # ------------------------------------------------------------ K5
     def parareal_coarse(self, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0, slice_steps,
                         rtol, max_it, U, F, C, iters, status, active, stream=None, elapsed=None,
-                        xss=None):
+                        xss=None, rp=None):
         ws = self.workspace(S, S)
         check(self.lib.mlmcp_parareal_coarse(
-            self.ctx, S, k, m, ptr(M), ptr(K), ptr(profile), float(omega), float(dt_c), float(t0),
+            self.ctx, S, k, m, ptr(M), ptr(K), ptr(rp), ptr(profile), float(omega), float(dt_c), float(t0),
             ptr(slice_k0), ptr(slice_steps), float(rtol), int(max_it), ptr(U), ptr(F), ptr(C),
             ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(xss), ptr(ws),
             0 if ws is None else ws.numel(), stream_handle(stream)), "mlmcp_parareal_coarse")
@@ -246,6 +264,16 @@ def kl_sigma(xi: torch.Tensor, basis: torch.Tensor, log_sigma0: float, scale: fl
     check(lib.mlmcp_kl_sigma(S, E, modes, ptr(xi), ptr(basis), float(log_sigma0), float(scale),
                              ptr(out), stream_handle(stream)), "mlmcp_kl_sigma")
     return out
+
+
+def region_params(params: torch.Tensor, R: int, mask: torch.Tensor | None, sigma_out=None,
+                  rp_out=None, stream=None):
+    """mlmcp_region_params: masked sigma [S, R] and/or (sigma, nu) pairs
+    [S, R, 2] from drawn parameters [S, 2R] (nu first, sigma second)."""
+    lib = _lib.load()
+    S = params.shape[0]
+    check(lib.mlmcp_region_params(S, int(R), ptr(params), ptr(mask), ptr(sigma_out), ptr(rp_out),
+                                  stream_handle(stream)), "mlmcp_region_params")
 
 
 def level_reduce(q_l: torch.Tensor, q_lm1: torch.Tensor | None, stream=None) -> torch.Tensor:

@@ -153,6 +153,84 @@ def source_profile(mesh: StructuredMesh, layout: str, j0: float = J0) -> np.ndar
     return prof
 
 
+# element slots of the region-linear operator of one interior point (i, j):
+# the six triangles around the node in increasing element index —
+# lower/upper of cell (i-1, j-1), upper of (i, j-1), lower of (i-1, j),
+# lower/upper of (i, j) — and the subsets each stencil coefficient sums over
+# (the hypotenuse entry NE couples the two triangles of the node's own cell)
+REGION_SLOTS = {"C": (0, 1, 2, 3, 4, 5), "E": (2, 4), "N": (3, 5), "NE": (4, 5)}
+
+
+@dataclass
+class RegionGrid:
+    """Region-linear description of the per-sample operator on a structured
+    grid: coefficient c of point p is  sum_e sigma_{r(e)} mw[c][e]  (mass) and
+    sum_e nu_{r(e)} kw[c][e]  (stiffness) over the slot's triangles, summed in
+    the assembly gather map's element order (bitwise the CSR values when
+    ``bitwise``).  code[p] packs the six triangles' regions, 4 bits each."""
+
+    code: np.ndarray        # uint32 [n_rows]
+    mw: np.ndarray          # [12]: C0..C5, E0, E1, N0, N1, NE0, NE1
+    kw: np.ndarray          # [12]
+    n_regions: int
+    bitwise: bool
+
+
+def region_grid(mesh: StructuredMesh, region: np.ndarray, n_regions: int):
+    """RegionGrid of a region-constant material layout, or None when the gather
+    map does not have the structured-grid form (checked entry by entry)."""
+    n, w = mesh.n, mesh.n - 1
+    if n_regions > 16 or w < 2:
+        return None
+    N = mesh.n_rows
+    p = np.arange(N)
+    i, j = p % w + 1, p // w + 1
+    csw, cs, cw, co = (j - 1) * n + i - 1, (j - 1) * n + i, j * n + i - 1, j * n + i
+    E6 = np.stack([2 * csw, 2 * csw + 1, 2 * cs + 1, 2 * cw, 2 * co, 2 * co + 1], axis=1)
+    rp, col, cptr = mesh.row_ptr.astype(np.int64), mesh.col, mesh.cptr.astype(np.int64)
+    mw, kw = np.zeros(12), np.zeros(12)
+    bitwise = True
+    base = 0
+    for name, off, es in (("C", 0, REGION_SLOTS["C"]), ("E", 1, REGION_SLOTS["E"]),
+                          ("N", w, REGION_SLOTS["N"]), ("NE", w + 1, REGION_SLOTS["NE"])):
+        has = np.ones(N, dtype=bool)
+        if name in ("E", "NE"):
+            has &= i + 1 < n
+        if name in ("N", "NE"):
+            has &= j + 1 < n
+        pp = p[has]
+        # CSR position of (pp, pp + off): columns are sorted per row
+        q = np.full(len(pp), -1, dtype=np.int64)
+        for d in range(int(np.max(rp[1:] - rp[:-1]))):
+            cand = rp[pp] + d
+            hit = (cand < rp[pp + 1]) & (col[np.minimum(cand, len(col) - 1)] == pp + off)
+            q[hit] = cand[hit]
+        if np.any(q < 0) or np.any(cptr[q + 1] - cptr[q] != len(es)):
+            return None
+        cols = np.stack([cptr[q] + t for t in range(len(es))], axis=1)
+        if not np.array_equal(mesh.celem[cols], E6[pp][:, list(es)]):
+            return None
+        cm, ck = mesh.cmw[cols], mesh.ckw[cols]
+        m0, k0 = cm[0], ck[0]
+        if not (np.array_equal(cm, np.broadcast_to(m0, cm.shape))
+                and np.array_equal(ck, np.broadcast_to(k0, ck.shape))):
+            bitwise = False
+            scale = max(np.max(np.abs(cm)), 1e-300), max(np.max(np.abs(ck)), 1e-300)
+            if (np.max(np.abs(cm - m0)) > 1e-14 * scale[0]
+                    or np.max(np.abs(ck - k0)) > 1e-14 * scale[1]):
+                return None
+        mw[base:base + len(es)] = m0
+        kw[base:base + len(es)] = k0
+        base += len(es)
+    reg = np.asarray(region, dtype=np.int64)[E6]            # [N, 6]
+    if reg.min() < 0 or reg.max() >= n_regions:
+        return None
+    code = np.zeros(N, dtype=np.uint64)
+    for e in range(6):
+        code |= reg[:, e].astype(np.uint64) << np.uint64(4 * e)
+    return RegionGrid(code.astype(np.uint32), mw, kw, int(n_regions), bitwise)
+
+
 def kl_basis(mesh: StructuredMesh) -> np.ndarray:
     """(KL_MODES, E): sqrt(lam_k) phi_k(c_e); modes (a,b) in {0..7}^2 ordered by
     (a+b, a); lam_k = k^-2 / sum_j j^-2; phi separable L2-normalised cosines."""

@@ -336,7 +336,7 @@ class MachineFamily(_BatchedFamily):
         Kv[:, dpos[1:] - 1] = -1.0 / h ** 2
         return Mv, Kv
 
-    def _assemble_host(self, params, M, K):
+    def _assemble_host(self, params, M, K, rp=None):
         import torch
         Mv, Kv = self.values(params)
         M.copy_(torch.from_numpy(Mv).pin_memory(), non_blocking=True)

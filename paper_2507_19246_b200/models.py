@@ -203,8 +203,14 @@ class _BatchedFamily:
         j = self._seq_job(np.zeros(0, dtype=np.int64), dt_fine)
         return {"qoi_mode": j.qoi_mode, "qoi_index": j.qoi_index, "qoi_from": j.qoi_from}
 
-    def _assemble_dev(self, params_dev, M, K):
+    def _assemble_dev(self, params_dev, M, K, rp=None):
         self._assemble_host(params_dev.cpu().numpy(), M, K)
+
+    def _new_rp(self, S: int):
+        """Region-parameter buffer of the region-linear operator (None: the
+        family streams its operator)."""
+        fn = getattr(self.solver, "new_region_params", None)
+        return fn(S) if fn is not None else None
 
     # ------------------------------------------------------------ batched
     def run_levels(self, draws, parareal_cfg: PararealConfig | None = None, levels=None,
@@ -237,17 +243,19 @@ class _BatchedFamily:
         nnz = sol.nnz
         M = torch.empty((int(offs[-1]), nnz), dtype=torch.float64, device=sol.device)
         K = torch.empty_like(M)
+        RP = self._new_rp(int(offs[-1]))
 
         def assemble_level(i):
             a, b = int(offs[i]), int(offs[i + 1])
             if b == a:
                 return
+            rp = RP[a:b] if RP is not None else None
             if params_dev is not None:
-                self._assemble_dev(params_dev[a:b], M[a:b], K[a:b])   # resident in HBM
+                self._assemble_dev(params_dev[a:b], M[a:b], K[a:b], rp=rp)   # resident in HBM
             else:
                 d = draws[i].get() if hasattr(draws[i], "get") else draws[i]
                 host = np.ascontiguousarray(np.asarray(d, dtype=float).reshape(b - a, -1))
-                self._assemble_host(host, M[a:b], K[a:b])
+                self._assemble_host(host, M[a:b], K[a:b], rp=rp)
 
         pr_level = None
         if parareal_cfg is not None:
@@ -276,13 +284,14 @@ class _BatchedFamily:
             with torch.cuda.stream(side):
                 pr = sol.run_parareal(M[a:b], K[a:b], 0.0, self.horizon, cfg.num_subintervals,
                                       cfg.dt_fine, cfg.dt_coarse, cfg.tolerance, cfg.k_max,
-                                      stream=side, **self._pr_qoi(cfg.dt_fine))
+                                      stream=side, rp=RP[a:b] if RP is not None else None,
+                                      **self._pr_qoi(cfg.dt_fine))
                 pr_q = self._finish_q(pr.qoi, cfg.dt_fine)
         for i in range(len(levels)):
             if i != pr_level:
                 assemble_level(i)
         jobs, where = self._level_jobs(levels, offs, pr_level)
-        res = sol.run_sequential(M, K, jobs) if jobs else []
+        res = sol.run_sequential(M, K, jobs, rp=RP) if jobs else []
         if pr is not None and side is not main:
             main.wait_stream(side)
             for t in (pr.qoi, pr.k_used, pr.defects):
@@ -553,14 +562,15 @@ class _BatchedFamily:
         t = time.perf_counter()
         M = torch.empty((len(params), sol.nnz), dtype=torch.float64, device=sol.device)
         K = torch.empty_like(M)
-        self._assemble_host(params, M, K)
+        RP = self._new_rp(len(params))
+        self._assemble_host(params, M, K, rp=RP)
         top = len(self.hierarchy) - 1
         dt = self.hierarchy[lvl].dt
         ks = None
         if parareal_cfg is not None:
             cfg = parareal_cfg.with_dt_fine(dt)
             pr = sol.run_parareal(M, K, 0.0, self.horizon, cfg.num_subintervals, cfg.dt_fine,
-                                  cfg.dt_coarse, cfg.tolerance, cfg.k_max,
+                                  cfg.dt_coarse, cfg.tolerance, cfg.k_max, rp=RP,
                                   **self._pr_qoi(cfg.dt_fine))
             from .parareal import raise_parareal_status
             raise_parareal_status(pr.status.cpu().numpy(), pr.fine_status.cpu().numpy())
@@ -568,7 +578,7 @@ class _BatchedFamily:
             ks = pr.k_used.cpu().numpy()
         else:
             from .solver import raise_on_status
-            r = sol.run_sequential(M, K, [self._seq_job(np.arange(len(params)), dt)])[0]
+            r = sol.run_sequential(M, K, [self._seq_job(np.arange(len(params)), dt)], rp=RP)[0]
             raise_on_status(r.status, "implicit Euler solve")
             q = self._finish_q(r.qoi, dt).cpu().numpy()
         wall = time.perf_counter() - t
@@ -678,13 +688,13 @@ class EddyCurrentFamily(_BatchedFamily):
     def _n_params(self) -> int:
         return fe.n_params(self.layout)
 
-    def _assemble_host(self, params, M, K):
+    def _assemble_host(self, params, M, K, rp=None):
         import torch
         p = torch.from_numpy(np.ascontiguousarray(params, dtype=np.float64)).pin_memory()
-        self.solver.assemble(p.to(self.solver.device, non_blocking=True), out=(M, K))
+        self.solver.assemble(p.to(self.solver.device, non_blocking=True), out=(M, K), rp_out=rp)
 
-    def _assemble_dev(self, params_dev, M, K):
-        self.solver.assemble(params_dev, out=(M, K))
+    def _assemble_dev(self, params_dev, M, K, rp=None):
+        self.solver.assemble(params_dev, out=(M, K), rp_out=rp)
 
 
 def eddy_current_family(config: int | str, device=None, **kw) -> EddyCurrentFamily:

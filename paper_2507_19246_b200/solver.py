@@ -24,7 +24,7 @@ import torch
 
 from . import _lib, fe
 from ._lib import ptr
-from .engine import DeviceSystem, F64, I32, kl_sigma, new_tasks, tasks_to_device
+from .engine import DeviceSystem, F64, I32, kl_sigma, new_tasks, region_params, tasks_to_device
 from .timeint import SingularSystemError, step_count
 
 DEFAULT_RTOL = 1e-13   # ||r||_2 <= 1e-13 ||b||_2, the stated PCG tolerance
@@ -119,8 +119,11 @@ class BatchSolver:
         self.periods = 1.0    # forcing periods in the family's horizon (set by the family)
 
     # ------------------------------------------------------------ sequential
-    def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
-        return _run_sequential(self, M, K, jobs, stream, keep_traj)
+    def run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False,
+                       rp=None):
+        """``rp``: [S, R, 2] region parameters of the M/K rows (region-linear
+        operator on the streaming tile path; None streams the operator)."""
+        return _run_sequential(self, M, K, jobs, stream, keep_traj, rp)
 
     def run_fused(self, M, K, jobs: list[SeqJob], pr=None, stream=None, grid_ctas: int = 0):
         return _run_fused(self, M, K, jobs, pr, stream, grid_ctas)
@@ -128,12 +131,12 @@ class BatchSolver:
     def run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
                      dt_coarse: float, tol: float, k_max: int, stream=None,
                      keep_traj: bool = False, qoi_mode: int | None = None,
-                     qoi_index: int = 0, qoi_from: int = -1) -> PararealBatchResult:
+                     qoi_index: int = 0, qoi_from: int = -1, rp=None) -> PararealBatchResult:
         """qoi_mode None / QOI_FINAL_ENERGY: 1/2 a(T)^T K a(T); otherwise the
         task QoI accumulated over the fine trajectory (global fine steps g >
         qoi_from), summed over slices."""
         return _run_parareal(self, M, K, t0, t1, m, dt_fine, dt_coarse, tol, k_max, stream,
-                             keep_traj, qoi_mode, qoi_index, qoi_from)
+                             keep_traj, qoi_mode, qoi_index, qoi_from, rp)
 
     def use_predictor(self) -> bool:
         """The steady-state predictor pays where the forced periodic response
@@ -212,14 +215,31 @@ class FESolver(BatchSolver):
             self.nu_const = torch.full((1,), fe.NU0, dtype=F64, device=dev)
             self.nu_index = torch.zeros(m.n_elem, dtype=I32, device=dev)
         else:
-            self.region = torch.tensor(fe.region_map(m, layout), dtype=I32, device=dev)
+            region = fe.region_map(m, layout)
+            self.region = torch.tensor(region, dtype=I32, device=dev)
             self.mask = torch.tensor(fe.conducting_mask(layout), dtype=F64, device=dev)
             self.n_regions = len(fe.conducting_mask(layout))
+            # region-linear operator of the streaming tile kernels (structured
+            # grids; the operator is computed from the per-sample region
+            # parameters instead of streamed: 112 -> 80 B/point per PCG iteration)
+            if not self.sys.sm_resident and os.environ.get("MLMCP_TILE_OPERATOR") != "stored":
+                self.sys.set_region_grid(fe.region_grid(m, region, self.n_regions))
+
+    @property
+    def region_mode(self) -> bool:
+        return self.sys.region_grid is not None
+
+    def new_region_params(self, S: int):
+        """[S, R, 2] buffer for assemble(rp_out=...) (None without a region grid)."""
+        if not self.region_mode:
+            return None
+        return torch.empty((S, self.n_regions, 2), dtype=F64, device=self.device)
 
     # ------------------------------------------------------------ K1
-    def assemble(self, params: torch.Tensor, stream=None, out=None):
+    def assemble(self, params: torch.Tensor, stream=None, out=None, rp_out=None):
         """Per-sample CSR values (M, K) [S, nnz] from parameters [S, P]
-        (written into ``out`` = (M, K) slices when given)."""
+        (written into ``out`` = (M, K) slices when given; ``rp_out`` [S, R, 2]
+        receives the region parameters of the region-linear operator)."""
         params = params.to(device=self.device, dtype=F64).contiguous()
         S = params.shape[0]
         if S == 0:
@@ -234,10 +254,11 @@ class FESolver(BatchSolver):
                                      self.nu_index, stream, out)
         R = self.n_regions
         # sigma masked to 0 in non-conducting regions *after* drawing (ParameterVector
-        # positivity, models.py:69-74); a plain elementwise product (plumbing)
-        nu = params[:, :R].contiguous()
-        sigma = (params[:, R:2 * R] * self.mask).contiguous()
-        return self.sys.assemble(S, sigma, R, self.region, nu, R, self.region, stream, out)
+        # positivity, models.py:69-74), and the (sigma, nu) pairs of the
+        # region-linear operator, in one libmlmcp launch
+        sigma = torch.empty((S, R), dtype=F64, device=self.device)
+        region_params(params, R, self.mask, sigma, rp_out, stream)
+        return self.sys.assemble(S, sigma, R, self.region, params, 2 * R, self.region, stream, out)
 
 
 
@@ -310,7 +331,8 @@ def _seq_results(self, st):
     return out
 
 
-def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False,
+                    rp=None):
     """All jobs in one batched launch (SM-resident path) or one launch per
     dt (streaming path).  Returns one SeqResult per job (device tensors)."""
     st = _seq_setup(self, M, K, jobs, stream, keep_traj)
@@ -330,7 +352,7 @@ def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool
             sel = st.tasks[st.tasks["dt"] == dt]
             self.sys.propagate(sel, M, K, self.profile, self.omega, self.step_rtol(),
                                self.max_it, st.xbuf, st.qoi, st.iters, st.status, None, stream,
-                               elapsed=st.elapsed, xss=st.xss)
+                               elapsed=st.elapsed, xss=st.xss, rp=rp)
     return _seq_results(self, st)
 
 
@@ -430,7 +452,7 @@ def _pr_result(self, st, K, stream=None) -> PararealBatchResult:
 def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
                   dt_coarse: float, tol: float, k_max: int, stream=None,
                   keep_traj: bool = False, qoi_mode: int | None = None,
-                  qoi_index: int = 0, qoi_from: int = -1) -> PararealBatchResult:
+                  qoi_index: int = 0, qoi_from: int = -1, rp=None) -> PararealBatchResult:
     """parareal_solve for the S samples whose operators are M/K rows 0..S-1
     (slice the level's M/K to pass a sub-batch), from the zero state:
     K_max rounds of [coarse sweep, fine slices, defect] launches."""
@@ -451,11 +473,11 @@ def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
         self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
                                  st.ck0_d, st.cst_d, self.step_rtol(), self.max_it, st.U, st.F,
                                  st.C, st.coarse_iters, st.status, st.active, stream,
-                                 elapsed=st.elapsed_c, xss=st.xss_c)
+                                 elapsed=st.elapsed_c, xss=st.xss_c, rp=rp)
         sel = st.all_tasks[st.n_idx >= k]
         self.sys.propagate(sel, M, K, self.profile, self.omega, self.step_rtol(), self.max_it,
                            st.buf, st.slice_qoi, st.fine_iters, st.fine_status, st.active, stream,
-                           tasks_dev=tables[k - 1], elapsed=st.elapsed_f, xss=st.xss_f)
+                           tasks_dev=tables[k - 1], elapsed=st.elapsed_f, xss=st.xss_f, rp=rp)
         self.sys.parareal_defect(S, k, m, k_max, st.U, st.F, tol, st.active, st.k_used,
                                  st.defects, stream)
     self.sys.parareal_finalize(S, m, st.U, st.F, st.k_used, stream)

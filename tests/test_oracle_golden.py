@@ -117,3 +117,25 @@ def test_fe_matrices_properties():
     ev = np.linalg.eigvalsh(M.toarray())
     assert ev.min() > -1e-9 * ev.max() and ev.min() < 1e-9 * ev.max()  # sigma = 0 regions: singular
     assert prof.sum() > 0
+
+
+def test_oracle_matches_reference_goldens_at_baseline_meshes():
+    """The oracle restatement (splu backend, one factorisation per propagator
+    call as timeint.py:64-75) reproduces BITWISE the reference-generated
+    fixtures at the BASELINE mesh sizes (oracle/make_large_goldens.py): a
+    config-3 level-1 coupled sample at 128^2 and one finest-level Parareal
+    sample (M=32, K<=6) — the oracle that checks the GPU at these sizes is
+    pinned to the reference there too."""
+    from oracle import mlmc_oracle as mo
+    cfg = mo.CONFIGS[3]
+    prob = mo.FEProblem(128, "kl64")
+    g = golden("cfg3_subset_l01")
+    i = int(np.nonzero((g["level"] == 1) & (g["k"] == 1))[0][0])
+    q_l, q_lm1, _ = mo.coupled(prob, cfg, 1, g["params"][i])
+    assert (q_l, q_lm1) == (g["q_l"][i], g["q_lm1"][i])
+    g2 = golden("cfg3_l2_parareal")
+    j = 46                                           # key 47
+    rec = mo.evaluate(prob, cfg, g2["params"][j], cfg.dts[2], True)
+    assert rec.k_used == g2["k_used"][j]
+    assert rec.q == g2["q_l"][j]
+    np.testing.assert_array_equal(np.array(rec.defects), g2["defects"][j][:rec.k_used])
