@@ -500,9 +500,9 @@ __global__ void form_tile_kernel(SArgs a, double dt) {
 // summed in the assembly gather map's element order with assemble_kernel's
 // and op_entry's arithmetic — the same doubles the stored path streams.
 // E / N / NE are 0 where the neighbour is a boundary node.
-__device__ __forceinline__ void region_coef(const SArgs& a, const double2* sp, int gx, int gy,
-                                            double dt, double (&A)[4], double (&Mo)[4]) {
-  const uint32_t code = __ldg(a.rcode + (int64_t)gy * a.wd + gx);
+__device__ __forceinline__ void region_coef(const SArgs& a, const double2* sp, uint32_t code,
+                                            int gx, int gy, double dt, double (&A)[4],
+                                            double (&Mo)[4]) {
   double2 p[6];
 #pragma unroll
   for (int e = 0; e < 6; ++e) p[e] = sp[(code >> (4 * e)) & 15u];
@@ -602,45 +602,25 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   }
   const double* Di = a.w.dinv + (int64_t)tk.sample * N;
   const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
-  const bool region = a.rcode != nullptr;
-  __shared__ double2 sp[16];          // region mode: (sigma_r, nu_r) of the task's sample
-  double dv[kTR];
-  if (region) {
-    // operator of the tile computed from the region parameters (no operator
-    // stream): own points here, the west column / south row in the halo loop
-    load_region_params(a, tk.sample, sp);
-    __syncthreads();
+  // operator of the tile and of its west column / south row: asynchronous
+  // copies into shared memory, overlapped with the vector loads below
 #pragma unroll
-    for (int r = 0; r < kTR; ++r) {
-      const int ly = sy * kTR + r;
-      const bool ok = colok && gy0 + r < a.gh;
-      double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4];
-      if (ok) region_coef(a, sp, gx, gy0 + r, tk.dt, A4, M4);
+  for (int r = 0; r < kTR; ++r) {
+    const int ly = sy * kTR + r;
+    const bool ok = colok && gy0 + r < a.gh;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) Ac[j * kTCN + (ly + 1) * kTCL + cx + 1] = A4[j];
-      dv[r] = ok ? 1.0 / A4[0] : 0.0;
-    }
-  } else {
-    // operator of the tile and of its west column / south row: asynchronous
-    // copies into shared memory, overlapped with the vector loads below
-#pragma unroll
-    for (int r = 0; r < kTR; ++r) {
-      const int ly = sy * kTR + r;
-      const bool ok = colok && gy0 + r < a.gh;
-      const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + (ly + 1) * kTCL + cx + 1], As + j * N + i, ok);
-    }
-    for (int h = threadIdx.x; h < kTH + 1 + kTW; h += kNT) {
-      const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
-      const int hx = tx0 + lx, hy = ty0 + ly;
-      const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
-      const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
-#pragma unroll
-      for (int q = 1; q < 4; ++q) cp8(&Ac[q * kTCN + (ly + 1) * kTCL + lx + 1], As + q * N + j, ok);
-    }
-    cp_commit();
+    for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + (ly + 1) * kTCL + cx + 1], As + j * N + i, ok);
   }
+  for (int h = threadIdx.x; h < kTH + 1 + kTW; h += kNT) {
+    const int lx = h <= kTH ? -1 : h - (kTH + 1), ly = h <= kTH ? h - 1 : -1;
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    const bool ok = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
+#pragma unroll
+    for (int q = 1; q < 4; ++q) cp8(&Ac[q * kTCN + (ly + 1) * kTCL + lx + 1], As + q * N + j, ok);
+  }
+  cp_commit();
   const bool odd = k & 1, upd = k > 0, first = k == 1;
   const double* td = a.w.td + t * kTD;
   const double alpha = upd ? td[D_ALPHA] : 0.0, beta = upd ? td[D_BETA] : 0.0;
@@ -660,31 +640,19 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
     else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
     else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
     const int hx = tx0 + lx, hy = ty0 + ly;
-    const bool in = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
     double u = 0.0;
-    double A4[4] = {0.0, 0.0, 0.0, 0.0};
-    if (region && in) {
-      double M4[4];
-      region_coef(a, sp, hx, hy, tk.dt, A4, M4);
-    }
-    if (in) {
+    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
       const int64_t j = (int64_t)hy * a.wd + hx;
       double r = __ldcg(Ro + j);
       if (upd) r = fma(-alpha, tile_s(first, beta, __ldcg(Wo + j), first ? 0.0 : __ldcg(So + j)), r);
-      u = (region ? 1.0 / A4[0] : __ldg(Di + j)) * r;
+      u = __ldg(Di + j) * r;
     }
     U[(ly + 1) * kTLD + lx + 1] = u;
-    // region mode: E, N, NE of the west column / south row (the W, S, SW
-    // coefficients of the tile's edge points)
-    if (region && ((lx == -1 && ly < kTH) || (ly == -1 && lx < kTW))) {
-#pragma unroll
-      for (int q = 1; q < 4; ++q) Ac[q * kTCN + (ly + 1) * kTCL + lx + 1] = A4[q];
-    }
   }
   // own points: update of iteration k-1, u_k
   double gam = 0.0;
   {
-    double rv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
+    double rv[kTR], dv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
 #pragma unroll
     for (int r = 0; r < kTR; ++r) {
       const bool ok = colok && gy0 + r < a.gh;
@@ -700,13 +668,11 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
     // D^-1 of the own points from the staged diagonal (this thread's own
     // copies: no barrier needed), the same correctly rounded 1/C as
     // form_tile_kernel's stored D^-1 (one 8-byte stream less per iteration)
-    if (!region) {
-      cp_wait_all();
+    cp_wait_all();
 #pragma unroll
-      for (int r = 0; r < kTR; ++r) {
-        const bool ok = colok && gy0 + r < a.gh;
-        dv[r] = ok ? 1.0 / Ac[(sy * kTR + r + 1) * kTCL + cx + 1] : 0.0;
-      }
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      dv[r] = ok ? 1.0 / Ac[(sy * kTR + r + 1) * kTCL + cx + 1] : 0.0;
     }
 #pragma unroll
     for (int r = 0; r < kTR; ++r) {
@@ -760,6 +726,176 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
   if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
 }
 
+// Region-mode iteration kernel (mlmcp_ctx_set_region_grid): tile_iter_kernel's
+// arithmetic with the operator computed from the task's region parameters
+// instead of streamed.  Every global load of the launch (own-point vectors,
+// the thread's halo point, the triangle-region codes) is issued before the
+// coefficient arithmetic, so the memory pipes stay busy while the operator is
+// formed; own-point coefficients of A land in shared memory (the neighbours'
+// W, S, SW), D^-1 = 1/C in registers.  HBM per point: read x r w s p, write
+// x r w s p = 80 B (the code array, 4 B per point shared by all tasks, stays
+// in L2).
+template <int kTH, int kTR, int kMinB>
+__global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(SArgs a) {
+  constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
+  constexpr int kNT = kTW * (kTH / kTR);
+  static_assert(kTHalo <= kNT, "one halo point per thread");
+  constexpr int kTCL = kTW + 1;
+  constexpr int kTCN = (kTH + 1) * kTCL;
+  extern __shared__ __align__(16) double tsm[];
+  double* U = tsm;                              // (kTH + 2) * kTLD
+  double* Ac = U + (kTH + 2) * kTLD;            // C, E, N, NE of the tile, W column, S row
+  __shared__ double red[2 * 4 * 32];
+  __shared__ double2 sp[16];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  const int t = blockIdx.y;
+  const mlmcp_task tk = a.tasks[t];
+  const int32_t* ti = a.w.ti + t * kTI;
+  int mode = 0;   // 0 skip, 1 run, 2 zero solution
+  if (threadIdx.x == 0 && task_live(a, tk, t)) {
+    const int st = ti[I_STATE];
+    mode = st == ST_RUN ? 1 : (st == ST_ZERO ? 2 : 0);
+  }
+  mode = bcast_int(mode);
+  if (mode == 0) return;
+  const int k = ti[I_IT_STEP];
+  const int64_t N = a.N, o = (int64_t)t * N;
+  const int tx0 = (blockIdx.x % a.ntx) * kTW, ty0 = (blockIdx.x / a.ntx) * kTH;
+  const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
+  const int gx = tx0 + cx;
+  const int gy0 = ty0 + sy * kTR;
+  const bool colok = gx < a.wd;
+  double* X = a.w.X + o;
+  if (mode == 2) {
+#pragma unroll
+    for (int r = 0; r < kTR; ++r)
+      if (colok && gy0 + r < a.gh) X[(int64_t)(gy0 + r) * a.wd + gx] = 0.0;
+    return;
+  }
+  const bool odd = k & 1, upd = k > 0, first = k == 1;
+  const double* td = a.w.td + t * kTD;
+  const double alpha = upd ? td[D_ALPHA] : 0.0, beta = upd ? td[D_BETA] : 0.0;
+  const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;   // r_{k-1} (k == 0: r_0)
+  const double* Wo = odd ? a.w.Wv + o : a.w.W1 + o;            // w_{k-1}
+  const double* So = odd ? a.w.S1 + o : a.w.Sv + o;            // s_{k-2}
+  double* Rn = odd ? a.w.R1 + o : a.w.R + o;
+  double* Sn = odd ? a.w.Sv + o : a.w.S1 + o;
+  double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
+  // ---- 1. every global load of the launch, issued up front
+  double rv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
+  uint32_t cd[kTR];
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const bool ok = colok && gy0 + r < a.gh;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+    cd[r] = ok ? __ldg(a.rcode + i) : 0u;
+    rv[r] = ok ? __ldcg(Ro + i) : 0.0;
+    wv[r] = (ok && upd) ? __ldcg(Wo + i) : 0.0;
+    sv[r] = (ok && upd && !first) ? __ldcg(So + i) : 0.0;
+    pv[r] = (ok && upd && !first) ? __ldcg(a.w.P + o + i) : 0.0;
+    xv[r] = (ok && upd) ? __ldcg(X + i) : 0.0;
+  }
+  int hlx = 0, hly = 0;
+  bool hin = false;
+  double hr = 0.0, hw = 0.0, hs = 0.0;
+  uint32_t hcode = 0u;
+  if (threadIdx.x < kTHalo) {
+    const int h = threadIdx.x;
+    if (h < kTW + 2) { hlx = h - 1; hly = -1; }
+    else if (h < 2 * (kTW + 2)) { hlx = h - (kTW + 2) - 1; hly = kTH; }
+    else if (h < 2 * (kTW + 2) + kTH) { hlx = -1; hly = h - 2 * (kTW + 2); }
+    else { hlx = kTW; hly = h - 2 * (kTW + 2) - kTH; }
+    const int hx = tx0 + hlx, hy = ty0 + hly;
+    hin = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
+    if (hin) {
+      const int64_t j = (int64_t)hy * a.wd + hx;
+      hcode = __ldg(a.rcode + j);
+      hr = __ldcg(Ro + j);
+      if (upd) {
+        hw = __ldcg(Wo + j);
+        if (!first) hs = __ldcg(So + j);
+      }
+    }
+  }
+  load_region_params(a, tk.sample, sp);
+  __syncthreads();
+  // ---- 2. the halo point: coefficients (W column / S row: E, N, NE into
+  // shared memory), u = D^-1 r_k
+  if (threadIdx.x < kTHalo) {
+    double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4];
+    double u = 0.0;
+    if (hin) {
+      region_coef(a, sp, hcode, tx0 + hlx, ty0 + hly, tk.dt, A4, M4);
+      double r = hr;
+      if (upd) r = fma(-alpha, tile_s(first, beta, hw, hs), r);
+      u = (1.0 / A4[0]) * r;
+    }
+    U[(hly + 1) * kTLD + hlx + 1] = u;
+    if ((hlx == -1 && hly < kTH) || (hly == -1 && hlx < kTW)) {
+#pragma unroll
+      for (int q = 1; q < 4; ++q) Ac[q * kTCN + (hly + 1) * kTCL + hlx + 1] = A4[q];
+    }
+  }
+  // ---- 3. own points: coefficients, update of iteration k-1, u_k
+  double gam = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const bool ok = colok && gy0 + r < a.gh;
+    const int ly = sy * kTR + r;
+    double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4];
+    if (ok) region_coef(a, sp, cd[r], gx, gy0 + r, tk.dt, A4, M4);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) Ac[j * kTCN + (ly + 1) * kTCL + cx + 1] = A4[j];
+    const double dv = ok ? 1.0 / A4[0] : 0.0;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+    double rk = rv[r];
+    if (upd) {
+      const double uo = dv * rv[r];
+      const double p = first ? uo : fma(beta, pv[r], uo);
+      const double sn = tile_s(first, beta, wv[r], sv[r]);
+      rk = fma(-alpha, sn, rv[r]);
+      if (ok) {
+        a.w.P[o + i] = p;
+        Sn[i] = sn;
+        X[i] = fma(alpha, p, xv[r]);
+        Rn[i] = rk;
+      }
+    }
+    const double u = dv * rk;
+    U[(ly + 1) * kTLD + cx + 1] = u;
+    gam = fma(rk, u, gam);
+  }
+  __syncthreads();
+  // ---- 4. w_k = A u_k (W, S, SW coefficients = E, N, NE of the west / south /
+  // south-west point), partial (r.u, w.u)
+  double del = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const int gy = gy0 + r;
+    if (!(colok && gy < a.gh)) continue;
+    const int64_t i = (int64_t)gy * a.wd + gx;
+    const int b = (sy * kTR + r + 1) * kTLD + cx + 1;
+    const int lc = (sy * kTR + r + 1) * kTCL + cx + 1;
+    const double c = Ac[lc], e = Ac[kTCN + lc], nn = Ac[2 * kTCN + lc], ne = Ac[3 * kTCN + lc];
+    const double cw = Ac[kTCN + lc - 1];
+    const double cs = Ac[2 * kTCN + lc - kTCL];
+    const double csw = Ac[3 * kTCN + lc - kTCL - 1];
+    const double uc = U[b];
+    double acc0 = c * uc, acc1 = csw * U[b - kTLD - 1];
+    acc0 = fma(cs, U[b - kTLD], acc0);
+    acc1 = fma(cw, U[b - 1], acc1);
+    acc0 = fma(e, U[b + 1], acc0);
+    acc1 = fma(nn, U[b + kTLD], acc1);
+    acc0 = fma(ne, U[b + kTLD + 1], acc0);
+    const double w = acc0 + acc1;
+    Wn[i] = w;
+    del = fma(w, uc, del);
+  }
+  double v[2] = {gam, del};
+  if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
+}
+
 template <int kTH, int kTR>
 constexpr size_t tile_iter_smem() {
   return sizeof(double) * ((kTH + 2) * kTLD + 4 * (kTH + 1) * (kTW + 1));
@@ -774,6 +910,8 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
   if (!attr) {
     MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_kernel<kTH, kTR, kMinB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_rg_kernel<kTH, kTR, kMinB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     attr = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -786,8 +924,13 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
-  MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_kernel<kTH, kTR, kMinB>, a));
-  MLMCP_LAUNCH_CHECK("tile_iter_kernel");
+  if (a.rcode != nullptr) {
+    MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_rg_kernel<kTH, kTR, kMinB>, a));
+    MLMCP_LAUNCH_CHECK("tile_iter_rg_kernel");
+  } else {
+    MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_kernel<kTH, kTR, kMinB>, a));
+    MLMCP_LAUNCH_CHECK("tile_iter_kernel");
+  }
   return MLMCP_OK;
 }
 
@@ -834,7 +977,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const int lc = (ly + 1) * kTCL + cx + 1, lv = (ly + 1) * kTLD + cx + 1;
     if (region) {
       double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4] = {0.0, 0.0, 0.0, 0.0};
-      if (ok) region_coef(a, sp, gx, gy0 + r, tk.dt, A4, M4);
+      if (ok) region_coef(a, sp, __ldg(a.rcode + i), gx, gy0 + r, tk.dt, A4, M4);
 #pragma unroll
       for (int j = 0; j < 4; ++j) Ac[j * kTCN + lc] = A4[j];
 #pragma unroll
@@ -872,7 +1015,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     // region mode: E, N, NE of A and M at the west column / south row
     if (region && ((lx == -1 && ly < kTH) || (ly == -1 && lx < kTW))) {
       double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4] = {0.0, 0.0, 0.0, 0.0};
-      if (ok) region_coef(a, sp, hx, hy, tk.dt, A4, M4);
+      if (ok) region_coef(a, sp, __ldg(a.rcode + j), hx, hy, tk.dt, A4, M4);
       const int lc = (ly + 1) * kTCL + lx + 1;
 #pragma unroll
       for (int q = 1; q < 4; ++q) {

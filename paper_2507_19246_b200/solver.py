@@ -223,7 +223,12 @@ class FESolver(BatchSolver):
             # grids; the operator is computed from the per-sample region
             # parameters instead of streamed: 112 -> 80 B/point per PCG iteration)
             if not self.sys.sm_resident and os.environ.get("MLMCP_TILE_OPERATOR") != "stored":
-                self.sys.set_region_grid(fe.region_grid(m, region, self.n_regions))
+                rg = fe.region_grid(m, region, self.n_regions)
+                if rg is not None:
+                    try:
+                        self.sys.set_region_grid(rg)
+                    except ValueError:       # no 2D grid view of the pattern (no tile path)
+                        self.sys.region_grid = None
 
     @property
     def region_mode(self) -> bool:
