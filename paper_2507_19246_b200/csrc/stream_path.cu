@@ -494,15 +494,33 @@ __global__ void form_tile_kernel(SArgs a, double dt) {
   a.w.dinv[(int64_t)s * a.N + i] = 1.0 / c;
 }
 
-// Region-linear operator at interior grid point (gx, gy): the symmetric half
-// (C, E, N, NE) of A = M + dt K (and of M) from the per-sample region
-// parameters sp[r] = (sigma_r, nu_r) of the six triangles around the point,
-// summed in the assembly gather map's element order with assemble_kernel's
-// and op_entry's arithmetic — the same doubles the stored path streams.
-// E / N / NE are 0 where the neighbour is a boundary node.
-__device__ __forceinline__ void region_coef(const SArgs& a, const double2* sp, uint32_t code,
-                                            int gx, int gy, double dt, double (&A)[4],
-                                            double (&Mo)[4]) {
+// Region-linear operator at interior grid point (gx, gy), from the point's
+// own six triangles (code: their regions, 4 bits each, in increasing element
+// order e0..e5 = SWl, SWu, Su, Wl, Ol, Ou) and the task's region parameters
+// sp[r] = (sigma_r, nu_r).  Every stencil coefficient of the point couples it
+// to a neighbour through triangles that touch the point, so all seven are
+// available here: C over e0..e5, E over (e2, e4), N (e3, e5), NE (e4, e5), and
+// W (e1, e3), S (e0, e2), SW (e0, e1) — the E, N, NE of the west, south and
+// south-west neighbours with the same weights, hence the same doubles.  Sums
+// run in the assembly gather map's element order with assemble_kernel's and
+// op_entry's arithmetic: bitwise the CSR values mlmcp_assemble writes.
+__device__ __forceinline__ double region_diag(const SArgs& a, const double2* sp, uint32_t code,
+                                              double dt, double* m_out = nullptr) {
+  double m = 0.0, k = 0.0;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    const double2 p = sp[(code >> (4 * e)) & 15u];
+    m = __dadd_rn(m, __dmul_rn(p.x, a.rmw[e]));
+    k = __dadd_rn(k, __dmul_rn(p.y, a.rkw[e]));
+  }
+  if (m_out) *m_out = m;
+  return op_entry(m, k, dt);
+}
+
+// slot order SW, S, W, C, E, N, NE (the CSR column order of a row)
+__device__ __forceinline__ void region_stencil(const SArgs& a, const double2* sp, uint32_t code,
+                                               int gx, int gy, double dt, double (&A)[7],
+                                               double (&Mo)[7]) {
   double2 p[6];
 #pragma unroll
   for (int e = 0; e < 6; ++e) p[e] = sp[(code >> (4 * e)) & 15u];
@@ -512,22 +530,25 @@ __device__ __forceinline__ void region_coef(const SArgs& a, const double2* sp, u
     m = __dadd_rn(m, __dmul_rn(p[e].x, a.rmw[e]));
     k = __dadd_rn(k, __dmul_rn(p[e].y, a.rkw[e]));
   }
-  Mo[0] = m;
-  A[0] = op_entry(m, k, dt);
-  const bool e_ok = gx + 1 < a.wd, n_ok = gy + 1 < a.gh;
-  const int e0[3] = {2, 3, 4}, e1[3] = {4, 5, 5};
-  const bool ok[3] = {e_ok, n_ok, e_ok && n_ok};
+  Mo[3] = m;
+  A[3] = op_entry(m, k, dt);
+  const bool w_ = gx > 0, s_ = gy > 0, e_ = gx + 1 < a.wd, n_ = gy + 1 < a.gh;
+  //                      SW      S       W       E       N       NE
+  const int slot[6] = {0, 1, 2, 4, 5, 6};
+  const int e0[6] = {0, 0, 1, 2, 3, 4}, e1[6] = {1, 2, 3, 4, 5, 5};
+  const int cw[6] = {10, 8, 6, 6, 8, 10};
+  const bool ok[6] = {w_ && s_, s_, w_, e_, n_, e_ && n_};
 #pragma unroll
-  for (int c = 0; c < 3; ++c) {
+  for (int c = 0; c < 6; ++c) {
     double mm = 0.0, kk = 0.0;
     if (ok[c]) {
-      mm = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].x, a.rmw[6 + 2 * c])),
-                     __dmul_rn(p[e1[c]].x, a.rmw[7 + 2 * c]));
-      kk = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].y, a.rkw[6 + 2 * c])),
-                     __dmul_rn(p[e1[c]].y, a.rkw[7 + 2 * c]));
+      mm = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].x, a.rmw[cw[c]])),
+                     __dmul_rn(p[e1[c]].x, a.rmw[cw[c] + 1]));
+      kk = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].y, a.rkw[cw[c]])),
+                     __dmul_rn(p[e1[c]].y, a.rkw[cw[c] + 1]));
     }
-    Mo[1 + c] = mm;
-    A[1 + c] = ok[c] ? op_entry(mm, kk, dt) : 0.0;
+    Mo[slot[c]] = mm;
+    A[slot[c]] = ok[c] ? op_entry(mm, kk, dt) : 0.0;
   }
 }
 
@@ -728,38 +749,37 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
 
 // Region-mode iteration kernel (mlmcp_ctx_set_region_grid): tile_iter_kernel's
 // arithmetic with the operator computed from the task's region parameters
-// instead of streamed.  Every global load of the launch (own-point vectors,
-// the thread's halo point, the triangle-region codes) is issued before the
-// coefficient arithmetic, so the memory pipes stay busy while the operator is
-// formed; own-point coefficients of A land in shared memory (the neighbours'
-// W, S, SW), D^-1 = 1/C in registers.  HBM per point: read x r w s p, write
-// x r w s p = 80 B (the code array, 4 B per point shared by all tasks, stays
-// in L2).
+// instead of streamed.  Every global load of the launch (task state, own-point
+// vectors, the thread's halo point, the triangle-region codes) is issued before
+// any dependent arithmetic; each point forms its own seven stencil
+// coefficients (region_stencil) right where the SpMV needs them, so shared
+// memory holds only u with its halo (9.5 KB per CTA) and no coefficient moves
+// between threads.  HBM per point: read x r w s p, write x r w s p = 80 B (the
+// 4-byte region codes are shared by every task and stay in L2).
 template <int kTH, int kTR, int kMinB>
 __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(SArgs a) {
   constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
   constexpr int kNT = kTW * (kTH / kTR);
   static_assert(kTHalo <= kNT, "one halo point per thread");
-  constexpr int kTCL = kTW + 1;
-  constexpr int kTCN = (kTH + 1) * kTCL;
   extern __shared__ __align__(16) double tsm[];
   double* U = tsm;                              // (kTH + 2) * kTLD
-  double* Ac = U + (kTH + 2) * kTLD;            // C, E, N, NE of the tile, W column, S row
   __shared__ double red[2 * 4 * 32];
   __shared__ double2 sp[16];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
+  // task state: every thread reads it (same addresses: broadcast loads; the
+  // previous launch has completed, and this launch's last tile of task t
+  // writes it only after every tile of t has read it)
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
   const int32_t* ti = a.w.ti + t * kTI;
-  int mode = 0;   // 0 skip, 1 run, 2 zero solution
-  if (threadIdx.x == 0 && task_live(a, tk, t)) {
-    const int st = ti[I_STATE];
-    mode = st == ST_RUN ? 1 : (st == ST_ZERO ? 2 : 0);
-  }
-  mode = bcast_int(mode);
-  if (mode == 0) return;
+  const double* td = a.w.td + t * kTD;
+  const int st = ti[I_STATE];
   const int k = ti[I_IT_STEP];
+  const int code_ok = ti[I_CODE];
+  const int act = (a.active != nullptr && tk.group >= 0) ? a.active[tk.group] : 1;
+  const double alpha_l = td[D_ALPHA], beta_l = td[D_BETA];
+  if (code_ok != MLMCP_ST_OK || act == 0 || (st != ST_RUN && st != ST_ZERO)) return;
   const int64_t N = a.N, o = (int64_t)t * N;
   const int tx0 = (blockIdx.x % a.ntx) * kTW, ty0 = (blockIdx.x / a.ntx) * kTH;
   const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
@@ -767,15 +787,14 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
   const int gy0 = ty0 + sy * kTR;
   const bool colok = gx < a.wd;
   double* X = a.w.X + o;
-  if (mode == 2) {
+  if (st == ST_ZERO) {
 #pragma unroll
     for (int r = 0; r < kTR; ++r)
       if (colok && gy0 + r < a.gh) X[(int64_t)(gy0 + r) * a.wd + gx] = 0.0;
     return;
   }
   const bool odd = k & 1, upd = k > 0, first = k == 1;
-  const double* td = a.w.td + t * kTD;
-  const double alpha = upd ? td[D_ALPHA] : 0.0, beta = upd ? td[D_BETA] : 0.0;
+  const double alpha = upd ? alpha_l : 0.0, beta = upd ? beta_l : 0.0;
   const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;   // r_{k-1} (k == 0: r_0)
   const double* Wo = odd ? a.w.Wv + o : a.w.W1 + o;            // w_{k-1}
   const double* So = odd ? a.w.S1 + o : a.w.Sv + o;            // s_{k-2}
@@ -796,21 +815,21 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
     pv[r] = (ok && upd && !first) ? __ldcg(a.w.P + o + i) : 0.0;
     xv[r] = (ok && upd) ? __ldcg(X + i) : 0.0;
   }
-  int hlx = 0, hly = 0;
-  bool hin = false;
+  int hb = -1;                 // shared-memory slot of this thread's halo point
   double hr = 0.0, hw = 0.0, hs = 0.0;
   uint32_t hcode = 0u;
   if (threadIdx.x < kTHalo) {
     const int h = threadIdx.x;
-    if (h < kTW + 2) { hlx = h - 1; hly = -1; }
-    else if (h < 2 * (kTW + 2)) { hlx = h - (kTW + 2) - 1; hly = kTH; }
-    else if (h < 2 * (kTW + 2) + kTH) { hlx = -1; hly = h - 2 * (kTW + 2); }
-    else { hlx = kTW; hly = h - 2 * (kTW + 2) - kTH; }
-    const int hx = tx0 + hlx, hy = ty0 + hly;
-    hin = hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh;
-    if (hin) {
+    int lx, ly;
+    if (h < kTW + 2) { lx = h - 1; ly = -1; }
+    else if (h < 2 * (kTW + 2)) { lx = h - (kTW + 2) - 1; ly = kTH; }
+    else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
+    else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
+    hb = (ly + 1) * kTLD + lx + 1;
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
       const int64_t j = (int64_t)hy * a.wd + hx;
-      hcode = __ldg(a.rcode + j);
+      hcode = __ldg(a.rcode + j) | 0x80000000u;    // bit 31: inside the grid
       hr = __ldcg(Ro + j);
       if (upd) {
         hw = __ldcg(Wo + j);
@@ -820,34 +839,22 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
   }
   load_region_params(a, tk.sample, sp);
   __syncthreads();
-  // ---- 2. the halo point: coefficients (W column / S row: E, N, NE into
-  // shared memory), u = D^-1 r_k
-  if (threadIdx.x < kTHalo) {
-    double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4];
+  // ---- 2. the halo point: u = D^-1 r_k with D = C of that point
+  if (hb >= 0) {
     double u = 0.0;
-    if (hin) {
-      region_coef(a, sp, hcode, tx0 + hlx, ty0 + hly, tk.dt, A4, M4);
+    if (hcode & 0x80000000u) {
       double r = hr;
       if (upd) r = fma(-alpha, tile_s(first, beta, hw, hs), r);
-      u = (1.0 / A4[0]) * r;
+      u = (1.0 / region_diag(a, sp, hcode & 0x00ffffffu, tk.dt)) * r;
     }
-    U[(hly + 1) * kTLD + hlx + 1] = u;
-    if ((hlx == -1 && hly < kTH) || (hly == -1 && hlx < kTW)) {
-#pragma unroll
-      for (int q = 1; q < 4; ++q) Ac[q * kTCN + (hly + 1) * kTCL + hlx + 1] = A4[q];
-    }
+    U[hb] = u;
   }
-  // ---- 3. own points: coefficients, update of iteration k-1, u_k
+  // ---- 3. own points: update of iteration k-1, u_k
   double gam = 0.0;
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const bool ok = colok && gy0 + r < a.gh;
-    const int ly = sy * kTR + r;
-    double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4];
-    if (ok) region_coef(a, sp, cd[r], gx, gy0 + r, tk.dt, A4, M4);
-#pragma unroll
-    for (int j = 0; j < 4; ++j) Ac[j * kTCN + (ly + 1) * kTCL + cx + 1] = A4[j];
-    const double dv = ok ? 1.0 / A4[0] : 0.0;
+    const double dv = ok ? 1.0 / region_diag(a, sp, cd[r], tk.dt) : 0.0;
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
     double rk = rv[r];
     if (upd) {
@@ -863,12 +870,11 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
       }
     }
     const double u = dv * rk;
-    U[(ly + 1) * kTLD + cx + 1] = u;
+    U[(sy * kTR + r + 1) * kTLD + cx + 1] = u;
     gam = fma(rk, u, gam);
   }
   __syncthreads();
-  // ---- 4. w_k = A u_k (W, S, SW coefficients = E, N, NE of the west / south /
-  // south-west point), partial (r.u, w.u)
+  // ---- 4. w_k = A u_k with the point's own stencil, partial (r.u, w.u)
   double del = 0.0;
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
@@ -876,24 +882,26 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
     if (!(colok && gy < a.gh)) continue;
     const int64_t i = (int64_t)gy * a.wd + gx;
     const int b = (sy * kTR + r + 1) * kTLD + cx + 1;
-    const int lc = (sy * kTR + r + 1) * kTCL + cx + 1;
-    const double c = Ac[lc], e = Ac[kTCN + lc], nn = Ac[2 * kTCN + lc], ne = Ac[3 * kTCN + lc];
-    const double cw = Ac[kTCN + lc - 1];
-    const double cs = Ac[2 * kTCN + lc - kTCL];
-    const double csw = Ac[3 * kTCN + lc - kTCL - 1];
+    double A7[7], M7[7];
+    region_stencil(a, sp, cd[r], gx, gy, tk.dt, A7, M7);
     const double uc = U[b];
-    double acc0 = c * uc, acc1 = csw * U[b - kTLD - 1];
-    acc0 = fma(cs, U[b - kTLD], acc0);
-    acc1 = fma(cw, U[b - 1], acc1);
-    acc0 = fma(e, U[b + 1], acc0);
-    acc1 = fma(nn, U[b + kTLD], acc1);
-    acc0 = fma(ne, U[b + kTLD + 1], acc0);
+    double acc0 = A7[3] * uc, acc1 = A7[0] * U[b - kTLD - 1];
+    acc0 = fma(A7[1], U[b - kTLD], acc0);
+    acc1 = fma(A7[2], U[b - 1], acc1);
+    acc0 = fma(A7[4], U[b + 1], acc0);
+    acc1 = fma(A7[5], U[b + kTLD], acc1);
+    acc0 = fma(A7[6], U[b + kTLD + 1], acc0);
     const double w = acc0 + acc1;
     Wn[i] = w;
     del = fma(w, uc, del);
   }
   double v[2] = {gam, del};
   if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
+}
+
+template <int kTH, int kTR>
+constexpr size_t tile_iter_rg_smem() {
+  return sizeof(double) * (kTH + 2) * kTLD;
 }
 
 template <int kTH, int kTR>
@@ -911,7 +919,8 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
     MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_kernel<kTH, kTR, kMinB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_rg_kernel<kTH, kTR, kMinB>,
-                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tile_iter_rg_smem<kTH, kTR>()));
     attr = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -925,6 +934,7 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
   if (a.rcode != nullptr) {
+    lc.dynamicSmemBytes = tile_iter_rg_smem<kTH, kTR>();
     MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_rg_kernel<kTH, kTR, kMinB>, a));
     MLMCP_LAUNCH_CHECK("tile_iter_rg_kernel");
   } else {
@@ -946,10 +956,12 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
   static_assert(kTHalo <= kTW * (kTH / kTR), "one halo point per thread");
   extern __shared__ __align__(16) double ism[];
-  double* Ac = ism;                 // [4][kTCN]
-  double* XV = Ac + 4 * kTCN;       // x_0 with halo
-  double* AV = XV + kTV;            // a_n with halo
-  double* Mc = AV + kTV;            // region mode: E, N, NE of M [3][kTCN]
+  const bool region = a.rcode != nullptr;
+  // region mode: each point forms its own stencils (region_stencil), no
+  // operator in shared memory
+  double* Ac = ism;                                  // [4][kTCN] (stored operator)
+  double* XV = region ? ism : Ac + 4 * kTCN;         // x_0 with halo
+  double* AV = XV + kTV;                             // a_n with halo
   __shared__ double red[2 * 4 * 32];
   __shared__ double2 sp[16];
   const int t = blockIdx.y;
@@ -960,11 +972,10 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
   const int gx = tx0 + cx, gy0 = ty0 + sy * kTR;
   const bool colok = gx < a.wd;
-  const bool region = a.rcode != nullptr;
   const double* As = a.w.A + (int64_t)tk.sample * 4 * N;
   const double* Ms = a.w.A + ((int64_t)a.S + tk.sample) * 4 * N;
   const double* An = a.w.Wv + o;   // a_n (step_end / copy_in)
-  double mown[kTR], dv[kTR];       // region mode: own C of M, D^-1
+  double dv[kTR];
   if (region) {
     load_region_params(a, tk.sample, sp);
     __syncthreads();
@@ -975,16 +986,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const bool ok = colok && gy0 + r < a.gh;
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
     const int lc = (ly + 1) * kTCL + cx + 1, lv = (ly + 1) * kTLD + cx + 1;
-    if (region) {
-      double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4] = {0.0, 0.0, 0.0, 0.0};
-      if (ok) region_coef(a, sp, __ldg(a.rcode + i), gx, gy0 + r, tk.dt, A4, M4);
-#pragma unroll
-      for (int j = 0; j < 4; ++j) Ac[j * kTCN + lc] = A4[j];
-#pragma unroll
-      for (int j = 0; j < 3; ++j) Mc[j * kTCN + lc] = M4[1 + j];
-      mown[r] = M4[0];
-      dv[r] = ok ? 1.0 / A4[0] : 0.0;
-    } else {
+    if (!region) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) cp8(&Ac[j * kTCN + lc], As + j * N + i, ok);
     }
@@ -1012,17 +1014,6 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const int64_t j = ok ? (int64_t)hy * a.wd + hx : 0;
     const int lv = (ly + 1) * kTLD + lx + 1;
     cp8(&AV[lv], An + j, ok);
-    // region mode: E, N, NE of A and M at the west column / south row
-    if (region && ((lx == -1 && ly < kTH) || (ly == -1 && lx < kTW))) {
-      double A4[4] = {0.0, 0.0, 0.0, 0.0}, M4[4] = {0.0, 0.0, 0.0, 0.0};
-      if (ok) region_coef(a, sp, __ldg(a.rcode + j), hx, hy, tk.dt, A4, M4);
-      const int lc = (ly + 1) * kTCL + lx + 1;
-#pragma unroll
-      for (int q = 1; q < 4; ++q) {
-        Ac[q * kTCN + lc] = A4[q];
-        Mc[(q - 1) * kTCN + lc] = M4[q];
-      }
-    }
   }
   cp_commit();
   // initial guess x_0 (the guess kernel's arithmetic, folded in) for the own
@@ -1119,17 +1110,13 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
                          kTCN + lc, 2 * kTCN + lc, 3 * kTCN + lc};
     const int vofs[7] = {b - kTLD - 1, b - kTLD, b - 1, b, b + 1, b + kTLD, b + kTLD + 1};
     const bool w_ = gx > 0, s_ = gy > 0;
-    double mco[7];
+    double mco[7], aco[7];
     if (region) {
-      // M's E, N, NE of the west / south / south-west points and the own point
-      mco[0] = Mc[2 * kTCN + lc - kTCL - 1];
-      mco[1] = Mc[kTCN + lc - kTCL];
-      mco[2] = Mc[lc - 1];
-      mco[3] = mown[r];
-      mco[4] = Mc[lc];
-      mco[5] = Mc[kTCN + lc];
-      mco[6] = Mc[2 * kTCN + lc];
+      region_stencil(a, sp, __ldg(a.rcode + i), gx, gy, tk.dt, aco, mco);
+      dv[r] = 1.0 / aco[3];
     } else {
+#pragma unroll
+      for (int d = 0; d < 7; ++d) aco[d] = Ac[cofs[d]];
       mco[0] = (w_ && s_) ? __ldg(Ms + 3 * N + i - a.wd - 1) : 0.0;
       mco[1] = s_ ? __ldg(Ms + 2 * N + i - a.wd) : 0.0;
       mco[2] = w_ ? __ldg(Ms + N + i - 1) : 0.0;
@@ -1142,7 +1129,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
 #pragma unroll
     for (int d = 0; d < 7; ++d) {
       mx = fma(mco[d], AV[vofs[d]], mx);
-      ax = fma(Ac[cofs[d]], XV[vofs[d]], ax);
+      ax = fma(aco[d], XV[vofs[d]], ax);
     }
     const double bv = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, prof[r])));
     a.w.R[o + i] = bv - ax;
@@ -1154,7 +1141,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
 
 template <int kTH, int kTR>
 constexpr size_t tile_init_smem(bool region = false) {
-  return sizeof(double) * ((region ? 7 : 4) * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
+  return sizeof(double) * ((region ? 0 : 4) * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
 }
 
 
@@ -1708,10 +1695,10 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     if (!attr) {
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<8, 2, 4>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tile_init_smem<8, 2>(true)));
+                                            (int)tile_init_smem<8, 2>(false)));
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<16, 4, 3>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tile_init_smem<16, 4>(true)));
+                                            (int)tile_init_smem<16, 4>(false)));
       attr = true;
     }
   }

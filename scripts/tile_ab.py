@@ -29,7 +29,12 @@ except Exception:
 cfg = get_config(cfg_i)
 qs = {}
 for mode in modes:
-    os.environ["MLMCP_TILE_OPERATOR"] = mode
+    op, _, tcfg = mode.partition("@")       # e.g. "region@3": MLMCP_TILE_CFG=3
+    os.environ["MLMCP_TILE_OPERATOR"] = op
+    if tcfg:
+        os.environ["MLMCP_TILE_CFG"] = tcfg
+    else:
+        os.environ.pop("MLMCP_TILE_CFG", None)
     fam = eddy_current_family(cfg_i, device="cuda:0")
     sol = fam.solver
     d = draw_level(fam.uncertain, 0, 0, range(1, S + 1))
@@ -69,7 +74,10 @@ for mode in modes:
           flush=True)
     del M, K, rp, res, fam, sol
     torch.cuda.empty_cache()
-if len(qs) == 2:
-    a, b = list(qs.values())
-    print(json.dumps({"max_rel_qoi_diff": float(np.max(np.abs(a - b) / np.abs(a))),
-                      "bitwise": bool(np.array_equal(a, b))}))
+if len(qs) >= 2:
+    vals = list(qs.values())
+    a = vals[0]
+    for name, b in list(qs.items())[1:]:
+        print(json.dumps({"vs_first": name,
+                          "max_rel_qoi_diff": float(np.max(np.abs(a - b) / np.maximum(np.abs(a), 1e-300))),
+                          "bitwise": bool(np.array_equal(a, b))}))

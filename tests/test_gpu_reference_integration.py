@@ -58,7 +58,7 @@ def _swap(monkeypatch, ref):
 
 CASES = {
     # family builder, hierarchy, horizon, Parareal (M, dt_coarse, tol, K_max), tolerance
-    "steinmetz": ("steinmetz_family", [1e-3, 1e-4], 0.02, (8, 1e-3, 1e-8, 8), 1e-9),
+    "steinmetz": ("steinmetz_family", [1e-3, 1e-4], 0.02, (10, 1e-3, 1e-8, 10), 1e-9),
     "synthetic": ("synthetic_family", [1e-3, 2.5e-4], 0.02, (4, 1e-3, 1e-8, 4), 1e-8),
 }
 
