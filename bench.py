@@ -341,15 +341,13 @@ def measured_peak():
 
 
 def ncu_traffic(kernel: str):
-    """dram bytes per launch of the roofline kernel from the committed ncu capture."""
+    """The committed ncu summary of the roofline kernel (profiles/ncu_top_kernel.json,
+    scripts/ncu_summary.py): dram bytes per PCG task-iteration and its source."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_top_kernel.json")) as fh:
-            d = json.load(fh)
-        ent = d.get(kernel) or {}
-        return ent.get("dram_bytes_per_launch"), ent.get("algorithmic_bytes_per_launch"), \
-            ent.get("source")
+            return json.load(fh).get(kernel) or {}
     except Exception:
-        return None, None, None
+        return {}
 
 
 class DeviceEstimate:
@@ -537,21 +535,32 @@ def main():
     d2h = 32 * cfg.levels + 16 * tasks + (8 * counts[-1] if pcfg else 0)
 
     if streaming:
-        kernel = "tile_iter_kernel<16,4,3> (one fused launch per PCG iteration)"
+        region = sol.region_mode()
+        kname = "tile_iter_rg_kernel" if region else "tile_iter_kernel"
+        kernel = f"{kname}<16,4,3> (one fused launch per PCG iteration)"
+        streamed = (80 if region else 112) * N          # bytes the kernel must move per task-iteration
         k_ms = it_ms / max(1, args.steps)
-        achieved = its / max(1, args.steps) * b_it / (k_ms / 1000.0) / 1e9
-        traffic, alg, src = ncu_traffic("tile_iter_kernel")
+        n_its = its / max(1, args.steps)
+        achieved = n_its * b_it / (k_ms / 1000.0) / 1e9
+        nc = ncu_traffic(kname)
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak, "traffic": traffic,
+                "frac": achieved / peak,
+                "traffic": nc.get("dram_bytes_per_task_iteration"),
+                "traffic_unit": "dram bytes per PCG task-iteration (ncu, one launch)",
                 "kernel": kernel,
-                "algorithmic_bytes": f"{its // max(1, args.steps)} PCG iterations per estimate x "
-                                     f"(8 nnz + 56 N) = x {b_it} B",
+                "algorithmic_bytes": f"{int(n_its)} PCG task-iterations per estimate x B_it "
+                                     f"(8 nnz + 56 N) = {b_it} B each (SURVEY 8(d))",
+                "streamed_bytes_per_task_iteration": streamed,
+                "frac_streamed": n_its * streamed / (k_ms / 1000.0) / 1e9 / peak,
                 "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms,
                 "launches_per_step": it_launches // max(1, args.steps), "peak_kind": peak_kind,
-                "ncu_algorithmic_bytes_per_launch": alg, "ncu_source": src,
-                "note": "achieved = PCG iterations x B_it / device time of the iteration launches "
-                        "(CUDA events on their stream inside libmlmcp, mlmcp_stream_timing), "
-                        "over the timed estimates; traffic = ncu dram bytes of one launch"}
+                "ncu_source": nc.get("source"), "ncu_launch": nc.get("launch"),
+                "note": "achieved = PCG task-iterations x B_it / device time of the iteration "
+                        "launches (CUDA events on their stream inside libmlmcp, "
+                        "mlmcp_stream_timing) over the timed estimates; B_it counts the "
+                        "per-sample operator (8 nnz); the region-linear kernel computes it from "
+                        "the sample's region parameters and streams only the PCG vectors "
+                        "(frac_streamed: the same time against those bytes)"}
     else:
         kernel = "fused_kernel<GridOp,2> (SM-resident; whole estimate in one persistent launch)"
         achieved = its / max(1, args.steps) * b_it / (ms / 1000.0) / 1e9

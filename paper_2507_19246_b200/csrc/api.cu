@@ -9,6 +9,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <unordered_map>
 #include <vector>
 
 #include "mlmcp_internal.cuh"
@@ -374,7 +375,8 @@ int mlmcp_ctx_destroy(mlmcp_ctx* c) {
   cudaFree(c->celem);
   cudaFree(c->cmw);
   cudaFree(c->ckw);
-  cudaFree(c->rcode);
+  cudaFree(c->rcls);
+  cudaFree(c->rckey);
   if (c->host_counters) cudaFreeHost(c->host_counters);
   if (c->step_exec) cudaGraphExecDestroy(c->step_exec);
   for (cudaEvent_t e : c->iter_ev)
@@ -449,8 +451,11 @@ int mlmcp_ctx_set_region_grid(mlmcp_ctx* c, int n_regions, const uint32_t* code,
   if (c == nullptr) return einval("null context");
   if (n_regions == 0) {   // unregister
     cudaSetDevice(c->device);
-    cudaFree(c->rcode);
-    c->rcode = nullptr;
+    cudaFree(c->rcls);
+    cudaFree(c->rckey);
+    c->rcls = nullptr;
+    c->rckey = nullptr;
+    c->rC = 0;
     c->rR = 0;
     return MLMCP_OK;
   }
@@ -462,12 +467,42 @@ int mlmcp_ctx_set_region_grid(mlmcp_ctx* c, int n_regions, const uint32_t* code,
     for (int e = 0; e < 6; ++e)
       if ((int)((code[i] >> (4 * e)) & 15u) >= n_regions)
         return einval("region grid: triangle region index out of range");
+  // classes: distinct (code, neighbour mask) keys; the mask bits say which of
+  // the SW, S, W, E, N, NE neighbours are interior points (Dirichlet rows drop
+  // the others).  More than 256 classes: no region mode (stored operator).
+  std::vector<uint8_t> cls((size_t)c->n);
+  std::vector<uint32_t> keys;
+  {
+    std::unordered_map<uint32_t, int> idx;
+    const int wd = c->cl_wd, gh = c->cl_h;
+    for (int i = 0; i < c->n && keys.size() <= 256; ++i) {
+      const int gx = i % wd, gy = i / wd;
+      const bool w = gx > 0, s = gy > 0, e = gx + 1 < wd, n = gy + 1 < gh;
+      const uint32_t mask = (uint32_t)(w && s) | ((uint32_t)s << 1) | ((uint32_t)w << 2) |
+                            ((uint32_t)e << 3) | ((uint32_t)n << 4) | ((uint32_t)(e && n) << 5);
+      const uint32_t key = (code[i] & 0x00ffffffu) | (mask << 24);
+      auto it = idx.find(key);
+      if (it == idx.end()) {
+        it = idx.emplace(key, (int)keys.size()).first;
+        keys.push_back(key);
+      }
+      cls[(size_t)i] = (uint8_t)(it->second & 255);
+    }
+  }
   MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
-  cudaFree(c->rcode);
-  c->rcode = nullptr;
-  MLMCP_CUDA_CHECK(cudaMalloc(&c->rcode, sizeof(uint32_t) * (size_t)c->n));
-  MLMCP_CUDA_CHECK(cudaMemcpy(c->rcode, code, sizeof(uint32_t) * (size_t)c->n,
-                              cudaMemcpyHostToDevice));
+  cudaFree(c->rcls);
+  cudaFree(c->rckey);
+  c->rcls = nullptr;
+  c->rckey = nullptr;
+  c->rC = 0;
+  if (keys.size() <= 256) {
+    MLMCP_CUDA_CHECK(cudaMalloc(&c->rcls, (size_t)c->n));
+    MLMCP_CUDA_CHECK(cudaMemcpy(c->rcls, cls.data(), (size_t)c->n, cudaMemcpyHostToDevice));
+    MLMCP_CUDA_CHECK(cudaMalloc(&c->rckey, sizeof(uint32_t) * keys.size()));
+    MLMCP_CUDA_CHECK(cudaMemcpy(c->rckey, keys.data(), sizeof(uint32_t) * keys.size(),
+                                cudaMemcpyHostToDevice));
+    c->rC = (int)keys.size();
+  }
   for (int i = 0; i < 12; ++i) {
     c->rmw[i] = mw[i];
     c->rkw[i] = kw[i];

@@ -62,7 +62,12 @@ struct Ctx {
   double* ckw = nullptr;
   // region-linear operator description (mlmcp_ctx_set_region_grid): the tile
   // kernels compute the operator from per-sample region parameters
-  uint32_t* rcode = nullptr;       // device [n]
+  // point classes: every interior point maps to one of rC distinct
+  // (six triangle regions, Dirichlet-neighbour mask) keys; the tile kernels
+  // form one stencil per class and task in shared memory
+  uint8_t* rcls = nullptr;         // device [n] class of each point
+  uint32_t* rckey = nullptr;       // device [rC] code (24 bits) | neighbour mask << 24
+  int rC = 0;
   int rR = 0;
   double rmw[12] = {0}, rkw[12] = {0};
   // pinned host counters for the streaming path

@@ -66,6 +66,7 @@ struct Work {
   double* R1;      // tile path: second buffers of r, w, s (ping-pong by iteration parity)
   double* W1;
   double* S1;
+  double* ctab;    // region mode: [T][15][rC] per-task class stencils (build_class_table)
   double* partial; // [T][nblk][4]
   double* td;      // [T][kTD]
   int32_t* ti;     // [T][kTI]
@@ -76,7 +77,7 @@ struct Work {
 inline size_t align_up(size_t x) { return (x + 255) & ~size_t(255); }
 
 struct Layout {
-  size_t off[16];
+  size_t off[17];
   size_t total;
 };
 
@@ -84,13 +85,13 @@ Layout make_layout(const Ctx* ctx, int T, int S) {
   // operator slots: ELL width, or the stencil width for the cooperative path
   const size_t N = ctx->n, W = std::max(ctx->max_row_nnz, ctx->stencil_w), T_ = T, S_ = S;
   const size_t nblk = (N + kThreads - 1) / kThreads;
-  size_t sizes[16] = {S_ * std::max(W, (size_t)8) * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
+  size_t sizes[17] = {S_ * std::max(W, (size_t)8) * N * 8, S_ * N * 8, T_ * N * 8, T_ * N * 8, T_ * N * 8,
                       T_ * N * 8,     T_ * N * 8, T_ * nblk * 4 * 8, T_ * kTD * 8,
                       T_ * kTI * 4,   T_ * 4,     64, kRingS * T_ * N * 8,
-                      T_ * N * 8,     T_ * N * 8, T_ * N * 8};
+                      T_ * N * 8,     T_ * N * 8, T_ * N * 8, T_ * 15 * (size_t)ctx->rC * 8};
   Layout L;
   size_t o = 0;
-  for (int i = 0; i < 16; ++i) {
+  for (int i = 0; i < 17; ++i) {
     L.off[i] = o;
     o += align_up(sizes[i]);
   }
@@ -117,6 +118,7 @@ Work carve(void* ws, const Layout& L) {
   w.R1 = reinterpret_cast<double*>(b + L.off[13]);
   w.W1 = reinterpret_cast<double*>(b + L.off[14]);
   w.S1 = reinterpret_cast<double*>(b + L.off[15]);
+  w.ctab = reinterpret_cast<double*>(b + L.off[16]);
   return w;
 }
 
@@ -150,9 +152,11 @@ struct SArgs {
   int use_cond;
   // region-linear operator (mlmcp_ctx_set_region_grid + per-sample region
   // parameters): the tile kernels compute the operator coefficients from the
-  // six triangles around each point instead of streaming them (rcode null:
+  // six triangles around each point instead of streaming them (rcls null:
   // the stored [S][4][N] symmetric halves of A and M)
-  const uint32_t* rcode;   // [N] six 4-bit triangle regions per point
+  const uint8_t* rcls;     // [N] point class (Ctx::rcls)
+  const uint32_t* rckey;   // [rC] class key: six 4-bit triangle regions | neighbour mask << 24
+  int rC;
   const double* rpar;      // [S][R][2] (sigma_r masked, nu_r)
   int R;
   double rmw[12], rkw[12]; // C0..C5, E0, E1, N0, N1, NE0, NE1
@@ -494,32 +498,21 @@ __global__ void form_tile_kernel(SArgs a, double dt) {
   a.w.dinv[(int64_t)s * a.N + i] = 1.0 / c;
 }
 
-// Region-linear operator at interior grid point (gx, gy), from the point's
-// own six triangles (code: their regions, 4 bits each, in increasing element
-// order e0..e5 = SWl, SWu, Su, Wl, Ol, Ou) and the task's region parameters
-// sp[r] = (sigma_r, nu_r).  Every stencil coefficient of the point couples it
-// to a neighbour through triangles that touch the point, so all seven are
-// available here: C over e0..e5, E over (e2, e4), N (e3, e5), NE (e4, e5), and
-// W (e1, e3), S (e0, e2), SW (e0, e1) — the E, N, NE of the west, south and
-// south-west neighbours with the same weights, hence the same doubles.  Sums
-// run in the assembly gather map's element order with assemble_kernel's and
-// op_entry's arithmetic: bitwise the CSR values mlmcp_assemble writes.
-__device__ __forceinline__ double region_diag(const SArgs& a, const double2* sp, uint32_t code,
-                                              double dt, double* m_out = nullptr) {
-  double m = 0.0, k = 0.0;
-#pragma unroll
-  for (int e = 0; e < 6; ++e) {
-    const double2 p = sp[(code >> (4 * e)) & 15u];
-    m = __dadd_rn(m, __dmul_rn(p.x, a.rmw[e]));
-    k = __dadd_rn(k, __dmul_rn(p.y, a.rkw[e]));
-  }
-  if (m_out) *m_out = m;
-  return op_entry(m, k, dt);
-}
-
-// slot order SW, S, W, C, E, N, NE (the CSR column order of a row)
+// Region-linear operator of one point class (Ctx::rckey): the six triangles
+// around the point (code: their regions, 4 bits each, in increasing element
+// order e0..e5 = SWl, SWu, Su, Wl, Ol, Ou), which of the SW, S, W, E, N, NE
+// neighbours are interior points (mask bits 0..5), and the task's region
+// parameters sp[r] = (sigma_r, nu_r).  Every stencil coefficient of the point
+// couples it to a neighbour through triangles that touch the point, so all
+// seven are available here: C over e0..e5, E over (e2, e4), N (e3, e5),
+// NE (e4, e5), and W (e1, e3), S (e0, e2), SW (e0, e1) — the E, N, NE of the
+// west, south and south-west neighbours with the same weights, hence the same
+// doubles.  Sums run in the assembly gather map's element order with
+// assemble_kernel's and op_entry's arithmetic: bitwise the CSR values
+// mlmcp_assemble writes.  Slot order SW, S, W, C, E, N, NE (the CSR column
+// order of a row).
 __device__ __forceinline__ void region_stencil(const SArgs& a, const double2* sp, uint32_t code,
-                                               int gx, int gy, double dt, double (&A)[7],
+                                               uint32_t mask, double dt, double (&A)[7],
                                                double (&Mo)[7]) {
   double2 p[6];
 #pragma unroll
@@ -532,24 +525,56 @@ __device__ __forceinline__ void region_stencil(const SArgs& a, const double2* sp
   }
   Mo[3] = m;
   A[3] = op_entry(m, k, dt);
-  const bool w_ = gx > 0, s_ = gy > 0, e_ = gx + 1 < a.wd, n_ = gy + 1 < a.gh;
   //                      SW      S       W       E       N       NE
   const int slot[6] = {0, 1, 2, 4, 5, 6};
   const int e0[6] = {0, 0, 1, 2, 3, 4}, e1[6] = {1, 2, 3, 4, 5, 5};
   const int cw[6] = {10, 8, 6, 6, 8, 10};
-  const bool ok[6] = {w_ && s_, s_, w_, e_, n_, e_ && n_};
 #pragma unroll
   for (int c = 0; c < 6; ++c) {
+    const bool ok = (mask >> c) & 1u;
     double mm = 0.0, kk = 0.0;
-    if (ok[c]) {
+    if (ok) {
       mm = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].x, a.rmw[cw[c]])),
                      __dmul_rn(p[e1[c]].x, a.rmw[cw[c] + 1]));
       kk = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].y, a.rkw[cw[c]])),
                      __dmul_rn(p[e1[c]].y, a.rkw[cw[c] + 1]));
     }
     Mo[slot[c]] = mm;
-    A[slot[c]] = ok[c] ? op_entry(mm, kk, dt) : 0.0;
+    A[slot[c]] = ok ? op_entry(mm, kk, dt) : 0.0;
   }
+}
+
+// The task's stencils, one per point class (once per propagate call; every
+// tile launch of the task copies them into shared memory, load_class_table):
+// tab[d * rC + c] holds A's slot d (0..6), tab[7 * rC + c] = 1 / A_C (the
+// Jacobi weight), tab[(8 + d) * rC + c] the mass matrix's slot d.
+__device__ __forceinline__ void load_region_params(const SArgs& a, int sample, double2* sp);
+__global__ void class_table_kernel(SArgs a) {
+  __shared__ double2 sp[16];
+  const int t = blockIdx.x;
+  const mlmcp_task tk = a.tasks[t];
+  load_region_params(a, tk.sample, sp);
+  __syncthreads();
+  const int C = a.rC;
+  double* tab = a.w.ctab + (int64_t)t * 15 * C;
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const uint32_t key = __ldg(a.rckey + c);
+    double A7[7], M7[7];
+    region_stencil(a, sp, key & 0x00ffffffu, key >> 24, tk.dt, A7, M7);
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+      tab[d * C + c] = A7[d];
+      tab[(8 + d) * C + c] = M7[d];
+    }
+    tab[7 * C + c] = 1.0 / A7[3];
+  }
+}
+
+// the first `rows` rows of task t's class table into shared memory (caller syncs)
+__device__ __forceinline__ void load_class_table(const SArgs& a, int t, double* tab, int rows) {
+  const int n = rows * a.rC;
+  const double* g = a.w.ctab + (int64_t)t * 15 * a.rC;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tab[i] = __ldg(g + i);
 }
 
 // the task's region parameters into shared memory (block-wide; caller syncs)
@@ -750,12 +775,14 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_kernel(SAr
 // Region-mode iteration kernel (mlmcp_ctx_set_region_grid): tile_iter_kernel's
 // arithmetic with the operator computed from the task's region parameters
 // instead of streamed.  Every global load of the launch (task state, own-point
-// vectors, the thread's halo point, the triangle-region codes) is issued before
-// any dependent arithmetic; each point forms its own seven stencil
-// coefficients (region_stencil) right where the SpMV needs them, so shared
-// memory holds only u with its halo (9.5 KB per CTA) and no coefficient moves
-// between threads.  HBM per point: read x r w s p, write x r w s p = 80 B (the
-// 4-byte region codes are shared by every task and stay in L2).
+// vectors, the thread's halo point, the point classes) is issued before any
+// dependent arithmetic; while they are in flight the CTA forms the task's
+// stencil of every point class (build_class_table: a few dozen classes, one
+// per thread), and each point then reads its seven coefficients and its
+// Jacobi weight from that table.  Shared memory: u with its halo (9.5 KB) and
+// the table (8 doubles per class).  HBM per point: read x r w s p, write
+// x r w s p = 80 B (the 1-byte point classes are shared by every task and stay
+// in L2).
 template <int kTH, int kTR, int kMinB>
 __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(SArgs a) {
   constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
@@ -763,8 +790,8 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
   static_assert(kTHalo <= kNT, "one halo point per thread");
   extern __shared__ __align__(16) double tsm[];
   double* U = tsm;                              // (kTH + 2) * kTLD
+  double* tab = tsm + (kTH + 2) * kTLD;         // [8][rC] class stencils, 1 / A_C
   __shared__ double red[2 * 4 * 32];
-  __shared__ double2 sp[16];
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" :::);
   // task state: every thread reads it (same addresses: broadcast loads; the
@@ -803,12 +830,12 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
   double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
   // ---- 1. every global load of the launch, issued up front
   double rv[kTR], wv[kTR], sv[kTR], pv[kTR], xv[kTR];
-  uint32_t cd[kTR];
+  int cd[kTR];
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const bool ok = colok && gy0 + r < a.gh;
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
-    cd[r] = ok ? __ldg(a.rcode + i) : 0u;
+    cd[r] = ok ? (int)__ldg(a.rcls + i) : 0;
     rv[r] = ok ? __ldcg(Ro + i) : 0.0;
     wv[r] = (ok && upd) ? __ldcg(Wo + i) : 0.0;
     sv[r] = (ok && upd && !first) ? __ldcg(So + i) : 0.0;
@@ -817,7 +844,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
   }
   int hb = -1;                 // shared-memory slot of this thread's halo point
   double hr = 0.0, hw = 0.0, hs = 0.0;
-  uint32_t hcode = 0u;
+  int hcl = -1;                // halo point's class (-1: outside the grid)
   if (threadIdx.x < kTHalo) {
     const int h = threadIdx.x;
     int lx, ly;
@@ -829,7 +856,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
     const int hx = tx0 + lx, hy = ty0 + ly;
     if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
       const int64_t j = (int64_t)hy * a.wd + hx;
-      hcode = __ldg(a.rcode + j) | 0x80000000u;    // bit 31: inside the grid
+      hcl = (int)__ldg(a.rcls + j);
       hr = __ldcg(Ro + j);
       if (upd) {
         hw = __ldcg(Wo + j);
@@ -837,15 +864,16 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
       }
     }
   }
-  load_region_params(a, tk.sample, sp);
+  load_class_table(a, t, tab, 8);
   __syncthreads();
+  const int C = a.rC;
   // ---- 2. the halo point: u = D^-1 r_k with D = C of that point
   if (hb >= 0) {
     double u = 0.0;
-    if (hcode & 0x80000000u) {
+    if (hcl >= 0) {
       double r = hr;
       if (upd) r = fma(-alpha, tile_s(first, beta, hw, hs), r);
-      u = (1.0 / region_diag(a, sp, hcode & 0x00ffffffu, tk.dt)) * r;
+      u = tab[7 * C + hcl] * r;
     }
     U[hb] = u;
   }
@@ -854,7 +882,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const bool ok = colok && gy0 + r < a.gh;
-    const double dv = ok ? 1.0 / region_diag(a, sp, cd[r], tk.dt) : 0.0;
+    const double dv = ok ? tab[7 * C + cd[r]] : 0.0;
     const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
     double rk = rv[r];
     if (upd) {
@@ -882,8 +910,9 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
     if (!(colok && gy < a.gh)) continue;
     const int64_t i = (int64_t)gy * a.wd + gx;
     const int b = (sy * kTR + r + 1) * kTLD + cx + 1;
-    double A7[7], M7[7];
-    region_stencil(a, sp, cd[r], gx, gy, tk.dt, A7, M7);
+    double A7[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d) A7[d] = tab[d * C + cd[r]];
     const double uc = U[b];
     double acc0 = A7[3] * uc, acc1 = A7[0] * U[b - kTLD - 1];
     acc0 = fma(A7[1], U[b - kTLD], acc0);
@@ -900,8 +929,8 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
 }
 
 template <int kTH, int kTR>
-constexpr size_t tile_iter_rg_smem() {
-  return sizeof(double) * (kTH + 2) * kTLD;
+constexpr size_t tile_iter_rg_smem(int n_classes = 256) {
+  return sizeof(double) * ((kTH + 2) * kTLD + 8 * n_classes);
 }
 
 template <int kTH, int kTR>
@@ -933,8 +962,8 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
-  if (a.rcode != nullptr) {
-    lc.dynamicSmemBytes = tile_iter_rg_smem<kTH, kTR>();
+  if (a.rcls != nullptr) {
+    lc.dynamicSmemBytes = tile_iter_rg_smem<kTH, kTR>(a.rC);
     MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_rg_kernel<kTH, kTR, kMinB>, a));
     MLMCP_LAUNCH_CHECK("tile_iter_rg_kernel");
   } else {
@@ -956,14 +985,14 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   constexpr int kTHalo = 2 * (kTW + 2) + 2 * kTH;
   static_assert(kTHalo <= kTW * (kTH / kTR), "one halo point per thread");
   extern __shared__ __align__(16) double ism[];
-  const bool region = a.rcode != nullptr;
-  // region mode: each point forms its own stencils (region_stencil), no
-  // operator in shared memory
+  const bool region = a.rcls != nullptr;
+  // region mode: the task's stencils per point class (build_class_table, A and
+  // M) instead of the staged operator
   double* Ac = ism;                                  // [4][kTCN] (stored operator)
   double* XV = region ? ism : Ac + 4 * kTCN;         // x_0 with halo
   double* AV = XV + kTV;                             // a_n with halo
+  double* tab = AV + kTV;                            // region: [15][rC]
   __shared__ double red[2 * 4 * 32];
-  __shared__ double2 sp[16];
   const int t = blockIdx.y;
   const mlmcp_task tk = a.tasks[t];
   if (!block_uniform(step < tk.n_steps && task_live(a, tk, t))) return;
@@ -976,10 +1005,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
   const double* Ms = a.w.A + ((int64_t)a.S + tk.sample) * 4 * N;
   const double* An = a.w.Wv + o;   // a_n (step_end / copy_in)
   double dv[kTR];
-  if (region) {
-    load_region_params(a, tk.sample, sp);
-    __syncthreads();
-  }
+  if (region) load_class_table(a, t, tab, 15);   // visible after the guess's sync
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const int ly = sy * kTR + r;
@@ -1112,8 +1138,13 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const bool w_ = gx > 0, s_ = gy > 0;
     double mco[7], aco[7];
     if (region) {
-      region_stencil(a, sp, __ldg(a.rcode + i), gx, gy, tk.dt, aco, mco);
-      dv[r] = 1.0 / aco[3];
+      const int C = a.rC, c = (int)__ldg(a.rcls + i);
+#pragma unroll
+      for (int d = 0; d < 7; ++d) {
+        aco[d] = tab[d * C + c];
+        mco[d] = tab[(8 + d) * C + c];
+      }
+      dv[r] = tab[7 * C + c];
     } else {
 #pragma unroll
       for (int d = 0; d < 7; ++d) aco[d] = Ac[cofs[d]];
@@ -1140,8 +1171,9 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
 }
 
 template <int kTH, int kTR>
-constexpr size_t tile_init_smem(bool region = false) {
-  return sizeof(double) * ((region ? 0 : 4) * (kTH + 1) * (kTW + 1) + 2 * (kTH + 2) * kTLD);
+constexpr size_t tile_init_smem(bool region = false, int n_classes = 256) {
+  return sizeof(double) * ((region ? 15 * n_classes : 4 * (kTH + 1) * (kTW + 1)) +
+                           2 * (kTH + 2) * kTLD);
 }
 
 
@@ -1656,7 +1688,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   const dim3 grid_rows((a.N + kThreads - 1) / kThreads, a.T);
   const dim3 grid_form((a.N + kThreads - 1) / kThreads, a.S);
   if (a.tile) {
-    if (a.rcode == nullptr) {   // region mode computes the operator in the tile kernels
+    if (a.rcls == nullptr) {   // region mode computes the operator in the tile kernels
       form_tile_kernel<<<grid_form, blk, 0, stream>>>(a, dt);
       MLMCP_LAUNCH_CHECK("form_tile_kernel");
     }
@@ -1674,15 +1706,19 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   const dim3 grid_tiles2(a.tile ? a.ntile : 1, a.T);
   copy_in_kernel<<<grid_rows, blk, 0, stream>>>(a);
   MLMCP_LAUNCH_CHECK("copy_in_kernel");
+  if (a.rcls != nullptr) {
+    class_table_kernel<<<a.T, 64, 0, stream>>>(a);
+    MLMCP_LAUNCH_CHECK("class_table_kernel");
+  }
   mark_fail_kernel<<<(a.T + 255) / 256, 256, 0, stream>>>(a, 0);
   MLMCP_LAUNCH_CHECK("mark_fail_kernel");
   auto launch_init = [&](cudaStream_t s, int step) -> int {
-    const bool rg = a.rcode != nullptr;
+    const bool rg = a.rcls != nullptr;
     if (a.tile && tcfg >= 3) {
-      tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(rg), s>>>(a, step);
+      tile_init_kernel<8, 2, 4><<<grid_tiles2, 256, tile_init_smem<8, 2>(rg, a.rC), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else if (a.tile) {
-      tile_init_kernel<16, 4, 3><<<grid_tiles2, 256, tile_init_smem<16, 4>(rg), s>>>(a, step);
+      tile_init_kernel<16, 4, 3><<<grid_tiles2, 256, tile_init_smem<16, 4>(rg, a.rC), s>>>(a, step);
       MLMCP_LAUNCH_CHECK("tile_init_kernel");
     } else {
       step_init_kernel<<<grid_rows, blk, 0, s>>>(a, step);
@@ -1695,10 +1731,12 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     if (!attr) {
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<8, 2, 4>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tile_init_smem<8, 2>(false)));
+                                            (int)std::max(tile_init_smem<8, 2>(false),
+                                                          tile_init_smem<8, 2>(true))));
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_init_kernel<16, 4, 3>,
                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                            (int)tile_init_smem<16, 4>(false)));
+                                            (int)std::max(tile_init_smem<16, 4>(false),
+                                                          tile_init_smem<16, 4>(true))));
       attr = true;
     }
   }
@@ -1890,7 +1928,9 @@ SArgs make_args(Ctx* ctx, int T, int S, const mlmcp_task* tasks, const double* M
   a.it_cond = 0;
   a.use_cond = 0;
   a.order = stream_order();
-  a.rcode = nullptr;
+  a.rcls = nullptr;
+  a.rckey = nullptr;
+  a.rC = 0;
   a.rpar = nullptr;
   a.R = 0;
   for (int i = 0; i < 12; ++i) a.rmw[i] = a.rkw[i] = 0.0;
@@ -1917,9 +1957,11 @@ bool region_on() {
 // and the caller passed the per-sample region parameters (the TMA variant
 // keeps the streamed operator)
 void set_region(const Ctx* ctx, SArgs& a, const double* rpar) {
-  if (!a.tile || ctx->rcode == nullptr || rpar == nullptr || tile_cfg() == 4 || !region_on())
+  if (!a.tile || ctx->rcls == nullptr || rpar == nullptr || tile_cfg() == 4 || !region_on())
     return;
-  a.rcode = ctx->rcode;
+  a.rcls = ctx->rcls;
+  a.rckey = ctx->rckey;
+  a.rC = ctx->rC;
   a.rpar = rpar;
   a.R = ctx->rR;
   for (int i = 0; i < 12; ++i) {
