@@ -535,32 +535,60 @@ def main():
     d2h = 32 * cfg.levels + 16 * tasks + (8 * counts[-1] if pcfg else 0)
 
     if streaming:
-        region = sol.region_mode()
-        kname = "tile_iter_rg_kernel" if region else "tile_iter_kernel"
-        kernel = f"{kname}<16,4,3> (one fused launch per PCG iteration)"
-        streamed = (80 if region else 112) * N          # bytes the kernel must move per task-iteration
+        region = sol.region_mode
+        band = region and sol.mesh.n - 1 <= 256 and os.environ.get("MLMCP_BAND", "1") != "0"
+        rw = region and os.environ.get("MLMCP_TILE_RW", "1") != "0"
         k_ms = it_ms / max(1, args.steps)
         n_its = its / max(1, args.steps)
-        achieved = n_its * b_it / (k_ms / 1000.0) / 1e9
-        nc = ncu_traffic(kname)
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                "frac": achieved / peak,
-                "traffic": nc.get("dram_bytes_per_task_iteration"),
-                "traffic_unit": "dram bytes per PCG task-iteration (ncu, one launch)",
-                "kernel": kernel,
-                "algorithmic_bytes": f"{int(n_its)} PCG task-iterations per estimate x B_it "
-                                     f"(8 nnz + 56 N) = {b_it} B each (SURVEY 8(d))",
-                "streamed_bytes_per_task_iteration": streamed,
-                "frac_streamed": n_its * streamed / (k_ms / 1000.0) / 1e9 / peak,
-                "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms,
-                "launches_per_step": it_launches // max(1, args.steps), "peak_kind": peak_kind,
-                "ncu_source": nc.get("source"), "ncu_launch": nc.get("launch"),
-                "note": "achieved = PCG task-iterations x B_it / device time of the iteration "
-                        "launches (CUDA events on their stream inside libmlmcp, "
-                        "mlmcp_stream_timing) over the timed estimates; B_it counts the "
-                        "per-sample operator (8 nnz); the region-linear kernel computes it from "
-                        "the sample's region parameters and streams only the PCG vectors "
-                        "(frac_streamed: the same time against those bytes)"}
+        achieved = n_its * b_it / (k_ms / 1000.0) / 1e9 if k_ms > 0 else None
+        if band:
+            nc = ncu_traffic("band_propagate_kernel")
+            roof = {"bound": "sm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak if achieved else None,
+                    "traffic": nc.get("dram_bytes_per_task_iteration"),
+                    "traffic_unit": "dram bytes per PCG task-iteration (ncu, one launch)",
+                    "kernel": "band_propagate_kernel (one 16-CTA cluster per task; PCG vectors "
+                              "in registers / shared memory for the whole solve)",
+                    "algorithmic_bytes": f"{int(n_its)} PCG task-iterations per estimate x B_it "
+                                         f"(8 nnz + 56 N) = {b_it} B each (SURVEY 8(d))",
+                    "sm_internal": {k: nc.get(k) for k in ("issue_slots_busy_pct", "ipc_active",
+                                                          "fp64_pipe_pct", "warps_active_pct")},
+                    "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms,
+                    "launches_per_step": it_launches // max(1, args.steps), "peak_kind": peak_kind,
+                    "ncu_source": nc.get("source"), "ncu_launch": nc.get("launch"),
+                    "note": "the PCG iterations of this kernel move no HBM bytes (vectors on chip, "
+                            "operator from per-class stencil tables): achieved = PCG "
+                            "task-iterations x B_it / device time of its launches (CUDA events "
+                            "inside libmlmcp) is the HBM bandwidth a streaming formulation would "
+                            "need for the same rate, frac > 1 = faster than any streaming "
+                            "kernel can be; the bound that limits it is inside the SM "
+                            "(sm_internal, from the committed ncu capture)"}
+        else:
+            kname = ("tile_iter_rw_kernel" if rw else "tile_iter_rg_kernel") if region \
+                else "tile_iter_kernel"
+            kernel = f"{kname}<16,4,3> (one fused launch per PCG iteration)"
+            # bytes the kernel must move per task-iteration: read + write of the PCG
+            # vectors it keeps in HBM (x r s p with w recomputed; + w; + the operator)
+            streamed = (64 if rw else 80 if region else 112) * N
+            nc = ncu_traffic(kname)
+            roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak,
+                    "traffic": nc.get("dram_bytes_per_task_iteration"),
+                    "traffic_unit": "dram bytes per PCG task-iteration (ncu, one launch)",
+                    "kernel": kernel,
+                    "algorithmic_bytes": f"{int(n_its)} PCG task-iterations per estimate x B_it "
+                                         f"(8 nnz + 56 N) = {b_it} B each (SURVEY 8(d))",
+                    "streamed_bytes_per_task_iteration": streamed,
+                    "frac_streamed": n_its * streamed / (k_ms / 1000.0) / 1e9 / peak,
+                    "kernel_ms_per_step": k_ms, "kernel_share_of_step": k_ms / ms,
+                    "launches_per_step": it_launches // max(1, args.steps), "peak_kind": peak_kind,
+                    "ncu_source": nc.get("source"), "ncu_launch": nc.get("launch"),
+                    "note": "achieved = PCG task-iterations x B_it / device time of the iteration "
+                            "launches (CUDA events on their stream inside libmlmcp, "
+                            "mlmcp_stream_timing) over the timed estimates; B_it counts the "
+                            "per-sample operator (8 nnz); the region-linear kernel computes it "
+                            "from the sample's region parameters and streams only the PCG "
+                            "vectors (frac_streamed: the same time against those bytes)"}
     else:
         kernel = "fused_kernel<GridOp,2> (SM-resident; whole estimate in one persistent launch)"
         achieved = its / max(1, args.steps) * b_it / (ms / 1000.0) / 1e9

@@ -25,6 +25,7 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 int cuda_fail(cudaError_t err, const char* what) {
   set_error(std::string(what) + ": " + cudaGetErrorString(err));
+  (void)cudaGetLastError();   // a non-sticky error must not surface in a later launch check
   return MLMCP_ECUDA;
 }
 

@@ -1,0 +1,752 @@
+// band_path.cu — cluster-resident implicit Euler for region-linear structured
+// grids of up to 256 x 256 interior points (config 2's 256^2 mesh: 65,025
+// unknowns per sample), one 16-CTA thread-block cluster per task.
+//
+// Same method and step semantics as the HBM-streaming tile path
+// (stream_path.cu; reference timeint.py:88-128): per step the periodic
+// steady-state predictor plus the extrapolated / least-squares transient guess
+// (ring of 8 past transients), the rhs b = M a_n + dt sin(wt) profile, and a
+// Chronopoulos-Gear PCG solve with the stopping rule r.B^-1.r <= rtol^2
+// b.B^-1.b.  What changes is where the PCG vectors live: a cluster of 16 CTAs
+// (one per SM, 1024 threads each) owns one task for all its steps; CTA c holds
+// the band of grid rows [16c, 16c+16) and each thread a column strip of 4 rows,
+// so the PCG vectors p, s, r, w stay in registers and x in shared memory for
+// the whole solve — a PCG iteration moves no global memory at all (the tile
+// path streams 64-80 B per point and iteration).  Global traffic per step is
+// the guess: 7 ring reads, 1 ring write and the steady state (2 reads) per
+// point, on a ring that stays L2-resident (7 concurrent clusters x 4.2 MB).
+//   * operator: the task's stencil of each point class (Ctx::rckey) formed once
+//     per task into shared memory (A, M and K rows, region_stencil of
+//     stream_path.cu's arithmetic), the point's class byte in shared memory;
+//   * preconditioner: 4-row strip block-Jacobi (L D L^T of each thread's strip,
+//     as the SM-resident and cluster paths), factors in shared memory;
+//   * neighbour values through a shared-memory exchange buffer; a band's first
+//     and last grid rows also go straight into the neighbouring CTAs' buffers
+//     (DSMEM), made visible by one cluster barrier;
+//   * dot products: warp butterfly, fixed-order sum of the CTA's 32 warp
+//     partials, the 16 CTA partials stored into every CTA (DSMEM), one cluster
+//     barrier, fixed-order sum — bitwise identical scalars in every CTA, hence
+//     one control flow for the whole cluster.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
+
+#include "mlmcp_internal.cuh"
+
+namespace mlmcp {
+namespace {
+
+namespace cg = cooperative_groups;
+
+constexpr int kR = 8;                    // grid rows per thread strip
+constexpr int kTX = 256;                 // column threads (grid columns per cluster)
+constexpr int kNS = 2;                   // strips per CTA
+constexpr int kCS = 16;                  // CTAs per cluster
+constexpr int kNT = kTX * kNS;           // 512 threads
+constexpr int kWarps = kNT / 32;
+constexpr int kHB = kR * kNS;            // 16 grid rows per CTA
+constexpr int kLD = kTX + 2;             // exchange-buffer row stride
+constexpr int kV = (kHB + 2) * kLD;      // one exchange buffer
+constexpr int kSlots = kHB * kTX;        // (row, column) slots per CTA
+constexpr int kRing = 8;                 // past transients (extrapolation order <= 7)
+constexpr int kMaxC = 256;               // point classes
+constexpr int kTabW = 24;                // per class: A (7 + pad), M (7 + pad), K (7 + pad)
+// shared memory (doubles): VA, VC[2], x, strip factors, class table, reduction
+// buffers, mbarriers
+constexpr int kRedD = 2 * 4 * kCS + 4 * kWarps;
+
+__constant__ double c_bd_extrap[8][8] = {
+    {1, 0, 0, 0, 0, 0, 0, 0},
+    {2, -1, 0, 0, 0, 0, 0, 0},
+    {3, -3, 1, 0, 0, 0, 0, 0},
+    {4, -6, 4, -1, 0, 0, 0, 0},
+    {5, -10, 10, -5, 1, 0, 0, 0},
+    {6, -15, 20, -15, 6, -1, 0, 0},
+    {7, -21, 35, -35, 21, -7, 1, 0},
+    {8, -28, 56, -70, 56, -28, 8, -1}};
+// least-squares degree-6 fit through the last 8 transients (stream_path.cu)
+__constant__ double c_bd_ls68[8] = {49.0 / 8, -119.0 / 8, 133.0 / 8, -35.0 / 8,
+                                    -77.0 / 8, 91.0 / 8, -41.0 / 8, 7.0 / 8};
+
+struct BdArgs {
+  const mlmcp_task* tasks;
+  int N, wd, gh;
+  const uint8_t* rcls;
+  const uint32_t* rckey;
+  int rC;
+  const double* rpar;      // [S][R][2] (sigma_r masked, nu_r)
+  int R;
+  double rmw[12], rkw[12];
+  const double* profile;
+  const double* xss;       // [slots][2][N] periodic steady states, or null
+  double omega, rtol2;
+  int max_it;
+  int order;
+  int ls_on;
+  double* ring;            // [T][kRing][N]
+  double* xbuf;
+  double* qoi;
+  int32_t* iters;
+  int32_t* status;
+  const int32_t* active;
+  int64_t* elapsed;
+};
+
+__device__ __forceinline__ void bd_arrive() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void bd_wait() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void bd_sync() {
+  bd_arrive();
+  bd_wait();
+}
+__device__ __forceinline__ uint32_t bd_smem(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ uint32_t bd_mapa(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+
+// mbarrier primitives: the PCG loop's halo exchange and dot-product all-reduce
+// signal completion through transaction-counting mbarriers in the receiving
+// CTA (st.async ... complete_tx) instead of cluster-wide barriers.
+__device__ __forceinline__ void mb_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(bd_smem(mb)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mb_expect(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(bd_smem(mb)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mb_wait(uint64_t* mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT%=;\n"
+      "}\n" ::"r"(bd_smem(mb)),
+      "r"(parity)
+      : "memory");
+}
+// 8-byte store into another CTA's shared memory, counted on its mbarrier
+__device__ __forceinline__ void st_async(uint32_t addr, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(
+                   addr),
+               "d"(v), "r"(mbar)
+               : "memory");
+}
+
+struct Th {
+  int x, k, rank, gy0;
+  int vb;          // exchange-buffer index of row 0
+  int sb;          // slot of row 0 (row r: sb + r * kTX)
+  int gr0;         // global point index of row 0 (row r: gr0 + r * wd)
+  int wd;
+  uint32_t okm;    // valid rows (bit r)
+  uint32_t cl[2];  // point classes of rows 0..7 (bytes)
+  __device__ bool ok(int r) const { return (okm >> r) & 1u; }
+  __device__ int row(int r) const { return gr0 + r * wd; }
+  __device__ int slot(int r) const { return sb + r * kTX; }
+  __device__ int cls(int r) const { return (cl[r >> 2] >> (8 * (r & 3))) & 255; }
+};
+
+struct Sh {
+  double* VA;     // exchange: a_n (the final state for the energy)
+  double* VC;     // exchange: u (PCG), two buffers by iteration parity
+  double* X;      // [kSlots] x
+  uint64_t* mb;   // mbarriers: [0..1] halo rows of VC[b], [2..3] CTA partials of
+                  // RED[b], [4] halo rows of VA
+  uint32_t ph;    // wait parity bits of the five mbarriers
+  int hb;         // VC buffer of the current iteration
+  double* PF;     // [2R-1][kNT] strip factors
+  double* TAB;    // [rC][kTabW]
+  double* RED;    // [2][4][kCS] CTA partials of every CTA, [4][kWarps] warp partials
+  int par;
+  __device__ double* vc() const { return VC + hb * kV; }
+};
+
+// strip block-Jacobi: L D L^T of the thread's 8-row tridiagonal block, the
+// factors in shared memory ([2R-1][kNT]: lf_0..lf_6, di_0..di_7)
+struct Pc {
+  double* f;
+  __device__ double lf(int r) const { return f[r * kNT + threadIdx.x]; }
+  __device__ double di(int r) const { return f[(kR - 1 + r) * kNT + threadIdx.x]; }
+};
+
+// Region-linear stencils (A = M + dt K, M and K; slot order SW, S, W, C, E, N, NE)
+// of one point class: stream_path.cu's region_stencil arithmetic.
+__device__ __forceinline__ void bd_stencil(const BdArgs& a, const double2* sp, uint32_t key,
+                                           double dt, double (&A)[7], double (&Mo)[7],
+                                           double (&Ko)[7]) {
+  const uint32_t code = key & 0x00ffffffu, mask = key >> 24;
+  double2 p[6];
+#pragma unroll
+  for (int e = 0; e < 6; ++e) p[e] = sp[(code >> (4 * e)) & 15u];
+  double m = 0.0, k = 0.0;
+#pragma unroll
+  for (int e = 0; e < 6; ++e) {
+    m = __dadd_rn(m, __dmul_rn(p[e].x, a.rmw[e]));
+    k = __dadd_rn(k, __dmul_rn(p[e].y, a.rkw[e]));
+  }
+  Mo[3] = m;
+  Ko[3] = k;
+  A[3] = op_entry(m, k, dt);
+  const int slot[6] = {0, 1, 2, 4, 5, 6};
+  const int e0[6] = {0, 0, 1, 2, 3, 4}, e1[6] = {1, 2, 3, 4, 5, 5};
+  const int cw[6] = {10, 8, 6, 6, 8, 10};
+#pragma unroll
+  for (int c = 0; c < 6; ++c) {
+    const bool ok = (mask >> c) & 1u;
+    double mm = 0.0, kk = 0.0;
+    if (ok) {
+      mm = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].x, a.rmw[cw[c]])),
+                     __dmul_rn(p[e1[c]].x, a.rmw[cw[c] + 1]));
+      kk = __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[c]].y, a.rkw[cw[c]])),
+                     __dmul_rn(p[e1[c]].y, a.rkw[cw[c] + 1]));
+    }
+    Mo[slot[c]] = mm;
+    Ko[slot[c]] = kk;
+    A[slot[c]] = ok ? op_entry(mm, kk, dt) : 0.0;
+  }
+}
+
+// Exchange of a vector with the neighbouring bands: own rows by plain stores,
+// the band's first / last row into the neighbouring CTAs' halo rows by
+// st.async counted on their mbarrier `mi` (one arrival: this CTA's expected
+// byte count).  bd_xwait (after a __syncthreads) waits for both halo rows.
+// Every buffer is rewritten only after the CTAs reading it have contributed to
+// an all-reduce in between, so no neighbour still reads what is overwritten.
+__device__ __forceinline__ void bd_xissue(const Th& th, const double (&v)[kR], double* V, Sh& sh,
+                                          int mi) {
+  uint64_t* mb = sh.mb + mi;
+#pragma unroll
+  for (int r = 0; r < kR; ++r) V[th.vb + r * kLD] = v[r];
+  if (th.k == 0 && th.rank > 0)
+    st_async(bd_mapa(bd_smem(V + (kHB + 1) * kLD + th.x + 1), th.rank - 1), v[0],
+             bd_mapa(bd_smem(mb), th.rank - 1));
+  if (th.k == kNS - 1 && th.rank < kCS - 1)
+    st_async(bd_mapa(bd_smem(V + th.x + 1), th.rank + 1), v[kR - 1],
+             bd_mapa(bd_smem(mb), th.rank + 1));
+  if (threadIdx.x == 0)
+    mb_expect(mb, 8u * kTX * ((th.rank > 0 ? 1u : 0u) + (th.rank < kCS - 1 ? 1u : 0u)));
+}
+__device__ __forceinline__ void bd_xwait(Sh& sh, int mi) {
+  mb_wait(sh.mb + mi, (sh.ph >> mi) & 1u);
+  sh.ph ^= 1u << mi;
+}
+
+// u into the next of the two PCG exchange buffers, halos waited for
+__device__ __forceinline__ void bd_exchange(const Th& th, const double (&v)[kR], Sh& sh) {
+  sh.hb ^= 1;
+  bd_xissue(th, v, sh.vc(), sh, sh.hb);
+  __syncthreads();
+  bd_xwait(sh, sh.hb);
+}
+
+// Calls f(r, nb) with the 7 neighbour values (SW, S, W, C, E, N, NE) of each of
+// the thread's rows in turn; W / E columns are read from the exchange buffer
+// row by row (few live registers), C / N / S from v.
+template <class F>
+__device__ __forceinline__ void bd_rows(const Th& th, const double (&v)[kR], const double* V,
+                                        F&& f) {
+  const int b = th.vb;
+  double sw = V[b - kLD - 1], so = V[b - kLD];
+  double w = V[b - 1], e = V[b + 1];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const double en = V[b + (r + 1) * kLD + 1];               // E of row r+1 = NE of row r
+    const double wn = r < kR - 1 ? V[b + (r + 1) * kLD - 1] : 0.0;
+    const double nb[7] = {sw, so, w, v[r], e, r < kR - 1 ? v[r + 1] : V[b + kR * kLD], en};
+    f(r, nb);
+    sw = w;
+    so = v[r];
+    w = wn;
+    e = en;
+  }
+}
+
+// row T (7 coefficients, 16-byte aligned) . neighbours, in tile_iter_kernel's order
+__device__ __forceinline__ double bd_dot7(const double* T, const double (&nb)[7]) {
+  const double2 t01 = *reinterpret_cast<const double2*>(T);
+  const double2 t23 = *reinterpret_cast<const double2*>(T + 2);
+  const double2 t45 = *reinterpret_cast<const double2*>(T + 4);
+  const double t6 = T[6];
+  double acc0 = t23.y * nb[3], acc1 = t01.x * nb[0];
+  acc0 = fma(t01.y, nb[1], acc0);
+  acc1 = fma(t23.x, nb[2], acc1);
+  acc0 = fma(t45.x, nb[4], acc0);
+  acc1 = fma(t45.y, nb[5], acc1);
+  acc0 = fma(t6, nb[6], acc0);
+  return acc0 + acc1;
+}
+
+// out = B v, B the operator part `off` (0: A, 8: M, 16: K) of the class table
+__device__ __forceinline__ void bd_apply(const Th& th, const Sh& sh, int off,
+                                         const double (&v)[kR], const double* V,
+                                         double (&out)[kR]) {
+  bd_rows(th, v, V, [&](int r, const double (&nb)[7]) {
+    out[r] = bd_dot7(sh.TAB + th.cls(r) * kTabW + off, nb);
+  });
+}
+
+// z = B^-1 r, B the strip's tridiagonal block
+__device__ __forceinline__ void bd_precond(const Pc& pc, const double (&r_)[kR],
+                                           double (&z)[kR]) {
+  double y[kR];
+  y[0] = r_[0];
+#pragma unroll
+  for (int r = 1; r < kR; ++r) y[r] = fma(-pc.lf(r - 1), y[r - 1], r_[r]);
+  z[kR - 1] = pc.di(kR - 1) * y[kR - 1];
+#pragma unroll
+  for (int r = kR - 2; r >= 0; --r) z[r] = fma(-pc.lf(r), z[r + 1], pc.di(r) * y[r]);
+}
+
+// Cluster all-reduce of NV <= 4 doubles: warp butterfly, the CTA's 16 warp
+// partials summed in warp order, the CTA totals stored into every CTA by
+// st.async and counted on the receiving CTA's mbarrier (no cluster barrier),
+// the 16 CTA totals summed in rank order.  Every thread of every CTA returns
+// bitwise identical totals.
+template <int NV>
+__device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  }
+  double* wp = sh.RED + 2 * 4 * kCS;        // [4][kWarps]
+  double* cp = sh.RED + sh.par * 4 * kCS;   // [4][kCS]
+  uint64_t* mb = sh.mb + 2 + sh.par;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) wp[k * kWarps + warp] = v[k];
+  }
+  __syncthreads();
+  static_assert(kWarps == 16 && kCS == 16, "16-lane butterflies");
+  if (warp == 0) {
+    // both half-warps sum the 16 warp partials in the same order
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = wp[k * kWarps + (lane & 15)];
+#pragma unroll
+      for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, 16);
+      v[k] = s;
+    }
+    if (lane < kCS) {
+      const uint32_t dst = bd_mapa(bd_smem(cp + rank), lane);
+      const uint32_t rmb = bd_mapa(bd_smem(mb), lane);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) st_async(dst + 8u * (uint32_t)(k * kCS), v[k], rmb);
+    }
+    if (lane == 0) mb_expect(mb, 8u * kCS * NV);
+  }
+  mb_wait(mb, (sh.ph >> (2 + sh.par)) & 1u);
+  sh.ph ^= 1u << (2 + sh.par);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = cp[k * kCS + (lane & 15)];
+#pragma unroll
+    for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, 16);
+    v[k] = s;
+  }
+  sh.par ^= 1;
+}
+
+// One implicit-Euler step; x (shared) holds a_{n+1} on exit; an = a_n,
+// x0 = the initial guess.  With `energy` the step's first reduction also
+// carries a_n^T K a_n (e_out = half of it).  Returns MLMCP_ST_*.
+__device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh, const Pc& pc,
+                                          const double (&an)[kR], const double (&x0)[kR],
+                                          double sf, double dt, bool energy, double& e_out,
+                                          int& iters) {
+#pragma unroll
+  for (int r = 0; r < kR; ++r) sh.X[th.slot(r)] = x0[r];
+  sh.hb ^= 1;
+  bd_xissue(th, an, sh.VA, sh, 4);
+  bd_xissue(th, x0, sh.vc(), sh, sh.hb);
+  __syncthreads();
+  bd_xwait(sh, 4);
+  bd_xwait(sh, sh.hb);
+  double res[kR], u[kR], p[kR], s[kR], w[kR];
+  double red[4] = {0.0, 0.0, 0.0, 0.0};
+  {
+    double bv[kR];
+    bd_rows(th, an, sh.VA, [&](int r, const double (&nb)[7]) {
+      const double* T = sh.TAB + th.cls(r) * kTabW;
+      const double mx = bd_dot7(T + 8, nb);
+      if (energy) red[3] = fma(an[r], bd_dot7(T + 16, nb), red[3]);
+      bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, __ldg(a.profile + th.row(r)))))
+                       : 0.0;
+    });
+    double ax[kR];
+    bd_apply(th, sh, 0, x0, sh.vc(), ax);
+#pragma unroll
+    for (int r = 0; r < kR; ++r) res[r] = th.ok(r) ? bv[r] - ax[r] : 0.0;
+    bd_precond(pc, bv, u);
+#pragma unroll
+    for (int r = 0; r < kR; ++r) red[2] = fma(bv[r], u[r], red[2]);
+  }
+  bd_precond(pc, res, u);
+  bd_exchange(th, u, sh);
+  bd_apply(th, sh, 0, u, sh.vc(), w);
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    red[0] = fma(res[r], u[r], red[0]);
+    red[1] = fma(w[r], u[r], red[1]);
+  }
+  bd_allsum_mb<4>(red, sh, th.rank);
+  e_out = 0.5 * red[3];
+  const double gamma = red[0];
+  double delta = red[1];
+  const double bnorm2 = red[2];
+  if (bnorm2 == 0.0) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r) sh.X[th.slot(r)] = 0.0;
+    return MLMCP_ST_OK;
+  }
+  const double tol2 = a.rtol2 * bnorm2;
+  if (gamma <= tol2) return MLMCP_ST_OK;
+  if (!isfinite(gamma)) return MLMCP_ST_NONFINITE;
+  if (!(delta > 0.0)) return MLMCP_ST_BREAKDOWN;
+  double alpha = gamma * fast_rcp(delta);
+  double inv_g = fast_rcp(gamma);
+  double c = inv_g * (delta * inv_g);
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    p[r] = sh.vc()[th.vb + r * kLD];   // u_0 (own rows of the exchange buffer)
+    s[r] = w[r];
+    const int sl = th.slot(r);
+    sh.X[sl] = fma(alpha, p[r], sh.X[sl]);
+    res[r] = fma(-alpha, s[r], res[r]);
+  }
+  int it = 1;
+  for (;;) {
+    double red2[2] = {0.0, 0.0};
+    {
+      double uk[kR];
+      bd_precond(pc, res, uk);
+      bd_exchange(th, uk, sh);
+      bd_apply(th, sh, 0, uk, sh.vc(), w);
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        red2[0] = fma(res[r], uk[r], red2[0]);
+        red2[1] = fma(w[r], uk[r], red2[1]);
+      }
+    }
+    bd_allsum_mb<2>(red2, sh, th.rank);
+    const double gnew = red2[0];
+    delta = red2[1];
+    if (gnew <= tol2) break;
+    if (!isfinite(gnew)) { iters += it; return MLMCP_ST_NONFINITE; }
+    if (it >= a.max_it) { iters += it; return MLMCP_ST_NOCONV; }
+    const double beta = gnew * inv_g;
+    const double den = fma(-(gnew * gnew), c, delta);
+    if (!(den > 0.0)) { iters += it; return MLMCP_ST_BREAKDOWN; }
+    alpha = gnew * fast_rcp(den);
+    inv_g = fast_rcp(gnew);
+    c = inv_g * (den * inv_g);
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      // u_k back from the exchange buffer (own rows: written only by this
+      // thread), so it need not stay in registers across the reduction
+      const double uk = sh.vc()[th.vb + r * kLD];
+      p[r] = fma(beta, p[r], uk);
+      s[r] = fma(beta, s[r], w[r]);
+      const int sl = th.slot(r);
+      sh.X[sl] = fma(alpha, p[r], sh.X[sl]);
+      res[r] = fma(-alpha, s[r], res[r]);
+    }
+    ++it;
+  }
+  iters += it;
+  return MLMCP_ST_OK;
+}
+
+// 1/2 x^T K x of the state in X over the cluster (every thread receives it)
+__device__ __forceinline__ double bd_energy(const Th& th, Sh& sh) {
+  double x[kR];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) x[r] = sh.X[th.slot(r)];
+  bd_xissue(th, x, sh.VA, sh, 4);
+  __syncthreads();
+  bd_xwait(sh, 4);
+  double kx[kR];
+  bd_apply(th, sh, 16, x, sh.VA, kx);
+  double v[1] = {0.0};
+#pragma unroll
+  for (int r = 0; r < kR; ++r) v[0] = fma(x[r], kx[r], v[0]);
+  bd_allsum_mb<1>(v, sh, th.rank);
+  return 0.5 * v[0];
+}
+
+__global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int live;
+  __shared__ double2 sp[16];
+  __shared__ double sc[4];
+  cg::cluster_group cl = cg::this_cluster();
+  Th th;
+  th.rank = (int)cl.block_rank();
+  th.x = threadIdx.x % kTX;
+  th.k = threadIdx.x / kTX;
+  th.gy0 = th.rank * kHB + th.k * kR;
+  th.vb = (th.k * kR + 1) * kLD + th.x + 1;
+  th.sb = th.k * kR * kTX + th.x;
+  th.wd = a.wd;
+  th.gr0 = th.gy0 * a.wd + th.x;
+  th.okm = 0u;
+#pragma unroll
+  for (int r = 0; r < kR; ++r)
+    if (th.x < a.wd && th.gy0 + r < a.gh) th.okm |= 1u << r;
+  const int ti = blockIdx.x / kCS;
+  const mlmcp_task t = a.tasks[ti];
+  const int64_t t_start = global_ns();
+  const int C = a.rC;
+  Sh sh;
+  sh.VA = smem;
+  sh.VC = sh.VA + kV;
+  sh.X = sh.VC + 2 * kV;
+  sh.PF = sh.X + kSlots;
+  sh.TAB = sh.PF + (2 * kR - 1) * kNT;
+  sh.RED = sh.TAB + kTabW * C;
+  sh.mb = reinterpret_cast<uint64_t*>(sh.RED + kRedD);
+  sh.ph = 0u;
+  sh.hb = 1;
+  sh.par = 0;
+  for (int i = threadIdx.x; i < 3 * kV; i += kNT) smem[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 5; ++i) mb_init(sh.mb + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (th.rank == 0 && threadIdx.x == 0) {
+    const int lv = (a.active == nullptr || t.group < 0)
+                       ? 1
+                       : (*((volatile const int32_t*)a.active + t.group) != 0);
+    for (int c = 0; c < kCS; ++c) *cl.map_shared_rank(&live, c) = lv;
+  }
+  if (threadIdx.x < a.R)
+    sp[threadIdx.x] = reinterpret_cast<const double2*>(a.rpar)[(int64_t)t.sample * a.R + threadIdx.x];
+  th.cl[0] = th.cl[1] = 0u;
+#pragma unroll
+  for (int r = 0; r < kR; ++r)
+    if (th.ok(r)) th.cl[r >> 2] |= (uint32_t)__ldg(a.rcls + th.row(r)) << (8 * (r & 3));
+  bd_sync();   // zeroed buffers, region parameters and the live flag visible
+  if (!live) return;   // cluster-uniform
+  for (int c = threadIdx.x; c < C; c += kNT) {
+    double A7[7], M7[7], K7[7];
+    bd_stencil(a, sp, __ldg(a.rckey + c), t.dt, A7, M7, K7);
+    double* T = sh.TAB + c * kTabW;
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+      T[d] = A7[d];
+      T[8 + d] = M7[d];
+      T[16 + d] = K7[d];
+    }
+    T[7] = T[15] = T[23] = 0.0;
+  }
+  __syncthreads();
+  Pc pc;   // strip block-Jacobi factors (ClOp::load's recurrence)
+  pc.f = sh.PF;
+  {
+    double d = th.ok(0) ? sh.TAB[th.cls(0) * kTabW + 3] : 0.0;
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      if (r > 0) {
+        const double nprev = th.ok(r - 1) ? sh.TAB[th.cls(r - 1) * kTabW + 5] : 0.0;
+        const double lf = (d != 0.0) ? nprev / d : 0.0;
+        sh.PF[(r - 1) * kNT + threadIdx.x] = lf;
+        d = (th.ok(r) ? sh.TAB[th.cls(r) * kTabW + 3] : 0.0) - lf * nprev;
+      }
+      sh.PF[(kR - 1 + r) * kNT + threadIdx.x] = (th.ok(r) && d != 0.0) ? 1.0 / d : 0.0;
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const double v = th.ok(r) ? __ldcg(a.xbuf + t.x_in + th.row(r)) : 0.0;
+    sh.X[th.slot(r)] = v;
+    if (t.traj >= 0 && th.ok(r)) a.xbuf[t.traj + th.row(r)] = v;
+  }
+  const bool pred = a.xss != nullptr && t.ss_slot >= 0 &&
+                    !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION);
+  const int max_order = (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : a.order;
+  const int64_t N = a.N;
+  double* ring = a.ring + (int64_t)ti * kRing * N;
+  const double* Xs = pred ? a.xss + (int64_t)t.ss_slot * 2 * N : nullptr;
+  const bool sum_e = t.qoi_mode == MLMCP_QOI_SUM_ENERGY && t.qoi_slot >= 0;
+  int iters = 0, code = MLMCP_ST_OK, fail_step = 0;
+  double acc = 0.0;
+  for (int step = 0; step < t.n_steps; ++step) {
+    const int64_t g = t.k0 + step + 1;
+    const double sf = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
+    if (threadIdx.x == 0 && pred) {
+      sincos(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)), &sc[0], &sc[1]);
+      sincos(__dmul_rn(a.omega, grid_time(t.t_base, g - 1, t.dt)), &sc[2], &sc[3]);
+    }
+    __syncthreads();
+    // guess: x0 = extrapolated transient + steady state; y_n joins the ring
+    const int pord = min(step, max_order);
+    double an[kR], x0[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      an[r] = sh.X[th.slot(r)];
+      x0[r] = 0.0;
+      if (!th.ok(r)) continue;
+      const int64_t j = th.row(r);
+      double sst = 0.0, ssn = 0.0;
+      if (pred) {
+        const double xr = __ldg(Xs + j), xi = __ldg(Xs + N + j);
+        sst = fma(xr, sc[0], xi * sc[1]);
+        ssn = fma(xr, sc[2], xi * sc[3]);
+      }
+      const double yn = an[r] - ssn;
+      double pv[kRing];
+#pragma unroll
+      for (int q = 1; q < kRing; ++q)
+        pv[q] = q <= pord ? __ldcg(ring + (int64_t)((step - q) & (kRing - 1)) * N + j) : 0.0;
+      double gv = yn;
+      if (pred && pord >= 7 && a.ls_on) {
+        gv = c_bd_ls68[0] * yn;
+#pragma unroll
+        for (int q = 1; q < 8; ++q) gv = fma(c_bd_ls68[q], pv[q], gv);
+      } else if (pord > 0) {
+        gv = c_bd_extrap[pord][0] * yn;
+#pragma unroll
+        for (int q = 1; q < kRing; ++q)
+          if (q <= pord) gv = fma(c_bd_extrap[pord][q], pv[q], gv);
+      }
+      ring[(int64_t)(step & (kRing - 1)) * N + j] = yn;
+      x0[r] = gv + sst;
+    }
+    // the energy of a_n (the state after the previous step) rides on this
+    // step's first reduction
+    const bool e_now = sum_e && step > 0 && t.k0 + step > t.qoi_from;
+    double e = 0.0;
+    code = bd_ie_step(th, a, sh, pc, an, x0, sf, t.dt, e_now, e, iters);
+    if (e_now) acc += e;
+    if (code != MLMCP_ST_OK) { fail_step = step; break; }
+    if (t.traj >= 0) {
+#pragma unroll
+      for (int r = 0; r < kR; ++r)
+        if (th.ok(r)) a.xbuf[t.traj + (int64_t)(step + 1) * N + th.row(r)] = sh.X[th.slot(r)];
+    }
+  }
+  if (code == MLMCP_ST_OK && t.n_steps > 0 && sum_e && t.k0 + t.n_steps > t.qoi_from)
+    acc += bd_energy(th, sh);
+  if (t.x_out >= 0) {
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+      if (th.ok(r)) a.xbuf[t.x_out + th.row(r)] = sh.X[th.slot(r)];
+  }
+  if (code == MLMCP_ST_OK && t.qoi_mode == MLMCP_QOI_FINAL_ENERGY && t.qoi_slot >= 0)
+    acc = bd_energy(th, sh);
+  if (th.rank == 0 && threadIdx.x == 0) {
+    if (t.qoi_slot >= 0 && t.qoi_mode != MLMCP_QOI_NONE) a.qoi[t.qoi_slot] = acc;
+    if (a.iters != nullptr && t.slot >= 0) atomicAdd(a.iters + t.slot, iters);
+    add_elapsed(a.elapsed, t.slot, t_start);
+    if (code != MLMCP_ST_OK) {
+      write_status(a.status, t.slot, code, fail_step, t.tag, t.tag);
+      if (a.active != nullptr && t.group >= 0) const_cast<int32_t*>(a.active)[t.group] = 0;
+    }
+  }
+  bd_sync();   // no CTA leaves while another may still address its shared memory
+}
+
+size_t band_smem_bytes(int n_classes) {
+  return sizeof(double) * (3 * kV + kSlots + (2 * kR - 1) * kNT + kTabW * n_classes + kRedD + 5);
+}
+
+}  // namespace
+
+// MLMCP_BAND=0 keeps 256^2 region grids on the tile path (A/B)
+bool band_usable(const Ctx* ctx) {
+  const char* e = getenv("MLMCP_BAND");
+  if (e && atoi(e) == 0) return false;
+  const char* s = getenv("MLMCP_STREAM_IMPL");
+  if (s && atoi(s) != 0) return false;
+  return ctx->rcls != nullptr && ctx->rC <= kMaxC && ctx->cl_wd > 0 && ctx->cl_wd <= kTX &&
+         ctx->cl_h <= kCS * kHB && band_smem_bytes(ctx->rC) <= 227 * 1024;
+}
+
+size_t band_ring_bytes(const Ctx* ctx, int n_tasks) {
+  return sizeof(double) * (size_t)n_tasks * kRing * (size_t)ctx->n;
+}
+
+int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* rpar,
+                   const double* profile, double omega, double rtol, int max_it, int order,
+                   int ls_on, const double* xss, double* ring, double* xbuf, double* qoi,
+                   int32_t* iters, int32_t* status, const int32_t* active, int64_t* elapsed,
+                   cudaStream_t stream) {
+  if (n_tasks == 0) return MLMCP_OK;
+  BdArgs a;
+  a.tasks = tasks;
+  a.N = ctx->n;
+  a.wd = ctx->cl_wd;
+  a.gh = ctx->cl_h;
+  a.rcls = ctx->rcls;
+  a.rckey = ctx->rckey;
+  a.rC = ctx->rC;
+  a.rpar = rpar;
+  a.R = ctx->rR;
+  for (int i = 0; i < 12; ++i) {
+    a.rmw[i] = ctx->rmw[i];
+    a.rkw[i] = ctx->rkw[i];
+  }
+  a.profile = profile;
+  a.xss = xss;
+  a.omega = omega;
+  a.rtol2 = rtol * rtol;
+  a.max_it = max_it;
+  a.order = std::max(0, std::min(order, kRing - 1));
+  a.ls_on = ls_on;
+  a.ring = ring;
+  a.xbuf = xbuf;
+  a.qoi = qoi;
+  a.iters = iters;
+  a.status = status;
+  a.active = active;
+  a.elapsed = elapsed;
+  const size_t smem = band_smem_bytes(a.rC);
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
+    MLMCP_CUDA_CHECK(cudaFuncSetAttribute(band_propagate_kernel,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    MLMCP_CUDA_CHECK(cudaFuncSetAttribute(band_propagate_kernel,
+                                          cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    attr_smem = smem;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_tasks * kCS));
+  cfg.blockDim = dim3(kNT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = kCS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  // mlmcp_stream_timing: device time of the launch (CUDA events on its stream)
+  if (ctx->time_iters) MLMCP_CUDA_CHECK(cudaEventRecord(ctx->iter_ev[0], stream));
+  MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&cfg, band_propagate_kernel, a));
+  MLMCP_LAUNCH_CHECK("band_propagate_kernel");
+  if (ctx->time_iters) {
+    MLMCP_CUDA_CHECK(cudaEventRecord(ctx->iter_ev[1], stream));
+    MLMCP_CUDA_CHECK(cudaEventSynchronize(ctx->iter_ev[1]));
+    float ms = 0.0f;
+    MLMCP_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->iter_ev[0], ctx->iter_ev[1]));
+    ctx->iter_ms += ms;
+    ctx->iter_launches += 1;
+  }
+  return MLMCP_OK;
+}
+
+}  // namespace mlmcp

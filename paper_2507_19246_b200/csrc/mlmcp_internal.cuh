@@ -237,6 +237,12 @@ size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks);
 bool coop_usable(const Ctx* ctx, int n_tasks);
 // cluster path (one thread-block cluster per task, grids up to 128 x 128)
 bool cluster_usable(const Ctx* ctx);
+bool band_usable(const Ctx* ctx);
+int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* rpar,
+                   const double* profile, double omega, double rtol, int max_it, int order,
+                   int ls_on, const double* xss, double* ring, double* xbuf, double* qoi,
+                   int32_t* iters, int32_t* status, const int32_t* active, int64_t* elapsed,
+                   cudaStream_t stream);
 int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
                       const double* K, const double* profile, double omega, double rtol,
                       int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,

@@ -928,6 +928,211 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rg_kernel(
   if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
 }
 
+// 7-point stencil product at smem offset b (row stride ld), in the summation
+// order of tile_iter_kernel: every path forms w = A u with the same doubles.
+template <int ld>
+__device__ __forceinline__ double stencil_apply(const double* U, int b, const double (&A7)[7]) {
+  double acc0 = A7[3] * U[b], acc1 = A7[0] * U[b - ld - 1];
+  acc0 = fma(A7[1], U[b - ld], acc0);
+  acc1 = fma(A7[2], U[b - 1], acc1);
+  acc0 = fma(A7[4], U[b + 1], acc0);
+  acc1 = fma(A7[5], U[b + ld], acc1);
+  acc0 = fma(A7[6], U[b + ld + 1], acc0);
+  return acc0 + acc1;
+}
+
+// Region-mode iteration kernel without a stored w (the default in region
+// mode): launch k recomputes w_{k-1} = A u_{k-1} from r_{k-1} instead of
+// reading it, so a PCG iteration streams read r s p x, write r s p x = 64 B
+// per point (tile_iter_rg_kernel: 80 B).  Launch k:
+//   u_{k-1} = D^-1 r_{k-1} on the tile + a two-point halo (r_{k-1} read there),
+//   w_{k-1} = A u_{k-1}, s_{k-1} = w_{k-1} + beta s_{k-2}, r_k = r_{k-1} - alpha
+//   s_{k-1}, u_k = D^-1 r_k on the tile + the one-point halo,
+//   p_{k-1} = u_{k-1} + beta p_{k-2}, x_k = x_{k-1} + alpha p_{k-1} (own points),
+//   w_k = A u_k (own points), partials (r_k.u_k, w_k.u_k);
+// launch 0 only forms u_0, w_0 and the partials.  Every value is computed with
+// tile_iter_kernel's arithmetic (stencil_apply, tile_s), so the iterates are
+// bitwise those of the stored-w kernels.  r and s keep their parity buffers
+// (a launch never writes what a neighbouring tile reads); p and x are
+// own-point only and updated in place.
+template <int kTH, int kTR, int kMinB>
+__global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rw_kernel(SArgs a) {
+  constexpr int kNT = kTW * (kTH / kTR);
+  constexpr int kL1 = kTW + 4;                      // smem row stride (two-point frame)
+  constexpr int kR1 = 2 * (kTW + 2) + 2 * kTH;      // one-point ring (164 at 64 x 16)
+  constexpr int kR2 = 2 * (kTW + 4) + 2 * (kTH + 2);  // second ring (172)
+  static_assert(kR1 <= kNT && kR2 <= kNT, "one ring point per thread and ring");
+  extern __shared__ __align__(16) double tsm[];
+  double* U1 = tsm;                                 // u_{k-1}: (kTH + 4) x kL1
+  double* U2 = tsm + (kTH + 4) * kL1;               // u_k, same frame
+  double* tab = U2 + (kTH + 4) * kL1;               // [8][rC]
+  __shared__ double red[2 * 4 * 32];
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" :::);
+  const int t = blockIdx.y;
+  const mlmcp_task tk = a.tasks[t];
+  const int32_t* ti = a.w.ti + t * kTI;
+  const double* td = a.w.td + t * kTD;
+  const int st = ti[I_STATE];
+  const int k = ti[I_IT_STEP];
+  const int code_ok = ti[I_CODE];
+  const int act = (a.active != nullptr && tk.group >= 0) ? a.active[tk.group] : 1;
+  const double alpha_l = td[D_ALPHA], beta_l = td[D_BETA];
+  if (code_ok != MLMCP_ST_OK || act == 0 || (st != ST_RUN && st != ST_ZERO)) return;
+  const int64_t N = a.N, o = (int64_t)t * N;
+  const int tx0 = (blockIdx.x % a.ntx) * kTW, ty0 = (blockIdx.x / a.ntx) * kTH;
+  const int cx = threadIdx.x % kTW, sy = threadIdx.x / kTW;
+  const int gx = tx0 + cx;
+  const int gy0 = ty0 + sy * kTR;
+  const bool colok = gx < a.wd;
+  double* X = a.w.X + o;
+  if (st == ST_ZERO) {
+#pragma unroll
+    for (int r = 0; r < kTR; ++r)
+      if (colok && gy0 + r < a.gh) X[(int64_t)(gy0 + r) * a.wd + gx] = 0.0;
+    return;
+  }
+  const bool odd = k & 1, upd = k > 0, first = k == 1;
+  const double alpha = upd ? alpha_l : 0.0, beta = upd ? beta_l : 0.0;
+  const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;   // r_{k-1} (k == 0: r_0)
+  const double* So = odd ? a.w.S1 + o : a.w.Sv + o;            // s_{k-2}
+  double* Rn = odd ? a.w.R1 + o : a.w.R + o;
+  double* Sn = odd ? a.w.Sv + o : a.w.S1 + o;
+  // ---- 1. every global load, issued up front
+  double rv[kTR], sv[kTR], pv[kTR], xv[kTR];
+  int cd[kTR];
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    const bool ok = colok && gy0 + r < a.gh;
+    const int64_t i = ok ? (int64_t)(gy0 + r) * a.wd + gx : 0;
+    cd[r] = ok ? (int)__ldg(a.rcls + i) : 0;
+    rv[r] = ok ? __ldcg(Ro + i) : 0.0;
+    sv[r] = (ok && upd && !first) ? __ldcg(So + i) : 0.0;
+    pv[r] = (ok && upd && !first) ? __ldcg(a.w.P + o + i) : 0.0;
+    xv[r] = (ok && upd) ? __ldcg(X + i) : 0.0;
+  }
+  // one-point ring point of this thread (threads < kR1): r_{k-1}, s_{k-2}, class
+  int b1 = -1, c1 = -1;            // smem offset; class (-1: outside the grid)
+  double r1 = 0.0, s1 = 0.0;
+  if (threadIdx.x < kR1) {
+    const int h = threadIdx.x;
+    int lx, ly;
+    if (h < kTW + 2) { lx = h - 1; ly = -1; }
+    else if (h < 2 * (kTW + 2)) { lx = h - (kTW + 2) - 1; ly = kTH; }
+    else if (h < 2 * (kTW + 2) + kTH) { lx = -1; ly = h - 2 * (kTW + 2); }
+    else { lx = kTW; ly = h - 2 * (kTW + 2) - kTH; }
+    b1 = (ly + 2) * kL1 + lx + 2;
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
+      const int64_t j = (int64_t)hy * a.wd + hx;
+      c1 = (int)__ldg(a.rcls + j);
+      r1 = __ldcg(Ro + j);
+      if (upd && !first) s1 = __ldcg(So + j);
+    }
+  }
+  // second ring point (threads >= kNT - kR2, launches k >= 1): r_{k-1}, class
+  int b2 = -1, c2 = -1;
+  double r2 = 0.0;
+  if (upd && threadIdx.x >= kNT - kR2) {
+    const int h = threadIdx.x - (kNT - kR2);
+    int lx, ly;
+    if (h < kTW + 4) { lx = h - 2; ly = -2; }
+    else if (h < 2 * (kTW + 4)) { lx = h - (kTW + 4) - 2; ly = kTH + 1; }
+    else if (h < 2 * (kTW + 4) + kTH + 2) { lx = -2; ly = h - 2 * (kTW + 4) - 1; }
+    else { lx = kTW + 1; ly = h - 2 * (kTW + 4) - (kTH + 2) - 1; }
+    b2 = (ly + 2) * kL1 + lx + 2;
+    const int hx = tx0 + lx, hy = ty0 + ly;
+    if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
+      const int64_t j = (int64_t)hy * a.wd + hx;
+      c2 = (int)__ldg(a.rcls + j);
+      r2 = __ldcg(Ro + j);
+    }
+  }
+  load_class_table(a, t, tab, 8);
+  __syncthreads();
+  const int C = a.rC;
+  const double* Dv = tab + 7 * C;
+  double gam = 0.0;
+  if (upd) {
+    // ---- 2. u_{k-1} on the tile and the two-point frame
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      U1[(sy * kTR + r + 2) * kL1 + cx + 2] = ok ? Dv[cd[r]] * rv[r] : 0.0;
+    }
+    if (b1 >= 0) U1[b1] = c1 >= 0 ? Dv[c1] * r1 : 0.0;
+    if (b2 >= 0) U1[b2] = c2 >= 0 ? Dv[c2] * r2 : 0.0;
+    __syncthreads();
+    // ---- 3. w_{k-1}, s_{k-1}, r_k, u_k on the tile and the one-point ring
+    if (b1 >= 0) {
+      double u = 0.0;
+      if (c1 >= 0) {
+        double A7[7];
+#pragma unroll
+        for (int d = 0; d < 7; ++d) A7[d] = tab[d * C + c1];
+        const double w = stencil_apply<kL1>(U1, b1, A7);
+        const double rk = fma(-alpha, tile_s(first, beta, w, s1), r1);
+        u = Dv[c1] * rk;
+      }
+      U2[b1] = u;
+    }
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      const int b = (sy * kTR + r + 2) * kL1 + cx + 2;
+      double u = 0.0;
+      if (ok) {
+        const int64_t i = (int64_t)(gy0 + r) * a.wd + gx;
+        double A7[7];
+#pragma unroll
+        for (int d = 0; d < 7; ++d) A7[d] = tab[d * C + cd[r]];
+        const double w = stencil_apply<kL1>(U1, b, A7);
+        const double uo = U1[b];
+        const double p = first ? uo : fma(beta, pv[r], uo);
+        const double sn = tile_s(first, beta, w, sv[r]);
+        const double rk = fma(-alpha, sn, rv[r]);
+        a.w.P[o + i] = p;
+        Sn[i] = sn;
+        X[i] = fma(alpha, p, xv[r]);
+        Rn[i] = rk;
+        u = Dv[cd[r]] * rk;
+        gam = fma(rk, u, gam);
+      }
+      U2[b] = u;
+    }
+  } else {
+    // ---- launch 0: u_0 on the tile and the one-point ring
+    if (b1 >= 0) U2[b1] = c1 >= 0 ? Dv[c1] * r1 : 0.0;
+#pragma unroll
+    for (int r = 0; r < kTR; ++r) {
+      const bool ok = colok && gy0 + r < a.gh;
+      const double u = ok ? Dv[cd[r]] * rv[r] : 0.0;
+      U2[(sy * kTR + r + 2) * kL1 + cx + 2] = u;
+      gam = fma(rv[r], u, gam);
+    }
+  }
+  __syncthreads();
+  // ---- 4. w_k = A u_k on the own points, partial (r.u, w.u)
+  double del = 0.0;
+#pragma unroll
+  for (int r = 0; r < kTR; ++r) {
+    if (!(colok && gy0 + r < a.gh)) continue;
+    const int b = (sy * kTR + r + 2) * kL1 + cx + 2;
+    double A7[7];
+#pragma unroll
+    for (int d = 0; d < 7; ++d) A7[d] = tab[d * C + cd[r]];
+    const double w = stencil_apply<kL1>(U2, b, A7);
+    del = fma(w, U2[b], del);
+  }
+  double v[2] = {gam, del};
+  if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0) cg_scalars(a, t, v[0], v[1]);
+}
+
+template <int kTH, int kTR>
+constexpr size_t tile_iter_rw_smem(int n_classes = 256) {
+  return sizeof(double) * (2 * (kTH + 4) * (kTW + 4) + 8 * n_classes);
+}
+
 template <int kTH, int kTR>
 constexpr size_t tile_iter_rg_smem(int n_classes = 256) {
   return sizeof(double) * ((kTH + 2) * kTLD + 8 * n_classes);
@@ -936,6 +1141,12 @@ constexpr size_t tile_iter_rg_smem(int n_classes = 256) {
 template <int kTH, int kTR>
 constexpr size_t tile_iter_smem() {
   return sizeof(double) * ((kTH + 2) * kTLD + 4 * (kTH + 1) * (kTW + 1));
+}
+
+// MLMCP_TILE_RW=0: region mode keeps the stored-w iteration kernel (A/B)
+bool rw_on() {
+  const char* e = getenv("MLMCP_TILE_RW");
+  return !(e && atoi(e) == 0);
 }
 
 // launch one tile iteration (programmatic dependent launch unless disabled)
@@ -950,6 +1161,9 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
     MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_rg_kernel<kTH, kTR, kMinB>,
                                           cudaFuncAttributeMaxDynamicSharedMemorySize,
                                           (int)tile_iter_rg_smem<kTH, kTR>()));
+    MLMCP_CUDA_CHECK(cudaFuncSetAttribute(tile_iter_rw_kernel<kTH, kTR, kMinB>,
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                          (int)tile_iter_rw_smem<kTH, kTR>()));
     attr = true;
   }
   cudaLaunchConfig_t lc = {};
@@ -962,7 +1176,11 @@ int launch_tile_iter(const SArgs& a, dim3 grid, cudaStream_t s, bool pdl) {
   at[0].val.programmaticStreamSerializationAllowed = 1;
   lc.attrs = at;
   lc.numAttrs = pdl ? 1 : 0;
-  if (a.rcls != nullptr) {
+  if (a.rcls != nullptr && rw_on()) {
+    lc.dynamicSmemBytes = tile_iter_rw_smem<kTH, kTR>(a.rC);
+    MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_rw_kernel<kTH, kTR, kMinB>, a));
+    MLMCP_LAUNCH_CHECK("tile_iter_rw_kernel");
+  } else if (a.rcls != nullptr) {
     lc.dynamicSmemBytes = tile_iter_rg_smem<kTH, kTR>(a.rC);
     MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&lc, tile_iter_rg_kernel<kTH, kTR, kMinB>, a));
     MLMCP_LAUNCH_CHECK("tile_iter_rg_kernel");
@@ -1606,6 +1824,12 @@ __global__ void step_next_kernel(int32_t* counters, int n_steps, cudaGraphCondit
 }
 
 // extrapolation order of the streaming paths' initial guesses (MLMCP_STREAM_ORDER)
+// MLMCP_LSGUESS=0: exact extrapolation instead of the least-squares guess
+int ls_on() {
+  const char* l = getenv("MLMCP_LSGUESS");
+  return (l && atoi(l) == 0) ? 0 : 1;
+}
+
 int stream_order() {
   const char* e = getenv("MLMCP_STREAM_ORDER");
   const int o = e ? atoi(e) : 7;   // measured: cfg2 10.0 -> 6.3, cfg4 8.6 -> 6.7 its/step vs order 4
@@ -2289,6 +2513,12 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
     return MLMCP_ENOMEM;
   }
   Work w = carve(ws, L);
+  // region-linear grids up to 256 x 256: one 16-CTA cluster per task keeps the
+  // PCG vectors on chip (band_path.cu)
+  if (band_usable(ctx) && rpar != nullptr && region_on())
+    return band_propagate(ctx, n_tasks, tasks, rpar, profile, omega, rtol, max_it,
+                          stream_order(), ls_on(), xss, w.ring, xbuf, qoi, iters, status, active,
+                          elapsed, stream);
   SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                       iters, status, active, w);
   set_region(ctx, a, rpar);

@@ -40,7 +40,7 @@ def main():
     agg = defaultdict(lambda: [0, 0.0])
     iv = []
     for e in ev:
-        name = e.name.split("(")[0].replace("void ", "").replace("mlmcp::(anonymous namespace)::", "")
+        name = e.name.replace("(anonymous namespace)::", "").replace("void ", "").split("(")[0]
         if name.startswith("Memcpy") or name.startswith("Memset"):
             name = name.split(" ")[0]
         dur = e.time_range.end - e.time_range.start     # us

@@ -1,7 +1,7 @@
 """Summarise one kernel launch of an ncu --set full capture into the JSON the
 bench reads (profiles/ncu_top_kernel.json): dram bytes per launch and per PCG
 task-iteration next to the algorithmic figures.
-usage: python scripts/ncu_summary.py REPORT.ncu-rep KEY TASKS POINTS NNZ BYTES_PER_POINT OUT.json [LAUNCH_DESC]"""
+usage: python scripts/ncu_summary.py REPORT.ncu-rep KEY TASK_ITERATIONS POINTS NNZ BYTES_PER_POINT OUT.json [LAUNCH_DESC]"""
 import csv
 import json
 import subprocess
@@ -26,12 +26,16 @@ def main():
     b_it = 8 * nnz + 56 * pts
     ent = {"kernel": d["Kernel Name"][0], "source": out, "launch": desc, "duration_ms": ms,
            "dram_read_bytes": rd, "dram_write_bytes": wr, "dram_bytes_per_launch": rd + wr,
-           "dram_gbs": (rd + wr) / (ms * 1e-3) / 1e9, "tasks_per_launch": tasks,
+           "dram_gbs": (rd + wr) / (ms * 1e-3) / 1e9, "task_iterations_per_launch": tasks,
            "dram_bytes_per_task_iteration": (rd + wr) / tasks,
            "algorithmic_bytes_per_task_iteration_B_it": b_it,
            "streamed_bytes_per_task_iteration": bpp * pts,
            "algorithmic_bytes_per_launch": tasks * b_it,
            "sm_throughput_pct": g("sm__throughput.avg.pct_of_peak_sustained_elapsed"),
+           "issue_slots_busy_pct": g("sm__inst_issued.avg.pct_of_peak_sustained_active"),
+           "ipc_active": g("sm__inst_executed.avg.per_cycle_active"),
+           "fp64_pipe_pct": g("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active")
+           if "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active" in d else None,
            "warps_active_pct": g("sm__warps_active.avg.pct_of_peak_sustained_active"),
            "registers": int(g("launch__registers_per_thread"))}
     with open(out, "w") as fh:

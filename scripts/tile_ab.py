@@ -4,7 +4,10 @@ vs the region-linear operator computed in the kernels (default).
 Prints one JSON line per mode: propagate-call time, PCG-iteration launch time
 (CUDA events inside libmlmcp), iterations, achieved GB/s against B_it and
 against the bytes the mode actually streams.
-usage: python scripts/tile_ab.py [CFG=2] [S=1024] [STEPS=32]"""
+Modes: stored, region (recompute-w kernel, 64 B/point), regionw (stored-w
+region kernel, 80 B/point), band (cluster-resident band path, 256^2 grids);
+"@n" appends MLMCP_TILE_CFG=n.
+usage: python scripts/tile_ab.py [CFG=2] [S=1024] [STEPS=32] [MODES]"""
 import json
 import os
 import sys
@@ -30,6 +33,10 @@ cfg = get_config(cfg_i)
 qs = {}
 for mode in modes:
     op, _, tcfg = mode.partition("@")       # e.g. "region@3": MLMCP_TILE_CFG=3
+    rw = op != "regionw"                    # "regionw": region operator, stored-w kernel
+    os.environ["MLMCP_TILE_RW"] = "1" if rw else "0"
+    os.environ["MLMCP_BAND"] = "1" if op == "band" else "0"   # "band": 16-CTA cluster path
+    op = "region" if op in ("regionw", "band") else op
     os.environ["MLMCP_TILE_OPERATOR"] = op
     if tcfg:
         os.environ["MLMCP_TILE_CFG"] = tcfg
@@ -59,8 +66,8 @@ for mode in modes:
     it_ms, launches = sol.sys.stream_timing(0)
     its = int(res.iters.to(torch.int64).sum().item())
     b_it = 8 * sol.nnz + 56 * sol.N
-    actual = (80 if sol.region_mode else 112) * sol.N
-    k_ms = it_ms / 2
+    actual = ((64 if rw else 80) if sol.region_mode else 112) * sol.N
+    k_ms = it_ms / 2 if it_ms > 0 else float(np.mean(times))   # band path: no iteration launches
     qs[mode] = res.qoi.cpu().numpy()
     print(json.dumps({"mode": mode, "region": sol.region_mode, "cfg": cfg_i, "S": S, "steps": steps,
                       "call_ms": float(np.mean(times)), "iter_kernel_ms": k_ms,
