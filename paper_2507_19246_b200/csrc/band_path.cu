@@ -33,6 +33,7 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <cstdio>
 
 #include "mlmcp_internal.cuh"
 
@@ -41,17 +42,18 @@ namespace {
 
 namespace cg = cooperative_groups;
 
-constexpr int kR = 8;                    // grid rows per thread strip
+constexpr int kR = 16;                   // grid rows per thread strip (the CTA's band)
 constexpr int kTX = 256;                 // column threads (grid columns per cluster)
-constexpr int kNS = 2;                   // strips per CTA
+constexpr int kNS = 1;                   // strips per CTA
 constexpr int kCS = 16;                  // CTAs per cluster
-constexpr int kNT = kTX * kNS;           // 512 threads
+constexpr int kNT = kTX * kNS;           // 256 threads
 constexpr int kWarps = kNT / 32;
 constexpr int kHB = kR * kNS;            // 16 grid rows per CTA
 constexpr int kLD = kTX + 2;             // exchange-buffer row stride
 constexpr int kV = (kHB + 2) * kLD;      // one exchange buffer
 constexpr int kSlots = kHB * kTX;        // (row, column) slots per CTA
 constexpr int kRing = 8;                 // past transients (extrapolation order <= 7)
+constexpr int kBandPts = kCS * kHB * kTX;  // ring slot pitch: rows of kTX points (compile-time offsets)
 constexpr int kMaxC = 256;               // point classes
 constexpr int kTabW = 24;                // per class: A (7 + pad), M (7 + pad), K (7 + pad)
 // shared memory (doubles): VA, VC[2], x, strip factors, class table, reduction
@@ -71,6 +73,18 @@ __constant__ double c_bd_extrap[8][8] = {
 __constant__ double c_bd_ls68[8] = {49.0 / 8, -119.0 / 8, 133.0 / 8, -35.0 / 8,
                                     -77.0 / 8, 91.0 / 8, -41.0 / 8, 7.0 / 8};
 
+// MLMCP_BAND_PROF=1: clock64 cycles of the step phases in CTA 0 of the first
+// cluster (trig + sync, guess, step start incl. its all-reduce, PCG loop)
+__device__ unsigned long long g_band_prof[8];
+#define BD_PROF(i, t0)                                                              \
+  do {                                                                            \
+    if ((a.prof & 1) && blockIdx.x == 0 && threadIdx.x == 0) {                          \
+      const long long t1_ = clock64();                                            \
+      g_band_prof[i] += (unsigned long long)(t1_ - (t0));                         \
+      (t0) = t1_;                                                                 \
+    }                                                                             \
+  } while (0)
+
 struct BdArgs {
   const mlmcp_task* tasks;
   int N, wd, gh;
@@ -86,13 +100,14 @@ struct BdArgs {
   int max_it;
   int order;
   int ls_on;
-  double* ring;            // [T][kRing][N]
+  double* ring;            // [T][kRing][kBandPts], point (gx, gy) at gy * kTX + gx
   double* xbuf;
   double* qoi;
   int32_t* iters;
   int32_t* status;
   const int32_t* active;
   int64_t* elapsed;
+  int prof;
 };
 
 __device__ __forceinline__ void bd_arrive() {
@@ -151,7 +166,7 @@ struct Th {
   int gr0;         // global point index of row 0 (row r: gr0 + r * wd)
   int wd;
   uint32_t okm;    // valid rows (bit r)
-  uint32_t cl[2];  // point classes of rows 0..7 (bytes)
+  uint32_t cl[kR / 4];  // point classes of the rows (bytes)
   __device__ bool ok(int r) const { return (okm >> r) & 1u; }
   __device__ int row(int r) const { return gr0 + r * wd; }
   __device__ int slot(int r) const { return sb + r * kTX; }
@@ -243,6 +258,20 @@ __device__ __forceinline__ void bd_xwait(Sh& sh, int mi) {
   sh.ph ^= 1u << mi;
 }
 
+// bd_xissue for a vector whose own rows are already in V: the band's edge rows
+// are read back from V and sent to the neighbours
+__device__ __forceinline__ void bd_xsend(const Th& th, double* V, Sh& sh, int mi) {
+  uint64_t* mb = sh.mb + mi;
+  if (th.k == 0 && th.rank > 0)
+    st_async(bd_mapa(bd_smem(V + (kHB + 1) * kLD + th.x + 1), th.rank - 1), V[th.vb],
+             bd_mapa(bd_smem(mb), th.rank - 1));
+  if (th.k == kNS - 1 && th.rank < kCS - 1)
+    st_async(bd_mapa(bd_smem(V + th.x + 1), th.rank + 1), V[th.vb + (kR - 1) * kLD],
+             bd_mapa(bd_smem(mb), th.rank + 1));
+  if (threadIdx.x == 0)
+    mb_expect(mb, 8u * kTX * ((th.rank > 0 ? 1u : 0u) + (th.rank < kCS - 1 ? 1u : 0u)));
+}
+
 // u into the next of the two PCG exchange buffers, halos waited for
 __device__ __forceinline__ void bd_exchange(const Th& th, const double (&v)[kR], Sh& sh) {
   sh.hb ^= 1;
@@ -269,6 +298,27 @@ __device__ __forceinline__ void bd_rows(const Th& th, const double (&v)[kR], con
     sw = w;
     so = v[r];
     w = wn;
+    e = en;
+  }
+}
+
+// bd_rows with the thread's own column (C, N, S) read from V as well
+template <class F>
+__device__ __forceinline__ void bd_rows_s(const Th& th, const double* V, F&& f) {
+  const int b = th.vb;
+  double sw = V[b - kLD - 1], so = V[b - kLD];
+  double w = V[b - 1], c = V[b], e = V[b + 1];
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const double en = V[b + (r + 1) * kLD + 1];
+    const double cn = V[b + (r + 1) * kLD];
+    const double wn = r < kR - 1 ? V[b + (r + 1) * kLD - 1] : 0.0;
+    const double nb[7] = {sw, so, w, c, e, cn, en};
+    f(r, nb);
+    sw = w;
+    so = c;
+    w = wn;
+    c = cn;
     e = en;
   }
 }
@@ -330,14 +380,14 @@ __device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) 
     for (int k = 0; k < NV; ++k) wp[k * kWarps + warp] = v[k];
   }
   __syncthreads();
-  static_assert(kWarps == 16 && kCS == 16, "16-lane butterflies");
+  static_assert(kWarps <= 32 && (kWarps & (kWarps - 1)) == 0 && kCS == 16, "butterfly widths");
   if (warp == 0) {
-    // both half-warps sum the 16 warp partials in the same order
+    // every group of kWarps lanes sums the warp partials in the same order
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
-      double s = wp[k * kWarps + (lane & 15)];
+      double s = wp[k * kWarps + (lane & (kWarps - 1))];
 #pragma unroll
-      for (int off = 8; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, 16);
+      for (int off = kWarps / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, kWarps);
       v[k] = s;
     }
     if (lane < kCS) {
@@ -360,18 +410,16 @@ __device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) 
   sh.par ^= 1;
 }
 
-// One implicit-Euler step; x (shared) holds a_{n+1} on exit; an = a_n,
-// x0 = the initial guess.  With `energy` the step's first reduction also
-// carries a_n^T K a_n (e_out = half of it).  Returns MLMCP_ST_*.
+// One implicit-Euler step.  On entry the guess phase has written a_n into
+// VA's own rows and the initial guess x0 into X and into the own rows of the
+// next PCG exchange buffer (sh.hb already advanced); X holds a_{n+1} on exit.
+// With `energy` the step's first reduction also carries a_n^T K a_n (e_out =
+// half of it).  Returns MLMCP_ST_*.
 __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh, const Pc& pc,
-                                          const double (&an)[kR], const double (&x0)[kR],
                                           double sf, double dt, bool energy, double& e_out,
                                           int& iters) {
-#pragma unroll
-  for (int r = 0; r < kR; ++r) sh.X[th.slot(r)] = x0[r];
-  sh.hb ^= 1;
-  bd_xissue(th, an, sh.VA, sh, 4);
-  bd_xissue(th, x0, sh.vc(), sh, sh.hb);
+  bd_xsend(th, sh.VA, sh, 4);
+  bd_xsend(th, sh.vc(), sh, sh.hb);
   __syncthreads();
   bd_xwait(sh, 4);
   bd_xwait(sh, sh.hb);
@@ -379,17 +427,17 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
   double red[4] = {0.0, 0.0, 0.0, 0.0};
   {
     double bv[kR];
-    bd_rows(th, an, sh.VA, [&](int r, const double (&nb)[7]) {
+    bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
       const double* T = sh.TAB + th.cls(r) * kTabW;
       const double mx = bd_dot7(T + 8, nb);
-      if (energy) red[3] = fma(an[r], bd_dot7(T + 16, nb), red[3]);
+      if (energy) red[3] = fma(nb[3], bd_dot7(T + 16, nb), red[3]);
       bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, __ldg(a.profile + th.row(r)))))
                        : 0.0;
     });
-    double ax[kR];
-    bd_apply(th, sh, 0, x0, sh.vc(), ax);
-#pragma unroll
-    for (int r = 0; r < kR; ++r) res[r] = th.ok(r) ? bv[r] - ax[r] : 0.0;
+    const double* V0 = sh.vc();
+    bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
+      res[r] = th.ok(r) ? bv[r] - bd_dot7(sh.TAB + th.cls(r) * kTabW, nb) : 0.0;
+    });
     bd_precond(pc, bv, u);
 #pragma unroll
     for (int r = 0; r < kR; ++r) red[2] = fma(bv[r], u[r], red[2]);
@@ -403,6 +451,7 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
     red[1] = fma(w[r], u[r], red[1]);
   }
   bd_allsum_mb<4>(red, sh, th.rank);
+  long long tp = clock64();
   e_out = 0.5 * red[3];
   const double gamma = red[0];
   double delta = red[1];
@@ -429,6 +478,7 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
   }
   int it = 1;
   for (;;) {
+    if (false) BD_PROF(7, tp);
     double red2[2] = {0.0, 0.0};
     {
       double uk[kR];
@@ -467,6 +517,7 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
     ++it;
   }
   iters += it;
+  BD_PROF(3, tp);
   return MLMCP_ST_OK;
 }
 
@@ -488,10 +539,11 @@ __device__ __forceinline__ double bd_energy(const Th& th, Sh& sh) {
 }
 
 __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
+  static_assert(kR % 4 == 0, "guess batches of four rows");
   extern __shared__ __align__(16) double smem[];
   __shared__ int live;
   __shared__ double2 sp[16];
-  __shared__ double sc[4];
+  __shared__ double sc[5];
   cg::cluster_group cl = cg::this_cluster();
   Th th;
   th.rank = (int)cl.block_rank();
@@ -534,7 +586,8 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
   }
   if (threadIdx.x < a.R)
     sp[threadIdx.x] = reinterpret_cast<const double2*>(a.rpar)[(int64_t)t.sample * a.R + threadIdx.x];
-  th.cl[0] = th.cl[1] = 0u;
+#pragma unroll
+  for (int i = 0; i < kR / 4; ++i) th.cl[i] = 0u;
 #pragma unroll
   for (int r = 0; r < kR; ++r)
     if (th.ok(r)) th.cl[r >> 2] |= (uint32_t)__ldg(a.rcls + th.row(r)) << (8 * (r & 3));
@@ -578,58 +631,87 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
                     !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION);
   const int max_order = (t.flags & MLMCP_TASK_NO_EXTRAPOLATION) ? 0 : a.order;
   const int64_t N = a.N;
-  double* ring = a.ring + (int64_t)ti * kRing * N;
+  // the thread's ring entries: slot sl, row r at rb[sl * kBandPts + r * kTX]
+  double* rb = a.ring + (int64_t)ti * kRing * kBandPts + th.gy0 * kTX + th.x;
   const double* Xs = pred ? a.xss + (int64_t)t.ss_slot * 2 * N : nullptr;
   const bool sum_e = t.qoi_mode == MLMCP_QOI_SUM_ENERGY && t.qoi_slot >= 0;
   int iters = 0, code = MLMCP_ST_OK, fail_step = 0;
   double acc = 0.0;
+  long long tq = clock64();
   for (int step = 0; step < t.n_steps; ++step) {
+    BD_PROF(4, tq);
     const int64_t g = t.k0 + step + 1;
-    const double sf = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
-    if (threadIdx.x == 0 && pred) {
+    // the step's trigonometry once per CTA, three warps in parallel
+    if (threadIdx.x == 0) sc[4] = sin(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)));
+    if (pred && threadIdx.x == 32)
       sincos(__dmul_rn(a.omega, grid_time(t.t_base, g, t.dt)), &sc[0], &sc[1]);
+    if (pred && threadIdx.x == 64)
       sincos(__dmul_rn(a.omega, grid_time(t.t_base, g - 1, t.dt)), &sc[2], &sc[3]);
-    }
     __syncthreads();
-    // guess: x0 = extrapolated transient + steady state; y_n joins the ring
+    BD_PROF(0, tq);
+    const double sf = sc[4];
+    // guess: x0 = extrapolated transient + steady state; y_n joins the ring.
+    // The weights of this step (least-squares fit or exact extrapolation, zero
+    // beyond the order) are rotated onto the ring slots, ww[s] = w[(step - s)
+    // & 7], so every slot index is a compile-time one; slots not yet written
+    // in this task are neither loaded nor weighted.
     const int pord = min(step, max_order);
-    double an[kR], x0[kR];
+    const int cur = step & (kRing - 1);
+    double w0, ww[kRing];
+    uint32_t valid = 0u;
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      an[r] = sh.X[th.slot(r)];
-      x0[r] = 0.0;
-      if (!th.ok(r)) continue;
-      const int64_t j = th.row(r);
-      double sst = 0.0, ssn = 0.0;
-      if (pred) {
-        const double xr = __ldg(Xs + j), xi = __ldg(Xs + N + j);
-        sst = fma(xr, sc[0], xi * sc[1]);
-        ssn = fma(xr, sc[2], xi * sc[3]);
+    for (int sl = 0; sl < kRing; ++sl) {
+      const int q = (step - sl) & (kRing - 1);
+      const double wq = (pred && pord >= 7 && a.ls_on) ? c_bd_ls68[q]
+                        : q <= pord                    ? c_bd_extrap[pord][q]
+                                                       : 0.0;
+      ww[sl] = (q >= 1 && q <= pord) ? wq : 0.0;
+      if (q >= 1 && q <= pord) valid |= 1u << sl;
+      if (q == 0) w0 = wq;
+    }
+    sh.hb ^= 1;
+    double* VN = sh.vc();     // the step's first exchange buffer (x0)
+#pragma unroll
+    for (int h = 0; h < kR; h += 4) {
+      double pv[4][kRing], xr[4], xi[4];   // four rows' loads in flight together
+#pragma unroll
+      for (int rr = 0; rr < 4; ++rr) {
+        const int r = h + rr;
+        const bool ok = th.ok(r) && pord > 0;
+        const int64_t j = th.row(r);
+        xr[rr] = (th.ok(r) && pred) ? __ldg(Xs + j) : 0.0;
+        xi[rr] = (th.ok(r) && pred) ? __ldg(Xs + N + j) : 0.0;
+#pragma unroll
+        for (int sl = 0; sl < kRing; ++sl)
+          pv[rr][sl] = (ok && ((valid >> sl) & 1u)) ? __ldcg(rb + sl * kBandPts + r * kTX) : 0.0;
       }
-      const double yn = an[r] - ssn;
-      double pv[kRing];
 #pragma unroll
-      for (int q = 1; q < kRing; ++q)
-        pv[q] = q <= pord ? __ldcg(ring + (int64_t)((step - q) & (kRing - 1)) * N + j) : 0.0;
-      double gv = yn;
-      if (pred && pord >= 7 && a.ls_on) {
-        gv = c_bd_ls68[0] * yn;
+      for (int rr = 0; rr < 4; ++rr) {
+        const int r = h + rr;
+        const double an = sh.X[th.slot(r)];
+        double x0 = 0.0;
+        if (th.ok(r)) {
+          const double sst = pred ? fma(xr[rr], sc[0], xi[rr] * sc[1]) : 0.0;
+          const double ssn = pred ? fma(xr[rr], sc[2], xi[rr] * sc[3]) : 0.0;
+          const double yn = an - ssn;
+          double gv = w0 * yn;
 #pragma unroll
-        for (int q = 1; q < 8; ++q) gv = fma(c_bd_ls68[q], pv[q], gv);
-      } else if (pord > 0) {
-        gv = c_bd_extrap[pord][0] * yn;
-#pragma unroll
-        for (int q = 1; q < kRing; ++q)
-          if (q <= pord) gv = fma(c_bd_extrap[pord][q], pv[q], gv);
+          for (int sl = 0; sl < kRing; ++sl) gv = fma(ww[sl], pv[rr][sl], gv);
+          rb[cur * kBandPts + r * kTX] = yn;
+          x0 = gv + sst;
+        }
+        sh.VA[th.vb + r * kLD] = an;
+        VN[th.vb + r * kLD] = x0;
+        sh.X[th.slot(r)] = x0;
       }
-      ring[(int64_t)(step & (kRing - 1)) * N + j] = yn;
-      x0[r] = gv + sst;
     }
     // the energy of a_n (the state after the previous step) rides on this
     // step's first reduction
     const bool e_now = sum_e && step > 0 && t.k0 + step > t.qoi_from;
     double e = 0.0;
-    code = bd_ie_step(th, a, sh, pc, an, x0, sf, t.dt, e_now, e, iters);
+    BD_PROF(1, tq);
+    code = bd_ie_step(th, a, sh, pc, sf, t.dt, e_now, e, iters);
+    BD_PROF(2, tq);
     if (e_now) acc += e;
     if (code != MLMCP_ST_OK) { fail_step = step; break; }
     if (t.traj >= 0) {
@@ -675,8 +757,8 @@ bool band_usable(const Ctx* ctx) {
          ctx->cl_h <= kCS * kHB && band_smem_bytes(ctx->rC) <= 227 * 1024;
 }
 
-size_t band_ring_bytes(const Ctx* ctx, int n_tasks) {
-  return sizeof(double) * (size_t)n_tasks * kRing * (size_t)ctx->n;
+size_t band_ring_bytes(int n_tasks) {
+  return sizeof(double) * (size_t)n_tasks * kRing * kBandPts;
 }
 
 int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* rpar,
@@ -713,6 +795,8 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
   a.status = status;
   a.active = active;
   a.elapsed = elapsed;
+  const char* pe = getenv("MLMCP_BAND_PROF");
+  a.prof = pe ? atoi(pe) : 0;   // bit 0: phase cycles; 2, 4: guess-load experiments
   const size_t smem = band_smem_bytes(a.rC);
   static size_t attr_smem = 0;
   if (smem > attr_smem) {
@@ -745,6 +829,12 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
     MLMCP_CUDA_CHECK(cudaEventElapsedTime(&ms, ctx->iter_ev[0], ctx->iter_ev[1]));
     ctx->iter_ms += ms;
     ctx->iter_launches += 1;
+  }
+  if (a.prof & 1) {
+    unsigned long long h[8];
+    MLMCP_CUDA_CHECK(cudaMemcpyFromSymbol(h, g_band_prof, sizeof(h)));
+    fprintf(stderr, "band prof cycles: trig %llu guess %llu stepstart+ie %llu pcg %llu tail %llu\n",
+            h[0], h[1], h[2], h[3], h[4]);
   }
   return MLMCP_OK;
 }

@@ -71,7 +71,7 @@ struct Cfg {
   static constexpr int kRing = 8;                // past states a_{n-1..n-8}
   static constexpr int kRedVals = 4;
   static constexpr int kRed = 2 * kRedVals * CS * kWarps;
-  static constexpr int kSmemDoubles = 3 * kV + kRing * kSlots + kRed;
+  static constexpr int kSmemDoubles = 4 * kV + kRing * kSlots + kRed + 4;   // + VC[1], mbarriers
   static_assert(TX % 32 == 0, "column threads must fill warps");
   static_assert((CS * kWarps) % 32 == 0 || CS * kWarps < 32, "reduction layout");
 };
@@ -98,6 +98,36 @@ __device__ __forceinline__ uint32_t map_rank(uint32_t addr, int rank) {
 }
 __device__ __forceinline__ void st_cluster(uint32_t addr, double v) {
   asm volatile("st.shared::cluster.f64 [%0], %1;\n" ::"r"(addr), "d"(v) : "memory");
+}
+
+// mbarrier primitives: the PCG loop's halo exchange and dot-product all-reduce
+// deliver their data with st.async into the receiving CTA and signal it on a
+// transaction-counting mbarrier there, instead of cluster-wide barriers
+// (the band path's protocol, band_path.cu).
+__device__ __forceinline__ void cl_mb_init(uint64_t* mb, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_addr(mb)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void cl_mb_expect(uint64_t* mb, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_addr(mb)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void cl_mb_wait(uint64_t* mb, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n"
+      "WAIT%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT%=;\n"
+      "}\n" ::"r"(smem_addr(mb)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void cl_st_async(uint32_t addr, double v, uint32_t mbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.f64 [%0], %1, [%2];\n" ::"r"(
+                   addr),
+               "d"(v), "r"(mbar)
+               : "memory");
 }
 
 template <class C>
@@ -269,12 +299,93 @@ template <class C>
 struct ClShared {
   double* VA;    // exchange: a_n (rhs), x (energy)
   double* VB;    // exchange: initial guess
-  double* VC;    // exchange: u (PCG iterations)
+  double* VC;    // exchange: u (PCG iterations), two buffers alternating by exchange
+  uint64_t* mb;  // mbarriers: [0..1] halo rows of VC[b], [2..3] CTA partials of red[b]
+  uint32_t ph;   // wait parity bits of the mbarriers
+  int hb;        // VC buffer of the current exchange
   const double* Ms;   // per-sample CSR mass values (M a_n once per step, from L2)
   double* ring;  // [kRing][kSlots] past states
   double* red;   // [2][kRedVals][CS][kWarps]
   int par;
 };
+
+// u into the next of the two PCG exchange buffers: own rows by plain stores,
+// the band's edge rows into the neighbouring CTAs' halo rows by st.async
+// counted on their mbarrier; then wait for this CTA's two halo rows.  Every
+// buffer is rewritten only after the CTAs reading it have contributed to an
+// all-reduce in between.
+template <class C>
+__device__ __forceinline__ double* cl_exchange(const Thr<C>& th, const double (&v)[C::R],
+                                               ClShared<C>& sh) {
+  sh.hb ^= 1;
+  double* V = sh.VC + sh.hb * C::kV;
+  uint64_t* mb = sh.mb + sh.hb;
+  const int b = th.vidx(0);
+#pragma unroll
+  for (int r = 0; r < C::R; ++r) V[b + r * C::LD] = v[r];
+  if (th.k == 0 && th.rank > 0)
+    cl_st_async(map_rank(smem_addr(V + (C::HB + 1) * C::LD + th.x + 1), th.rank - 1), v[0],
+                map_rank(smem_addr(mb), th.rank - 1));
+  if (th.k == C::NS - 1 && th.rank < C::CS - 1)
+    cl_st_async(map_rank(smem_addr(V + th.x + 1), th.rank + 1), v[C::R - 1],
+                map_rank(smem_addr(mb), th.rank + 1));
+  if (threadIdx.x == 0)
+    cl_mb_expect(mb, 8u * C::TX * ((th.rank > 0 ? 1u : 0u) + (th.rank < C::CS - 1 ? 1u : 0u)));
+  __syncthreads();
+  cl_mb_wait(mb, (sh.ph >> sh.hb) & 1u);
+  sh.ph ^= 1u << sh.hb;
+  return V;
+}
+
+// Cluster all-reduce of NV <= 4 doubles without a cluster barrier: warp
+// butterfly, the CTA's warp partials summed in warp order, the CTA totals
+// stored into every CTA by st.async (counted on its mbarrier), the CTA totals
+// summed in rank order.  Bitwise identical totals in every thread of every CTA.
+template <class C, int NV>
+__device__ __forceinline__ void cl_allsum_mb(double (&v)[NV], ClShared<C>& sh, int rank) {
+  constexpr int W = C::kWarps, CS = C::CS;
+  static_assert((W & (W - 1)) == 0 && W <= 32 && (CS & (CS - 1)) == 0 && CS <= 32, "widths");
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
+  }
+  double* wp = sh.red + 2 * 4 * CS;          // [4][W]
+  double* cp = sh.red + sh.par * 4 * CS;     // [4][CS]
+  uint64_t* mb = sh.mb + 2 + sh.par;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) wp[k * W + warp] = v[k];
+  }
+  __syncthreads();
+  if (warp == 0) {
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+      double s = wp[k * W + (lane & (W - 1))];
+#pragma unroll
+      for (int off = W / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, W);
+      v[k] = s;
+    }
+    if (lane < CS) {
+      const uint32_t dst = map_rank(smem_addr(cp + rank), lane);
+      const uint32_t rmb = map_rank(smem_addr(mb), lane);
+#pragma unroll
+      for (int k = 0; k < NV; ++k) cl_st_async(dst + 8u * (uint32_t)(k * CS), v[k], rmb);
+    }
+    if (lane == 0) cl_mb_expect(mb, 8u * CS * NV);
+  }
+  cl_mb_wait(mb, (sh.ph >> (2 + sh.par)) & 1u);
+  sh.ph ^= 1u << (2 + sh.par);
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    double s = cp[k * CS + (lane & (CS - 1))];
+#pragma unroll
+    for (int off = CS / 2; off > 0; off >>= 1) s += __shfl_xor_sync(0xffffffffu, s, off, CS);
+    v[k] = s;
+  }
+  sh.par ^= 1;
+}
 
 // 1/2 x^T B x over the cluster (every thread receives it)
 template <class C>
@@ -288,7 +399,7 @@ __device__ __forceinline__ double cl_energy(const Thr<C>& th, const ClArgs& A,
   double v[1] = {0.0};
 #pragma unroll
   for (int r = 0; r < C::R; ++r) v[0] = fma(x[r], bx[r], v[0]);
-  cl_allsum<C, 1>(v, sh.red, sh.par, th.rank, cl);
+  cl_allsum_mb<C, 1>(v, sh, th.rank);
   return 0.5 * v[0];
 }
 
@@ -325,15 +436,14 @@ __device__ __forceinline__ int cl_ie_step(const ClOp<C>& op, const Thr<C>& th, c
     for (int r = 0; r < R; ++r) red3[2] = fma(bv[r], u[r], red3[2]);
   }
   op.precond(res, u);
-  publish<C>(th, u, sh.VC, cl);
-  cl_sync();
-  op.apply(th, u, sh.VC, w);
+  const double* VU = cl_exchange<C>(th, u, sh);
+  op.apply(th, u, VU, w);
 #pragma unroll
   for (int r = 0; r < R; ++r) {
     red3[0] += res[r] * u[r];
     red3[1] += w[r] * u[r];
   }
-  cl_allsum<C, 3>(red3, sh.red, sh.par, th.rank, cl);
+  cl_allsum_mb<C, 3>(red3, sh, th.rank);
   const double gamma = red3[0];
   double delta = red3[1];
   const double bnorm2 = red3[2];
@@ -359,16 +469,15 @@ __device__ __forceinline__ int cl_ie_step(const ClOp<C>& op, const Thr<C>& th, c
   int it = 1;
   for (;;) {
     op.precond(res, u);
-    publish<C>(th, u, sh.VC, cl);
-    cl_sync();
-    op.apply(th, u, sh.VC, w);
+    const double* VUk = cl_exchange<C>(th, u, sh);
+    op.apply(th, u, VUk, w);
     double red2[2] = {0.0, 0.0};
 #pragma unroll
     for (int r = 0; r < R; ++r) {
       red2[0] = fma(res[r], u[r], red2[0]);
       red2[1] = fma(w[r], u[r], red2[1]);
     }
-    cl_allsum<C, 2>(red2, sh.red, sh.par, th.rank, cl);
+    cl_allsum_mb<C, 2>(red2, sh, th.rank);
     const double gnew = red2[0];
     delta = red2[1];
     if (gnew <= tol2) break;
@@ -437,10 +546,17 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_propagate_kernel(ClArg
   sh.VA = smem;
   sh.VB = sh.VA + C::kV;
   sh.VC = sh.VB + C::kV;
-  sh.ring = sh.VC + C::kV;
+  sh.ring = sh.VC + 2 * C::kV;
   sh.red = sh.ring + C::kRing * C::kSlots;
+  sh.mb = reinterpret_cast<uint64_t*>(sh.red + C::kRed);
+  sh.ph = 0u;
+  sh.hb = 1;
   sh.par = 0;
-  for (int i = threadIdx.x; i < 3 * C::kV; i += C::kThreads) smem[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) cl_mb_init(sh.mb + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < 4 * C::kV; i += C::kThreads) smem[i] = 0.0;
   if (th.rank == 0 && threadIdx.x == 0) {
     const int lv = (a.active == nullptr || t.group < 0)
                        ? 1
@@ -541,10 +657,17 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a
   sh.VA = smem;
   sh.VB = sh.VA + C::kV;
   sh.VC = sh.VB + C::kV;
-  sh.ring = sh.VC + C::kV;
+  sh.ring = sh.VC + 2 * C::kV;
   sh.red = sh.ring + C::kRing * C::kSlots;
+  sh.mb = reinterpret_cast<uint64_t*>(sh.red + C::kRed);
+  sh.ph = 0u;
+  sh.hb = 1;
   sh.par = 0;
-  for (int i = threadIdx.x; i < 3 * C::kV; i += C::kThreads) smem[i] = 0.0;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 4; ++i) cl_mb_init(sh.mb + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < 4 * C::kV; i += C::kThreads) smem[i] = 0.0;
   if (th.rank == 0 && threadIdx.x == 0) {
     const int lv = *((volatile const int32_t*)a.active + s) != 0;
     for (int c = 0; c < C::CS; ++c) *cl.map_shared_rank(&live, c) = lv;

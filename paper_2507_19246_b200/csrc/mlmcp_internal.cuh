@@ -238,6 +238,7 @@ bool coop_usable(const Ctx* ctx, int n_tasks);
 // cluster path (one thread-block cluster per task, grids up to 128 x 128)
 bool cluster_usable(const Ctx* ctx);
 bool band_usable(const Ctx* ctx);
+size_t band_ring_bytes(int n_tasks);
 int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* rpar,
                    const double* profile, double omega, double rtol, int max_it, int order,
                    int ls_on, const double* xss, double* ring, double* xbuf, double* qoi,

@@ -2515,10 +2515,11 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
   Work w = carve(ws, L);
   // region-linear grids up to 256 x 256: one 16-CTA cluster per task keeps the
   // PCG vectors on chip (band_path.cu)
-  if (band_usable(ctx) && rpar != nullptr && region_on())
+  if (band_usable(ctx) && rpar != nullptr && region_on() &&
+      band_ring_bytes(n_tasks) <= ws_bytes)   // the band path uses the workspace as its ring
     return band_propagate(ctx, n_tasks, tasks, rpar, profile, omega, rtol, max_it,
-                          stream_order(), ls_on(), xss, w.ring, xbuf, qoi, iters, status, active,
-                          elapsed, stream);
+                          stream_order(), ls_on(), xss, static_cast<double*>(ws), xbuf, qoi,
+                          iters, status, active, elapsed, stream);
   SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
                       iters, status, active, w);
   set_region(ctx, a, rpar);
