@@ -7,12 +7,20 @@ SRC := $(wildcard paper_2507_19246_b200/csrc/*.cu)
 HDR := $(wildcard paper_2507_19246_b200/csrc/*.cuh) include/mlmcp.h
 LIB := paper_2507_19246_b200/libmlmcp.so
 
+CHECKED := paper_2507_19246_b200/libmlmcp_checked.so
+
 all: $(LIB)
+
+# device-side bounds / invariant checks (MLMCP_DCHECK), same ABI
+checked: $(CHECKED)
+
+$(CHECKED): $(SRC) $(HDR)
+	$(NVCC) $(NVFLAGS) -DMLMCP_CHECKED -shared -o $@ $(SRC)
 
 $(LIB): $(SRC) $(HDR)
 	$(NVCC) $(NVFLAGS) -shared -o $@ $(SRC)
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(CHECKED)
 
-.PHONY: all clean
+.PHONY: all clean checked

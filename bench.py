@@ -566,7 +566,7 @@ def main():
         else:
             kname = ("tile_iter_rw_kernel" if rw else "tile_iter_rg_kernel") if region \
                 else "tile_iter_kernel"
-            kernel = f"{kname}<16,4,3> (one fused launch per PCG iteration)"
+            kernel = f"{kname}<16,4,{4 if rw else 3}> (one fused launch per PCG iteration)"
             # bytes the kernel must move per task-iteration: read + write of the PCG
             # vectors it keeps in HBM (x r s p with w recomputed; + w; + the operator)
             streamed = (64 if rw else 80 if region else 112) * N

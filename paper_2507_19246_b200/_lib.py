@@ -20,7 +20,10 @@ import threading
 import numpy as np
 
 LIB_NAME = "libmlmcp.so"
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), LIB_NAME)
+# MLMCP_LIB selects another in-tree build (e.g. libmlmcp_checked.so, the
+# device-side-checked build of scripts/checked_suite.sh)
+LIB_PATH = os.environ.get("MLMCP_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)),
+                                                       LIB_NAME)
 
 EINVAL = -22
 ECUDA = -5

@@ -108,6 +108,7 @@ struct BdArgs {
   const int32_t* active;
   int64_t* elapsed;
   int prof;
+  int dbg_sync;            // MLMCP_BAND_SYNC=1: cluster barriers around every exchange / all-reduce
 };
 
 __device__ __forceinline__ void bd_arrive() {
@@ -181,6 +182,7 @@ struct Sh {
                   // RED[b], [4] halo rows of VA
   uint32_t ph;    // wait parity bits of the five mbarriers
   int hb;         // VC buffer of the current iteration
+  int dbg;        // BdArgs::dbg_sync
   double* PF;     // [2R-1][kNT] strip factors
   double* TAB;    // [rC][kTabW]
   double* RED;    // [2][4][kCS] CTA partials of every CTA, [4][kWarps] warp partials
@@ -241,7 +243,9 @@ __device__ __forceinline__ void bd_stencil(const BdArgs& a, const double2* sp, u
 // an all-reduce in between, so no neighbour still reads what is overwritten.
 __device__ __forceinline__ void bd_xissue(const Th& th, const double (&v)[kR], double* V, Sh& sh,
                                           int mi) {
+  if (sh.dbg) bd_sync();
   uint64_t* mb = sh.mb + mi;
+  MLMCP_DCHECK(th.vb - kLD - 1 >= 0 && th.vb + kR * kLD + 1 < kV);
 #pragma unroll
   for (int r = 0; r < kR; ++r) V[th.vb + r * kLD] = v[r];
   if (th.k == 0 && th.rank > 0)
@@ -256,11 +260,13 @@ __device__ __forceinline__ void bd_xissue(const Th& th, const double (&v)[kR], d
 __device__ __forceinline__ void bd_xwait(Sh& sh, int mi) {
   mb_wait(sh.mb + mi, (sh.ph >> mi) & 1u);
   sh.ph ^= 1u << mi;
+  if (sh.dbg) bd_sync();
 }
 
 // bd_xissue for a vector whose own rows are already in V: the band's edge rows
 // are read back from V and sent to the neighbours
 __device__ __forceinline__ void bd_xsend(const Th& th, double* V, Sh& sh, int mi) {
+  if (sh.dbg) bd_sync();
   uint64_t* mb = sh.mb + mi;
   if (th.k == 0 && th.rank > 0)
     st_async(bd_mapa(bd_smem(V + (kHB + 1) * kLD + th.x + 1), th.rank - 1), V[th.vb],
@@ -372,6 +378,7 @@ __device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) 
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
   }
+  if (sh.dbg) bd_sync();
   double* wp = sh.RED + 2 * 4 * kCS;        // [4][kWarps]
   double* cp = sh.RED + sh.par * 4 * kCS;   // [4][kCS]
   uint64_t* mb = sh.mb + 2 + sh.par;
@@ -400,6 +407,7 @@ __device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) 
   }
   mb_wait(mb, (sh.ph >> (2 + sh.par)) & 1u);
   sh.ph ^= 1u << (2 + sh.par);
+  if (sh.dbg) bd_sync();
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double s = cp[k * kCS + (lane & 15)];
@@ -572,6 +580,16 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
   sh.mb = reinterpret_cast<uint64_t*>(sh.RED + kRedD);
   sh.ph = 0u;
   sh.hb = 1;
+  sh.dbg = a.dbg_sync;
+#ifdef MLMCP_CHECKED
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    MLMCP_DCHECK((size_t)(reinterpret_cast<char*>(sh.mb + 5) - reinterpret_cast<char*>(smem)) <= dyn);
+    MLMCP_DCHECK(th.gy0 * kTX + th.x + (kR - 1) * kTX < kBandPts);
+    MLMCP_DCHECK(C >= 1 && C <= kMaxC && a.R >= 1 && a.R <= 16);
+  }
+#endif
   sh.par = 0;
   for (int i = threadIdx.x; i < 3 * kV; i += kNT) smem[i] = 0.0;
   if (threadIdx.x == 0) {
@@ -589,8 +607,13 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
 #pragma unroll
   for (int i = 0; i < kR / 4; ++i) th.cl[i] = 0u;
 #pragma unroll
-  for (int r = 0; r < kR; ++r)
+  for (int r = 0; r < kR; ++r) {
+    MLMCP_DCHECK(!th.ok(r) || (th.row(r) >= 0 && th.row(r) < a.N));
     if (th.ok(r)) th.cl[r >> 2] |= (uint32_t)__ldg(a.rcls + th.row(r)) << (8 * (r & 3));
+  }
+#ifdef MLMCP_CHECKED
+  for (int r = 0; r < kR; ++r) MLMCP_DCHECK(th.cls(r) < a.rC);
+#endif
   bd_sync();   // zeroed buffers, region parameters and the live flag visible
   if (!live) return;   // cluster-uniform
   for (int c = threadIdx.x; c < C; c += kNT) {
@@ -796,7 +819,9 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
   a.active = active;
   a.elapsed = elapsed;
   const char* pe = getenv("MLMCP_BAND_PROF");
-  a.prof = pe ? atoi(pe) : 0;   // bit 0: phase cycles; 2, 4: guess-load experiments
+  a.prof = pe ? atoi(pe) : 0;   // bit 0: phase cycles
+  const char* ds = getenv("MLMCP_BAND_SYNC");
+  a.dbg_sync = (ds && atoi(ds) != 0) ? 1 : 0;
   const size_t smem = band_smem_bytes(a.rC);
   static size_t attr_smem = 0;
   if (smem > attr_smem) {

@@ -45,6 +45,8 @@ struct ClArgs {
   const int32_t* gpos;   // [7][N]: CSR position of direction SW,S,W,C,E,N,NE, or -1
   const double* M;
   const double* K;
+  const double* M7;      // [S][7][N] mass values in stencil-slot layout (direct loads), or null
+  int dbg_sync;          // MLMCP_CLUSTER_SYNC=1 (race check of the mbarrier protocol)
   const double* profile;
   double omega, rtol2;
   int max_it;
@@ -223,6 +225,24 @@ struct ClOp {
       out[r] = acc0 + acc1;
     }
   }
+  // out = M v from the stencil-slot layout (M7s = the sample's [7][N] slice):
+  // apply_vals' sums with direct, coalesced loads instead of the gpos gather
+  // (zero slots add exact zeros)
+  __device__ static void apply_m7(const Thr<C>& th, const ClArgs& A, const double* __restrict__ M7s,
+                                  const double (&v)[R], const double* V, double (&out)[R]) {
+    double nb[R][7];
+    neighbours(th, v, V, nb);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      double acc = 0.0;
+      if (th.ok(r, A)) {
+        const int rw = th.row(r, A);
+#pragma unroll
+        for (int j = 0; j < 7; ++j) acc = fma(__ldg(M7s + (int64_t)j * A.N + rw), nb[r][j], acc);
+      }
+      out[r] = acc;
+    }
+  }
   // out = B v for per-sample CSR values B (the energy, and M a_n once per step)
   __device__ static void apply_vals(const Thr<C>& th, const ClArgs& A,
                                     const double* __restrict__ vals, const double (&v)[R],
@@ -303,7 +323,9 @@ struct ClShared {
   uint64_t* mb;  // mbarriers: [0..1] halo rows of VC[b], [2..3] CTA partials of red[b]
   uint32_t ph;   // wait parity bits of the mbarriers
   int hb;        // VC buffer of the current exchange
+  int dbg;       // MLMCP_CLUSTER_SYNC=1: cluster barriers around every exchange / all-reduce
   const double* Ms;   // per-sample CSR mass values (M a_n once per step, from L2)
+  const double* M7s;  // the same in stencil-slot layout [7][N], or null
   double* ring;  // [kRing][kSlots] past states
   double* red;   // [2][kRedVals][CS][kWarps]
   int par;
@@ -317,10 +339,12 @@ struct ClShared {
 template <class C>
 __device__ __forceinline__ double* cl_exchange(const Thr<C>& th, const double (&v)[C::R],
                                                ClShared<C>& sh) {
+  if (sh.dbg) cl_sync();
   sh.hb ^= 1;
   double* V = sh.VC + sh.hb * C::kV;
   uint64_t* mb = sh.mb + sh.hb;
   const int b = th.vidx(0);
+  MLMCP_DCHECK(b - C::LD - 1 >= 0 && b + C::R * C::LD + 1 < C::kV);
 #pragma unroll
   for (int r = 0; r < C::R; ++r) V[b + r * C::LD] = v[r];
   if (th.k == 0 && th.rank > 0)
@@ -334,6 +358,7 @@ __device__ __forceinline__ double* cl_exchange(const Thr<C>& th, const double (&
   __syncthreads();
   cl_mb_wait(mb, (sh.ph >> sh.hb) & 1u);
   sh.ph ^= 1u << sh.hb;
+  if (sh.dbg) cl_sync();
   return V;
 }
 
@@ -351,6 +376,7 @@ __device__ __forceinline__ void cl_allsum_mb(double (&v)[NV], ClShared<C>& sh, i
 #pragma unroll
     for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
   }
+  if (sh.dbg) cl_sync();
   double* wp = sh.red + 2 * 4 * CS;          // [4][W]
   double* cp = sh.red + sh.par * 4 * CS;     // [4][CS]
   uint64_t* mb = sh.mb + 2 + sh.par;
@@ -377,6 +403,7 @@ __device__ __forceinline__ void cl_allsum_mb(double (&v)[NV], ClShared<C>& sh, i
   }
   cl_mb_wait(mb, (sh.ph >> (2 + sh.par)) & 1u);
   sh.ph ^= 1u << (2 + sh.par);
+  if (sh.dbg) cl_sync();
 #pragma unroll
   for (int k = 0; k < NV; ++k) {
     double s = cp[k * CS + (lane & (CS - 1))];
@@ -419,7 +446,8 @@ __device__ __forceinline__ int cl_ie_step(const ClOp<C>& op, const Thr<C>& th, c
   double red3[3] = {0.0, 0.0, 0.0};
   {
     double mx[R], ax[R], bv[R];
-    ClOp<C>::apply_vals(th, A, sh.Ms, an, sh.VA, mx);
+    if (sh.M7s != nullptr) ClOp<C>::apply_m7(th, A, sh.M7s, an, sh.VA, mx);
+    else ClOp<C>::apply_vals(th, A, sh.Ms, an, sh.VA, mx);
     op.apply(th, x, sh.VB, ax);
 #pragma unroll
     for (int r = 0; r < R; ++r) {
@@ -552,6 +580,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_propagate_kernel(ClArg
   sh.ph = 0u;
   sh.hb = 1;
   sh.par = 0;
+  sh.dbg = a.dbg_sync;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) cl_mb_init(sh.mb + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -571,6 +600,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_propagate_kernel(ClArg
   ClOp<C> op;
   op.load(th, a, Ms, Ks, t.dt);
   sh.Ms = Ms;
+  sh.M7s = a.M7 ? a.M7 + (int64_t)t.sample * 7 * a.N : nullptr;
   double x[R];
 #pragma unroll
   for (int r = 0; r < R; ++r) {
@@ -663,6 +693,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a
   sh.ph = 0u;
   sh.hb = 1;
   sh.par = 0;
+  sh.dbg = a.dbg_sync;
   if (threadIdx.x == 0) {
     for (int i = 0; i < 4; ++i) cl_mb_init(sh.mb + i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -680,6 +711,7 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a
   ClOp<C> op;
   op.load(th, a, Ms, Ks, cc.dt_c);
   sh.Ms = Ms;
+  sh.M7s = nullptr;
   double* Us = cc.U + (int64_t)s * (cc.m + 1) * N;
   const double* Fs = cc.F + (int64_t)s * (cc.m + 1) * N;
   double* Cs = cc.C + (int64_t)s * cc.m * N;
@@ -726,6 +758,17 @@ __global__ void __launch_bounds__(C::kThreads, 1) cluster_coarse_kernel(ClArgs a
   cl_sync();   // no CTA leaves while another may still address its shared memory
 }
 
+// per-sample mass values into the stencil-slot layout [S][7][N] (SW..NE; 0 where
+// the neighbour is a Dirichlet node)
+__global__ void m7_kernel(int S, int N, int64_t nnz, const int32_t* gpos, const double* M,
+                          double* M7) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (int64_t)7 * N) return;
+  const int s = blockIdx.y;
+  const int q = gpos[i];
+  M7[(int64_t)s * 7 * N + i] = q >= 0 ? M[(int64_t)s * nnz + q] : 0.0;
+}
+
 // 128 column threads x 4 strips of 4 rows, 8 CTAs: grids up to 128 x 128
 using Cfg128 = Cfg<4, 128, 4, 8>;
 
@@ -755,6 +798,11 @@ int launch(const ClArgs& a, int n_tasks, cudaStream_t stream) {
   return MLMCP_OK;
 }
 
+int cluster_dbg_sync() {
+  const char* e = getenv("MLMCP_CLUSTER_SYNC");
+  return (e && atoi(e) != 0) ? 1 : 0;
+}
+
 int order_pref() {
   const char* e = getenv("MLMCP_CLUSTER_ORDER");
   const int o = e ? atoi(e) : 7;   // higher orders pay: smooth states in time
@@ -773,12 +821,22 @@ bool cluster_usable(const Ctx* ctx) {
          ctx->cl_h <= Cfg128::CS * Cfg128::HB;
 }
 
-int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
+int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                       const double* K, const double* profile, double omega, double rtol,
                       int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                      const int32_t* active, int64_t* elapsed, cudaStream_t stream) {
+                      const int32_t* active, int64_t* elapsed, void* ws, size_t ws_bytes,
+                      cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
   ClArgs a;
+  a.M7 = nullptr;
+  a.dbg_sync = cluster_dbg_sync();
+  if (ws != nullptr && ws_bytes >= sizeof(double) * (size_t)S * 7 * (size_t)ctx->n) {
+    double* m7 = static_cast<double*>(ws);
+    m7_kernel<<<dim3((unsigned)((7 * (int64_t)ctx->n + 255) / 256), (unsigned)S), 256, 0, stream>>>(
+        S, ctx->n, ctx->nnz, ctx->cl_pos, M, m7);
+    MLMCP_LAUNCH_CHECK("m7_kernel");
+    a.M7 = m7;
+  }
   a.tasks = tasks;
   a.N = ctx->n;
   a.wd = ctx->cl_wd;
@@ -810,6 +868,8 @@ int cluster_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, cons
   if (S == 0 || k >= m) return MLMCP_OK;
   using Cf = Cfg128;
   ClArgs a{};
+  a.M7 = nullptr;
+  a.dbg_sync = cluster_dbg_sync();
   a.N = ctx->n;
   a.wd = ctx->cl_wd;
   a.gh = ctx->cl_h;

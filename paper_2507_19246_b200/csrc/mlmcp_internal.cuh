@@ -102,6 +102,26 @@ int cuda_fail(cudaError_t err, const char* what);
     if (_e != cudaSuccess) return ::mlmcp::cuda_fail(_e, what);  \
   } while (0)
 
+// Device-side bounds / invariant checks of the checked build (make checked:
+// -DMLMCP_CHECKED, libmlmcp_checked.so).  compute-sanitizer is not available on
+// the GPU pool, so the GPU suite runs once against this build (scripts/
+// checked_suite.sh): a failed check prints its location and traps the kernel.
+#ifdef MLMCP_CHECKED
+#include <cstdio>
+#define MLMCP_DCHECK(c)                                                                  \
+  do {                                                                                   \
+    if (!(c)) {                                                                          \
+      printf("MLMCP_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__,   \
+             (int)blockIdx.x, (int)threadIdx.x, #c);                                    \
+      __trap();                                                                          \
+    }                                                                                    \
+  } while (0)
+#else
+#define MLMCP_DCHECK(c) \
+  do {                  \
+  } while (0)
+#endif
+
 // ------------------------------------------------------------------ device
 // Reciprocal to ~1 ulp: MUFU approximation + two Newton steps (no slow-path
 // branch, so it schedules freely; deterministic).
@@ -244,10 +264,11 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
                    int ls_on, const double* xss, double* ring, double* xbuf, double* qoi,
                    int32_t* iters, int32_t* status, const int32_t* active, int64_t* elapsed,
                    cudaStream_t stream);
-int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* M,
+int cluster_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                       const double* K, const double* profile, double omega, double rtol,
                       int max_it, double* xbuf, double* qoi, int32_t* iters, int32_t* status,
-                      const int32_t* active, int64_t* elapsed, cudaStream_t stream);
+                      const int32_t* active, int64_t* elapsed, void* ws, size_t ws_bytes,
+                      cudaStream_t stream);
 int cluster_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,
                             const double* profile, double omega, double dt_c, double t0,
                             const int64_t* slice_k0, const int32_t* slice_steps, double rtol,

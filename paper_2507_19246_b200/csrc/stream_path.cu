@@ -1052,6 +1052,12 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_iter_rw_kernel(
   __syncthreads();
   const int C = a.rC;
   const double* Dv = tab + 7 * C;
+#ifdef MLMCP_CHECKED
+  for (int r = 0; r < kTR; ++r) MLMCP_DCHECK(cd[r] >= 0 && cd[r] < C);
+  MLMCP_DCHECK(c1 < C && c2 < C);
+  MLMCP_DCHECK(b1 < (kTH + 4) * kL1 && b2 < (kTH + 4) * kL1);
+  MLMCP_DCHECK((int64_t)(gy0 + kTR - 1) * a.wd + gx < N || !colok || gy0 + kTR - 1 >= a.gh);
+#endif
   double gam = 0.0;
   if (upd) {
     // ---- 2. u_{k-1} on the tile and the two-point frame
@@ -1969,8 +1975,12 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
       if (tcfg == 4) {
         tile_tma_kernel<<<grid_tma, kXThreads, kXSmem, s>>>(a);
         MLMCP_LAUNCH_CHECK("tile_tma_kernel");
-      } else if (tcfg == 1) {
+      } else if (tcfg == 1 && !(a.rcls != nullptr && rw_on())) {
         if (const int rc = launch_tile_iter<16, 4, 3>(a, grid_tiles2, s, pdl_on())) return rc;
+      } else if (tcfg == 1) {
+        // the recompute-w kernel fits 64 registers: 4 CTAs per SM (config 4:
+        // 154 -> 140 ms on the iteration launches, scripts/tile_ab.py region@2)
+        if (const int rc = launch_tile_iter<16, 4, 4>(a, grid_tiles2, s, pdl_on())) return rc;
       } else if (tcfg == 2) {
         if (const int rc = launch_tile_iter<16, 4, 4>(a, grid_tiles2, s, pdl_on())) return rc;
       } else {
@@ -2506,8 +2516,8 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
   // (cluster_path.cu); it predicts by extrapolation only, so batches that
   // carry periodic steady states stay on the kernels below
   if (cluster_usable(ctx) && !(any_ss && xss != nullptr))
-    return cluster_propagate(ctx, n_tasks, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
-                             iters, status, active, elapsed, stream);
+    return cluster_propagate(ctx, n_tasks, tasks, S, M, K, profile, omega, rtol, max_it, xbuf,
+                             qoi, iters, status, active, elapsed, ws, ws_bytes, stream);
   if (ws == nullptr || ws_bytes < L.total) {
     set_error("streaming workspace too small: need " + std::to_string(L.total) + " bytes");
     return MLMCP_ENOMEM;

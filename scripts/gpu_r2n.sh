@@ -1,0 +1,10 @@
+#!/bin/bash
+# round-2 GPU call N: cluster path on mbarriers (config 3) — parity suite, config-3 estimate,
+# per-level times, ncu of the cluster kernel
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gputests.log 2>&1; echo tests=$?
+grep -E "passed|failed|FAILED" gpurun_out/gputests.log | head -20
+timeout 600 python scripts/config_runs.py 3 > gpurun_out/cfg3.jsonl 2>&1; echo cfg3=$?; tail -2 gpurun_out/cfg3.jsonl | cut -c1-400
+timeout 600 python scripts/level_times.py 3 > gpurun_out/level_times3.log 2>&1; echo lt3=$?; tail -4 gpurun_out/level_times3.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:cluster_propagate -c 1 -f -o gpurun_out/prof_cluster python scripts/level_times.py 3 > gpurun_out/ncu_cluster.log 2>&1; echo ncu=$?
