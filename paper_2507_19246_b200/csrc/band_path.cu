@@ -774,8 +774,8 @@ size_t band_smem_bytes(int n_classes) {
 bool band_usable(const Ctx* ctx) {
   const char* e = getenv("MLMCP_BAND");
   if (e && atoi(e) == 0) return false;
-  const char* s = getenv("MLMCP_STREAM_IMPL");
-  if (s && atoi(s) != 0) return false;
+  const char* s = getenv("MLMCP_STREAM_IMPL");   // 5: the band path also on <= 128^2 grids
+  if (s && atoi(s) != 0 && atoi(s) != 5) return false;
   return ctx->rcls != nullptr && ctx->rC <= kMaxC && ctx->cl_wd > 0 && ctx->cl_wd <= kTX &&
          ctx->cl_h <= kCS * kHB && band_smem_bytes(ctx->rC) <= 227 * 1024;
 }

@@ -812,11 +812,11 @@ int order_pref() {
 }  // namespace
 
 bool cluster_usable(const Ctx* ctx) {
-  // MLMCP_STREAM_IMPL: 1 two-launch, 2 cooperative, 3 cluster, 4 tile, default
+  // MLMCP_STREAM_IMPL: 1 two-launch, 2 cooperative, 3 cluster, 4 tile, 5 band, default
   // auto (cluster when it fits)
   const char* e = getenv("MLMCP_STREAM_IMPL");
   const int impl = e ? atoi(e) : 0;
-  if (impl == 1 || impl == 2 || impl == 4) return false;
+  if (impl == 1 || impl == 2 || impl == 4 || impl == 5) return false;
   return ctx->cl_wd > 0 && ctx->cl_wd <= Cfg128::TX &&
          ctx->cl_h <= Cfg128::CS * Cfg128::HB;
 }

@@ -1401,360 +1401,6 @@ constexpr size_t tile_init_smem(bool region = false, int n_classes = 256) {
 }
 
 
-// ------------------------------------------------------ TMA-staged tile kernel
-// Warp-specialised persistent variant of tile_iter_kernel (one CTA per SM,
-// 8 consumer warps + 1 producer warp).  The producer walks the CTA's
-// (task, tile) items and stages each into one of two shared-memory buffers with
-// bulk asynchronous copies (cp.async.bulk, one per tile row and array:
-// r, w, s, D^-1 with the one-point halo, the operator's symmetric half with the
-// west column / south row, x, p, C own points), signalled on the stage's
-// full mbarrier (expect_tx); consumers release the stage on its empty
-// mbarrier.  Rows are copied from 16-byte-aligned addresses, so a row's
-// shared-memory image keeps the parity of its global element index (the
-// consumers' index arithmetic adds it back).  The consumers' arithmetic is
-// tile_iter_kernel's, on 64 x 16 tiles; their reduction tail (fence, arrival
-// counter) overlaps the next item's copies.
-constexpr int kXW = 64, kXH = 8, kXR = 2, kXSt = 4;   // tile, rows per thread, stages
-constexpr int kXCons = kXW * (kXH / kXR);          // 256 consumer threads
-constexpr int kXThreads = kXCons + 32;             // + producer warp
-constexpr int kXRW = kXW + 4;                      // halo row buffer: 66 columns + parity, even
-constexpr int kXOW = kXW + 2;                      // own-row buffer: 64 columns + parity, even
-constexpr int kXHalo = 2 * (kXW + 2) + 2 * kXH;    // 164
-constexpr int kXULD = kXW + 2;
-struct XStage {
-  double r[(kXH + 2) * kXRW], w[(kXH + 2) * kXRW], s[(kXH + 2) * kXRW], d[(kXH + 2) * kXRW];
-  double e[(kXH + 1) * kXRW], n[(kXH + 1) * kXRW], ne[(kXH + 1) * kXRW];
-  double c[kXH * kXOW], x[kXH * kXOW], p[kXH * kXOW];
-};
-struct XMeta {
-  int t, mode, k, sample, tx0, ty0, tile;
-  double alpha, beta;
-};
-constexpr size_t kXSmem = kXSt * sizeof(XStage) + sizeof(double) * ((kXH + 2) * kXULD + 2 * 4 * 32) +
-                          kXSt * sizeof(XMeta) + 2 * kXSt * sizeof(uint64_t) + 64;
-
-__device__ __forceinline__ uint32_t s_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* b, int count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(s_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(s_u32(b)) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(s_u32(b)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n XW_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra XW_%=;\n}\n" ::"r"(s_u32(b)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          s_u32(dst)),
-      "l"(src), "r"(bytes), "r"(s_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void cons_bar() { asm volatile("bar.sync 1, %0;" ::"n"(kXCons) : "memory"); }
-__device__ __forceinline__ int gpar(const double* p) { return (int)(((uintptr_t)p >> 3) & 1); }
-
-// consumers' all-reduce of NV doubles (fixed order: bitwise identical totals)
-template <int NV>
-__device__ __forceinline__ void cons_allsum(double (&v)[NV], double* red, int& par) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) v[k] += __shfl_xor_sync(0xffffffffu, v[k], off);
-  }
-  double* buf = red + par * (4 * 32);
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < NV; ++k) buf[k * 32 + warp] = v[k];
-  }
-  cons_bar();
-#pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    double s = 0.0;
-#pragma unroll
-    for (int q = 0; q < kXCons / 32; ++q) s += buf[k * 32 + q];
-    v[k] = s;
-  }
-  par ^= 1;
-}
-
-// one row copy of the producer: logical columns [c0, c0 + len) of grid row gy
-// of the array at `base`, into the row buffer `row` (clamped to the grid)
-__device__ __forceinline__ uint32_t x_row(const SArgs& a, const double* base, int gy, int c0,
-                                          int len, double* row, uint64_t* bar, bool issue) {
-  if (gy < 0 || gy >= a.gh) return 0;
-  const int cs = max(c0, 0), ce = min(c0 + len, a.wd);
-  if (cs >= ce) return 0;
-  const double* r0 = base + (int64_t)gy * a.wd;
-  const double* src = r0 + cs;
-  const double* srca = src - gpar(src);
-  const double* end = r0 + ce;
-  const double* enda = end + gpar(end);
-  const uint32_t bytes = (uint32_t)((enda - srca) * sizeof(double));
-  if (issue) bulk_g2s(row + (cs - c0) + gpar(r0 + c0) - gpar(src), srca, bytes, bar);
-  return bytes;
-}
-
-__device__ void x_produce(const SArgs& a, XStage* stg, XMeta* meta, uint64_t* full,
-                          uint64_t* empty) {
-  const int lane = threadIdx.x & 31;
-  const int n_items = a.T * a.ntile;
-  int it = 0;
-  for (int q = blockIdx.x; q < n_items; q += gridDim.x, ++it) {
-    const int st = it % kXSt;
-    if (it >= kXSt) mbar_wait(&empty[st], ((it / kXSt) & 1) ^ 1);
-    XMeta m;
-    m.t = q / a.ntile;
-    m.tile = q - m.t * a.ntile;
-    m.tx0 = (m.tile % a.ntx) * kXW;
-    m.ty0 = (m.tile / a.ntx) * kXH;
-    const mlmcp_task tk = a.tasks[m.t];
-    const int32_t* ti = a.w.ti + m.t * kTI;
-    m.mode = 0;
-    if (task_live(a, tk, m.t)) {
-      const int s = ti[I_STATE];
-      m.mode = s == ST_RUN ? 1 : (s == ST_ZERO ? 2 : 0);
-    }
-    m.k = ti[I_IT_STEP];
-    m.sample = tk.sample;
-    const bool upd = m.k > 0, first = m.k == 1, odd = m.k & 1;
-    m.alpha = upd ? a.w.td[m.t * kTD + D_ALPHA] : 0.0;
-    m.beta = upd ? a.w.td[m.t * kTD + D_BETA] : 0.0;
-    if (m.mode != 1) {
-      if (lane == 0) {
-        meta[st] = m;
-        mbar_arrive(&full[st]);
-      }
-      continue;
-    }
-    const int64_t N = a.N, o = (int64_t)m.t * N;
-    const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;
-    const double* Wo = odd ? a.w.Wv + o : a.w.W1 + o;
-    const double* So = odd ? a.w.S1 + o : a.w.Sv + o;
-    const double* Di = a.w.dinv + (int64_t)m.sample * N;
-    const double* As = a.w.A + (int64_t)m.sample * 4 * N;
-    XStage& S = stg[st];
-    // copy list: 18 halo rows of r, d (w, s), 17 of e, n, ne, 16 own rows of c (x, p)
-    uint32_t bytes = 0;
-    for (int pass = 0; pass < 2; ++pass) {
-      const bool issue = pass == 1;
-      for (int ci = lane; ci < 10 * (kXH + 2); ci += 32) {
-        const int arr = ci / (kXH + 2), rr = ci - arr * (kXH + 2);
-        const double* base = nullptr;
-        double* buf = nullptr;
-        int ly, c0 = m.tx0 - 1, len = kXW + 2, rw = kXRW;
-        switch (arr) {
-          case 0: base = Ro; buf = S.r; break;
-          case 1: base = Di; buf = S.d; break;
-          case 2: base = upd ? Wo : nullptr; buf = S.w; break;
-          case 3: base = (upd && !first) ? So : nullptr; buf = S.s; break;
-          case 4: base = As + N; buf = S.e; len = kXW + 1; break;
-          case 5: base = As + 2 * N; buf = S.n; len = kXW + 1; break;
-          case 6: base = As + 3 * N; buf = S.ne; len = kXW + 1; break;
-          case 7: base = As; buf = S.c; c0 = m.tx0; len = kXW; rw = kXOW; break;
-          case 8: base = upd ? a.w.X + o : nullptr; buf = S.x; c0 = m.tx0; len = kXW; rw = kXOW; break;
-          default: base = (upd && !first) ? a.w.P + o : nullptr; buf = S.p; c0 = m.tx0; len = kXW; rw = kXOW; break;
-        }
-        const int nrows = arr < 4 ? kXH + 2 : (arr < 7 ? kXH + 1 : kXH);
-        if (base == nullptr || rr >= nrows) continue;
-        ly = (arr < 7 ? rr - 1 : rr);
-        const uint32_t b = x_row(a, base, m.ty0 + ly, c0, len, buf + rr * rw, &full[st], issue);
-        if (!issue) bytes += b;
-      }
-      if (!issue) {
-#pragma unroll
-        for (int off = 16; off > 0; off >>= 1) bytes += __shfl_xor_sync(0xffffffffu, bytes, off);
-        if (lane == 0) {
-          meta[st] = m;
-          mbar_arrive_tx(&full[st], bytes);
-        }
-        __syncwarp();
-      }
-    }
-  }
-}
-
-__device__ void x_consume(const SArgs& a, XStage* stg, XMeta* meta, uint64_t* full,
-                          uint64_t* empty, double* U, double* red) {
-  __shared__ int s_last;
-  const int lane = threadIdx.x & 31;
-  const int cx = threadIdx.x % kXW, sy = threadIdx.x / kXW;
-  const int n_items = a.T * a.ntile;
-  int par = 0, it = 0;
-  for (int q = blockIdx.x; q < n_items; q += gridDim.x, ++it) {
-    const int st = it % kXSt;
-    mbar_wait(&full[st], (it / kXSt) & 1);
-    const XMeta m = meta[st];
-    const XStage& S = stg[st];
-    const int64_t N = a.N, o = (int64_t)m.t * N;
-    const int gx = m.tx0 + cx;
-    double* X = a.w.X + o;
-    if (m.mode != 1) {
-      if (m.mode == 2) {
-#pragma unroll
-        for (int rr = 0; rr < kXR; ++rr) {
-          const int gy = m.ty0 + sy * kXR + rr;
-          if (gx < a.wd && gy < a.gh) X[(int64_t)gy * a.wd + gx] = 0.0;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-      continue;
-    }
-    const bool odd = m.k & 1, upd = m.k > 0, first = m.k == 1;
-    const double alpha = m.alpha, beta = m.beta;
-    const double* Ro = (odd || !upd) ? a.w.R + o : a.w.R1 + o;
-    const double* Di = a.w.dinv + (int64_t)m.sample * N;
-    const double* As = a.w.A + (int64_t)m.sample * 4 * N;
-    double* Rn = odd ? a.w.R1 + o : a.w.R + o;
-    double* Sn = odd ? a.w.Sv + o : a.w.S1 + o;
-    double* Wn = odd ? a.w.W1 + o : a.w.Wv + o;
-    // parity of the first logical column of a row: equal for every per-task
-    // vector (same 256-byte-aligned regions, same offset), separate for D^-1, A
-    auto hp = [&](const double* base, int gy) { return gpar(base + (int64_t)gy * a.wd + m.tx0 - 1); };
-    auto op = [&](const double* base, int gy) { return gpar(base + (int64_t)gy * a.wd + m.tx0); };
-    if (threadIdx.x < kXHalo) {
-      const int h = threadIdx.x;
-      int lx, ly;
-      if (h < kXW + 2) { lx = h - 1; ly = -1; }
-      else if (h < 2 * (kXW + 2)) { lx = h - (kXW + 2) - 1; ly = kXH; }
-      else if (h < 2 * (kXW + 2) + kXH) { lx = -1; ly = h - 2 * (kXW + 2); }
-      else { lx = kXW; ly = h - 2 * (kXW + 2) - kXH; }
-      const int hx = m.tx0 + lx, hy = m.ty0 + ly;
-      double u = 0.0;
-      if (hx >= 0 && hx < a.wd && hy >= 0 && hy < a.gh) {
-        const int bi = (ly + 1) * kXRW + lx + 1;
-        const int pv = hp(Ro, hy), pd = hp(Di, hy);
-        double r = S.r[bi + pv];
-        if (upd) r = fma(-alpha, tile_s(first, beta, S.w[bi + pv], first ? 0.0 : S.s[bi + pv]), r);
-        u = S.d[bi + pd] * r;
-      }
-      U[(ly + 1) * kXULD + lx + 1] = u;
-    }
-    double gam = 0.0;
-#pragma unroll
-    for (int rr = 0; rr < kXR; ++rr) {
-      const int ly = sy * kXR + rr, gy = m.ty0 + ly;
-      const bool ok = gx < a.wd && gy < a.gh;
-      double u = 0.0;
-      if (ok) {
-        const int64_t i = (int64_t)gy * a.wd + gx;
-        const int bi = (ly + 1) * kXRW + cx + 1;
-        const int pv = hp(Ro, gy), pd = hp(Di, gy);
-        const double ro = S.r[bi + pv], dv = S.d[bi + pd];
-        double rk = ro;
-        if (upd) {
-          const int oi = ly * kXOW + cx + op(X, gy);
-          const double uo = dv * ro;
-          const double p = first ? uo : fma(beta, S.p[oi], uo);
-          const double s = tile_s(first, beta, S.w[bi + pv], first ? 0.0 : S.s[bi + pv]);
-          rk = fma(-alpha, s, ro);
-          a.w.P[o + i] = p;
-          Sn[i] = s;
-          X[i] = fma(alpha, p, S.x[oi]);
-          Rn[i] = rk;
-        }
-        u = dv * rk;
-        gam = fma(rk, u, gam);
-      }
-      U[(ly + 1) * kXULD + cx + 1] = u;
-    }
-    cons_bar();
-    double del = 0.0;
-#pragma unroll
-    for (int rr = 0; rr < kXR; ++rr) {
-      const int ly = sy * kXR + rr, gy = m.ty0 + ly;
-      if (!(gx < a.wd && gy < a.gh)) continue;
-      const int b = (ly + 1) * kXULD + cx + 1;
-      const int ci = ly * kXOW + cx + op(As, gy);
-      const int ei = (ly + 1) * kXRW + cx + 1 + hp(As + N, gy);
-      const int ni = (ly + 1) * kXRW + cx + 1 + hp(As + 2 * N, gy);
-      const int nei = (ly + 1) * kXRW + cx + 1 + hp(As + 3 * N, gy);
-      const int nsi = ly * kXRW + cx + 1 + hp(As + 2 * N, gy - 1);
-      const int nswi = ly * kXRW + cx + hp(As + 3 * N, gy - 1);
-      const double uc = U[b];
-      double acc0 = S.c[ci] * uc, acc1 = S.ne[nswi] * U[b - kXULD - 1];
-      acc0 = fma(S.n[nsi], U[b - kXULD], acc0);
-      acc1 = fma(S.e[ei - 1], U[b - 1], acc1);
-      acc0 = fma(S.e[ei], U[b + 1], acc0);
-      acc1 = fma(S.n[ni], U[b + kXULD], acc1);
-      acc0 = fma(S.ne[nei], U[b + kXULD + 1], acc0);
-      const double w = acc0 + acc1;
-      Wn[(int64_t)gy * a.wd + gx] = w;
-      del = fma(w, uc, del);
-    }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);   // this warp is done with the stage
-    double v[2] = {gam, del};
-    cons_allsum<2>(v, red, par);
-    if (threadIdx.x == 0) {
-      double* dst = a.w.partial + ((int64_t)m.t * a.nblk + m.tile) * 4;
-      dst[0] = v[0];
-      dst[1] = v[1];
-      __threadfence();
-      s_last = atomicAdd(a.w.arrive + m.t, 1) == a.ntile - 1;
-    }
-    cons_bar();
-    if (s_last) {
-      __threadfence();
-      double acc[2] = {0.0, 0.0};
-      for (int b = threadIdx.x; b < a.ntile; b += kXCons) {
-        const double* src = a.w.partial + ((int64_t)m.t * a.nblk + b) * 4;
-        acc[0] += __ldcg(src);
-        acc[1] += __ldcg(src + 1);
-      }
-      cons_allsum<2>(acc, red, par);
-      if (threadIdx.x == 0) {
-        a.w.arrive[m.t] = 0;
-        cg_scalars(a, m.t, acc[0], acc[1]);
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kXThreads, 1) tile_tma_kernel(SArgs a) {
-  extern __shared__ __align__(128) double xsm[];
-  XStage* stg = reinterpret_cast<XStage*>(xsm);
-  double* U = reinterpret_cast<double*>(stg + kXSt);
-  double* red = U + (kXH + 2) * kXULD;
-  XMeta* meta = reinterpret_cast<XMeta*>(red + 2 * 4 * 32);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(meta + kXSt);   // full[kXSt], empty[kXSt]
-  if (threadIdx.x == 0) {
-    for (int i = 0; i < kXSt; ++i) {
-      mbar_init(&bars[i], 1);
-      mbar_init(&bars[kXSt + i], kXCons / 32);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  if (threadIdx.x >= kXCons) x_produce(a, stg, meta, bars, bars + kXSt);
-  else x_consume(a, stg, meta, bars, bars + kXSt, U, red);
-}
-
-int tile_tma_grid() {
-  static int g = 0;
-  if (g == 0) {
-    int dev = 0, sms = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaFuncSetAttribute(tile_tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kXSmem);
-    g = sms > 0 ? sms : 148;
-  }
-  return g;
-}
-
 // mode 0: per-step (trajectory store + SUM_ENERGY accumulation);
 // mode 1: finalize (x_out, FINAL_ENERGY / SUM write-out, iters, status)
 __global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step_arg, int mode) {
@@ -1857,12 +1503,13 @@ bool tile_usable(const Ctx* ctx) {
   return ntile <= (ctx->n + kThreads - 1) / kThreads;   // partial-sum slots
 }
 
-// MLMCP_TILE_CFG: 1 tile_iter_kernel<16,4,3> (default), 2 <16,4,4>, 3 <8,2,4>,
-// 4 the TMA-staged warp-specialised kernel (experimental); 64x32 tiles at
-// 2 CTAs/SM measured 11% slower than the default
+// MLMCP_TILE_CFG: 1 default (<16,4,3>; the recompute-w region kernel <16,4,4>),
+// 2 <16,4,4>, 3 <8,2,4>; 64x32 tiles at 2 CTAs/SM measured 11% slower than the
+// default.  (A warp-specialised variant staging tiles with cp.async.bulk row
+// copies measured 2.3x slower and was removed.)
 int tile_cfg() {
   const char* e = getenv("MLMCP_TILE_CFG");
-  return e ? std::max(1, std::min(4, atoi(e))) : 1;
+  return e ? std::max(1, std::min(3, atoi(e))) : 1;
 }
 
 // MLMCP_TILE_PDL=0 disables programmatic dependent launch of the tile
@@ -1927,7 +1574,6 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
     MLMCP_LAUNCH_CHECK("form_ell_kernel");
   }
   const int tcfg = tile_cfg();
-  const dim3 grid_tma(a.tile && tcfg == 4 ? tile_tma_grid() : 1);
   if (a.tile) {   // 64-column tiles of 16 rows (variants 3, 4: 8 rows)
     const int th = tcfg >= 3 ? 8 : 16;
     a.ntx = (a.wd + kTW - 1) / kTW;
@@ -1972,10 +1618,7 @@ int run_steps(Ctx* ctx, SArgs& a, int n_steps_max, double dt, cudaStream_t strea
   }
   auto launch_iteration = [&](cudaStream_t s) -> int {
     if (a.tile) {
-      if (tcfg == 4) {
-        tile_tma_kernel<<<grid_tma, kXThreads, kXSmem, s>>>(a);
-        MLMCP_LAUNCH_CHECK("tile_tma_kernel");
-      } else if (tcfg == 1 && !(a.rcls != nullptr && rw_on())) {
+      if (tcfg == 1 && !(a.rcls != nullptr && rw_on())) {
         if (const int rc = launch_tile_iter<16, 4, 3>(a, grid_tiles2, s, pdl_on())) return rc;
       } else if (tcfg == 1) {
         // the recompute-w kernel fits 64 registers: 4 CTAs per SM (config 4:
@@ -2191,7 +1834,7 @@ bool region_on() {
 // and the caller passed the per-sample region parameters (the TMA variant
 // keeps the streamed operator)
 void set_region(const Ctx* ctx, SArgs& a, const double* rpar) {
-  if (!a.tile || ctx->rcls == nullptr || rpar == nullptr || tile_cfg() == 4 || !region_on())
+  if (!a.tile || ctx->rcls == nullptr || rpar == nullptr || !region_on())
     return;
   a.rcls = ctx->rcls;
   a.rckey = ctx->rckey;

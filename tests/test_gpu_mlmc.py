@@ -335,14 +335,16 @@ def test_fused_scheduler_coarse_failure_ends_chains(cuda):
     (40, {"MLMCP_STREAM_IMPL": "4"}),                               # one ragged tile column
     (72, {"MLMCP_STREAM_IMPL": "4"}),                               # 64 + 7 columns
     (72, {"MLMCP_STREAM_IMPL": "4", "MLMCP_TILE_CFG": "3"}),        # 8-row tiles
-    (72, {"MLMCP_STREAM_IMPL": "4", "MLMCP_TILE_CFG": "4"}),        # TMA-staged variant
+    (40, {"MLMCP_STREAM_IMPL": "5"}),                               # band path: 13 empty CTAs
+    (72, {"MLMCP_STREAM_IMPL": "5"}),                               # band path, ragged rows
     (72, {"MLMCP_STREAM_IMPL": "4", "MLMCP_STREAM_GRAPH": "1"}),    # device-driven step loop
     (72, {"MLMCP_STREAM_IMPL": "1", "MLMCP_STREAM_GRAPH": "1"}),
 ])
 def test_tile_path_ragged_grids_vs_oracle(cuda, n, env, monkeypatch):
     """The tile kernels on grids whose width / height are not multiples of the
     tile (edge tiles, halo clamping), every variant and the graph-driven step
-    loop: sequential and Parareal vs the splu oracle (QoI 1e-8, K equal)."""
+    loop, and the band path on grids that leave part of its 16 x 16-row
+    cluster empty: sequential and Parareal vs the splu oracle (QoI 1e-8, K equal)."""
     from paper_2507_19246_b200 import fe
     from paper_2507_19246_b200.models import (EddyCurrentFamily, ParameterVector, QoIKind,
                                               UncertainInput, make_hierarchy)
