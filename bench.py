@@ -111,11 +111,37 @@ def _cpu_task(args):
     return mo.coupled(prob, cfg, level, p)
 
 
+_REF = {}
+
+
+def reference_timeint():
+    """The UNMODIFIED reference's timeint module from baseline/_ref (installed by
+    scripts/install_reference.sh; it travels to the GPU box with the snapshot)
+    with the splu backend of SURVEY §8(c) in its module globals
+    (timeint.py:17,64-75: _factorize / lu_solve), or None when absent."""
+    if "timeint" in _REF:
+        return _REF["timeint"]
+    ref = os.path.join(ROOT, "baseline", "_ref")
+    mod = None
+    if os.path.isdir(os.path.join(ref, "mlmc_parareal")):
+        if ref not in sys.path:
+            sys.path.insert(0, ref)
+        import scipy.sparse as sp
+        from scipy.sparse.linalg import splu
+        from mlmc_parareal import timeint as mod
+        mod._factorize = lambda model, dt: splu(sp.csc_matrix(model.mass + dt * model.stiffness))
+        mod.lu_solve = lambda lu, rhs: lu.solve(rhs)
+    _REF["timeint"] = mod
+    return mod
+
+
 def _cpu_level0_task(args):
-    """One level-0 solve of key (seed, 0, k) through the oracle port of the
-    reference (timeint.py:88-111 with the splu backend), the
-    QoI included; returns (factorisation seconds, seconds per time step, steps).
-    The factorisation is timed on its own (one extra splu of the same matrix)."""
+    """One level-0 solve of key (seed, 0, k) on the host: the reference's own
+    implicit_euler_solve (timeint.py:88-111, splu backend) when
+    baseline/_ref holds it, else the oracle port (bitwise the same algorithm);
+    the QoI included.  Returns (factorisation seconds, seconds per time step,
+    steps, kind).  The factorisation is timed on its own (one extra splu of
+    the same matrix)."""
     from oracle import ie_oracle
     from oracle import mlmc_oracle as mo
     cfg_i, k, seed = args
@@ -123,14 +149,29 @@ def _cpu_level0_task(args):
     p = mo.draw(cfg, seed, 0, k)
     dt = cfg.dts[0]
     model = prob.model(p)
+    n = cfg.steps(0) if hasattr(cfg, "steps") else int(round(cfg.horizon / dt))
+    ti = reference_timeint()
+    if ti is not None:
+        t0 = time.perf_counter()
+        ti._factorize(model, dt)
+        t_f = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        tr = ti.implicit_euler_solve(model, 0.0, cfg.horizon, dt, model.initial_state)
+        if cfg.qoi == "energy_T":
+            q = mo.energy(model, tr.states[-1])
+        else:   # time average over the last window, right end points (models.py:337-339)
+            n_w = int(round(cfg.avg_window / dt))
+            q = sum(mo.energy(model, a) for a in tr.states[n + 1 - n_w:]) * dt / cfg.avg_window
+        t_all = time.perf_counter() - t0
+        del tr, q
+        return t_f, max(0.0, t_all - t_f) / n, n, "reference"
     t0 = time.perf_counter()
     ie_oracle.factorize(model, dt)
     t_f = time.perf_counter() - t0
     t0 = time.perf_counter()
     mo.evaluate(prob, cfg, p, dt, False)
     t_all = time.perf_counter() - t0
-    n = cfg.steps(0) if hasattr(cfg, "steps") else int(round(cfg.horizon / dt))
-    return t_f, max(0.0, t_all - t_f) / n, n
+    return t_f, max(0.0, t_all - t_f) / n, n, "port"
 
 
 def cpu_model():
@@ -157,6 +198,11 @@ def run_cpu_model_sample(cfg_i: int, seed: int, cores: int, pool):
     wall = time.perf_counter() - t
     t_f = float(np.mean([r[0] for r in res]))
     t_s = float(np.mean([r[1] for r in res]))
+    kind = res[0][3]
+    who = ("the unmodified reference from baseline/_ref (its implicit_euler_solve, "
+           "timeint.py:88-111, with scipy splu in its _factorize/lu_solve, SURVEY §8(c))"
+           if kind == "reference" else
+           "oracle port of the reference (timeint.py:88-111 with scipy splu, SURVEY §8(c))")
     cpu_s = 0.0
     for lvl, n in enumerate(cfg.samples):
         f = 1 if lvl == 0 else 2
@@ -169,10 +215,9 @@ def run_cpu_model_sample(cfg_i: int, seed: int, cores: int, pool):
               f"splu factorisation {t_f * 1e3:.0f} ms and {t_s * 1e3:.2f} ms per time step "
               f"measured under full-core load; the full estimate's "
               f"{sum(cfg.samples)} coupled samples extrapolated from them "
-              f"({full_wall:.0f} s on {cores} cores); oracle port of the reference "
-              f"(timeint.py:88-111 with scipy splu, SURVEY §8(c)), ProcessPool x{cores}, "
+              f"({full_wall:.0f} s on {cores} cores); {who}, ProcessPool x{cores}, "
               f"OPENBLAS_NUM_THREADS=1, CPU {cpu_model()}")
-    return rate, wall, sample
+    return rate, wall, sample, kind
 
 
 def cpu_sample_counts(cfg, cores: int, target_s: float):
@@ -203,7 +248,7 @@ def run_cpu_subset(cfg_i: int, counts, seed: int, cores: int, pool):
     sample = (f"config-{cfg_i} subset N_l={list(counts)} (keys 1..N_l), {steps} seq-equivalent "
               f"sample-timesteps in {wall:.2f} s; oracle port of the reference (dense LU as "
               f"shipped), ProcessPool x{cores}, OPENBLAS_NUM_THREADS=1, CPU {cpu_model()}")
-    return steps / wall, wall, sample
+    return steps / wall, wall, sample, "port"
 
 
 class CpuBaseline:
@@ -226,7 +271,7 @@ class CpuBaseline:
             list(self.pool.map(_cpu_task, [(self.cfg_i, 0, 1, 99)] * self.cores))
 
     def step(self, seed: int):
-        """(rate, wall seconds, sample description)."""
+        """(rate, wall seconds, sample description, kind: "reference" | "port")."""
         if self.model_based:
             return run_cpu_model_sample(self.cfg_i, seed, self.cores, self.pool)
         counts = cpu_sample_counts(self.cfg, self.cores, 2.0)
@@ -247,9 +292,10 @@ def workload_name(cfg_i, cfg, counts, pcfg):
 
 
 def reference_arm(args):
-    """--impl reference: the reference algorithm (oracle port; the reference is
-    pure Python, pinned bitwise to the oracle, and cannot travel) on all host
-    cores; rank 0 only."""
+    """--impl reference: the reference algorithm on all host cores, rank 0 only:
+    the unmodified reference's implicit_euler_solve from baseline/_ref (splu
+    backend) when installed there, else the oracle port (bitwise the same
+    algorithm on every pinned case)."""
     if int(os.environ.get("RANK", "0")) != 0:
         return
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
@@ -259,9 +305,9 @@ def reference_arm(args):
     cb.warm()
     for w in range(args.warmup):
         cb.step(1000 + w)
-    rates, walls, sample = [], [], ""
+    rates, walls, sample, kind = [], [], "", "port"
     for s in range(args.steps):
-        r, w, sample = cb.step(s)
+        r, w, sample, kind = cb.step(s)
         rates.append(r)
         walls.append(w)
     cb.close()
@@ -276,7 +322,7 @@ def reference_arm(args):
                        "sampled_per_step": sample,
                        "sample_wall_ms": 1000.0 * float(np.mean(walls)),
                        "parallelism": f"{cb.cores} host processes"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.cores, "kind": "port",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb.cores, "kind": kind,
                              "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -619,9 +665,9 @@ def main():
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cb = CpuBaseline(args.config)
         cb.warm()
-        rate, w, sample = cb.step(cfg.seed)
+        rate, w, sample, kind = cb.step(cfg.seed)
         cb.close()
-        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cb.cores, "kind": "port",
+        out["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cb.cores, "kind": kind,
                                "sample": sample}
     if rank == 0:
         print(json.dumps(out), flush=True)

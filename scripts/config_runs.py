@@ -23,6 +23,9 @@ def run(cfg_i):
     fam = eddy_current_family(cfg_i, device="cuda:0")
     mlmc_estimate(fam, policy=FixedSamples(tuple(min(n, 2) for n in cfg.samples)),
                   parareal_cfg=pcfg, seed=cfg.seed)
+    import bench
+    clocks = bench.ClockSampler()     # nvidia-smi clocks / throttle reasons during the calls
+    clocks.start()
     walls = []
     while True:   # configs that finish in seconds: a second (warm) call is the one reported
         torch.cuda.synchronize()
@@ -33,6 +36,7 @@ def run(cfg_i):
         walls.append(time.perf_counter() - t)
         if len(walls) == 2 or walls[0] > 5.0:
             break
+    clk = clocks.stop(torch.cuda.current_device())
     wall = walls[-1]
     steps = cfg.seq_equiv_steps(1)
     ks = sorted({int(k) for lv in res.per_level for k in (getattr(lv, "parareal_k", None) or [])})
@@ -41,7 +45,7 @@ def run(cfg_i):
             "expectation": res.expectation, "rmse_estimate": res.rmse_estimate,
             "wall_s": wall, "seq_equiv_sample_timesteps": steps,
             "sample_timesteps_per_s": steps / wall, "parareal_k_values": ks,
-            "calls_s": walls, "gpus": 1}
+            "calls_s": walls, "gpus": 1, "clocks": clk}
 
 
 if __name__ == "__main__":
