@@ -53,6 +53,10 @@ constexpr int kLD = kTX + 2;             // exchange-buffer row stride
 constexpr int kV = (kHB + 2) * kLD;      // one exchange buffer
 constexpr int kSlots = kHB * kTX;        // (row, column) slots per CTA
 constexpr int kRing = 8;                 // past transients (extrapolation order <= 7)
+#ifndef MLMCP_BAND_GB
+#define MLMCP_BAND_GB 8
+#endif
+constexpr int kGB = MLMCP_BAND_GB;       // guess rows whose ring loads are in flight together
 constexpr int kBandPts = kCS * kHB * kTX;  // ring slot pitch: rows of kTX points (compile-time offsets)
 constexpr int kMaxC = 256;               // point classes
 constexpr int kTabW = 24;                // per class: A (7 + pad), M (7 + pad), K (7 + pad)
@@ -187,6 +191,7 @@ struct Sh {
   double* TAB;    // [rC][kTabW]
   double* RED;    // [2][4][kCS] CTA partials of every CTA, [4][kWarps] warp partials
   int par;
+  bool pf_tab;    // the source profile is a function of the point class (TAB[c][15])
   __device__ double* vc() const { return VC + hb * kV; }
 };
 
@@ -344,6 +349,22 @@ __device__ __forceinline__ double bd_dot7(const double* T, const double (&nb)[7]
   return acc0 + acc1;
 }
 
+// bd_dot7 that also returns the row's pad entry T[7] (one 16-byte load of T[6..7])
+__device__ __forceinline__ double bd_dot7p(const double* T, const double (&nb)[7], double& t7) {
+  const double2 t01 = *reinterpret_cast<const double2*>(T);
+  const double2 t23 = *reinterpret_cast<const double2*>(T + 2);
+  const double2 t45 = *reinterpret_cast<const double2*>(T + 4);
+  const double2 t67 = *reinterpret_cast<const double2*>(T + 6);
+  double acc0 = t23.y * nb[3], acc1 = t01.x * nb[0];
+  acc0 = fma(t01.y, nb[1], acc0);
+  acc1 = fma(t23.x, nb[2], acc1);
+  acc0 = fma(t45.x, nb[4], acc0);
+  acc1 = fma(t45.y, nb[5], acc1);
+  acc0 = fma(t67.x, nb[6], acc0);
+  t7 = t67.y;
+  return acc0 + acc1;
+}
+
 // out = B v, B the operator part `off` (0: A, 8: M, 16: K) of the class table
 __device__ __forceinline__ void bd_apply(const Th& th, const Sh& sh, int off,
                                          const double (&v)[kR], const double* V,
@@ -437,10 +458,11 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
     double bv[kR];
     bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
       const double* T = sh.TAB + th.cls(r) * kTabW;
-      const double mx = bd_dot7(T + 8, nb);
+      double pf;   // the point's source profile: its class's M-row pad entry
+      const double mx = bd_dot7p(T + 8, nb, pf);
       if (energy) red[3] = fma(nb[3], bd_dot7(T + 16, nb), red[3]);
-      bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, __ldg(a.profile + th.row(r)))))
-                       : 0.0;
+      if (!sh.pf_tab) pf = th.ok(r) ? __ldg(a.profile + th.row(r)) : 0.0;
+      bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, pf))) : 0.0;
     });
     const double* V0 = sh.vc();
     bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
@@ -547,7 +569,7 @@ __device__ __forceinline__ double bd_energy(const Th& th, Sh& sh) {
 }
 
 __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
-  static_assert(kR % 4 == 0, "guess batches of four rows");
+  static_assert(kR % kGB == 0, "guess batches of kGB rows");
   extern __shared__ __align__(16) double smem[];
   __shared__ int live;
   __shared__ double2 sp[16];
@@ -629,6 +651,29 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
     T[7] = T[15] = T[23] = 0.0;
   }
   __syncthreads();
+  {
+    // The source profile (dt sin(wt) profile_i in the rhs) depends only on which
+    // of the point's six triangles carry the source, i.e. on its class: every
+    // thread stores its points' values into their classes' M-row pad slot and
+    // the step start reads it with the M row.  A class whose points disagree
+    // bitwise (non-uniform element areas) keeps the global loads (CTA-wide).
+    __shared__ int pf_bad;
+    if (threadIdx.x == 0) pf_bad = 0;
+    double pfv[kR];
+#pragma unroll
+    for (int r = 0; r < kR; ++r) {
+      pfv[r] = th.ok(r) ? __ldg(a.profile + th.row(r)) : 0.0;
+      if (th.ok(r)) sh.TAB[th.cls(r) * kTabW + 15] = pfv[r];
+    }
+    __syncthreads();
+    bool bad = false;
+#pragma unroll
+    for (int r = 0; r < kR; ++r)
+      if (th.ok(r) && !(sh.TAB[th.cls(r) * kTabW + 15] == pfv[r])) bad = true;
+    if (bad) pf_bad = 1;
+    __syncthreads();
+    sh.pf_tab = pf_bad == 0;
+  }
   Pc pc;   // strip block-Jacobi factors (ClOp::load's recurrence)
   pc.f = sh.PF;
   {
@@ -695,10 +740,10 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
     sh.hb ^= 1;
     double* VN = sh.vc();     // the step's first exchange buffer (x0)
 #pragma unroll
-    for (int h = 0; h < kR; h += 4) {
-      double pv[4][kRing], xr[4], xi[4];   // four rows' loads in flight together
+    for (int h = 0; h < kR; h += kGB) {
+      double pv[kGB][kRing], xr[kGB], xi[kGB];   // kGB rows' loads in flight together
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
+      for (int rr = 0; rr < kGB; ++rr) {
         const int r = h + rr;
         const bool ok = th.ok(r) && pord > 0;
         const int64_t j = th.row(r);
@@ -709,7 +754,7 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
           pv[rr][sl] = (ok && ((valid >> sl) & 1u)) ? __ldcg(rb + sl * kBandPts + r * kTX) : 0.0;
       }
 #pragma unroll
-      for (int rr = 0; rr < 4; ++rr) {
+      for (int rr = 0; rr < kGB; ++rr) {
         const int r = h + rr;
         const double an = sh.X[th.slot(r)];
         double x0 = 0.0;
