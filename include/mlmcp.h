@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 9
+#define MLMCP_ABI_VERSION 10
 
 /* return codes */
 #define MLMCP_OK 0
@@ -65,6 +65,7 @@ extern "C" {
 #define MLMCP_ST_BREAKDOWN 2 /* PCG curvature <= 0    -> SingularSystemError */
 #define MLMCP_ST_NONFINITE 3 /* non-finite residual   -> SingularSystemError */
 #define MLMCP_ST_SINGULAR 4  /* zero pivot (direct)   -> SingularSystemError */
+#define MLMCP_ST_UNSUPPORTED 5 /* task flag this path does not run -> ValueError */
 
 /* QoI modes of a task */
 #define MLMCP_QOI_NONE 0
@@ -114,6 +115,19 @@ typedef struct mlmcp_task {
                                          bitwise semigroup); default:
                                          polynomial extrapolation of the task's
                                          state history (fewer PCG iterations) */
+/* Homogeneous correction solve (the fine propagator is affine, so
+ * F(U^k) = F(U^{k-1}) + Phi(U^k - U^{k-1}) with Phi the propagator without
+ * source; parareal.py:185-188 recomputes F(U^k) from scratch): the source term
+ * is dropped, x_in holds the increment, the terminal state is ADDED to
+ * xbuf[x_out .. x_out+N) (which holds the solution being corrected, F^{k-1}),
+ * and the stopping rule's reference norm is max(b.B^-1.b, sum_i (M_ii
+ * x_out_i)^2 / A_ii), so the correction is solved to the absolute accuracy
+ * of a full solve instead of relative to its own (small) right-hand side.
+ * Runs on the HBM-streaming tile kernels (structured grids; a batch that
+ * carries it never takes the cluster / band / cooperative kernels); qoi_mode
+ * must be MLMCP_QOI_NONE.  Other paths report MLMCP_ST_UNSUPPORTED (or
+ * EINVAL for non-grid patterns). */
+#define MLMCP_TASK_CORRECTION 2
 
 /* ---- library ---------------------------------------------------------- */
 int mlmcp_abi_version(void);
@@ -256,6 +270,27 @@ int mlmcp_parareal_defect(mlmcp_ctx* ctx, int S, int k, int m, int k_max,
                           const double* U_d, const double* F_d, double tol,
                           int32_t* active_d, int32_t* k_used_d,
                           double* defect_d, void* stream);
+
+/* Increments of the Parareal boundary states for correction fine solves
+ * (MLMCP_TASK_CORRECTION): mode 0 snapshots D[s][n] = U[s][n] (before the
+ * coarse sweep of iteration k), mode 1 forms D[s][n] = U[s][n] - D[s][n]
+ * (after it), for n = k-1 .. m-1 and the active samples.  U, D: [S][m+1][N]. */
+int mlmcp_parareal_delta(mlmcp_ctx* ctx, int S, int k, int m, const double* U_d, double* D_d,
+                         int mode, const int32_t* active_d, void* stream);
+
+/* Which kernels mlmcp_propagate runs a batch of n_tasks tasks over S
+ * operators on (with_ss: tasks carry periodic steady states; with_rp: region
+ * parameters are passed; correction: the batch carries MLMCP_TASK_CORRECTION):
+ * MLMCP_PATH_*. */
+#define MLMCP_PATH_DIRECT 0
+#define MLMCP_PATH_SMALL 1
+#define MLMCP_PATH_CLUSTER 2
+#define MLMCP_PATH_BAND 3
+#define MLMCP_PATH_COOP 4
+#define MLMCP_PATH_TILE 5
+#define MLMCP_PATH_ELL 6
+int mlmcp_propagate_path(const mlmcp_ctx* ctx, int n_tasks, int S, int with_ss, int with_rp,
+                         int correction);
 
 /* U[s][n] = F[s][n] for n >= k_used[s]. */
 int mlmcp_parareal_finalize(mlmcp_ctx* ctx, int S, int m, double* U_d,

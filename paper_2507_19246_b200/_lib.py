@@ -29,16 +29,19 @@ EINVAL = -22
 ECUDA = -5
 ENOMEM = -12
 
-ST_OK, ST_NOCONV, ST_BREAKDOWN, ST_NONFINITE, ST_SINGULAR = 0, 1, 2, 3, 4
+ST_OK, ST_NOCONV, ST_BREAKDOWN, ST_NONFINITE, ST_SINGULAR, ST_UNSUPPORTED = 0, 1, 2, 3, 4, 5
 STATUS_NAMES = {ST_NOCONV: "PCG did not converge within max_it",
                 ST_BREAKDOWN: "PCG breakdown (operator not SPD)",
                 ST_NONFINITE: "non-finite residual",
-                ST_SINGULAR: "(M + dt K) is singular"}
+                ST_SINGULAR: "(M + dt K) is singular",
+                ST_UNSUPPORTED: "task flag not supported on this path"}
 STATUS_INTS = 4
 
 QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2, 3, 4
 TASK_NO_EXTRAPOLATION = 1
-ABI_VERSION = 9
+TASK_CORRECTION = 2
+PATH_DIRECT, PATH_SMALL, PATH_CLUSTER, PATH_BAND, PATH_COOP, PATH_TILE, PATH_ELL = range(7)
+ABI_VERSION = 10
 DIRECT_MAX_ROWS = 4
 
 # mlmcp_task (96 bytes, natural alignment)
@@ -81,7 +84,7 @@ EXPORTS = (
     "mlmcp_ctx_set_path", "mlmcp_ctx_set_region_grid", "mlmcp_region_params",
     "mlmcp_stream_timing", "mlmcp_assemble", "mlmcp_kl_sigma", "mlmcp_workspace_bytes",
     "mlmcp_propagate", "mlmcp_periodic_workspace_bytes", "mlmcp_periodic_state", "mlmcp_parareal_coarse", "mlmcp_parareal_defect",
-    "mlmcp_parareal_finalize", "mlmcp_energy", "mlmcp_level_reduce", "mlmcp_draw_uniform",
+    "mlmcp_parareal_finalize", "mlmcp_parareal_delta", "mlmcp_propagate_path", "mlmcp_energy", "mlmcp_level_reduce", "mlmcp_draw_uniform",
     "mlmcp_draw_uniform_host", "mlmcp_fused_workspace_bytes", "mlmcp_run_fused",
 )
 
@@ -124,6 +127,10 @@ _SIGS = {
     "mlmcp_parareal_defect": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
                                              ctypes.c_int, P, P, F64, P, P, P, P]),
     "mlmcp_parareal_finalize": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, P, P, P, P]),
+    "mlmcp_parareal_delta": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
+                                            ctypes.c_int, P, P]),
+    "mlmcp_propagate_path": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                            ctypes.c_int, ctypes.c_int]),
     "mlmcp_fused_workspace_bytes": (SZ, [ctypes.c_int, ctypes.c_int, ctypes.c_int]),
     "mlmcp_run_fused": (ctypes.c_int, [P, ctypes.c_int, P, P, P, F64, F64, ctypes.c_int, P, P,
                                        ctypes.c_int, P, SZ, P]),

@@ -155,6 +155,19 @@ __global__ void finalize_kernel(int S, int m, int N, double* U, const double* F,
   }
 }
 
+// D[s][n] = U[s][n] (mode 0) or U[s][n] - D[s][n] (mode 1) for n = k-1 .. m-1
+__global__ void delta_kernel(int S, int k, int m, int N, const double* U, double* D, int mode,
+                             const int32_t* active) {
+  const int s = blockIdx.y;
+  if (active != nullptr && active[s] == 0) return;
+  const int64_t n64 = N;
+  for (int n = max(k - 1, 0); n < m; ++n) {
+    const int64_t o = ((int64_t)s * (m + 1) + n) * n64;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x)
+      D[o + i] = mode == 0 ? U[o + i] : U[o + i] - D[o + i];
+  }
+}
+
 // ---------------------------------------------------------------- K7 level reduce
 // Fixed-order reduction: thread j sums samples j, j+1024, ... in order, then a
 // fixed tree.  Bitwise independent of how the sample slots were filled.
@@ -700,6 +713,27 @@ int mlmcp_parareal_finalize(mlmcp_ctx* c, int S, int m, double* U, const double*
   finalize_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(S, m, c->n, U, F, k_used);
   MLMCP_LAUNCH_CHECK("finalize_kernel");
   return MLMCP_OK;
+}
+
+int mlmcp_parareal_delta(mlmcp_ctx* c, int S, int k, int m, const double* U, double* D, int mode,
+                         const int32_t* active, void* stream) {
+  if (c == nullptr) return einval("null context");
+  if (S < 0 || m < 1 || k < 1 || k > m || !U || !D || (mode != 0 && mode != 1))
+    return einval("bad Parareal delta arguments");
+  if (S == 0) return MLMCP_OK;
+  MLMCP_CUDA_CHECK(cudaSetDevice(c->device));
+  dim3 grid(std::min((c->n + 255) / 256, 64), S);
+  delta_kernel<<<grid, 256, 0, (cudaStream_t)stream>>>(S, k, m, c->n, U, D, mode, active);
+  MLMCP_LAUNCH_CHECK("delta_kernel");
+  return MLMCP_OK;
+}
+
+int mlmcp_propagate_path(const mlmcp_ctx* c, int n_tasks, int S, int with_ss, int with_rp,
+                         int correction) {
+  if (c == nullptr) return einval("null context");
+  if (use_direct(c)) return MLMCP_PATH_DIRECT;
+  if (use_small(c)) return MLMCP_PATH_SMALL;
+  return stream_path_of(c, n_tasks, S, with_ss != 0, with_rp != 0, correction != 0);
 }
 
 int mlmcp_energy(mlmcp_ctx* c, int n, const int32_t* sample, const int64_t* xoff,

@@ -204,6 +204,10 @@ __global__ void __launch_bounds__(128) direct_propagate_kernel(DirectArgs a) {
   const int64_t t_start = global_ns();
   const mlmcp_task t = a.tasks[tid];
   if (a.active != nullptr && t.group >= 0 && a.active[t.group] == 0) return;
+  if (t.flags & MLMCP_TASK_CORRECTION) {   // tile-path-only task kind
+    write_status(a.status, t.slot, MLMCP_ST_UNSUPPORTED, 0, t.tag, t.tag);
+    return;
+  }
   const int n = a.n;
   double m[NM][NM], lu[NM][NM], x[NM], prof[NM], b[NM], xprev[NM];
   int piv[NM];

@@ -253,6 +253,10 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
                            int32_t* status, const int32_t* active, void* ws, size_t ws_bytes,
                            cudaStream_t stream);
 
+// MLMCP_PATH_* of a streaming batch (stream_propagate's dispatch)
+int stream_path_of(const Ctx* ctx, int n_tasks, int S, bool with_ss, bool with_rp,
+                   bool correction);
+
 size_t coop_workspace_bytes(const Ctx* ctx, int n_tasks);
 bool coop_usable(const Ctx* ctx, int n_tasks);
 // cluster path (one thread-block cluster per task, grids up to 128 x 128)

@@ -879,6 +879,10 @@ __global__ void __launch_bounds__(kSmallThreads, OCC) small_propagate_kernel(Sma
   const mlmcp_task t = a.tasks[blockIdx.x];
   const int64_t t_start = global_ns();
   if (!group_active(a.active, t.group)) return;
+  if (t.flags & MLMCP_TASK_CORRECTION) {   // tile-path-only task kind
+    if (threadIdx.x == 0) write_status(a.status, t.slot, MLMCP_ST_UNSUPPORTED, 0, t.tag, t.tag);
+    return;
+  }
   SmallShared sh = setup_shared<Op::R>(smem, a.buf_doubles);
   run_task<Op>(a, t, sh, t_start, t.tag);   // PropagatorError(k, k) quirk, parareal.py:189-192
 }

@@ -351,10 +351,12 @@ __global__ void __launch_bounds__(kThreads) guess_kernel(SArgs a, int step_arg) 
 }
 
 // Last block of a task's step start: b.D^-1.b of the stopping rule, state
-__device__ __forceinline__ void step_scalars(const SArgs& a, int t, double bb) {
+// bb = b.D^-1.b of the step; bstop (>= bb) the reference of the stopping rule
+// (bb itself except for correction solves, MLMCP_TASK_CORRECTION)
+__device__ __forceinline__ void step_scalars(const SArgs& a, int t, double bb, double bstop = -1.0) {
   double* td = a.w.td + t * kTD;
   int32_t* ti = a.w.ti + t * kTI;
-  td[D_BB] = bb;
+  td[D_BB] = bstop >= 0.0 ? bstop : bb;
   ti[I_IT_STEP] = 0;
   ti[I_FIRST] = 1;
   atomicAdd(a.w.counters + 0, 1);
@@ -1309,7 +1311,8 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     return gv + sst;
   };
   const int64_t g = tk.k0 + step + 1;
-  const double sf = sin(__dmul_rn(a.omega, grid_time(tk.t_base, g, tk.dt)));
+  const bool corr = (tk.flags & MLMCP_TASK_CORRECTION) != 0;
+  const double sf = corr ? 0.0 : sin(__dmul_rn(a.omega, grid_time(tk.t_base, g, tk.dt)));
   double prof[kTR];
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
@@ -1347,7 +1350,7 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     XV[lv] = x0;
   }
   __syncthreads();
-  double bb = 0.0;
+  double bb = 0.0, bref = 0.0;
 #pragma unroll
   for (int r = 0; r < kTR; ++r) {
     const int ly = sy * kTR + r, gy = gy0 + r;
@@ -1389,6 +1392,16 @@ __global__ void __launch_bounds__(kTW * (kTH / kTR), kMinB) tile_init_kernel(SAr
     const double bv = __dadd_rn(mx, __dmul_rn(tk.dt, __dmul_rn(sf, prof[r])));
     a.w.R[o + i] = bv - ax;
     bb += bv * dv[r] * bv;
+    if (corr) {   // reference magnitude: the diagonal part of M applied to the corrected solution
+      const double mf = mco[3] * __ldcg(a.xbuf + tk.x_out + i);
+      bref += mf * dv[r] * mf;
+    }
+  }
+  if (corr) {   // block-uniform (one task per blockIdx.y)
+    double v[2] = {bb, bref};
+    if (task_reduce<2>(v, a, t, red, a.ntile) && threadIdx.x == 0)
+      step_scalars(a, t, v[0], fmax(v[0], v[1]));
+    return;
   }
   double v[1] = {bb};
   if (task_reduce<1>(v, a, t, red, a.ntile) && threadIdx.x == 0) step_scalars(a, t, v[0]);
@@ -1425,7 +1438,10 @@ __global__ void __launch_bounds__(kThreads) step_end_kernel(SArgs a, int step_ar
     const int64_t g = tk.k0 + step + 1;
     energy = tk.qoi_mode == MLMCP_QOI_SUM_ENERGY && g > tk.qoi_from && tk.qoi_slot >= 0;
   } else {
-    if (tk.x_out >= 0 && i < a.N) a.xbuf[tk.x_out + i] = X[i];
+    if (tk.x_out >= 0 && i < a.N) {
+      if (tk.flags & MLMCP_TASK_CORRECTION) a.xbuf[tk.x_out + i] += X[i];
+      else a.xbuf[tk.x_out + i] = X[i];
+    }
     energy = tk.qoi_mode == MLMCP_QOI_FINAL_ENERGY && tk.qoi_slot >= 0 && !code_now;
   }
   double e = 0.0;
@@ -2153,8 +2169,31 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
     }
     steps_max = std::max(steps_max, t.n_steps);
   }
-  bool any_ss = false;
-  for (const auto& t : h) any_ss |= (t.ss_slot >= 0 && !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION));
+  bool any_ss = false, any_corr = false;
+  for (const auto& t : h) {
+    any_ss |= (t.ss_slot >= 0 && !(t.flags & MLMCP_TASK_NO_EXTRAPOLATION));
+    any_corr |= (t.flags & MLMCP_TASK_CORRECTION) != 0;
+    if ((t.flags & MLMCP_TASK_CORRECTION) && t.qoi_mode != MLMCP_QOI_NONE) {
+      set_error("correction tasks (MLMCP_TASK_CORRECTION) carry no QoI");
+      return MLMCP_EINVAL;
+    }
+  }
+  if (any_corr) {   // correction solves run on the tile kernels only
+    if (!tile_usable(ctx)) {
+      set_error("MLMCP_TASK_CORRECTION needs the streaming tile path (structured grid)");
+      return MLMCP_EINVAL;
+    }
+    if (ws == nullptr || ws_bytes < L.total) {
+      set_error("streaming workspace too small: need " + std::to_string(L.total) + " bytes");
+      return MLMCP_ENOMEM;
+    }
+    Work w = carve(ws, L);
+    SArgs a = make_args(ctx, n_tasks, S, tasks, M, K, profile, omega, rtol, max_it, xbuf, qoi,
+                        iters, status, active, w);
+    set_region(ctx, a, rpar);
+    a.xss = xss;
+    return run_steps(ctx, a, steps_max, h[0].dt, stream);
+  }
   // one thread-block cluster per task when a sample's grid fits a cluster
   // (cluster_path.cu); it predicts by extrapolation only, so batches that
   // carry periodic steady states stay on the kernels below
@@ -2193,6 +2232,16 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
                           stream);
   }
   return run_steps(ctx, a, steps_max, h[0].dt, stream);
+}
+
+int stream_path_of(const Ctx* ctx, int n_tasks, int S, bool with_ss, bool with_rp,
+                   bool correction) {
+  (void)S;
+  if (correction) return tile_usable(ctx) ? MLMCP_PATH_TILE : MLMCP_PATH_ELL;
+  if (cluster_usable(ctx) && !with_ss) return MLMCP_PATH_CLUSTER;
+  if (band_usable(ctx) && with_rp && region_on()) return MLMCP_PATH_BAND;
+  if (coop_usable(ctx, n_tasks) && !with_ss) return MLMCP_PATH_COOP;
+  return tile_usable(ctx) ? MLMCP_PATH_TILE : MLMCP_PATH_ELL;
 }
 
 int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const double* K,

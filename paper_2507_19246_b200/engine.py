@@ -247,6 +247,19 @@ class DeviceSystem:
         check(self.lib.mlmcp_parareal_finalize(self.ctx, S, m, ptr(U), ptr(F), ptr(k_used),
                                                stream_handle(stream)), "mlmcp_parareal_finalize")
 
+    def parareal_delta(self, S, k, m, U, D, mode: int, active, stream=None):
+        """mode 0: D = U (snapshot before the coarse sweep of iteration k);
+        mode 1: D = U - D (after it), slices k-1 .. m-1 of the active samples."""
+        check(self.lib.mlmcp_parareal_delta(self.ctx, S, k, m, ptr(U), ptr(D), int(mode),
+                                            ptr(active), stream_handle(stream)),
+              "mlmcp_parareal_delta")
+
+    def propagate_path(self, n_tasks: int, S: int, with_ss: bool, with_rp: bool,
+                       correction: bool = False) -> int:
+        """_lib.PATH_* of an mlmcp_propagate batch of this shape."""
+        return int(self.lib.mlmcp_propagate_path(self.ctx, int(n_tasks), int(S), int(with_ss),
+                                                 int(with_rp), int(correction)))
+
     def energy(self, sample_idx: torch.Tensor, x_off: torch.Tensor, xbuf, K, stream=None):
         out = torch.empty(len(sample_idx), dtype=F64, device=self.device)
         check(self.lib.mlmcp_energy(self.ctx, len(sample_idx), ptr(sample_idx), ptr(x_off),

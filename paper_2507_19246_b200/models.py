@@ -655,7 +655,7 @@ class EddyCurrentFamily(_BatchedFamily):
         hold per sample: the M/K values, the per-task workspace of ONE
         propagate launch (one task per sample and dt; m fine tasks per sample
         on the Parareal level) and the states of every task (2 per sample
-        above level 0; U, F, C on the Parareal level), plus the steady states
+        above level 0; U, F, C, D on the Parareal level), plus the steady states
         of the predictor.  ``level`` None: the most demanding sequential level."""
         import torch
         sol = self.solver
@@ -670,7 +670,8 @@ class EddyCurrentFamily(_BatchedFamily):
         lvl = 1 if level is None else int(level)
         if parareal_cfg is not None and lvl == top:
             m = parareal_cfg.num_subintervals
-            tasks, states, ss = m, (3 * m + 2) * N8, 2
+            # U, F, C and the increments D of the correction fine solves
+            tasks, states, ss = m, (4 * m + 3) * N8, 2
         else:
             tasks, states, ss = 1, (2 if lvl > 0 else 1) * N8, (2 if lvl > 0 else 1)
         per = 16 * sol.nnz + per_op + tasks * per_task + states

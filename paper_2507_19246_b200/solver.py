@@ -364,7 +364,8 @@ def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool
 # ------------------------------------------------------------ Parareal
 def _pr_setup(self, M, K, S: int, row0: int, t0: float, t1: float, m: int, dt_fine: float,
               dt_coarse: float, k_max: int, stream=None, keep_traj: bool = False,
-              qoi_mode: int | None = None, qoi_index: int = 0, qoi_from: int = -1):
+              qoi_mode: int | None = None, qoi_index: int = 0, qoi_from: int = -1,
+              correction: bool = False, rp_on: bool = False):
     """Buffers, fine task tables and predictor states of a Parareal batch whose
     operators are M/K rows row0 .. row0+S-1."""
     from types import SimpleNamespace
@@ -376,9 +377,18 @@ def _pr_setup(self, M, K, S: int, row0: int, t0: float, t1: float, m: int, dt_fi
     uf_size = S * (m + 1) * N
     traj_steps = int(fst.max()) + 1
     traj_size = S * m * traj_steps * N if keep_traj else 0
-    buf = torch.zeros(2 * uf_size + traj_size, dtype=F64, device=dev)
+    # correction fine solves (iterations k >= 2): F^k = F^{k-1} + Phi(U^k - U^{k-1})
+    corr = (correction and not keep_traj and k_max > 1
+            and (qoi_mode is None or qoi_mode == _lib.QOI_FINAL_ENERGY)
+            and os.environ.get("MLMCP_PR_CORRECTION", "1") != "0"
+            and self.sys.propagate_path(S * m, S, self.use_predictor(), rp_on,
+                                        False) == _lib.PATH_TILE)
+    d_size = uf_size if corr else 0
+    buf = torch.zeros(2 * uf_size + d_size + traj_size, dtype=F64, device=dev)
     st = SimpleNamespace(S=S, row0=row0, m=m, k_max=k_max, t0=t0, dt_coarse=dt_coarse,
                          uf_size=uf_size, traj_steps=traj_steps, buf=buf, keep_traj=keep_traj,
+                         corr=corr, traj_off=2 * uf_size + d_size,
+                         D=buf[2 * uf_size:3 * uf_size].view(S, m + 1, N) if corr else None,
                          U=buf[:uf_size].view(S, m + 1, N),
                          F=buf[uf_size:2 * uf_size].view(S, m + 1, N),
                          C=torch.zeros((S, m, N), dtype=F64, device=dev),
@@ -405,7 +415,7 @@ def _pr_setup(self, M, K, S: int, row0: int, t0: float, t1: float, m: int, dt_fi
     all_tasks["x_in"] = (s_idx * (m + 1) + (n_idx - 1)) * N
     all_tasks["x_out"] = uf_size + (s_idx * (m + 1) + n_idx) * N
     if keep_traj:
-        all_tasks["traj"] = 2 * uf_size + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
+        all_tasks["traj"] = st.traj_off + ((s_idx * m + (n_idx - 1)) * traj_steps) * N
     all_tasks["group"] = s_idx
     all_tasks["slot"] = s_idx * m + (n_idx - 1)
     if qoi_mode is not None and qoi_mode != _lib.QOI_FINAL_ENERGY:
@@ -429,6 +439,16 @@ def _pr_setup(self, M, K, S: int, row0: int, t0: float, t1: float, m: int, dt_fi
         if os.environ.get("MLMCP_PREDICTOR") == "fine":
             st.xss_c = None
     st.all_tasks, st.n_idx = all_tasks, n_idx
+    if corr:
+        # slice n at iteration k >= 2 solves the homogeneous problem from
+        # D[s][n-1] = U^k_{n-1} - U^{k-1}_{n-1} and adds its end state to F_n
+        ct = all_tasks.copy()
+        ct["x_in"] = 2 * uf_size + (s_idx * (m + 1) + (n_idx - 1)) * N
+        ct["flags"] = _lib.TASK_CORRECTION
+        ct["ss_slot"] = -1
+        ct["qoi_slot"] = -1
+        ct["qoi_mode"] = _lib.QOI_NONE
+        st.corr_tasks = ct
     return st
 
 
@@ -448,7 +468,7 @@ def _pr_result(self, st, K, stream=None) -> PararealBatchResult:
         qoi = self.sys.energy(ev[0], ev[1], st.buf, K, stream)
     traj = None
     if st.keep_traj:
-        traj = st.buf[2 * st.uf_size:].view(S, m, st.traj_steps, N)
+        traj = st.buf[st.traj_off:].view(S, m, st.traj_steps, N)
     return PararealBatchResult(qoi, st.k_used, st.defects, st.status, st.fine_status, st.U, st.F,
                                traj, st.fine_iters, st.coarse_iters,
                                (st.elapsed_c, st.elapsed_f) if self.timing else None)
@@ -463,23 +483,28 @@ def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
     K_max rounds of [coarse sweep, fine slices, defect] launches."""
     S = M.shape[0]
     st = _pr_setup(self, M, K, S, 0, t0, t1, m, dt_fine, dt_coarse, k_max, stream, keep_traj,
-                   qoi_mode, qoi_index, qoi_from)
+                   qoi_mode, qoi_index, qoi_from, correction=True, rp_on=rp is not None)
     dev = self.device
-    key = ("pr", st.all_tasks.tobytes(), k_max)
+    key = ("pr", st.all_tasks.tobytes(), k_max, st.corr)
     tables = self._task_cache.get(key)
     if tables is None:
         tables = []
         for k in range(1, k_max + 1):
-            sel = st.all_tasks[st.n_idx >= k].copy()
+            src = st.corr_tasks if (st.corr and k >= 2) else st.all_tasks
+            sel = src[st.n_idx >= k].copy()
             sel["tag"] = k
             tables.append(tasks_to_device(sel, dev))
         self._task_cache[key] = tables
     for k in range(1, k_max + 1):
+        if st.corr and k >= 2:     # U^{k-1} before the sweep overwrites it
+            self.sys.parareal_delta(S, k, m, st.U, st.D, 0, st.active, stream)
         self.sys.parareal_coarse(S, k, m, M, K, self.profile, self.omega, dt_coarse, t0,
                                  st.ck0_d, st.cst_d, self.step_rtol(), self.max_it, st.U, st.F,
                                  st.C, st.coarse_iters, st.status, st.active, stream,
                                  elapsed=st.elapsed_c, xss=st.xss_c, rp=rp)
-        sel = st.all_tasks[st.n_idx >= k]
+        if st.corr and k >= 2:
+            self.sys.parareal_delta(S, k, m, st.U, st.D, 1, st.active, stream)
+        sel = (st.corr_tasks if (st.corr and k >= 2) else st.all_tasks)[st.n_idx >= k]
         self.sys.propagate(sel, M, K, self.profile, self.omega, self.step_rtol(), self.max_it,
                            st.buf, st.slice_qoi, st.fine_iters, st.fine_status, st.active, stream,
                            tasks_dev=tables[k - 1], elapsed=st.elapsed_f, xss=st.xss_f, rp=rp)
@@ -487,6 +512,7 @@ def _run_parareal(self, M, K, t0: float, t1: float, m: int, dt_fine: float,
                                  st.defects, stream)
     self.sys.parareal_finalize(S, m, st.U, st.F, st.k_used, stream)
     self._keep = tables
+    self._last_pr_corr = st.corr
     return _pr_result(self, st, K, stream)
 
 
@@ -629,5 +655,7 @@ def raise_on_status(status: torch.Tensor, what: str):
     if len(bad):
         i = int(bad[0])
         code, step = int(st[i, 0]), int(st[i, 1])
+        if code == _lib.ST_UNSUPPORTED:
+            raise ValueError(f"{what}: task {i}: {_lib.STATUS_NAMES[code]}")
         raise SingularSystemError(f"{what}: task {i}: {_lib.STATUS_NAMES.get(code, code)} "
                                   f"at step {step}", step_index=step)

@@ -33,7 +33,11 @@ def wrap(name):
         e0.record()
         r = fn(*a, **k)
         e1.record()
-        ev.append((name, e0, e1))
+        its = None
+        if name == "propagate" and len(a) > 9 and a[9] is not None:
+            slots = torch.from_numpy(np.asarray(a[0]["slot"], dtype=np.int64)).to(a[9].device)
+            its = a[9].index_select(0, slots.clamp(min=0))     # this call's PCG iterations per task
+        ev.append((name, e0, e1, its))
         return r
     setattr(sysobj, name, w)
 
@@ -52,7 +56,7 @@ fam.check_status()
 tot = {}
 per_k = []
 k = 0
-for name, a, z in ev:
+for name, a, z, its in ev:
     ms = a.elapsed_time(z)
     tot[name] = tot.get(name, 0.0) + ms
     if name == "parareal_coarse":
@@ -60,6 +64,9 @@ for name, a, z in ev:
         per_k.append({"k": k, "coarse_ms": ms})
     elif name == "propagate" and per_k:
         per_k[-1]["fine_ms"] = per_k[-1].get("fine_ms", 0.0) + ms
+        if its is not None:
+            per_k[-1]["fine_tasks"] = int(its.numel())
+            per_k[-1]["fine_pcg_iters"] = int(its.sum())
 print(json.dumps({"config": cfg_i, "S": S, "total_ms": e0.elapsed_time(e1),
                   "phase_ms": tot, "per_k": per_k,
                   "k_used": sorted(set(b.k_used.cpu().tolist())),
