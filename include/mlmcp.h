@@ -214,7 +214,10 @@ size_t mlmcp_workspace_bytes(const mlmcp_ctx* ctx, int n_tasks, int S);
 
 /* region_params_d (optional, may be NULL): [S][R][2] region parameters of
  * the S operators (mlmcp_region_params) when the context has a region grid:
- * the streaming tile kernels then compute the operator on the fly. */
+ * the streaming tile kernels then compute the operator on the fly.
+ * Streaming batches need one dt per call (EINVAL otherwise), except on the
+ * band path (MLMCP_PATH_BAND), whose tasks carry their own dt: a level's fine
+ * and coarse solves then go into one launch, longest tasks first. */
 int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
                     int S, const double* M_d, const double* K_d,
                     const double* region_params_d, const double* profile_d, double omega, double rtol,

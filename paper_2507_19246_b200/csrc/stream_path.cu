@@ -2042,16 +2042,17 @@ __global__ void __launch_bounds__(kThreads) pspmv_kernel(PArgs a) {
     for (int q = a.row_ptr[i]; q < a.row_ptr[i + 1]; ++q) {
       const int c = a.col[q];
       const double xr = pr[c], xi = pi[c];
-      mr = fma(Ms[q], xr, mr);
-      mi = fma(Ms[q], xi, mi);
-      kr = fma(Ks[q], xr, kr);
-      ki = fma(Ks[q], xi, ki);
+      const double mq = __ldcs(Ms + q), kq = __ldcs(Ks + q);   // read once: evict first
+      mr = fma(mq, xr, mr);
+      mi = fma(mq, xi, mi);
+      kr = fma(kq, xr, kr);
+      ki = fma(kq, xi, ki);
     }
     // Zr p = c1 M p + dt K p;  Zi p = sn M p;  q = Zr p + i Zi p
     const double zr_r = fma(c1, mr, dt * kr), zr_i = fma(c1, mi, dt * ki);
     const double qr = zr_r - sn * mi, qi = zr_i + sn * mr;
-    pvec(a, t, PV_QR)[i] = qr;
-    pvec(a, t, PV_QI)[i] = qi;
+    __stcs(pvec(a, t, PV_QR) + i, qr);
+    __stcs(pvec(a, t, PV_QI) + i, qi);
     v[0] = pr[i] * qr - pi[i] * qi;
     v[1] = pr[i] * qi + pi[i] * qr;
   }
@@ -2078,18 +2079,19 @@ __global__ void __launch_bounds__(kThreads) pupdate_kernel(PArgs a) {
   const double ar = td[3], ai = td[4];
   double v[3] = {0.0, 0.0, 0.0};
   if (i < a.N) {
-    const double pr = pvec(a, t, PV_PR)[i], pi = pvec(a, t, PV_PI)[i];
-    const double qr = pvec(a, t, PV_QR)[i], qi = pvec(a, t, PV_QI)[i];
-    pvec(a, t, PV_XR)[i] += ar * pr - ai * pi;
-    pvec(a, t, PV_XI)[i] += ar * pi + ai * pr;
-    const double rr = pvec(a, t, PV_RR)[i] - (ar * qr - ai * qi);
-    const double ri = pvec(a, t, PV_RI)[i] - (ar * qi + ai * qr);
-    pvec(a, t, PV_RR)[i] = rr;
-    pvec(a, t, PV_RI)[i] = ri;
-    const double dr = pvec(a, t, PV_DR)[i], di = pvec(a, t, PV_DI)[i];
+    // every vector is read / written once per launch: streamed (evict first)
+    const double pr = __ldcs(pvec(a, t, PV_PR) + i), pi = __ldcs(pvec(a, t, PV_PI) + i);
+    const double qr = __ldcs(pvec(a, t, PV_QR) + i), qi = __ldcs(pvec(a, t, PV_QI) + i);
+    __stcs(pvec(a, t, PV_XR) + i, __ldcs(pvec(a, t, PV_XR) + i) + (ar * pr - ai * pi));
+    __stcs(pvec(a, t, PV_XI) + i, __ldcs(pvec(a, t, PV_XI) + i) + (ar * pi + ai * pr));
+    const double rr = __ldcs(pvec(a, t, PV_RR) + i) - (ar * qr - ai * qi);
+    const double ri = __ldcs(pvec(a, t, PV_RI) + i) - (ar * qi + ai * qr);
+    __stcs(pvec(a, t, PV_RR) + i, rr);
+    __stcs(pvec(a, t, PV_RI) + i, ri);
+    const double dr = __ldcs(pvec(a, t, PV_DR) + i), di = __ldcs(pvec(a, t, PV_DI) + i);
     const double zr = dr * rr - di * ri, zi = dr * ri + di * rr;
-    pvec(a, t, PV_ZR)[i] = zr;
-    pvec(a, t, PV_ZI)[i] = zi;
+    __stcs(pvec(a, t, PV_ZR) + i, zr);
+    __stcs(pvec(a, t, PV_ZI) + i, zi);
     v[0] = rr * zr - ri * zi;
     v[1] = rr * zi + ri * zr;
     v[2] = rr * rr + ri * ri;
@@ -2117,9 +2119,9 @@ __global__ void __launch_bounds__(kThreads) ppupd_kernel(PArgs a) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= a.N) return;
   const double br = a.td[t * 8 + 5], bi = a.td[t * 8 + 6];
-  const double pr = pvec(a, t, PV_PR)[i], pi = pvec(a, t, PV_PI)[i];
-  pvec(a, t, PV_PR)[i] = pvec(a, t, PV_ZR)[i] + (br * pr - bi * pi);
-  pvec(a, t, PV_PI)[i] = pvec(a, t, PV_ZI)[i] + (br * pi + bi * pr);
+  const double pr = __ldcs(pvec(a, t, PV_PR) + i), pi = __ldcs(pvec(a, t, PV_PI) + i);
+  __stcs(pvec(a, t, PV_PR) + i, __ldcs(pvec(a, t, PV_ZR) + i) + (br * pr - bi * pi));
+  __stcs(pvec(a, t, PV_PI) + i, __ldcs(pvec(a, t, PV_ZI) + i) + (br * pi + bi * pr));
 }
 
 __global__ void pfinal_kernel(PArgs a) {
@@ -2148,17 +2150,16 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
                      size_t ws_bytes, cudaStream_t stream) {
   if (n_tasks == 0) return MLMCP_OK;
   const Layout L = make_layout(ctx, n_tasks, S);
-  // the streaming path needs one dt per call (one ELL operator per sample)
+  // the streaming kernels need one dt per call (one operator per sample); the
+  // band path forms each task's class table from its own dt and takes any mix
   std::vector<mlmcp_task> h(n_tasks);
   MLMCP_CUDA_CHECK(cudaMemcpyAsync(h.data(), tasks, sizeof(mlmcp_task) * n_tasks,
                                    cudaMemcpyDeviceToHost, stream));
   MLMCP_CUDA_CHECK(cudaStreamSynchronize(stream));
   int steps_max = 0;
+  bool mixed_dt = false;
   for (const auto& t : h) {
-    if (t.dt != h[0].dt) {
-      set_error("streaming path: all tasks of one call must share dt");
-      return MLMCP_EINVAL;
-    }
+    mixed_dt |= t.dt != h[0].dt;
     if (t.sample < 0 || t.sample >= S) {
       set_error("task sample index out of range");
       return MLMCP_EINVAL;
@@ -2177,6 +2178,13 @@ int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, cons
       set_error("correction tasks (MLMCP_TASK_CORRECTION) carry no QoI");
       return MLMCP_EINVAL;
     }
+  }
+  const bool band_call = !any_corr && !(cluster_usable(ctx) && !(any_ss && xss != nullptr)) &&
+                         band_usable(ctx) && rpar != nullptr && region_on() && ws != nullptr &&
+                         ws_bytes >= L.total && band_ring_bytes(n_tasks) <= ws_bytes;
+  if (mixed_dt && !band_call) {
+    set_error("streaming path: all tasks of one call must share dt");
+    return MLMCP_EINVAL;
   }
   if (any_corr) {   // correction solves run on the tile kernels only
     if (!tile_usable(ctx)) {

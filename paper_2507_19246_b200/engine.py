@@ -87,7 +87,9 @@ class DeviceSystem:
             check(self.lib.mlmcp_ctx_set_assembly(self.ctx, int(n_elem), len(celem), np_ptr(cptr),
                                                   np_ptr(celem), np_ptr(cmw), np_ptr(ckw)),
                   "mlmcp_ctx_set_assembly")
-        self._ws = None
+        self._ws_by_stream = {}     # streaming workspace of each stream that launches
+        self.band_low_priority = False   # set by families that keep two calls in flight
+        self._band_streams = {}
         self._fused_ws = {}
         self.region_grid = None
 
@@ -132,14 +134,26 @@ class DeviceSystem:
             return False
         return self.n_rows <= self.small_max_rows
 
-    def workspace(self, n_tasks: int, S: int) -> torch.Tensor | None:
+    def workspace(self, n_tasks: int, S: int, stream=None) -> torch.Tensor | None:
+        """The streaming workspace of ``stream`` (default: the current stream).
+        One buffer per launching stream, grown on demand and kept between
+        calls, so calls in flight on different streams never share one."""
         nbytes = int(self.lib.mlmcp_workspace_bytes(self.ctx, int(n_tasks), int(S)))
         if nbytes == 0:
             return None
-        if self._ws is None or self._ws.numel() < nbytes:
-            self._ws = None
-            self._ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
-        return self._ws
+        s = stream if stream is not None else torch.cuda.current_stream()
+        key = s.cuda_stream
+        ws = self._ws_by_stream.get(key)
+        if ws is None or ws.numel() < nbytes:
+            self._ws_by_stream.pop(key, None)
+            ws = None
+            with torch.cuda.stream(s):      # owned by the stream's allocator pool
+                ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
+            self._ws_by_stream[key] = ws
+        return ws
+
+    def workspace_bytes_held(self) -> int:
+        return sum(w.numel() for w in self._ws_by_stream.values())
 
     # ------------------------------------------------------------ K1
     def assemble(self, S: int, sigma: torch.Tensor, sigma_stride: int, sigma_index,
@@ -183,20 +197,41 @@ class DeviceSystem:
             return None
         S = M.shape[0]
         td = tasks_dev if tasks_dev is not None else tasks_to_device(tasks, self.device)
-        ws = self.workspace(n, S)
+        ws = self.workspace(n, S, stream)
+        launch_on = stream
+        cur = None
+        if self.band_low_priority and self.propagate_path(
+                n, S, xss is not None, rp is not None) == _lib.PATH_BAND:
+            # calls in flight on two (high-priority) streams: the band launch
+            # goes to a low-priority stream paired with the caller's, so that
+            # the OTHER call's preparation kernels are dispatched to the SMs the
+            # band clusters leave idle ahead of this launch's pending clusters
+            cur = stream if stream is not None else torch.cuda.current_stream()
+            launch_on = self._band_stream(cur)
+            launch_on.wait_stream(cur)
         check(self.lib.mlmcp_propagate(self.ctx, n, ptr(td), S, ptr(M), ptr(K), ptr(rp), ptr(profile),
                                        float(omega), float(rtol), int(max_it), ptr(xss),
                                        ptr(xbuf), ptr(qoi),
                                        ptr(iters), ptr(status), ptr(active), ptr(elapsed), ptr(ws),
-                                       0 if ws is None else ws.numel(), stream_handle(stream)),
+                                       0 if ws is None else ws.numel(), stream_handle(launch_on)),
               "mlmcp_propagate")
+        if cur is not None:
+            cur.wait_stream(launch_on)
         return td
+
+    def _band_stream(self, cur):
+        st = self._band_streams.get(cur.cuda_stream)
+        if st is None:
+            lo, _ = torch.cuda.Stream.priority_range()
+            st = torch.cuda.Stream(device=self.device, priority=lo)
+            self._band_streams[cur.cuda_stream] = st
+        return st
 
     # ------------------------------------------------------------ K5
     def parareal_coarse(self, S, k, m, M, K, profile, omega, dt_c, t0, slice_k0, slice_steps,
                         rtol, max_it, U, F, C, iters, status, active, stream=None, elapsed=None,
                         xss=None, rp=None):
-        ws = self.workspace(S, S)
+        ws = self.workspace(S, S, stream)
         check(self.lib.mlmcp_parareal_coarse(
             self.ctx, S, k, m, ptr(M), ptr(K), ptr(rp), ptr(profile), float(omega), float(dt_c), float(t0),
             ptr(slice_k0), ptr(slice_steps), float(rtol), int(max_it), ptr(U), ptr(F), ptr(C),

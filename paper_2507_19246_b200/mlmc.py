@@ -266,24 +266,105 @@ def _family_caps(family, n_levels: int, parareal_cfg):
     return None if any(c is None for c in caps) else [max(1, int(c)) for c in caps]
 
 
+def plan_calls(ranges, caps, pipelined: bool = False):
+    """The run_levels calls of one estimate as (level, c0, c1) sample ranges.
+    One call at a time: level by level in chunks of <= caps[l].  Pipelined (two
+    calls in flight, family.call_streams): each call may hold 0.8 of its cap
+    (the caps budget half of the free HBM per call), a level's chunks are
+    balanced, and the finest level goes first — its few long tasks start
+    early and the later calls' short tasks fill the cluster slots they leave.
+    Per-sample results do not depend on the plan."""
+    calls = []
+    for lvl, (a, b) in enumerate(ranges):
+        if b <= a:
+            continue
+        cap = max(1, int(caps[lvl] * 0.8)) if pipelined else caps[lvl]
+        if pipelined:
+            n = -(-(b - a) // cap)
+            size = -(-(b - a) // n)
+        else:
+            size = cap
+        calls += [(lvl, c0, min(b, c0 + size)) for c0 in range(a, b, size)]
+    if pipelined:
+        calls.sort(key=lambda c: -c[0])
+    return calls
+
+
+def run_level_calls(family, calls, launch, parareal_cfg=None, on_token=None):
+    """Issue ``launch(lvl, c0, c1)`` for every planned call.  With
+    family.call_streams() the calls alternate between two streams so that one
+    call's host-synchronised preparation (assembly, periodic steady states)
+    overlaps the previous call's asynchronous propagate launch; a stream's
+    previous call is completed (synchronised, statuses checked or handed to
+    ``on_token``) before the stream is reused, so at most two calls hold
+    memory.  ``launch`` runs under the call's stream and must leave its
+    results in buffers the caller reduces after this function returns (the
+    current stream waits for both streams at the end)."""
+    streams = None
+    if len(calls) > 1 and hasattr(family, "call_streams"):
+        streams = family.call_streams(parareal_cfg)
+
+    def done(tok):
+        if tok is None:
+            return
+        if on_token is not None:
+            on_token(tok)
+        else:
+            family.check_status(tok)
+
+    if not streams:
+        for c in calls:
+            launch(*c)
+            if on_token is not None and hasattr(family, "take_last"):
+                on_token(family.take_last())
+            elif hasattr(family, "check_status"):
+                family.check_status()
+        return
+    import torch
+    main = torch.cuda.current_stream()
+    inflight = [None] * len(streams)
+    try:
+        for i, c in enumerate(calls):
+            k = i % len(streams)
+            s = streams[k]
+            if inflight[k] is not None:
+                s.synchronize()
+                tok, inflight[k] = inflight[k], None
+                done(tok)
+                del tok
+            s.wait_stream(main)
+            with torch.cuda.stream(s):
+                launch(*c)
+                inflight[k] = family.take_last()
+        for k, s in enumerate(streams):
+            if inflight[k] is not None:
+                s.synchronize()
+                tok, inflight[k] = inflight[k], None
+                done(tok)
+                del tok
+    finally:
+        for s in streams:
+            main.wait_stream(s)
+
+
 def _run_chunked(family, ranges, counts, caps, seed: int, parareal_cfg, dev):
     """Evaluate the rank's sample ranges in run_levels calls of <= caps[l]
-    samples (level by level, keys unchanged) into per-level slot buffers.
-    The caps are computed once by the caller (no per-call re-sizing)."""
+    samples (keys unchanged) into per-level slot buffers.  The caps are
+    computed once by the caller (no per-call re-sizing); the calls follow
+    plan_calls / run_level_calls (two in flight where the family allows)."""
     import torch
     slots = [torch.zeros((n, 4), dtype=torch.float64, device=dev) for n in counts]
-    last = None
-    for lvl, (a, b) in enumerate(ranges):
-        cap = caps[lvl]
-        for c0 in range(a, b, cap):
-            c1 = min(b, c0 + cap)
-            d = draw_level(family.uncertain, seed, lvl, range(c0 + 1, c1 + 1))
-            out = family.run_levels([d], parareal_cfg, levels=[lvl], _no_chunk=True)
-            if hasattr(family, "check_status"):
-                family.check_status()
-            _fill_slots(slots[lvl], out[0], c0, c1)
-            last = out
-    return slots, last
+    pipelined = bool(hasattr(family, "call_streams") and family.call_streams(parareal_cfg))
+    last = [None]
+
+    def launch(lvl, c0, c1):
+        d = draw_level(family.uncertain, seed, lvl, range(c0 + 1, c1 + 1))
+        out = family.run_levels([d], parareal_cfg, levels=[lvl], _no_chunk=True)
+        _fill_slots(slots[lvl], out[0], c0, c1)
+        last[0] = out
+
+    run_level_calls(family, plan_calls(ranges, caps, pipelined), launch, parareal_cfg)
+    return slots, last[0]
 
 
 def _level_costs(hierarchy, counts, parareal_cfg, ks, wall: float):

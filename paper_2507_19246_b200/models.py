@@ -522,12 +522,14 @@ class _BatchedFamily:
         self._graph_launches = n_launch
         return out
 
-    def status_flag(self):
-        """0-d device tensor: any failed task in the last run (no host sync)."""
+    def status_flag(self, token=None):
+        """0-d device tensor: any failed task in the last run, or in the run
+        ``token`` (take_last) stands for (no host sync)."""
         import torch
-        if getattr(self, "_last", None) is None:
+        last = token if token is not None else getattr(self, "_last", None)
+        if last is None:
             return None
-        res, pr, _, _ = self._last
+        res, pr, _, _ = last
         sts = [r.status for r in res]
         if pr is not None:
             sts += [pr.status, pr.fine_status]
@@ -536,18 +538,32 @@ class _BatchedFamily:
             return None
         return torch.stack([(st[:, 0] != 0).any() for st in sts]).any()
 
-    def check_status(self):
+    def check_status(self, token=None):
         """Raise SingularSystemError / PropagatorError for failed samples of the
-        last run."""
+        last run (or of the run ``token`` stands for)."""
         from .parareal import raise_parareal_status
         from .solver import raise_on_status
-        if getattr(self, "_last", None) is None:
+        last = token if token is not None else getattr(self, "_last", None)
+        if last is None:
             return
-        res, pr, _, _ = self._last
+        res, pr, _, _ = last
         for r in res:
             raise_on_status(r.status, "implicit Euler solve")
         if pr is not None:
             raise_parareal_status(pr.status.cpu().numpy(), pr.fine_status.cpu().numpy())
+
+    def take_last(self):
+        """Detach the last run's statuses and operator buffers as a token for
+        status_flag / check_status, so that the next run_levels call can be
+        issued before this one has been checked (mlmc.run_level_calls)."""
+        tok = getattr(self, "_last", None)
+        self._last = None
+        return tok
+
+    def call_streams(self, parareal_cfg=None):
+        """CUDA streams on which run_levels calls may be in flight together
+        (mlmc.run_level_calls), or None when calls run one after the other."""
+        return None
 
     def coupled_batch(self, params, level, parareal_cfg=None) -> CoupledBatch:
         lvl = self._level_index(level)
@@ -682,9 +698,37 @@ class EddyCurrentFamily(_BatchedFamily):
         # memory torch's caching allocator holds but no tensor uses, and the
         # engine workspace (replaced, not added, by the next call) are free too
         reclaim = torch.cuda.memory_reserved(sol.device) - torch.cuda.memory_allocated(sol.device)
-        cur_ws = sol.sys._ws.numel() if sol.sys._ws is not None else 0
+        cur_ws = sol.sys.workspace_bytes_held()
         avail = free + max(0, reclaim) + cur_ws
         return max(1, int(0.5 * avail // max(per, 1)))
+
+    def call_streams(self, parareal_cfg=None):
+        """Two streams for the band path (region-linear grids up to 256^2
+        without Parareal: config 2).  A band launch is one asynchronous kernel
+        that holds 112 of the 148 SMs (seven 16-CTA clusters, one per GPC that
+        has 16 SMs), so the next call's assembly and periodic steady-state
+        solves (grid-wide streaming kernels, host-synchronised on their own
+        stream) run on the idle SMs meanwhile, and its band clusters take over
+        cluster slots as the previous launch's last tasks drain.
+        MLMCP_PIPELINE=0 keeps one call at a time."""
+        import os
+
+        import torch
+
+        from . import _lib
+        sol = self.solver
+        if (os.environ.get("MLMCP_PIPELINE", "1") == "0" or parareal_cfg is not None
+                or sol.sys.sm_resident or not getattr(sol, "region_mode", False)):
+            return None
+        if sol.sys.propagate_path(16, 16, sol.use_predictor(), True) != _lib.PATH_BAND:
+            return None
+        st = getattr(self, "_call_streams", None)
+        if st is None:
+            _, hi = torch.cuda.Stream.priority_range()
+            st = [torch.cuda.Stream(device=sol.device, priority=hi) for _ in range(2)]
+            self._call_streams = st
+            sol.sys.band_low_priority = True
+        return st
 
     def _n_params(self) -> int:
         return fe.n_params(self.layout)

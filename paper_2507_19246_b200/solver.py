@@ -352,6 +352,15 @@ def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool
                            tasks_dev=st.td, elapsed=st.elapsed, xss=st.xss)
         if self.events is not None:
             self.events[1].record(cur)
+    elif (rp is not None and self.sys.propagate_path(st.T, M.shape[0], st.xss is not None, True)
+          == _lib.PATH_BAND):
+        # band path: every task carries its own dt, so a level's fine and coarse
+        # solves share ONE launch (longest tasks first: the short ones fill the
+        # cluster slots the long ones leave at the end of the launch)
+        order = np.argsort(-st.tasks["n_steps"], kind="stable")
+        self.sys.propagate(st.tasks[order], M, K, self.profile, self.omega, self.step_rtol(),
+                           self.max_it, st.xbuf, st.qoi, st.iters, st.status, None, stream,
+                           elapsed=st.elapsed, xss=st.xss, rp=rp)
     else:
         for dt in sorted(set(st.tasks["dt"].tolist())):
             sel = st.tasks[st.tasks["dt"] == dt]

@@ -396,3 +396,31 @@ def test_streaming_coarse_failure_maps_to_propagator_error(cuda, impl, monkeypat
     with pytest.raises(PropagatorError) as ei:
         fam.check_status()
     assert (ei.value.interval, ei.value.iteration) == (1, 1)
+
+
+def test_pipelined_calls_bitwise(cuda, monkeypatch):
+    """Config 2 (256^2, band path) with its calls two in flight on two streams
+    (mlmc.run_level_calls: finest level first, balanced chunks) against one
+    call at a time (MLMCP_PIPELINE=0): level sums and the estimate bitwise
+    equal, and the plan covers every sample exactly once."""
+    from paper_2507_19246_b200.mlmc import FixedSamples, mlmc_estimate, plan_calls
+    from paper_2507_19246_b200.models import EddyCurrentFamily
+    fam = large_family(2)
+    monkeypatch.setattr(EddyCurrentFamily, "max_samples_per_call",
+                        lambda self, parareal_cfg=None, level=None: 3)
+    counts = (7, 4, 2, 1)
+    assert fam.call_streams(None) is not None and len(fam.call_streams(None)) == 2
+    calls = plan_calls([(0, n) for n in counts], [3] * 4, pipelined=True)
+    assert [c[0] for c in calls] == sorted((c[0] for c in calls), reverse=True)
+    for lvl, n in enumerate(counts):
+        cover = sorted((c0, c1) for l, c0, c1 in calls if l == lvl)
+        assert cover[0][0] == 0 and cover[-1][1] == n
+        assert all(a[1] == b[0] for a, b in zip(cover, cover[1:]))
+        assert all(c1 - c0 <= 2 for c0, c1 in cover)      # 0.8 of the cap
+    piped = mlmc_estimate(fam, policy=FixedSamples(counts), seed=0)
+    monkeypatch.setenv("MLMCP_PIPELINE", "0")
+    assert fam.call_streams(None) is None
+    serial = mlmc_estimate(fam, policy=FixedSamples(counts), seed=0)
+    assert piped.expectation == serial.expectation
+    for a, b in zip(piped.per_level, serial.per_level):
+        assert (a.n, a.mean_y, a.var_y) == (b.n, b.mean_y, b.var_y)
