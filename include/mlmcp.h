@@ -51,7 +51,7 @@
 extern "C" {
 #endif
 
-#define MLMCP_ABI_VERSION 10
+#define MLMCP_ABI_VERSION 11
 
 /* return codes */
 #define MLMCP_OK 0
@@ -238,11 +238,16 @@ int mlmcp_propagate(mlmcp_ctx* ctx, int n_tasks, const mlmcp_task* tasks_d,
  * COCG iterations (optional).  SM-resident path: one CTA per item, no
  * workspace; streaming path (meshes > 1024 rows): grid-wide COCG kernels in
  * ws_d (mlmcp_periodic_workspace_bytes), host-synchronous like
- * mlmcp_propagate.  EINVAL on the direct path. */
+ * mlmcp_propagate.  region_params_d (optional, may be NULL): the S operators'
+ * region parameters (mlmcp_region_params) when the context has a region
+ * grid; the streaming kernels then apply the operator from per-class stencil
+ * tables instead of streaming the CSR values of M and K (176 instead of 336
+ * HBM bytes per point and COCG iteration).  EINVAL on the direct path. */
 size_t mlmcp_periodic_workspace_bytes(const mlmcp_ctx* ctx, int n);
 int mlmcp_periodic_state(mlmcp_ctx* ctx, int n, const int32_t* sample_d,
                          const double* dt_d, int S, const double* M_d,
-                         const double* K_d, const double* profile_d,
+                         const double* K_d, const double* region_params_d,
+                         const double* profile_d,
                          double omega, double rtol, int max_it, double* X_d,
                          int32_t* iters_d, void* ws_d, size_t ws_bytes,
                          void* stream);

@@ -41,7 +41,7 @@ QOI_NONE, QOI_FINAL_ENERGY, QOI_SUM_ENERGY, QOI_ELECTRICAL, QOI_JOULE = 0, 1, 2,
 TASK_NO_EXTRAPOLATION = 1
 TASK_CORRECTION = 2
 PATH_DIRECT, PATH_SMALL, PATH_CLUSTER, PATH_BAND, PATH_COOP, PATH_TILE, PATH_ELL = range(7)
-ABI_VERSION = 10
+ABI_VERSION = 11
 DIRECT_MAX_ROWS = 4
 
 # mlmcp_task (96 bytes, natural alignment)
@@ -119,7 +119,7 @@ _SIGS = {
     "mlmcp_ctx_set_region_grid": (ctypes.c_int, [P, ctypes.c_int, P, P, P]),
     "mlmcp_region_params": (ctypes.c_int, [ctypes.c_int, ctypes.c_int, P, P, P, P, P]),
     "mlmcp_periodic_workspace_bytes": (SZ, [P, ctypes.c_int]),
-    "mlmcp_periodic_state": (ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_int, P, P, P, F64,
+    "mlmcp_periodic_state": (ctypes.c_int, [P, ctypes.c_int, P, P, ctypes.c_int, P, P, P, P, F64,
                                             F64, ctypes.c_int, P, P, P, SZ, P]),
     "mlmcp_parareal_coarse": (ctypes.c_int, [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P,
                                              P, P, F64, F64, F64, P, P, F64, ctypes.c_int, P, P,

@@ -629,7 +629,8 @@ size_t mlmcp_periodic_workspace_bytes(const mlmcp_ctx* c, int n) {
 }
 
 int mlmcp_periodic_state(mlmcp_ctx* c, int n, const int32_t* sample, const double* dt, int S,
-                         const double* M, const double* K, const double* profile, double omega,
+                         const double* M, const double* K, const double* rpar,
+                         const double* profile, double omega,
                          double rtol, int max_it, double* X, int32_t* iters, void* ws,
                          size_t ws_bytes, void* stream) {
   if (c == nullptr) return einval("null context");
@@ -642,8 +643,8 @@ int mlmcp_periodic_state(mlmcp_ctx* c, int n, const int32_t* sample, const doubl
   if (use_small(c))
     return small_periodic(c, n, sample, dt, M, K, profile, omega, rtol, max_it, X, iters,
                           (cudaStream_t)stream);
-  return stream_periodic(c, n, sample, dt, M, K, profile, omega, rtol, max_it, X, iters, ws,
-                         ws_bytes, (cudaStream_t)stream);
+  return stream_periodic(c, n, sample, dt, M, K, rpar, profile, omega, rtol, max_it, X, iters,
+                         ws, ws_bytes, (cudaStream_t)stream);
 }
 
 size_t mlmcp_fused_workspace_bytes(int S, int m, int k_max) {

@@ -236,9 +236,9 @@ void draw_uniform_cpu(uint64_t seed, uint64_t level, int64_t k_first, int n, int
 size_t stream_workspace_bytes(const Ctx* ctx, int n_tasks, int S);
 size_t stream_periodic_workspace_bytes(const Ctx* ctx, int n);
 int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
-                    const double* K, const double* profile, double omega, double rtol,
-                    int max_it, double* X, int32_t* iters, void* ws, size_t ws_bytes,
-                    cudaStream_t stream);
+                    const double* K, const double* rpar, const double* profile, double omega,
+                    double rtol, int max_it, double* X, int32_t* iters, void* ws,
+                    size_t ws_bytes, cudaStream_t stream);
 
 int stream_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, int S, const double* M,
                      const double* K, const double* rpar, const double* profile, double omega, double rtol,

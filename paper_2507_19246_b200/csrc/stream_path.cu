@@ -1932,6 +1932,15 @@ struct PArgs {
   int32_t* arrive;   // [T]
   int32_t* counters; // [0] live, [1] done
   double* X;         // [T][2][N] output
+  // region-linear operator (structured grid with a region grid + per-sample
+  // region parameters): Z = (1 - e^{-i w dt}) M + dt K from the task's stencil
+  // of each point class instead of the streamed CSR values of M and K
+  const uint8_t* rcls;
+  const uint32_t* rckey;
+  int rC, R, wd;
+  const double* rpar;
+  double rmw[12], rkw[12];
+  double* ctab;      // [T][rC][16]: Re Z (7), Re D^-1, Im Z (7), Im D^-1
 };
 
 enum : int { PV_XR = 0, PV_XI, PV_RR, PV_RI, PV_PR, PV_PI, PV_ZR, PV_ZI, PV_QR, PV_QI, PV_DR,
@@ -2122,6 +2131,210 @@ __global__ void __launch_bounds__(kThreads) ppupd_kernel(PArgs a) {
   const double pr = __ldcs(pvec(a, t, PV_PR) + i), pi = __ldcs(pvec(a, t, PV_PI) + i);
   __stcs(pvec(a, t, PV_PR) + i, __ldcs(pvec(a, t, PV_ZR) + i) + (br * pr - bi * pi));
   __stcs(pvec(a, t, PV_PI) + i, __ldcs(pvec(a, t, PV_ZI) + i) + (br * pi + bi * pr));
+}
+
+// ---- region-linear variant (config 2: 256^2 blocks8 grids) -----------------
+// The same COCG iteration with Z applied from the task's class table: a PCG-
+// style launch triple moves read p, write q | read p q x r, write x r | read
+// r p, write p = 176 B per point and iteration instead of 336 (no streamed
+// M / K values, no stored D^-1 and z).  These launches run next to another
+// call's band kernel on the SMs its clusters leave idle (mlmc.run_level_calls),
+// so their HBM / L2 traffic is what they cost the estimate.
+constexpr int kPTW = 16;   // doubles per class in PArgs::ctab
+
+__global__ void ptab_kernel(PArgs a) {
+  __shared__ double2 sp[16];
+  const int t = blockIdx.x;
+  const int s = a.sample[t];
+  if (threadIdx.x < a.R)
+    sp[threadIdx.x] = reinterpret_cast<const double2*>(a.rpar)[(int64_t)s * a.R + threadIdx.x];
+  __syncthreads();
+  double c1, sn, dt;
+  item_cs(a, t, c1, sn, dt);
+  for (int c = threadIdx.x; c < a.rC; c += blockDim.x) {
+    const uint32_t key = __ldg(a.rckey + c);
+    const uint32_t code = key & 0x00ffffffu, mask = key >> 24;
+    double2 p[6];
+#pragma unroll
+    for (int e = 0; e < 6; ++e) p[e] = sp[(code >> (4 * e)) & 15u];
+    double M7[7], K7[7];
+    double m = 0.0, k = 0.0;
+#pragma unroll
+    for (int e = 0; e < 6; ++e) {
+      m = __dadd_rn(m, __dmul_rn(p[e].x, a.rmw[e]));
+      k = __dadd_rn(k, __dmul_rn(p[e].y, a.rkw[e]));
+    }
+    M7[3] = m;
+    K7[3] = k;
+    const int slot[6] = {0, 1, 2, 4, 5, 6};
+    const int e0[6] = {0, 0, 1, 2, 3, 4}, e1[6] = {1, 2, 3, 4, 5, 5};
+    const int cw[6] = {10, 8, 6, 6, 8, 10};
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+      const bool ok = (mask >> j) & 1u;
+      M7[slot[j]] = ok ? __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[j]].x, a.rmw[cw[j]])),
+                                   __dmul_rn(p[e1[j]].x, a.rmw[cw[j] + 1]))
+                       : 0.0;
+      K7[slot[j]] = ok ? __dadd_rn(__dadd_rn(0.0, __dmul_rn(p[e0[j]].y, a.rkw[cw[j]])),
+                                   __dmul_rn(p[e1[j]].y, a.rkw[cw[j] + 1]))
+                       : 0.0;
+    }
+    double* T = a.ctab + ((int64_t)t * a.rC + c) * kPTW;
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+      T[d] = fma(c1, M7[d], dt * K7[d]);
+      T[8 + d] = sn * M7[d];
+    }
+    const double dr = T[3], di = T[11], den = dr * dr + di * di;
+    T[7] = den > 0.0 ? dr / den : 0.0;
+    T[15] = den > 0.0 ? -di / den : 0.0;
+  }
+}
+
+__device__ __forceinline__ void ptab_load(const PArgs& a, int t, double* tab) {
+  const double* g = a.ctab + (int64_t)t * a.rC * kPTW;
+  for (int i = threadIdx.x; i < a.rC * kPTW; i += blockDim.x) tab[i] = __ldg(g + i);
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(kThreads) pinit_rg_kernel(PArgs a) {
+  extern __shared__ __align__(16) double ptab[];
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  ptab_load(a, t, ptab);
+  const double dt = a.dt[t];
+  double v[3] = {0.0, 0.0, 0.0};
+  if (i < a.N) {
+    const double* T = ptab + (int)__ldg(a.rcls + i) * kPTW;
+    const double ir = T[7], ii = T[15];
+    const double b = dt * a.profile[i];
+    pvec(a, t, PV_XR)[i] = 0.0;
+    pvec(a, t, PV_XI)[i] = 0.0;
+    pvec(a, t, PV_RR)[i] = b;
+    pvec(a, t, PV_RI)[i] = 0.0;
+    pvec(a, t, PV_PR)[i] = ir * b;
+    pvec(a, t, PV_PI)[i] = ii * b;
+    v[0] = b * ir * b;
+    v[1] = b * ii * b;
+    v[2] = b * b;
+  }
+  if (ptask_reduce<3>(v, a, t, red) && threadIdx.x == 0) {
+    double* td = a.td + t * 8;
+    td[0] = v[0];
+    td[1] = v[1];
+    td[2] = v[2];
+    a.ti[t * 4 + 0] = v[2] > 0.0 ? 1 : 0;
+    a.ti[t * 4 + 1] = 0;
+    atomicAdd(a.counters + 0, 1);
+    if (!(v[2] > 0.0)) atomicAdd(a.counters + 1, 1);
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) pspmv_rg_kernel(PArgs a) {
+  extern __shared__ __align__(16) double ptab[];
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  if (!block_uniform(a.ti[t * 4] == 1)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  ptab_load(a, t, ptab);
+  double v[2] = {0.0, 0.0};
+  if (i < a.N) {
+    const double* T = ptab + (int)__ldg(a.rcls + i) * kPTW;
+    const double* pr = pvec(a, t, PV_PR);
+    const double* pi = pvec(a, t, PV_PI);
+    const int off[7] = {-a.wd - 1, -a.wd, -1, 0, 1, a.wd, a.wd + 1};
+    double qr = 0.0, qi = 0.0, pcr = 0.0, pci = 0.0;
+#pragma unroll
+    for (int d = 0; d < 7; ++d) {
+      const double zr = T[d], zi = T[8 + d];
+      if (zr != 0.0 || zi != 0.0) {      // a zero coefficient: no such neighbour
+        const double xr = pr[i + off[d]], xi = pi[i + off[d]];
+        qr = fma(zr, xr, fma(-zi, xi, qr));
+        qi = fma(zr, xi, fma(zi, xr, qi));
+        if (d == 3) {
+          pcr = xr;
+          pci = xi;
+        }
+      }
+    }
+    __stcs(pvec(a, t, PV_QR) + i, qr);
+    __stcs(pvec(a, t, PV_QI) + i, qi);
+    v[0] = pcr * qr - pci * qi;
+    v[1] = pcr * qi + pci * qr;
+  }
+  if (ptask_reduce<2>(v, a, t, red) && threadIdx.x == 0) {
+    double* td = a.td + t * 8;
+    const double den = v[0] * v[0] + v[1] * v[1];
+    if (!(den > 0.0)) {
+      a.ti[t * 4] = 2;
+      atomicAdd(a.counters + 1, 1);
+    } else {
+      td[3] = (td[0] * v[0] + td[1] * v[1]) / den;
+      td[4] = (td[1] * v[0] - td[0] * v[1]) / den;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) pupdate_rg_kernel(PArgs a) {
+  extern __shared__ __align__(16) double ptab[];
+  __shared__ double red[2 * 4 * 32];
+  const int t = blockIdx.y;
+  if (!block_uniform(a.ti[t * 4] == 1)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  ptab_load(a, t, ptab);
+  const double* td = a.td + t * 8;
+  const double ar = td[3], ai = td[4];
+  double v[3] = {0.0, 0.0, 0.0};
+  if (i < a.N) {
+    const double* T = ptab + (int)__ldg(a.rcls + i) * kPTW;
+    const double pr = pvec(a, t, PV_PR)[i], pi = pvec(a, t, PV_PI)[i];
+    const double qr = __ldcs(pvec(a, t, PV_QR) + i), qi = __ldcs(pvec(a, t, PV_QI) + i);
+    __stcs(pvec(a, t, PV_XR) + i, __ldcs(pvec(a, t, PV_XR) + i) + (ar * pr - ai * pi));
+    __stcs(pvec(a, t, PV_XI) + i, __ldcs(pvec(a, t, PV_XI) + i) + (ar * pi + ai * pr));
+    const double rr = __ldcs(pvec(a, t, PV_RR) + i) - (ar * qr - ai * qi);
+    const double ri = __ldcs(pvec(a, t, PV_RI) + i) - (ar * qi + ai * qr);
+    pvec(a, t, PV_RR)[i] = rr;
+    pvec(a, t, PV_RI)[i] = ri;
+    const double dr = T[7], di = T[15];
+    const double zr = dr * rr - di * ri, zi = dr * ri + di * rr;
+    v[0] = rr * zr - ri * zi;
+    v[1] = rr * zi + ri * zr;
+    v[2] = rr * rr + ri * ri;
+  }
+  if (ptask_reduce<3>(v, a, t, red) && threadIdx.x == 0) {
+    double* tdw = a.td + t * 8;
+    int32_t* ti = a.ti + t * 4;
+    ti[1] += 1;
+    const double rden = tdw[0] * tdw[0] + tdw[1] * tdw[1];
+    if (v[2] <= a.rtol2 * tdw[2] || !isfinite(v[2]) || ti[1] >= a.max_it || !(rden > 0.0)) {
+      ti[0] = 2;
+      atomicAdd(a.counters + 1, 1);
+    } else {
+      tdw[5] = (v[0] * tdw[0] + v[1] * tdw[1]) / rden;
+      tdw[6] = (v[1] * tdw[0] - v[0] * tdw[1]) / rden;
+      tdw[0] = v[0];
+      tdw[1] = v[1];
+    }
+  }
+}
+
+// p = D^-1 r + beta p (z recomputed from r, not stored)
+__global__ void __launch_bounds__(kThreads) ppupd_rg_kernel(PArgs a) {
+  extern __shared__ __align__(16) double ptab[];
+  const int t = blockIdx.y;
+  if (!block_uniform(a.ti[t * 4] == 1)) return;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  ptab_load(a, t, ptab);
+  if (i >= a.N) return;
+  const double* T = ptab + (int)__ldg(a.rcls + i) * kPTW;
+  const double br = a.td[t * 8 + 5], bi = a.td[t * 8 + 6];
+  const double rr = pvec(a, t, PV_RR)[i], ri = pvec(a, t, PV_RI)[i];
+  const double dr = T[7], di = T[15];
+  const double zr = dr * rr - di * ri, zi = dr * ri + di * rr;
+  const double pr = pvec(a, t, PV_PR)[i], pi = pvec(a, t, PV_PI)[i];
+  pvec(a, t, PV_PR)[i] = zr + (br * pr - bi * pi);
+  pvec(a, t, PV_PI)[i] = zi + (br * pi + bi * pr);
 }
 
 __global__ void pfinal_kernel(PArgs a) {
@@ -2359,13 +2572,14 @@ int stream_parareal_coarse(Ctx* ctx, int S, int k, int m, const double* M, const
 size_t stream_periodic_workspace_bytes(const Ctx* ctx, int n) {
   const size_t N = ctx->n, T = n, nblk = (N + kThreads - 1) / kThreads;
   return align_up(T * kPV * N * 8) + align_up(T * nblk * 4 * 8) + align_up(T * 8 * 8) +
-         align_up(T * 4 * 4) + align_up(T * 4) + 64;
+         align_up(T * 4 * 4) + align_up(T * 4) + 64 +
+         align_up(T * (size_t)std::max(ctx->rC, 0) * kPTW * 8);
 }
 
 int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, const double* M,
-                    const double* K, const double* profile, double omega, double rtol,
-                    int max_it, double* X, int32_t* iters, void* ws, size_t ws_bytes,
-                    cudaStream_t stream) {
+                    const double* K, const double* rpar, const double* profile, double omega,
+                    double rtol, int max_it, double* X, int32_t* iters, void* ws,
+                    size_t ws_bytes, cudaStream_t stream) {
   if (n == 0) return MLMCP_OK;
   const size_t need = stream_periodic_workspace_bytes(ctx, n);
   if (ws == nullptr || ws_bytes < need) {
@@ -2401,16 +2615,53 @@ int stream_periodic(Ctx* ctx, int n, const int32_t* sample, const double* dt, co
   a.arrive = reinterpret_cast<int32_t*>(b);
   b += align_up(T * 4);
   a.counters = reinterpret_cast<int32_t*>(b);
+  b += 64;
+  // region-linear grids: Z from per-class stencil tables (MLMCP_PERIODIC_REGION=0:
+  // the streamed CSR values, A/B)
+  const char* pe = getenv("MLMCP_PERIODIC_REGION");
+  const bool rg = rpar != nullptr && ctx->rcls != nullptr && ctx->rC > 0 && region_on() &&
+                  ctx->cl_wd > 0 && !(pe && atoi(pe) == 0);
+  size_t tab_smem = 0;
+  if (rg) {
+    a.rcls = ctx->rcls;
+    a.rckey = ctx->rckey;
+    a.rC = ctx->rC;
+    a.R = ctx->rR;
+    a.wd = ctx->cl_wd;
+    a.rpar = rpar;
+    for (int i = 0; i < 12; ++i) {
+      a.rmw[i] = ctx->rmw[i];
+      a.rkw[i] = ctx->rkw[i];
+    }
+    a.ctab = reinterpret_cast<double*>(b);
+    tab_smem = sizeof(double) * kPTW * (size_t)a.rC;
+  }
   MLMCP_CUDA_CHECK(cudaMemsetAsync(a.arrive, 0, sizeof(int32_t) * T, stream));
   MLMCP_CUDA_CHECK(cudaMemsetAsync(a.counters, 0, 2 * sizeof(int32_t), stream));
   const dim3 grid((a.N + kThreads - 1) / kThreads, n);
-  pinit_kernel<<<grid, kThreads, 0, stream>>>(a);
-  MLMCP_LAUNCH_CHECK("pinit_kernel");
+  if (rg) {
+    ptab_kernel<<<n, 64, 0, stream>>>(a);
+    MLMCP_LAUNCH_CHECK("ptab_kernel");
+    pinit_rg_kernel<<<grid, kThreads, tab_smem, stream>>>(a);
+    MLMCP_LAUNCH_CHECK("pinit_rg_kernel");
+  } else {
+    pinit_kernel<<<grid, kThreads, 0, stream>>>(a);
+    MLMCP_LAUNCH_CHECK("pinit_kernel");
+  }
   int32_t* hc = ctx->host_counters;
   int done_iters = 0;
   while (done_iters < max_it) {
     const int chunk = done_iters == 0 ? 16 : 4;
     for (int c = 0; c < chunk; ++c) {
+      if (rg) {
+        pspmv_rg_kernel<<<grid, kThreads, tab_smem, stream>>>(a);
+        MLMCP_LAUNCH_CHECK("pspmv_rg_kernel");
+        pupdate_rg_kernel<<<grid, kThreads, tab_smem, stream>>>(a);
+        MLMCP_LAUNCH_CHECK("pupdate_rg_kernel");
+        ppupd_rg_kernel<<<grid, kThreads, tab_smem, stream>>>(a);
+        MLMCP_LAUNCH_CHECK("ppupd_rg_kernel");
+        continue;
+      }
       pspmv_kernel<<<grid, kThreads, 0, stream>>>(a);
       MLMCP_LAUNCH_CHECK("pspmv_kernel");
       pupdate_kernel<<<grid, kThreads, 0, stream>>>(a);

@@ -256,7 +256,8 @@ class DeviceSystem:
 
     # ------------------------------------------------------------ predictor
     def periodic_state(self, sample_idx: torch.Tensor, dts: torch.Tensor, M, K, profile,
-                       omega: float, rtol: float = 1e-8, max_it: int = 500, stream=None):
+                       omega: float, rtol: float = 1e-8, max_it: int = 500, stream=None,
+                       rp=None):
         """X [n, 2, N]: periodic steady states of the implicit-Euler iteration
         for (sample_idx[i], dts[i]) (initial-guess predictor)."""
         n = len(sample_idx)
@@ -267,7 +268,7 @@ class DeviceSystem:
             if nbytes:     # streaming path: grid-wide COCG in a workspace
                 ws = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
             check(self.lib.mlmcp_periodic_state(self.ctx, n, ptr(sample_idx), ptr(dts),
-                                                M.shape[0], ptr(M), ptr(K), ptr(profile),
+                                                M.shape[0], ptr(M), ptr(K), ptr(rp), ptr(profile),
                                                 float(omega), float(rtol), int(max_it), ptr(X),
                                                 None, ptr(ws), nbytes, stream_handle(stream)),
                   "mlmcp_periodic_state")

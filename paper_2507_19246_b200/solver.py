@@ -33,6 +33,13 @@ DEFAULT_RTOL = 1e-13   # ||r||_2 <= 1e-13 ||b||_2, the stated PCG tolerance (DES
 # error is up to kappa * rtol; 1e-14 keeps the per-step state error at the
 # 1e-13 warm-start level for < 1 extra iteration per step.
 PREDICTOR_RTOL = 1e-14
+# COCG tolerance of the periodic steady states: they only feed initial guesses.
+# Streaming meshes (config-2 estimate): 1e-8 -> 1e-6 costs 1% more PCG
+# iterations and saves 30% of the COCG iterations (1e-5 costs 9%); on the
+# SM-resident path (configs 0/1, least-squares guesses at rtol 1e-14) 1e-6
+# costs 26% of the config-1 estimate, so 1e-8 stays there.
+SS_RTOL_STREAMING = 1e-6
+SS_RTOL_RESIDENT = 1e-8
 DEFAULT_MAX_IT = 20000
 
 
@@ -158,7 +165,7 @@ class BatchSolver:
     def step_rtol(self) -> float:
         return min(self.rtol, PREDICTOR_RTOL) if self.use_predictor() else self.rtol
 
-    def steady_states(self, samples: np.ndarray, dts: np.ndarray, M, K, stream=None):
+    def steady_states(self, samples: np.ndarray, dts: np.ndarray, M, K, stream=None, rp=None):
         """X [n, 2, N] for (sample, dt) pairs (mlmcp_periodic_state)."""
         key = ("ss", samples.tobytes(), dts.tobytes())
         v = self._task_cache.get(key)
@@ -167,8 +174,10 @@ class BatchSolver:
                  torch.tensor(dts.astype(np.float64), device=self.device))
             self._task_cache[key] = v
         return self.sys.periodic_state(v[0], v[1], M, K, self.profile, self.omega,
-                                       rtol=float(os.environ.get("MLMCP_SS_RTOL", "1e-8")),
-                                       stream=stream)
+                                       rtol=float(os.environ.get(
+                                           "MLMCP_SS_RTOL", SS_RTOL_RESIDENT if self.sys.sm_resident
+                                           else SS_RTOL_STREAMING)),
+                                       stream=stream, rp=rp)
 
     def _grid_tensors(self, ck0, cst):
         key = ("grid", ck0.tobytes(), cst.tobytes())
@@ -269,7 +278,7 @@ class FESolver(BatchSolver):
 
 
 # ------------------------------------------------------------ sequential
-def _seq_setup(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False):
+def _seq_setup(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = False, rp=None):
     """Task table (longest first), buffers and predictor states of a batch of
     sequential jobs."""
     from types import SimpleNamespace
@@ -310,7 +319,7 @@ def _seq_setup(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool = Fa
                                   if self.timing else None))
     if T and self.use_predictor():
         tasks["ss_slot"] = idx
-        st.xss = self.steady_states(tasks["sample"], tasks["dt"], M, K, stream)
+        st.xss = self.steady_states(tasks["sample"], tasks["dt"], M, K, stream, rp=rp)
     if self.sys.sm_resident and T:
         order = np.argsort(-tasks["n_steps"], kind="stable")   # longest first
         key = (tasks.tobytes(), N)
@@ -340,7 +349,7 @@ def _run_sequential(self, M, K, jobs: list[SeqJob], stream=None, keep_traj: bool
                     rp=None):
     """All jobs in one batched launch (SM-resident path) or one launch per
     dt (streaming path).  Returns one SeqResult per job (device tensors)."""
-    st = _seq_setup(self, M, K, jobs, stream, keep_traj)
+    st = _seq_setup(self, M, K, jobs, stream, keep_traj, rp=rp)
     if st.T == 0:
         return _seq_results(self, st)
     cur = stream if stream is not None else torch.cuda.current_stream()

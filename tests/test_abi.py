@@ -30,7 +30,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_counters():
     lib = _lib.load()
-    assert lib.mlmcp_abi_version() == _lib.ABI_VERSION == 10
+    assert lib.mlmcp_abi_version() == _lib.ABI_VERSION == 11
     assert _lib.launch_count() >= 0
 
 

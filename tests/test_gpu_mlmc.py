@@ -424,3 +424,31 @@ def test_pipelined_calls_bitwise(cuda, monkeypatch):
     assert piped.expectation == serial.expectation
     for a, b in zip(piped.per_level, serial.per_level):
         assert (a.n, a.mean_y, a.var_y) == (b.n, b.mean_y, b.var_y)
+
+
+def test_periodic_region_vs_csr(cuda, monkeypatch):
+    """Periodic steady states on a region-linear grid: the class-table COCG
+    kernels (region parameters passed) against the kernels that stream the CSR
+    values of M and K, both solved to 1e-12."""
+    import torch
+    from paper_2507_19246_b200.mlmc import draw_level
+    fam = large_family(2)
+    sol = fam.solver
+    S = 3
+    pd = torch.from_numpy(draw_level(fam.uncertain, 0, 1, range(1, S + 1))).cuda()
+    M = torch.empty((S, sol.nnz), dtype=torch.float64, device="cuda")
+    K = torch.empty_like(M)
+    rp = sol.new_region_params(S)
+    sol.assemble(pd, out=(M, K), rp_out=rp)
+    sidx = torch.tensor([0, 1, 2, 0], dtype=torch.int32, device="cuda")
+    dts = torch.tensor([T / 64, T / 64, T / 128, T / 512], dtype=torch.float64, device="cuda")
+    kw = dict(rtol=1e-12, max_it=2000)
+    x_rg = sol.sys.periodic_state(sidx, dts, M, K, sol.profile, sol.omega, rp=rp, **kw)
+    x_csr = sol.sys.periodic_state(sidx, dts, M, K, sol.profile, sol.omega, rp=None, **kw)
+    monkeypatch.setenv("MLMCP_PERIODIC_REGION", "0")
+    x_off = sol.sys.periodic_state(sidx, dts, M, K, sol.profile, sol.omega, rp=rp, **kw)
+    torch.cuda.synchronize()
+    assert torch.equal(x_csr, x_off)                      # the knob selects the CSR kernels
+    scale = x_csr.abs().amax(dim=(1, 2), keepdim=True)
+    assert float(((x_rg - x_csr).abs() / scale).max()) <= 1e-9
+    assert float(scale.min()) > 0.0
