@@ -79,7 +79,7 @@ __constant__ double c_bd_ls68[8] = {49.0 / 8, -119.0 / 8, 133.0 / 8, -35.0 / 8,
 
 // MLMCP_BAND_PROF=1: clock64 cycles of the step phases in CTA 0 of the first
 // cluster (trig + sync, guess, step start incl. its all-reduce, PCG loop)
-__device__ unsigned long long g_band_prof[8];
+__device__ unsigned long long g_band_prof[16];   // [8..13]: PCG-iteration phases (prof bit 1)
 #define BD_PROF(i, t0)                                                              \
   do {                                                                            \
     if ((a.prof & 1) && blockIdx.x == 0 && threadIdx.x == 0) {                          \
@@ -88,6 +88,23 @@ __device__ unsigned long long g_band_prof[8];
       (t0) = t1_;                                                                 \
     }                                                                             \
   } while (0)
+
+// PCG-iteration phases: compiled in only with -DMLMCP_BAND_PROF2 (the probes
+// split the iteration into basic blocks)
+#ifdef MLMCP_BAND_PROF2
+#define BD_PROF2(i, t0)                                                             \
+  do {                                                                            \
+    if ((a.prof & 2) && blockIdx.x == 0 && threadIdx.x == 0) {                          \
+      const long long t1_ = clock64();                                            \
+      g_band_prof[i] += (unsigned long long)(t1_ - (t0));                         \
+      (t0) = t1_;                                                                 \
+    }                                                                             \
+  } while (0)
+#define BD_PROF2_T0(t) long long t = clock64()
+#else
+#define BD_PROF2(i, t0) do { } while (0)
+#define BD_PROF2_T0(t) do { } while (0)
+#endif
 
 struct BdArgs {
   const mlmcp_task* tasks;
@@ -173,6 +190,7 @@ struct Th {
   uint32_t okm;    // valid rows (bit r)
   uint32_t cl[kR / 4];  // point classes of the rows (bytes)
   __device__ bool ok(int r) const { return (okm >> r) & 1u; }
+  __device__ bool chg(int r) const { return (okm >> (16 + r)) & 1u; }   // class(r) != class(r-1)
   __device__ int row(int r) const { return gr0 + r * wd; }
   __device__ int slot(int r) const { return sb + r * kTX; }
   __device__ int cls(int r) const { return (cl[r >> 2] >> (8 * (r & 3))) & 255; }
@@ -283,12 +301,12 @@ __device__ __forceinline__ void bd_xsend(const Th& th, double* V, Sh& sh, int mi
     mb_expect(mb, 8u * kTX * ((th.rank > 0 ? 1u : 0u) + (th.rank < kCS - 1 ? 1u : 0u)));
 }
 
-// u into the next of the two PCG exchange buffers, halos waited for
-__device__ __forceinline__ void bd_exchange(const Th& th, const double (&v)[kR], Sh& sh) {
+// u into the next of the two PCG exchange buffers; the halo rows are waited for
+// later (bd_xwait(sh, sh.hb)), after the rows that do not need them
+__device__ __forceinline__ void bd_exchange_begin(const Th& th, const double (&v)[kR], Sh& sh) {
   sh.hb ^= 1;
   bd_xissue(th, v, sh.vc(), sh, sh.hb);
   __syncthreads();
-  bd_xwait(sh, sh.hb);
 }
 
 // Calls f(r, nb) with the 7 neighbour values (SW, S, W, C, E, N, NE) of each of
@@ -365,12 +383,84 @@ __device__ __forceinline__ double bd_dot7p(const double* T, const double (&nb)[7
   return acc0 + acc1;
 }
 
+// A stencil row held in registers across the rows of a strip: a thread's rows
+// almost always share one point class (region interiors; the class changes at
+// the domain's first / last row and on region boundaries), so the row is
+// reloaded only where Th::chg marks a change (bit 16 + r of okm) instead of
+// four shared-memory loads per row.  Same doubles, same summation order as
+// bd_dot7.
+struct Row7 {
+  double2 t01, t23, t45;
+  double t6;
+  __device__ __forceinline__ void load(const double* T) {
+    t01 = *reinterpret_cast<const double2*>(T);
+    t23 = *reinterpret_cast<const double2*>(T + 2);
+    t45 = *reinterpret_cast<const double2*>(T + 4);
+    t6 = T[6];
+  }
+  __device__ __forceinline__ double dot(const double (&nb)[7]) const {
+    double acc0 = t23.y * nb[3], acc1 = t01.x * nb[0];
+    acc0 = fma(t01.y, nb[1], acc0);
+    acc1 = fma(t23.x, nb[2], acc1);
+    acc0 = fma(t45.x, nb[4], acc0);
+    acc1 = fma(t45.y, nb[5], acc1);
+    acc0 = fma(t6, nb[6], acc0);
+    return acc0 + acc1;
+  }
+};
+
+// out = A v for a v just handed to bd_exchange_begin: the rows 1 .. kR-2 of
+// the strip need no other band's values and are formed while the neighbouring
+// CTAs' halo rows are still in flight; rows 0 and kR-1 follow the wait.  Per
+// row the same doubles in the same order as bd_apply.
+__device__ __forceinline__ void bd_apply_overlap(const Th& th, Sh& sh, const double (&v)[kR],
+                                                 double (&out)[kR]) {
+  const double* V = sh.vc();
+  const int b = th.vb;
+  Row7 row;
+  row.load(sh.TAB + th.cls(1) * kTabW);
+  {
+    double sw = V[b - 1], so = v[0];
+    double w = V[b + kLD - 1], e = V[b + kLD + 1];
+#pragma unroll
+    for (int r = 1; r < kR - 1; ++r) {
+      if (r > 1 && th.chg(r)) row.load(sh.TAB + th.cls(r) * kTabW);
+      const double en = V[b + (r + 1) * kLD + 1];
+      const double wn = V[b + (r + 1) * kLD - 1];
+      const double nb[7] = {sw, so, w, v[r], e, v[r + 1], en};
+      out[r] = row.dot(nb);
+      sw = w;
+      so = v[r];
+      w = wn;
+      e = en;
+    }
+  }
+  bd_xwait(sh, sh.hb);
+  {
+    row.load(sh.TAB + th.cls(0) * kTabW);
+    const double nb[7] = {V[b - kLD - 1], V[b - kLD], V[b - 1], v[0], V[b + 1], v[1],
+                          V[b + kLD + 1]};
+    out[0] = row.dot(nb);
+  }
+  {
+    constexpr int r = kR - 1;
+    row.load(sh.TAB + th.cls(r) * kTabW);
+    const double nb[7] = {V[b + (r - 1) * kLD - 1], v[r - 1], V[b + r * kLD - 1], v[r],
+                          V[b + r * kLD + 1], V[b + kR * kLD], V[b + kR * kLD + 1]};
+    out[r] = row.dot(nb);
+  }
+}
+
 // out = B v, B the operator part `off` (0: A, 8: M, 16: K) of the class table
 __device__ __forceinline__ void bd_apply(const Th& th, const Sh& sh, int off,
                                          const double (&v)[kR], const double* V,
                                          double (&out)[kR]) {
+  Row7 row;
+  const double* T0 = sh.TAB + off;
+  row.load(T0 + th.cls(0) * kTabW);
   bd_rows(th, v, V, [&](int r, const double (&nb)[7]) {
-    out[r] = bd_dot7(sh.TAB + th.cls(r) * kTabW + off, nb);
+    if (r > 0 && th.chg(r)) row.load(T0 + th.cls(r) * kTabW);
+    out[r] = row.dot(nb);
   });
 }
 
@@ -456,25 +546,45 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
   double red[4] = {0.0, 0.0, 0.0, 0.0};
   {
     double bv[kR];
-    bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
-      const double* T = sh.TAB + th.cls(r) * kTabW;
-      double pf;   // the point's source profile: its class's M-row pad entry
-      const double mx = bd_dot7p(T + 8, nb, pf);
-      if (energy) red[3] = fma(nb[3], bd_dot7(T + 16, nb), red[3]);
-      if (!sh.pf_tab) pf = th.ok(r) ? __ldg(a.profile + th.row(r)) : 0.0;
-      bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, pf))) : 0.0;
-    });
+    {
+      // M and K rows held across the strip's rows (Row7); the M row's pad entry
+      // is the class's source profile
+      Row7 mrow, krow;
+      double pfc;
+      const double* T = sh.TAB + th.cls(0) * kTabW;
+      mrow.load(T + 8);
+      pfc = T[15];
+      if (energy) krow.load(T + 16);
+      bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
+        if (r > 0 && th.chg(r)) {
+          const double* Tr = sh.TAB + th.cls(r) * kTabW;
+          mrow.load(Tr + 8);
+          pfc = Tr[15];
+          if (energy) krow.load(Tr + 16);
+        }
+        const double mx = mrow.dot(nb);
+        if (energy) red[3] = fma(nb[3], krow.dot(nb), red[3]);
+        double pf = pfc;   // the point's source profile: its class's M-row pad entry
+        if (!sh.pf_tab) pf = th.ok(r) ? __ldg(a.profile + th.row(r)) : 0.0;
+        bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, pf))) : 0.0;
+      });
+    }
     const double* V0 = sh.vc();
-    bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
-      res[r] = th.ok(r) ? bv[r] - bd_dot7(sh.TAB + th.cls(r) * kTabW, nb) : 0.0;
-    });
+    {
+      Row7 arow;
+      arow.load(sh.TAB + th.cls(0) * kTabW);
+      bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
+        if (r > 0 && th.chg(r)) arow.load(sh.TAB + th.cls(r) * kTabW);
+        res[r] = th.ok(r) ? bv[r] - arow.dot(nb) : 0.0;
+      });
+    }
     bd_precond(pc, bv, u);
 #pragma unroll
     for (int r = 0; r < kR; ++r) red[2] = fma(bv[r], u[r], red[2]);
   }
   bd_precond(pc, res, u);
-  bd_exchange(th, u, sh);
-  bd_apply(th, sh, 0, u, sh.vc(), w);
+  bd_exchange_begin(th, u, sh);
+  bd_apply_overlap(th, sh, u, w);
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
     red[0] = fma(res[r], u[r], red[0]);
@@ -508,20 +618,24 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
   }
   int it = 1;
   for (;;) {
-    if (false) BD_PROF(7, tp);
+    BD_PROF2_T0(t2);
     double red2[2] = {0.0, 0.0};
     {
       double uk[kR];
       bd_precond(pc, res, uk);
-      bd_exchange(th, uk, sh);
-      bd_apply(th, sh, 0, uk, sh.vc(), w);
+      BD_PROF2(8, t2);
+      bd_exchange_begin(th, uk, sh);
+      BD_PROF2(9, t2);
+      bd_apply_overlap(th, sh, uk, w);
 #pragma unroll
       for (int r = 0; r < kR; ++r) {
         red2[0] = fma(res[r], uk[r], red2[0]);
         red2[1] = fma(w[r], uk[r], red2[1]);
       }
+      BD_PROF2(10, t2);
     }
     bd_allsum_mb<2>(red2, sh, th.rank);
+    BD_PROF2(11, t2);
     const double gnew = red2[0];
     delta = red2[1];
     if (gnew <= tol2) break;
@@ -544,6 +658,7 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
       sh.X[sl] = fma(alpha, p[r], sh.X[sl]);
       res[r] = fma(-alpha, s[r], res[r]);
     }
+    BD_PROF2(12, t2);
     ++it;
   }
   iters += it;
@@ -633,6 +748,9 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
     MLMCP_DCHECK(!th.ok(r) || (th.row(r) >= 0 && th.row(r) < a.N));
     if (th.ok(r)) th.cl[r >> 2] |= (uint32_t)__ldg(a.rcls + th.row(r)) << (8 * (r & 3));
   }
+#pragma unroll
+  for (int r = 1; r < kR; ++r)
+    if (th.cls(r) != th.cls(r - 1)) th.okm |= 1u << (16 + r);
 #ifdef MLMCP_CHECKED
   for (int r = 0; r < kR; ++r) MLMCP_DCHECK(th.cls(r) < a.rC);
 #endif
@@ -900,11 +1018,14 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
     ctx->iter_ms += ms;
     ctx->iter_launches += 1;
   }
-  if (a.prof & 1) {
-    unsigned long long h[8];
+  if (a.prof & 3) {
+    unsigned long long h[16];
     MLMCP_CUDA_CHECK(cudaMemcpyFromSymbol(h, g_band_prof, sizeof(h)));
     fprintf(stderr, "band prof cycles: trig %llu guess %llu stepstart+ie %llu pcg %llu tail %llu\n",
             h[0], h[1], h[2], h[3], h[4]);
+    if (a.prof & 2)
+      fprintf(stderr, "band prof pcg phases: precond %llu exchange %llu apply+dots %llu "
+              "allsum %llu update %llu\n", h[8], h[9], h[10], h[11], h[12]);
   }
   return MLMCP_OK;
 }
