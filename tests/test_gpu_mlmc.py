@@ -50,6 +50,7 @@ def check_estimate(n, dts, counts, pr):
         g = res.per_level[lvl]
         assert g.n == st.n
         assert abs(g.mean_y - st.mean) <= 1e-8 * abs(E)
+        assert abs(g.var_y - st.var) <= 1e-8 * abs(E)          # V_l, same absolute bar
         if lvl == len(counts) - 1 and pr:
             assert g.parareal_k == [r[2] for r in ora[lvl]]
     assert abs(res.expectation - E) <= 1e-8 * abs(E)
