@@ -647,6 +647,25 @@ def main():
                             "need for the same rate, frac > 1 = faster than any streaming "
                             "kernel can be; the bound that limits it is inside the SM "
                             "(sm_internal, from the committed ncu capture)"}
+        elif k_ms <= 0.0:
+            # cluster path (grids <= 128^2: config 3): no per-iteration launches to
+            # time; the whole estimate's device time stands in for the kernel's
+            nc = ncu_traffic("cluster_propagate_kernel")
+            achieved = n_its * b_it / (ms / 1000.0) / 1e9
+            roof = {"bound": "sm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "traffic": None,
+                    "kernel": "cluster_propagate_kernel (one 8-CTA cluster per task; operator "
+                              "and PCG vectors in registers / shared memory)",
+                    "algorithmic_bytes": f"{int(n_its)} PCG task-iterations per estimate x B_it "
+                                         f"(8 nnz + 56 N) = {b_it} B each (SURVEY 8(d))",
+                    "sm_internal": {k: nc.get(k) for k in ("issue_slots_busy_pct", "ipc_active",
+                                                          "fp64_pipe_pct", "warps_active_pct")},
+                    "peak_kind": peak_kind, "ncu_source": nc.get("source"),
+                    "ncu_launch": nc.get("launch"),
+                    "note": "no HBM traffic per PCG iteration; achieved = PCG task-iterations x "
+                            "B_it over the whole estimate's device time (Parareal sweeps and "
+                            "defects included), the bandwidth a streaming formulation would "
+                            "need; the bound is inside the SM / cluster (sm_internal)"}
         else:
             kname = ("tile_iter_rw_kernel" if rw else "tile_iter_rg_kernel") if region \
                 else "tile_iter_kernel"

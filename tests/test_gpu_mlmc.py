@@ -453,3 +453,25 @@ def test_periodic_region_vs_csr(cuda, monkeypatch):
     scale = x_csr.abs().amax(dim=(1, 2), keepdim=True)
     assert float(((x_rg - x_csr).abs() / scale).max()) <= 1e-9
     assert float(scale.min()) > 0.0
+
+
+def test_run_levels_direct_chunking_bitwise(cuda, monkeypatch):
+    """run_levels called directly with more samples than the per-call cap
+    (_run_levels_chunked): per-sample Q_l, Q_{l-1}, K and iteration counts
+    bitwise those of one call."""
+    from paper_2507_19246_b200.mlmc import draw_level
+    from paper_2507_19246_b200.parareal import PararealConfig
+    fam = small_family()
+    pcfg = PararealConfig(4, T / 128, T / 16, 1e-8, 4)
+    draws = [draw_level(fam.uncertain, 0, lvl, range(1, n + 1)) for lvl, n in enumerate((7, 5, 4))]
+    ref = fam.run_levels(draws, pcfg)
+    ref = [(b.q_l.cpu().numpy(), b.q_lm1.cpu().numpy(), b.k_used.cpu().numpy(),
+            b.iters.cpu().numpy()) for b in ref]
+    monkeypatch.setattr(type(fam), "max_samples_per_call", lambda self, cfg=None, level=None: 3)
+    got = fam.run_levels(draws, pcfg)
+    fam.check_status()
+    for b, (ql, qm, ku, its) in zip(got, ref):
+        np.testing.assert_array_equal(b.q_l.cpu().numpy(), ql)
+        np.testing.assert_array_equal(b.q_lm1.cpu().numpy(), qm)
+        np.testing.assert_array_equal(b.k_used.cpu().numpy(), ku)
+        np.testing.assert_array_equal(b.iters.cpu().numpy(), its)
