@@ -76,6 +76,16 @@ __constant__ double c_bd_extrap[8][8] = {
 // least-squares degree-6 fit through the last 8 transients (stream_path.cu)
 __constant__ double c_bd_ls68[8] = {49.0 / 8, -119.0 / 8, 133.0 / 8, -35.0 / 8,
                                     -77.0 / 8, 91.0 / 8, -41.0 / 8, 7.0 / 8};
+// degree-5 / degree-4 fits through the same 8 transients.  The degree trades
+// truncation error against the amplification of the previous solves' errors
+// (sum |w| = 69 / 25.5 / 11.2 for degrees 6 / 5 / 4): measured PCG iterations
+// per step at dt = T/64: 3.04 / 4.30 / 6.32, T/128: 3.21 / 3.57 / 5.76, T/256:
+// 2.82 / 2.56 / 3.44, T/512: 2.71 / 2.17 / 2.29 — degree 6 up to 192 steps per
+// period, degree 5 beyond (MLMCP_BAND_LSDEG = 4 / 5 / 6 forces one, A/B)
+__constant__ double c_bd_ls58[8] = {36.0 / 8, -54.0 / 8, 16.0 / 8, 30.0 / 8,
+                                    -12.0 / 8, -26.0 / 8, 24.0 / 8, -6.0 / 8};
+__constant__ double c_bd_ls48[8] = {175.0 / 56, -125.0 / 56, -75.0 / 56, 45.0 / 56,
+                                    81.0 / 56, 5.0 / 56, -85.0 / 56, 35.0 / 56};
 
 // MLMCP_BAND_PROF=1: clock64 cycles of the step phases in CTA 0 of the first
 // cluster (trig + sync, guess, step start incl. its all-reduce, PCG loop)
@@ -821,6 +831,8 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
   double* rb = a.ring + (int64_t)ti * kRing * kBandPts + th.gy0 * kTX + th.x;
   const double* Xs = pred ? a.xss + (int64_t)t.ss_slot * 2 * N : nullptr;
   const bool sum_e = t.qoi_mode == MLMCP_QOI_SUM_ENERGY && t.qoi_slot >= 0;
+  // least-squares degree of the guess: by the task's steps per period
+  const int lsdeg = a.ls_on > 1 ? a.ls_on : (a.omega * t.dt * 192.0 < 6.283185307179586 ? 5 : 6);
   int iters = 0, code = MLMCP_ST_OK, fail_step = 0;
   double acc = 0.0;
   long long tq = clock64();
@@ -848,7 +860,9 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
 #pragma unroll
     for (int sl = 0; sl < kRing; ++sl) {
       const int q = (step - sl) & (kRing - 1);
-      const double wq = (pred && pord >= 7 && a.ls_on) ? c_bd_ls68[q]
+      const double wq = (pred && pord >= 7 && a.ls_on) ? (lsdeg == 5   ? c_bd_ls58[q]
+                                                          : lsdeg == 4 ? c_bd_ls48[q]
+                                                                       : c_bd_ls68[q])
                         : q <= pord                    ? c_bd_extrap[pord][q]
                                                        : 0.0;
       ww[sl] = (q >= 1 && q <= pord) ? wq : 0.0;
@@ -974,6 +988,10 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
   a.max_it = max_it;
   a.order = std::max(0, std::min(order, kRing - 1));
   a.ls_on = ls_on;
+  if (const char* ld = getenv("MLMCP_BAND_LSDEG")) {
+    const int d = atoi(ld);
+    if (ls_on && d >= 4 && d <= 6) a.ls_on = d;
+  }
   a.ring = ring;
   a.xbuf = xbuf;
   a.qoi = qoi;

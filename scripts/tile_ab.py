@@ -50,7 +50,7 @@ for mode in modes:
     K = torch.empty_like(M)
     rp = sol.new_region_params(S)
     sol.assemble(pd, out=(M, K), rp_out=rp)
-    job = fam._seq_job(np.arange(S), fam.hierarchy[0].dt)
+    job = fam._seq_job(np.arange(S), fam.hierarchy[int(os.environ.get("TILE_AB_LEVEL", "0"))].dt)
     job.n_steps = steps
     times = []
     for r in range(3):
