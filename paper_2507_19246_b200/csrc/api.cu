@@ -471,6 +471,7 @@ int mlmcp_ctx_set_region_grid(mlmcp_ctx* c, int n_regions, const uint32_t* code,
     c->rckey = nullptr;
     c->rC = 0;
     c->rR = 0;
+    c->band_sigs = 0;
     return MLMCP_OK;
   }
   if (n_regions < 1 || n_regions > 16 || !code || !mw || !kw)
@@ -509,6 +510,7 @@ int mlmcp_ctx_set_region_grid(mlmcp_ctx* c, int n_regions, const uint32_t* code,
   c->rcls = nullptr;
   c->rckey = nullptr;
   c->rC = 0;
+  c->band_sigs = 0;
   if (keys.size() <= 256) {
     MLMCP_CUDA_CHECK(cudaMalloc(&c->rcls, (size_t)c->n));
     MLMCP_CUDA_CHECK(cudaMemcpy(c->rcls, cls.data(), (size_t)c->n, cudaMemcpyHostToDevice));
@@ -516,6 +518,7 @@ int mlmcp_ctx_set_region_grid(mlmcp_ctx* c, int n_regions, const uint32_t* code,
     MLMCP_CUDA_CHECK(cudaMemcpy(c->rckey, keys.data(), sizeof(uint32_t) * keys.size(),
                                 cudaMemcpyHostToDevice));
     c->rC = (int)keys.size();
+    c->band_sigs = band_max_signatures(cls.data(), c->cl_wd, c->cl_h);
   }
   for (int i = 0; i < 12; ++i) {
     c->rmw[i] = mw[i];

@@ -33,7 +33,9 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <array>
 #include <cstdio>
+#include <vector>
 
 #include "mlmcp_internal.cuh"
 
@@ -59,6 +61,8 @@ constexpr int kRing = 8;                 // past transients (extrapolation order
 constexpr int kGB = MLMCP_BAND_GB;       // guess rows whose ring loads are in flight together
 constexpr int kBandPts = kCS * kHB * kTX;  // ring slot pitch: rows of kTX points (compile-time offsets)
 constexpr int kMaxC = 256;               // point classes
+constexpr int kMaxSig = 32;              // distinct strip signatures (class sequences) per CTA
+constexpr int kPF = (2 * kR - 1) * kMaxSig;   // strip factors, one set per signature
 constexpr int kTabW = 24;                // per class: A (7 + pad), M (7 + pad), K (7 + pad)
 // shared memory (doubles): VA, VC[2], x, strip factors, class table, reduction
 // buffers, mbarriers
@@ -215,7 +219,8 @@ struct Sh {
   uint32_t ph;    // wait parity bits of the five mbarriers
   int hb;         // VC buffer of the current iteration
   int dbg;        // BdArgs::dbg_sync
-  double* PF;     // [2R-1][kNT] strip factors
+  double* PF;     // [kMaxSig][2R-1] strip factors, one set per strip signature
+  double* XS;     // [2][kSlots] the task's periodic steady state (Re, Im), predictor only
   double* TAB;    // [rC][kTabW]
   double* RED;    // [2][4][kCS] CTA partials of every CTA, [4][kWarps] warp partials
   int par;
@@ -223,12 +228,16 @@ struct Sh {
   __device__ double* vc() const { return VC + hb * kV; }
 };
 
-// strip block-Jacobi: L D L^T of the thread's 8-row tridiagonal block, the
-// factors in shared memory ([2R-1][kNT]: lf_0..lf_6, di_0..di_7)
+// strip block-Jacobi: L D L^T of the thread's 16-row tridiagonal block.  The
+// factors depend only on the strip's signature — the classes of its rows and
+// which rows exist — and a band has a handful of those (region interiors,
+// region boundary columns, the domain's first / last column), so one set per
+// signature is kept in shared memory ([sig][2R-1]: lf_0..lf_14, di_0..di_15)
+// and the threads of a signature read it by broadcast.
 struct Pc {
-  double* f;
-  __device__ double lf(int r) const { return f[r * kNT + threadIdx.x]; }
-  __device__ double di(int r) const { return f[(kR - 1 + r) * kNT + threadIdx.x]; }
+  const double* f;   // the thread's signature's set
+  __device__ double lf(int r) const { return f[r]; }
+  __device__ double di(int r) const { return f[kR - 1 + r]; }
 };
 
 // Region-linear stencils (A = M + dt K, M and K; slot order SW, S, W, C, E, N, NE)
@@ -722,7 +731,8 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
   sh.VC = sh.VA + kV;
   sh.X = sh.VC + 2 * kV;
   sh.PF = sh.X + kSlots;
-  sh.TAB = sh.PF + (2 * kR - 1) * kNT;
+  sh.XS = sh.PF + kPF;
+  sh.TAB = sh.XS + 2 * kSlots;
   sh.RED = sh.TAB + kTabW * C;
   sh.mb = reinterpret_cast<uint64_t*>(sh.RED + kRedD);
   sh.ph = 0u;
@@ -803,19 +813,54 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
     sh.pf_tab = pf_bad == 0;
   }
   Pc pc;   // strip block-Jacobi factors (ClOp::load's recurrence)
-  pc.f = sh.PF;
   {
-    double d = th.ok(0) ? sh.TAB[th.cls(0) * kTabW + 3] : 0.0;
+    // the thread's strip signature: its rows' classes and validity.  The first
+    // thread with a signature leads it; leaders are numbered in thread order
+    // (sh.X is free until the state is loaded below: signature words, leader
+    // flags and dense numbers live there meanwhile).
+    uint32_t* sw = reinterpret_cast<uint32_t*>(sh.X);        // [kNT][5]
+    int* lead = reinterpret_cast<int*>(sw + 5 * kNT);        // [kNT] leader thread
+    int* dense = lead + kNT;                                 // [kNT] signature number of a leader
+    const uint32_t mine[5] = {th.cl[0], th.cl[1], th.cl[2], th.cl[3], th.okm & 0xffffu};
 #pragma unroll
-    for (int r = 0; r < kR; ++r) {
-      if (r > 0) {
-        const double nprev = th.ok(r - 1) ? sh.TAB[th.cls(r - 1) * kTabW + 5] : 0.0;
-        const double lf = (d != 0.0) ? nprev / d : 0.0;
-        sh.PF[(r - 1) * kNT + threadIdx.x] = lf;
-        d = (th.ok(r) ? sh.TAB[th.cls(r) * kTabW + 3] : 0.0) - lf * nprev;
+    for (int k = 0; k < 5; ++k) sw[threadIdx.x * 5 + k] = mine[k];
+    __syncthreads();
+    int ld = threadIdx.x;
+    for (int j = 0; j < (int)threadIdx.x; ++j) {
+      bool same = true;
+#pragma unroll
+      for (int k = 0; k < 5; ++k) same = same && sw[j * 5 + k] == mine[k];
+      if (same) {
+        ld = j;
+        break;
       }
-      sh.PF[(kR - 1 + r) * kNT + threadIdx.x] = (th.ok(r) && d != 0.0) ? 1.0 / d : 0.0;
     }
+    lead[threadIdx.x] = ld;
+    __syncthreads();
+    if (ld == (int)threadIdx.x) {
+      int n = 0;
+      for (int j = 0; j < (int)threadIdx.x; ++j) n += lead[j] == j;
+      dense[threadIdx.x] = n;
+    }
+    __syncthreads();
+    const int sig = dense[ld];
+    MLMCP_DCHECK(sig >= 0 && sig < kMaxSig);
+    double* F = sh.PF + (sig < kMaxSig ? sig : 0) * (2 * kR - 1);
+    pc.f = F;
+    if (ld == (int)threadIdx.x && sig < kMaxSig) {
+      double d = th.ok(0) ? sh.TAB[th.cls(0) * kTabW + 3] : 0.0;
+#pragma unroll
+      for (int r = 0; r < kR; ++r) {
+        if (r > 0) {
+          const double nprev = th.ok(r - 1) ? sh.TAB[th.cls(r - 1) * kTabW + 5] : 0.0;
+          const double lf = (d != 0.0) ? nprev / d : 0.0;
+          F[r - 1] = lf;
+          d = (th.ok(r) ? sh.TAB[th.cls(r) * kTabW + 3] : 0.0) - lf * nprev;
+        }
+        F[kR - 1 + r] = (th.ok(r) && d != 0.0) ? 1.0 / d : 0.0;
+      }
+    }
+    __syncthreads();   // factors written; sh.X free again
   }
 #pragma unroll
   for (int r = 0; r < kR; ++r) {
@@ -830,6 +875,14 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
   // the thread's ring entries: slot sl, row r at rb[sl * kBandPts + r * kTX]
   double* rb = a.ring + (int64_t)ti * kRing * kBandPts + th.gy0 * kTX + th.x;
   const double* Xs = pred ? a.xss + (int64_t)t.ss_slot * 2 * N : nullptr;
+  // the task's periodic steady state stays in shared memory for all its steps
+  // (it was re-read from L2 in every guess: a fifth of the guess's traffic)
+#pragma unroll
+  for (int r = 0; r < kR; ++r) {
+    const int64_t j = th.row(r);
+    sh.XS[th.slot(r)] = (th.ok(r) && pred) ? __ldg(Xs + j) : 0.0;
+    sh.XS[kSlots + th.slot(r)] = (th.ok(r) && pred) ? __ldg(Xs + N + j) : 0.0;
+  }
   const bool sum_e = t.qoi_mode == MLMCP_QOI_SUM_ENERGY && t.qoi_slot >= 0;
   // least-squares degree of the guess: by the task's steps per period
   const int lsdeg = a.ls_on > 1 ? a.ls_on : (a.omega * t.dt * 192.0 < 6.283185307179586 ? 5 : 6);
@@ -878,9 +931,8 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
       for (int rr = 0; rr < kGB; ++rr) {
         const int r = h + rr;
         const bool ok = th.ok(r) && pord > 0;
-        const int64_t j = th.row(r);
-        xr[rr] = (th.ok(r) && pred) ? __ldg(Xs + j) : 0.0;
-        xi[rr] = (th.ok(r) && pred) ? __ldg(Xs + N + j) : 0.0;
+        xr[rr] = sh.XS[th.slot(r)];
+        xi[rr] = sh.XS[kSlots + th.slot(r)];
 #pragma unroll
         for (int sl = 0; sl < kRing; ++sl)
           pv[rr][sl] = (ok && ((valid >> sl) & 1u)) ? __ldcg(rb + sl * kBandPts + r * kTX) : 0.0;
@@ -942,7 +994,7 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
 }
 
 size_t band_smem_bytes(int n_classes) {
-  return sizeof(double) * (3 * kV + kSlots + (2 * kR - 1) * kNT + kTabW * n_classes + kRedD + 5);
+  return sizeof(double) * (3 * kV + kSlots + kPF + 2 * kSlots + kTabW * n_classes + kRedD + 5);
 }
 
 }  // namespace
@@ -954,7 +1006,29 @@ bool band_usable(const Ctx* ctx) {
   const char* s = getenv("MLMCP_STREAM_IMPL");   // 5: the band path also on <= 128^2 grids
   if (s && atoi(s) != 0 && atoi(s) != 5) return false;
   return ctx->rcls != nullptr && ctx->rC <= kMaxC && ctx->cl_wd > 0 && ctx->cl_wd <= kTX &&
-         ctx->cl_h <= kCS * kHB && band_smem_bytes(ctx->rC) <= 227 * 1024;
+         ctx->cl_h <= kCS * kHB && band_smem_bytes(ctx->rC) <= 227 * 1024 &&
+         ctx->band_sigs > 0 && ctx->band_sigs <= kMaxSig;
+}
+
+// The largest number of distinct strip signatures (16 row classes + validity
+// of a column's strip) in any 16-row band of the grid; 0 when the grid does
+// not fit the band decomposition.  Host side, once per region grid.
+int band_max_signatures(const uint8_t* cls, int wd, int gh) {
+  if (cls == nullptr || wd <= 0 || wd > kTX || gh <= 0 || gh > kCS * kHB) return 0;
+  int worst = 0;
+  for (int band = 0; band * kHB < gh; ++band) {
+    std::vector<std::array<int, kR>> sigs;
+    for (int x = 0; x < kTX; ++x) {
+      std::array<int, kR> sg;
+      for (int r = 0; r < kR; ++r) {
+        const int gy = band * kHB + r;
+        sg[r] = (x < wd && gy < gh) ? (int)cls[(size_t)gy * wd + x] : -1;
+      }
+      if (std::find(sigs.begin(), sigs.end(), sg) == sigs.end()) sigs.push_back(sg);
+    }
+    worst = std::max(worst, (int)sigs.size());
+  }
+  return worst;
 }
 
 size_t band_ring_bytes(int n_tasks) {

@@ -69,6 +69,7 @@ struct Ctx {
   uint32_t* rckey = nullptr;       // device [rC] code (24 bits) | neighbour mask << 24
   int rC = 0;
   int rR = 0;
+  int band_sigs = 0;               // most distinct strip signatures in a 16-row band (band path)
   double rmw[12] = {0}, rkw[12] = {0};
   // pinned host counters for the streaming path
   int32_t* host_counters = nullptr;
@@ -263,6 +264,7 @@ bool coop_usable(const Ctx* ctx, int n_tasks);
 bool cluster_usable(const Ctx* ctx);
 bool band_usable(const Ctx* ctx);
 size_t band_ring_bytes(int n_tasks);
+int band_max_signatures(const uint8_t* cls, int wd, int gh);
 int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double* rpar,
                    const double* profile, double omega, double rtol, int max_it, int order,
                    int ls_on, const double* xss, double* ring, double* xbuf, double* qoi,
