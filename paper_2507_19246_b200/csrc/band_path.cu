@@ -4,29 +4,33 @@
 //
 // Same method and step semantics as the HBM-streaming tile path
 // (stream_path.cu; reference timeint.py:88-128): per step the periodic
-// steady-state predictor plus the extrapolated / least-squares transient guess
-// (ring of 8 past transients), the rhs b = M a_n + dt sin(wt) profile, and a
-// Chronopoulos-Gear PCG solve with the stopping rule r.B^-1.r <= rtol^2
-// b.B^-1.b.  What changes is where the PCG vectors live: a cluster of 16 CTAs
-// (one per SM, 1024 threads each) owns one task for all its steps; CTA c holds
-// the band of grid rows [16c, 16c+16) and each thread a column strip of 4 rows,
-// so the PCG vectors p, s, r, w stay in registers and x in shared memory for
-// the whole solve — a PCG iteration moves no global memory at all (the tile
-// path streams 64-80 B per point and iteration).  Global traffic per step is
-// the guess: 7 ring reads, 1 ring write and the steady state (2 reads) per
-// point, on a ring that stays L2-resident (7 concurrent clusters x 4.2 MB).
+// steady-state predictor plus the least-squares transient guess (ring of 8 past
+// transients), the rhs b = M a_n + dt sin(wt) profile, and a Chronopoulos-Gear
+// PCG solve with the stopping rule r.B^-1.r <= rtol^2 b.B^-1.b.  What changes
+// is where the PCG vectors live: a cluster of 16 CTAs (one per SM, 256 threads
+// each) owns one task for all its steps; CTA c holds the band of grid rows
+// [16c, 16c+16) and each thread a column strip of 16 rows, so the PCG vectors
+// p, s, r, w stay in registers and x in shared memory for the whole solve — a
+// PCG iteration moves no global memory at all (the tile path streams 64 B per
+// point and iteration).  Global traffic per step is the guess: 7 ring reads and
+// 1 ring write per point, on a ring that stays L2-resident (7 concurrent
+// clusters x 4.2 MB).
 //   * operator: the task's stencil of each point class (Ctx::rckey) formed once
 //     per task into shared memory (A, M and K rows, region_stencil of
-//     stream_path.cu's arithmetic), the point's class byte in shared memory;
-//   * preconditioner: 4-row strip block-Jacobi (L D L^T of each thread's strip,
-//     as the SM-resident and cluster paths), factors in shared memory;
-//   * neighbour values through a shared-memory exchange buffer; a band's first
-//     and last grid rows also go straight into the neighbouring CTAs' buffers
-//     (DSMEM), made visible by one cluster barrier;
-//   * dot products: warp butterfly, fixed-order sum of the CTA's 32 warp
-//     partials, the 16 CTA partials stored into every CTA (DSMEM), one cluster
-//     barrier, fixed-order sum — bitwise identical scalars in every CTA, hence
-//     one control flow for the whole cluster.
+//     stream_path.cu's arithmetic); a thread keeps the row of its strip's class
+//     in registers and reloads it only where the class changes (Row7);
+//   * preconditioner: 16-row strip block-Jacobi (L D L^T of each strip), one
+//     set of factors per strip signature (class sequence) in shared memory;
+//   * the task's periodic steady state in shared memory for all its steps;
+//   * neighbour values through a shared-memory exchange frame; a band's first
+//     and last grid rows also go straight into the neighbouring CTAs' frames
+//     (st.async, counted on a transaction mbarrier there); the rows that need
+//     no other band's values are formed before the wait for the halo rows;
+//   * dot products: warp butterfly, fixed-order sum of the CTA's 8 warp
+//     partials, the 16 CTA partials stored into every CTA (st.async on an
+//     mbarrier), fixed-order sum — bitwise identical scalars in every CTA,
+//     hence one control flow for the whole cluster; no cluster barrier in the
+//     step loop.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <math.h>
@@ -371,43 +375,13 @@ __device__ __forceinline__ void bd_rows_s(const Th& th, const double* V, F&& f) 
   }
 }
 
-// row T (7 coefficients, 16-byte aligned) . neighbours, in tile_iter_kernel's order
-__device__ __forceinline__ double bd_dot7(const double* T, const double (&nb)[7]) {
-  const double2 t01 = *reinterpret_cast<const double2*>(T);
-  const double2 t23 = *reinterpret_cast<const double2*>(T + 2);
-  const double2 t45 = *reinterpret_cast<const double2*>(T + 4);
-  const double t6 = T[6];
-  double acc0 = t23.y * nb[3], acc1 = t01.x * nb[0];
-  acc0 = fma(t01.y, nb[1], acc0);
-  acc1 = fma(t23.x, nb[2], acc1);
-  acc0 = fma(t45.x, nb[4], acc0);
-  acc1 = fma(t45.y, nb[5], acc1);
-  acc0 = fma(t6, nb[6], acc0);
-  return acc0 + acc1;
-}
-
-// bd_dot7 that also returns the row's pad entry T[7] (one 16-byte load of T[6..7])
-__device__ __forceinline__ double bd_dot7p(const double* T, const double (&nb)[7], double& t7) {
-  const double2 t01 = *reinterpret_cast<const double2*>(T);
-  const double2 t23 = *reinterpret_cast<const double2*>(T + 2);
-  const double2 t45 = *reinterpret_cast<const double2*>(T + 4);
-  const double2 t67 = *reinterpret_cast<const double2*>(T + 6);
-  double acc0 = t23.y * nb[3], acc1 = t01.x * nb[0];
-  acc0 = fma(t01.y, nb[1], acc0);
-  acc1 = fma(t23.x, nb[2], acc1);
-  acc0 = fma(t45.x, nb[4], acc0);
-  acc1 = fma(t45.y, nb[5], acc1);
-  acc0 = fma(t67.x, nb[6], acc0);
-  t7 = t67.y;
-  return acc0 + acc1;
-}
-
 // A stencil row held in registers across the rows of a strip: a thread's rows
 // almost always share one point class (region interiors; the class changes at
 // the domain's first / last row and on region boundaries), so the row is
 // reloaded only where Th::chg marks a change (bit 16 + r of okm) instead of
-// four shared-memory loads per row.  Same doubles, same summation order as
-// bd_dot7.
+// four shared-memory loads per row.  The row's seven coefficients (16-byte
+// aligned in the class table) times the neighbours, summed in
+// tile_iter_kernel's order.
 struct Row7 {
   double2 t01, t23, t45;
   double t6;
