@@ -212,3 +212,46 @@ def test_toy_family_chunked_estimate_bitwise():
     b = mlmc_estimate(toy_family(h, cap=3), policy=FixedSamples((23, 9, 4)), seed=5)
     assert a.expectation == b.expectation
     assert [(s.sum_y, s.sum_y2) for s in a.per_level] == [(s.sum_y, s.sum_y2) for s in b.per_level]
+
+
+def test_plan_calls_cover_and_order():
+    """mlmc.plan_calls: every sample of every level in exactly one call; one
+    call at a time keeps the level order and the caps; the pipelined plan keeps
+    each call within 0.8 of its cap, balances a level's chunks and starts with
+    the finest level."""
+    from paper_2507_19246_b200.mlmc import plan_calls
+    ranges = [(0, 4096), (10, 1034), (0, 0), (5, 69)]
+    caps = [3335, 2620, 2620, 2620]
+    for pipelined in (False, True):
+        calls = plan_calls(ranges, caps, pipelined)
+        for lvl, (a, b) in enumerate(ranges):
+            mine = sorted((c0, c1) for l, c0, c1 in calls if l == lvl)
+            if b <= a:
+                assert not mine
+                continue
+            assert mine[0][0] == a and mine[-1][1] == b
+            assert all(x[1] == y[0] for x, y in zip(mine, mine[1:]))
+            lim = int(caps[lvl] * 0.8) if pipelined else caps[lvl]
+            assert all(0 < c1 - c0 <= lim for c0, c1 in mine)
+        lv = [c[0] for c in calls]
+        assert lv == sorted(lv, reverse=pipelined)
+    piped = plan_calls(ranges, caps, True)
+    sizes0 = [c1 - c0 for l, c0, c1 in piped if l == 0]
+    assert sizes0 == [2048, 2048]                      # balanced, not 2668 + 1428
+
+
+def test_run_level_calls_without_streams_checks_each_call():
+    """run_level_calls on a family without call streams: calls in plan order,
+    the status check after each one."""
+    from paper_2507_19246_b200.mlmc import run_level_calls
+
+    class Fam:
+        def __init__(self):
+            self.log = []
+
+        def check_status(self, token=None):
+            self.log.append("check")
+
+    fam = Fam()
+    run_level_calls(fam, [(0, 0, 2), (1, 0, 1)], lambda l, a, b: fam.log.append((l, a, b)))
+    assert fam.log == [(0, 0, 2), "check", (1, 0, 1), "check"]
