@@ -522,6 +522,45 @@ __device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) 
   sh.par ^= 1;
 }
 
+// The step start's stencil passes: b = M a_n + dt sin(wt) profile (a_n in VA)
+// with, when kEnergy, a_n^T K a_n accumulated into e2; then r_0 = b - A x_0
+// (x_0 in the current exchange frame).  M / K / A rows held across the strip
+// (Row7); the M row's pad entry is the class's source profile (kPfTab), global
+// loads otherwise.
+template <bool kEnergy, bool kPfTab>
+__device__ __forceinline__ void bd_start_passes(const Th& th, const BdArgs& a, const Sh& sh,
+                                                double sf, double dt, double (&bv)[kR],
+                                                double (&res)[kR], double& e2) {
+  {
+    Row7 mrow, krow;
+    double pfc;
+    const double* T = sh.TAB + th.cls(0) * kTabW;
+    mrow.load(T + 8);
+    pfc = T[15];
+    if (kEnergy) krow.load(T + 16);
+    bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
+      if (r > 0 && th.chg(r)) {
+        const double* Tr = sh.TAB + th.cls(r) * kTabW;
+        mrow.load(Tr + 8);
+        pfc = Tr[15];
+        if (kEnergy) krow.load(Tr + 16);
+      }
+      const double mx = mrow.dot(nb);
+      if (kEnergy) e2 = fma(nb[3], krow.dot(nb), e2);
+      double pf = pfc;
+      if (!kPfTab) pf = th.ok(r) ? __ldg(a.profile + th.row(r)) : 0.0;
+      bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, pf))) : 0.0;
+    });
+  }
+  const double* V0 = sh.vc();
+  Row7 arow;
+  arow.load(sh.TAB + th.cls(0) * kTabW);
+  bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
+    if (r > 0 && th.chg(r)) arow.load(sh.TAB + th.cls(r) * kTabW);
+    res[r] = th.ok(r) ? bv[r] - arow.dot(nb) : 0.0;
+  });
+}
+
 // One implicit-Euler step.  On entry the guess phase has written a_n into
 // VA's own rows and the initial guess x0 into X and into the own rows of the
 // next PCG exchange buffer (sh.hb already advanced); X holds a_{n+1} on exit.
@@ -539,37 +578,14 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
   double red[4] = {0.0, 0.0, 0.0, 0.0};
   {
     double bv[kR];
-    {
-      // M and K rows held across the strip's rows (Row7); the M row's pad entry
-      // is the class's source profile
-      Row7 mrow, krow;
-      double pfc;
-      const double* T = sh.TAB + th.cls(0) * kTabW;
-      mrow.load(T + 8);
-      pfc = T[15];
-      if (energy) krow.load(T + 16);
-      bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
-        if (r > 0 && th.chg(r)) {
-          const double* Tr = sh.TAB + th.cls(r) * kTabW;
-          mrow.load(Tr + 8);
-          pfc = Tr[15];
-          if (energy) krow.load(Tr + 16);
-        }
-        const double mx = mrow.dot(nb);
-        if (energy) red[3] = fma(nb[3], krow.dot(nb), red[3]);
-        double pf = pfc;   // the point's source profile: its class's M-row pad entry
-        if (!sh.pf_tab) pf = th.ok(r) ? __ldg(a.profile + th.row(r)) : 0.0;
-        bv[r] = th.ok(r) ? __dadd_rn(mx, __dmul_rn(dt, __dmul_rn(sf, pf))) : 0.0;
-      });
-    }
-    const double* V0 = sh.vc();
-    {
-      Row7 arow;
-      arow.load(sh.TAB + th.cls(0) * kTabW);
-      bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
-        if (r > 0 && th.chg(r)) arow.load(sh.TAB + th.cls(r) * kTabW);
-        res[r] = th.ok(r) ? bv[r] - arow.dot(nb) : 0.0;
-      });
+    // the two stencil passes, specialised on (energy, profile from the class
+    // table): no uniform branches between the rows
+    if (energy) {
+      if (sh.pf_tab) bd_start_passes<true, true>(th, a, sh, sf, dt, bv, res, red[3]);
+      else bd_start_passes<true, false>(th, a, sh, sf, dt, bv, res, red[3]);
+    } else {
+      if (sh.pf_tab) bd_start_passes<false, true>(th, a, sh, sf, dt, bv, res, red[3]);
+      else bd_start_passes<false, false>(th, a, sh, sf, dt, bv, res, red[3]);
     }
     bd_precond(pc, bv, u);
 #pragma unroll
