@@ -209,6 +209,16 @@ struct Th {
   uint32_t cl[kR / 4];  // point classes of the rows (bytes)
   __device__ bool ok(int r) const { return (okm >> r) & 1u; }
   __device__ bool chg(int r) const { return (okm >> (16 + r)) & 1u; }   // class(r) != class(r-1)
+  // no class change among the rows 1 .. kR-3 (the rows 0, 1, kR-2, kR-1 always
+  // load their own stencil row: the domain's first / last rows and a region
+  // boundary at a band edge land there, so nearly every strip qualifies)
+  __device__ bool mid_uniform() const { return ((okm >> 18) & ((1u << (kR - 4)) - 1u)) == 0u; }
+  // row r reloads its stencil row: always at the strip's ends, in between only
+  // where the class changes (kCheck; compiled out for mid-uniform strips)
+  template <bool kCheck>
+  __device__ bool reload(int r) const {
+    return r <= 1 || r >= kR - 2 || (kCheck && chg(r));
+  }
   __device__ int row(int r) const { return gr0 + r * wd; }
   __device__ int slot(int r) const { return sb + r * kTX; }
   __device__ int cls(int r) const { return (cl[r >> 2] >> (8 * (r & 3))) & 255; }
@@ -406,18 +416,18 @@ struct Row7 {
 // the strip need no other band's values and are formed while the neighbouring
 // CTAs' halo rows are still in flight; rows 0 and kR-1 follow the wait.  Per
 // row the same doubles in the same order as bd_apply.
-__device__ __forceinline__ void bd_apply_overlap(const Th& th, Sh& sh, const double (&v)[kR],
-                                                 double (&out)[kR]) {
+template <bool kCheck>
+__device__ __forceinline__ void bd_apply_mid(const Th& th, const Sh& sh, const double (&v)[kR],
+                                             double (&out)[kR]) {
   const double* V = sh.vc();
   const int b = th.vb;
   Row7 row;
-  row.load(sh.TAB + th.cls(1) * kTabW);
   {
     double sw = V[b - 1], so = v[0];
     double w = V[b + kLD - 1], e = V[b + kLD + 1];
 #pragma unroll
     for (int r = 1; r < kR - 1; ++r) {
-      if (r > 1 && th.chg(r)) row.load(sh.TAB + th.cls(r) * kTabW);
+      if (th.reload<kCheck>(r)) row.load(sh.TAB + th.cls(r) * kTabW);
       const double en = V[b + (r + 1) * kLD + 1];
       const double wn = V[b + (r + 1) * kLD - 1];
       const double nb[7] = {sw, so, w, v[r], e, v[r + 1], en};
@@ -428,6 +438,15 @@ __device__ __forceinline__ void bd_apply_overlap(const Th& th, Sh& sh, const dou
       e = en;
     }
   }
+}
+
+__device__ __forceinline__ void bd_apply_overlap(const Th& th, Sh& sh, const double (&v)[kR],
+                                                 double (&out)[kR]) {
+  const double* V = sh.vc();
+  const int b = th.vb;
+  if (th.mid_uniform()) bd_apply_mid<false>(th, sh, v, out);
+  else bd_apply_mid<true>(th, sh, v, out);
+  Row7 row;
   bd_xwait(sh, sh.hb);
   {
     row.load(sh.TAB + th.cls(0) * kTabW);
@@ -527,19 +546,15 @@ __device__ __forceinline__ void bd_allsum_mb(double (&v)[NV], Sh& sh, int rank) 
 // (x_0 in the current exchange frame).  M / K / A rows held across the strip
 // (Row7); the M row's pad entry is the class's source profile (kPfTab), global
 // loads otherwise.
-template <bool kEnergy, bool kPfTab>
+template <bool kEnergy, bool kPfTab, bool kCheck>
 __device__ __forceinline__ void bd_start_passes(const Th& th, const BdArgs& a, const Sh& sh,
                                                 double sf, double dt, double (&bv)[kR],
                                                 double (&res)[kR], double& e2) {
   {
     Row7 mrow, krow;
-    double pfc;
-    const double* T = sh.TAB + th.cls(0) * kTabW;
-    mrow.load(T + 8);
-    pfc = T[15];
-    if (kEnergy) krow.load(T + 16);
+    double pfc = 0.0;
     bd_rows_s(th, sh.VA, [&](int r, const double (&nb)[7]) {
-      if (r > 0 && th.chg(r)) {
+      if (r == 0 || th.reload<kCheck>(r)) {
         const double* Tr = sh.TAB + th.cls(r) * kTabW;
         mrow.load(Tr + 8);
         pfc = Tr[15];
@@ -554,9 +569,8 @@ __device__ __forceinline__ void bd_start_passes(const Th& th, const BdArgs& a, c
   }
   const double* V0 = sh.vc();
   Row7 arow;
-  arow.load(sh.TAB + th.cls(0) * kTabW);
   bd_rows_s(th, V0, [&](int r, const double (&nb)[7]) {
-    if (r > 0 && th.chg(r)) arow.load(sh.TAB + th.cls(r) * kTabW);
+    if (r == 0 || th.reload<kCheck>(r)) arow.load(sh.TAB + th.cls(r) * kTabW);
     res[r] = th.ok(r) ? bv[r] - arow.dot(nb) : 0.0;
   });
 }
@@ -580,12 +594,16 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
     double bv[kR];
     // the two stencil passes, specialised on (energy, profile from the class
     // table): no uniform branches between the rows
-    if (energy) {
-      if (sh.pf_tab) bd_start_passes<true, true>(th, a, sh, sf, dt, bv, res, red[3]);
-      else bd_start_passes<true, false>(th, a, sh, sf, dt, bv, res, red[3]);
-    } else {
-      if (sh.pf_tab) bd_start_passes<false, true>(th, a, sh, sf, dt, bv, res, red[3]);
-      else bd_start_passes<false, false>(th, a, sh, sf, dt, bv, res, red[3]);
+    const int variant = (energy ? 4 : 0) | (sh.pf_tab ? 2 : 0) | (th.mid_uniform() ? 0 : 1);
+    switch (variant) {
+      case 0: bd_start_passes<false, false, false>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      case 1: bd_start_passes<false, false, true>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      case 2: bd_start_passes<false, true, false>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      case 3: bd_start_passes<false, true, true>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      case 4: bd_start_passes<true, false, false>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      case 5: bd_start_passes<true, false, true>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      case 6: bd_start_passes<true, true, false>(th, a, sh, sf, dt, bv, res, red[3]); break;
+      default: bd_start_passes<true, true, true>(th, a, sh, sf, dt, bv, res, red[3]); break;
     }
     bd_precond(pc, bv, u);
 #pragma unroll
