@@ -949,17 +949,17 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
       for (int rr = 0; rr < kGB; ++rr) {
         const int r = h + rr;
         const double an = sh.X[th.slot(r)];
-        double x0 = 0.0;
-        if (th.ok(r)) {
-          const double sst = pred ? fma(xr[rr], sc[0], xi[rr] * sc[1]) : 0.0;
-          const double ssn = pred ? fma(xr[rr], sc[2], xi[rr] * sc[3]) : 0.0;
-          const double yn = an - ssn;
-          double gv = w0 * yn;
+        // straight-line per row (no branch between the unrolled rows): without
+        // the predictor XS holds zeros, rows outside the grid hold zeros and
+        // only skip the ring store
+        const double sst = pred ? fma(xr[rr], sc[0], xi[rr] * sc[1]) : 0.0;
+        const double ssn = pred ? fma(xr[rr], sc[2], xi[rr] * sc[3]) : 0.0;
+        const double yn = an - ssn;
+        double gv = w0 * yn;
 #pragma unroll
-          for (int sl = 0; sl < kRing; ++sl) gv = fma(ww[sl], pv[rr][sl], gv);
-          rb[cur * kBandPts + r * kTX] = yn;
-          x0 = gv + sst;
-        }
+        for (int sl = 0; sl < kRing; ++sl) gv = fma(ww[sl], pv[rr][sl], gv);
+        if (th.ok(r)) rb[cur * kBandPts + r * kTX] = yn;
+        const double x0 = th.ok(r) ? gv + sst : 0.0;
         sh.VA[th.vb + r * kLD] = an;
         VN[th.vb + r * kLD] = x0;
         sh.X[th.slot(r)] = x0;
