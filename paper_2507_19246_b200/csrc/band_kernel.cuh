@@ -1,8 +1,9 @@
 // band_kernel.cuh — device code of the band path (band_path.cu includes it twice:
-// namespace bd0 with kDbg = false, the production kernel, and bd1 with kDbg =
-// true, the barrier-serialised debug mode MLMCP_BAND_SYNC=1 — a compile-time
-// switch, because runtime checks between the phases of a PCG iteration split
-// its straight-line code and cost 3% of the kernel).  Not a standalone header.
+// namespace bd0 with kDbg = kProf = false, the production kernel, bd1 with kDbg =
+// true, the barrier-serialised debug mode MLMCP_BAND_SYNC=1, bd2 with the cycle
+// probes of MLMCP_BAND_PROF=1 — compile-time switches, because runtime checks
+// between the phases of a PCG iteration split its straight-line code and cost
+// 3% of the kernel).  Not a standalone header.
 struct Th {
   int x, k, rank, gy0;
   int vb;          // exchange-buffer index of row 0
@@ -421,7 +422,7 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
     red[1] = fma(w[r], u[r], red[1]);
   }
   bd_allsum_mb<4>(red, sh, th.rank);
-  long long tp = clock64();
+  long long tp = kProf ? clock64() : 0;
   e_out = 0.5 * red[3];
   const double gamma = red[0];
   double delta = red[1];
@@ -698,7 +699,7 @@ __global__ void __launch_bounds__(kNT, 1) band_propagate_kernel(BdArgs a) {
   const int lsdeg = a.ls_on > 1 ? a.ls_on : (a.omega * t.dt * 192.0 < 6.283185307179586 ? 5 : 6);
   int iters = 0, code = MLMCP_ST_OK, fail_step = 0;
   double acc = 0.0;
-  long long tq = clock64();
+  long long tq = kProf ? clock64() : 0;
   for (int step = 0; step < t.n_steps; ++step) {
     BD_PROF(4, tq);
     const int64_t g = t.k0 + step + 1;

@@ -100,7 +100,7 @@ __constant__ double c_bd_ls48[8] = {175.0 / 56, -125.0 / 56, -75.0 / 56, 45.0 / 
 __device__ unsigned long long g_band_prof[16];   // [8..13]: PCG-iteration phases (prof bit 1)
 #define BD_PROF(i, t0)                                                              \
   do {                                                                            \
-    if ((a.prof & 1) && blockIdx.x == 0 && threadIdx.x == 0) {                          \
+    if (kProf && (a.prof & 1) && blockIdx.x == 0 && threadIdx.x == 0) {                 \
       const long long t1_ = clock64();                                            \
       g_band_prof[i] += (unsigned long long)(t1_ - (t0));                         \
       (t0) = t1_;                                                                 \
@@ -201,13 +201,17 @@ __device__ __forceinline__ void st_async(uint32_t addr, double v, uint32_t mbar)
 
 // device code: production (bd0) and barrier-serialised debug (bd1) instantiations
 namespace bd0 {
-constexpr bool kDbg = false;
+constexpr bool kDbg = false, kProf = false;
 #include "band_kernel.cuh"
 }  // namespace bd0
 namespace bd1 {
-constexpr bool kDbg = true;
+constexpr bool kDbg = true, kProf = false;
 #include "band_kernel.cuh"
 }  // namespace bd1
+namespace bd2 {   // MLMCP_BAND_PROF=1: per-phase cycle probes
+constexpr bool kDbg = false, kProf = true;
+#include "band_kernel.cuh"
+}  // namespace bd2
 
 size_t band_smem_bytes(int n_classes) {
   return sizeof(double) * (3 * kV + kSlots + kPF + 2 * kSlots + kTabW * n_classes + kRedD + 5);
@@ -296,7 +300,8 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
   const size_t smem = band_smem_bytes(a.rC);
   static size_t attr_smem = 0;
   if (smem > attr_smem) {
-    for (auto k : {bd0::band_propagate_kernel, bd1::band_propagate_kernel}) {
+    for (auto k : {bd0::band_propagate_kernel, bd1::band_propagate_kernel,
+                   bd2::band_propagate_kernel}) {
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                             (int)smem));
       MLMCP_CUDA_CHECK(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
@@ -319,8 +324,11 @@ int band_propagate(Ctx* ctx, int n_tasks, const mlmcp_task* tasks, const double*
   if (ctx->time_iters) MLMCP_CUDA_CHECK(cudaEventRecord(ctx->iter_ev[0], stream));
   // MLMCP_BAND_SYNC=1: the instantiation with a cluster barrier before and
   // after every exchange and all-reduce (bd1), otherwise the production kernel
-  MLMCP_CUDA_CHECK(cudaLaunchKernelEx(
-      &cfg, a.dbg_sync ? bd1::band_propagate_kernel : bd0::band_propagate_kernel, a));
+  MLMCP_CUDA_CHECK(cudaLaunchKernelEx(&cfg,
+                                      a.dbg_sync ? bd1::band_propagate_kernel
+                                      : a.prof   ? bd2::band_propagate_kernel
+                                                 : bd0::band_propagate_kernel,
+                                      a));
   MLMCP_LAUNCH_CHECK("band_propagate_kernel");
   if (ctx->time_iters) {
     MLMCP_CUDA_CHECK(cudaEventRecord(ctx->iter_ev[1], stream));
