@@ -108,10 +108,10 @@ __device__ __forceinline__ void bd_xissue(const Th& th, const double (&v)[kR], d
   MLMCP_DCHECK(th.vb - kLD - 1 >= 0 && th.vb + kR * kLD + 1 < kV);
 #pragma unroll
   for (int r = 0; r < kR; ++r) V[th.vb + r * kLD] = v[r];
-  if (th.k == 0 && th.rank > 0)
+  if ((kNS == 1 || th.k == 0) && th.rank > 0)
     st_async(bd_mapa(bd_smem(V + (kHB + 1) * kLD + th.x + 1), th.rank - 1), v[0],
              bd_mapa(bd_smem(mb), th.rank - 1));
-  if (th.k == kNS - 1 && th.rank < kCS - 1)
+  if ((kNS == 1 || th.k == kNS - 1) && th.rank < kCS - 1)
     st_async(bd_mapa(bd_smem(V + th.x + 1), th.rank + 1), v[kR - 1],
              bd_mapa(bd_smem(mb), th.rank + 1));
   if (threadIdx.x == 0)
@@ -128,10 +128,10 @@ __device__ __forceinline__ void bd_xwait(Sh& sh, int mi) {
 __device__ __forceinline__ void bd_xsend(const Th& th, double* V, Sh& sh, int mi) {
   if (kDbg) bd_sync();
   uint64_t* mb = sh.mb + mi;
-  if (th.k == 0 && th.rank > 0)
+  if ((kNS == 1 || th.k == 0) && th.rank > 0)
     st_async(bd_mapa(bd_smem(V + (kHB + 1) * kLD + th.x + 1), th.rank - 1), V[th.vb],
              bd_mapa(bd_smem(mb), th.rank - 1));
-  if (th.k == kNS - 1 && th.rank < kCS - 1)
+  if ((kNS == 1 || th.k == kNS - 1) && th.rank < kCS - 1)
     st_async(bd_mapa(bd_smem(V + th.x + 1), th.rank + 1), V[th.vb + (kR - 1) * kLD],
              bd_mapa(bd_smem(mb), th.rank + 1));
   if (threadIdx.x == 0)
@@ -470,11 +470,15 @@ __device__ __forceinline__ int bd_ie_step(const Th& th, const BdArgs& a, Sh& sh,
     const double gnew = red2[0];
     delta = red2[1];
     if (gnew <= tol2) break;
-    if (!isfinite(gnew)) { iters += it; return MLMCP_ST_NONFINITE; }
-    if (it >= a.max_it) { iters += it; return MLMCP_ST_NOCONV; }
     const double beta = gnew * inv_g;
     const double den = fma(-(gnew * gnew), c, delta);
-    if (!(den > 0.0)) { iters += it; return MLMCP_ST_BREAKDOWN; }
+    // one exit test per iteration (the order of the codes is the former one)
+    if (!isfinite(gnew) || it >= a.max_it || !(den > 0.0)) {
+      iters += it;
+      return !isfinite(gnew) ? MLMCP_ST_NONFINITE
+             : it >= a.max_it ? MLMCP_ST_NOCONV
+                              : MLMCP_ST_BREAKDOWN;
+    }
     alpha = gnew * fast_rcp(den);
     inv_g = fast_rcp(gnew);
     c = inv_g * (den * inv_g);
