@@ -406,6 +406,7 @@ def test_pipelined_calls_bitwise(cuda, monkeypatch):
     equal, and the plan covers every sample exactly once."""
     from paper_2507_19246_b200.mlmc import FixedSamples, mlmc_estimate, plan_calls
     from paper_2507_19246_b200.models import EddyCurrentFamily
+    monkeypatch.delenv("MLMCP_PIPELINE", raising=False)
     fam = large_family(2)
     monkeypatch.setattr(EddyCurrentFamily, "max_samples_per_call",
                         lambda self, parareal_cfg=None, level=None: 3)
